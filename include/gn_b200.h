@@ -1,0 +1,128 @@
+/*
+ * gn_b200.h -- C ABI of the B200 Graph-Normalization (GN) engine.
+ *
+ * The reference (graphnorm, pure Python) has no FFI; its "operator API" is the
+ * Python function set exported by graphnorm/__init__.py:3-54.  Each entry
+ * point below replaces the arithmetic behind one of those functions; the
+ * Python drop-in (paper_2605_05330_b200) binds them with ctypes and keeps the
+ * reference signatures, exceptions and messages.  Plain pointers and sizes
+ * only -- no torch types.
+ *
+ * Conventions
+ *   - every function returns int status (GN_OK = 0); gn_last_error() gives a
+ *     thread-local message for the last failure on the calling thread;
+ *   - host pointers unless GN_DEVICE_IO is set (then x0 / x_out are device
+ *     pointers in the graph's dtype);
+ *   - a gn_graph is immutable after creation and safe for concurrent use by
+ *     any number of threads (reference: graph.py:31-33, SPEC "unrestricted
+ *     concurrent reads"); each call runs on its own CUDA stream and
+ *     workspace, so calls are re-entrant.
+ */
+#ifndef GN_B200_H
+#define GN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GN_ABI_VERSION 1
+
+/* dtypes of the device state */
+#define GN_F64 0
+#define GN_F32 1
+
+/* status codes.  NEGATIVE / NOT_NORMALIZABLE / NONFINITE map one-to-one onto
+ * the three NormalizationError raises of run_wrgn (dynamics.py:147,149,176). */
+#define GN_OK 0
+#define GN_ERR_ARG 1
+#define GN_ERR_CUDA 2
+#define GN_ERR_NEGATIVE 3
+#define GN_ERR_NOT_NORMALIZABLE 4
+#define GN_ERR_NONFINITE 5
+#define GN_ERR_NOMEM 6
+#define GN_ERR_NODEV 7
+#define GN_ERR_ZERO_DENOM 8 /* fitness(): d <= 0 (dynamics.py:246-247) */
+#define GN_ERR_ZERO_MASS 9  /* simplex_state(): mass <= 0 (dynamics.py:231-232) */
+
+/* run flags */
+#define GN_TRACE 0x1u      /* energy / pre_energy per iteration (record_trace) */
+#define GN_EARLY_EXIT 0x2u /* stop at gamma==final and step_inf < 1e-12 (dynamics.py:177) */
+#define GN_EXACT 0x4u      /* one thread per row, sequential sums: bitwise equal to scipy */
+#define GN_DEVICE_IO 0x8u  /* x0 / x_out are device pointers of the graph dtype */
+#define GN_NO_CHECK 0x10u  /* skip the x0 checks (gn_step has none: dynamics.py:111-119) */
+#define GN_NO_CLIP 0x20u   /* return the raw state (gn_step) instead of clip(x,0,1) */
+#define GN_NONFINITE_OK 0x40u /* do not stop on a non-finite state (gn_step) */
+
+typedef struct gn_graph gn_graph;
+
+typedef struct gn_run_stats {
+    double loop_ms;        /* CUDA-event time of the device loop kernel(s) */
+    double total_ms;       /* CUDA-event time of the whole call incl. copies */
+    int64_t launches;      /* kernels this call launched */
+    int64_t grid_blocks;   /* blocks of the persistent loop kernel */
+    int64_t block_threads; /* threads per block */
+    int64_t h2d_bytes;     /* host->device bytes of the call */
+    int64_t d2h_bytes;     /* device->host bytes of the call */
+} gn_run_stats;
+
+int gn_abi_version(void);
+const char* gn_last_error(void);
+int gn_device_count(int* count);
+/* total kernels launched by this process through the engine */
+int64_t gn_launch_count(void);
+
+/* WeightedGraph (graph.py:22-75): CSR with sorted, symmetric, deduplicated
+ * rows; w > 0.  v = sqrt(w) is formed on the device (IEEE sqrt, bitwise equal
+ * to numpy's).  Column indices are int32 (as scipy's csr copy, graph.py:46).
+ * block_hint > 0 overrides the persistent grid size (tuning / tests). */
+int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices,
+                    const double* w, int dtype, int device, gn_graph** out);
+int gn_graph_destroy(gn_graph* g);
+int gn_graph_info(const gn_graph* g, int64_t* n, int64_t* nnz, int* dtype,
+                  int* device, int64_t* device_bytes, int* num_bins);
+int gn_graph_set_grid(gn_graph* g, int blocks);
+
+/* run_wrgn (dynamics.py:129-180).  gammas[k] = schedule.gamma_at(k) for
+ * k < iters (computed on the host with the reference formula, bitwise).
+ * Outputs (host, may be NULL): x_out (n fp64, clipped to [0,1]);
+ * step_inf / fallbacks (iters); mass[k] = w.x_{k+1} (the objective);
+ * energy / pre_energy (iters, GN_TRACE); x_hist (iters*n fp64, test aid).
+ * *iters_run = trace length; on GN_ERR_NONFINITE *fail_iter = k. */
+int gn_run(gn_graph* g, const void* x0, const double* gammas, int iters,
+           double final_gamma, uint32_t flags, void* x_out, double* step_inf,
+           int64_t* fallbacks, double* mass, double* energy, double* pre_energy,
+           double* x_hist, int* iters_run, int* fail_iter, gn_run_stats* stats);
+
+/* gn_step (dynamics.py:111-119): one unclipped, unchecked step. */
+int gn_step(gn_graph* g, const double* x, double gamma, uint32_t flags,
+            double* out, int64_t* nfb);
+
+/* is_normalizable (dynamics.py:122-126): all(x + A x > 0). */
+int gn_is_normalizable(gn_graph* g, const double* x, int* ok);
+/* out = A @ in, fp64, per-row sequential order (scipy csr_matvec). */
+int gn_spmv(gn_graph* g, const double* in, double* out);
+/* energy (dynamics.py:210-219) and weighted_mass (222-224), fp64. */
+int gn_energy(gn_graph* g, const double* x, double gamma, double* energy);
+int gn_weighted_mass(gn_graph* g, const double* x, double* mass);
+/* simplex_state (dynamics.py:227-233) and fitness (236-250), fp64. */
+int gn_simplex_state(gn_graph* g, const double* x, double* p_out);
+int gn_fitness(gn_graph* g, const double* p, double gamma, double* f_out,
+               double* fbar);
+
+/* round_to_mis (dynamics.py:253-277) + MisSolution.from_members
+ * (graph.py:178-186).  x is host fp64 (or, with GN_DEVICE_IO, a device array
+ * of the graph dtype).  selected: n bytes (0/1).  weight is numpy's pairwise
+ * sum over members in ascending order (bitwise equal to w[idx].sum()). */
+int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
+             double* weight, int* independent, int* maximal, int64_t* count);
+/* is_independent / is_maximal_independent / set_weight (graph.py:134-162)
+ * on a 0/1 membership mask. */
+int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight,
+                     int* independent, int* maximal, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GN_B200_H */

@@ -1,0 +1,352 @@
+"""Weighted regularized graph-normalization dynamics on the B200 engine.
+
+Drop-in for graphnorm.dynamics (/root/reference/pkg/src/graphnorm/dynamics.py):
+same names, signatures, return types, exceptions and messages.  Every step,
+reduction, check and the rounding run in the CUDA engine (libgnb200.so) --
+there is no CPU path.  Host-side code here only prepares inputs (the gamma
+table, the seeded start vectors) and unpacks results.
+
+Engine options are keyword-only extras the reference does not have:
+``dtype`` ("fp64" default = the reference arithmetic, or "fp32"),
+``exact`` (one thread per row, sequential sums: fp64 is then bitwise equal to
+the reference) and ``device`` (CUDA ordinal).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _engine as E
+from .graph import MisSolution, device_graph, dtype_code
+
+# dynamics.py:21-24
+SAFE_DIV_THRESHOLD = 1e-9
+FALLBACK_VALUE = 0.5
+
+CLAMP_FLOOR = 1e-3
+
+_DEFAULTS = {"dtype": "fp64", "exact": False, "device": 0}
+
+
+def set_engine_defaults(dtype=None, exact=None, device=None) -> dict:
+    """Change the engine options used when a call does not pass them."""
+    if dtype is not None:
+        dtype_code(dtype)
+        _DEFAULTS["dtype"] = dtype
+    if exact is not None:
+        _DEFAULTS["exact"] = bool(exact)
+    if device is not None:
+        _DEFAULTS["device"] = int(device)
+    return dict(_DEFAULTS)
+
+
+def _opt(name, value):
+    return _DEFAULTS[name] if value is None else value
+
+
+class NormalizationError(ValueError):
+    """Raised when a state has a zero closed neighborhood sum."""
+
+
+@dataclass(frozen=True)
+class GammaSchedule:
+    """Interpolation plan for the regularization parameter (dynamics.py:31-73).
+
+    linear mode moves gamma from gamma0 at step 0 to gamma1 at the last
+    step; constant mode holds gamma0 throughout.
+    """
+
+    gamma0: float
+    gamma1: float
+    iterations: int
+    mode: str = "linear"
+
+    def __post_init__(self):
+        if self.mode not in ("constant", "linear"):
+            raise ValueError(f"unknown schedule mode {self.mode!r}")
+        if self.iterations < 1:
+            raise ValueError("iterations must be positive")
+        if self.mode == "linear" and self.iterations < 2:
+            raise ValueError("linear mode needs at least 2 iterations")
+        if self.gamma0 < 0 or self.gamma1 < 0:
+            raise ValueError("gamma must be nonnegative")
+
+    @classmethod
+    def constant(cls, gamma: float, iterations: int) -> "GammaSchedule":
+        return cls(gamma, gamma, iterations, mode="constant")
+
+    @classmethod
+    def pursuit(cls, gamma0: float = 0.9, gamma1: float = 1.5, iterations: int = 1000) -> "GammaSchedule":
+        """Default graduated schedule: linear 0.9 -> 1.5 over 1000 steps."""
+        return cls(gamma0, gamma1, iterations, mode="linear")
+
+    def gamma_at(self, k: int) -> float:
+        if self.mode == "constant":
+            return self.gamma0
+        p = float(k) / float(self.iterations - 1)
+        return p * self.gamma1 + (1.0 - p) * self.gamma0
+
+    @property
+    def final_gamma(self) -> float:
+        return self.gamma0 if self.mode == "constant" else self.gamma1
+
+    def table(self) -> np.ndarray:
+        """gamma_at(k) for every k, with the same IEEE operations (bitwise)."""
+        if self.mode == "constant":
+            return np.full(self.iterations, float(self.gamma0), dtype=np.float64)
+        p = np.arange(self.iterations, dtype=np.float64) / float(self.iterations - 1)
+        return p * float(self.gamma1) + (1.0 - p) * float(self.gamma0)
+
+
+@dataclass
+class SolveTrace:
+    """Per-iteration record of one trajectory (dynamics.py:76-99).
+
+    gamma, step_inf, and fallbacks are always populated.  The energy and
+    mass series are filled only when the run records a full trace.
+    ``objective`` is an engine extra: the relaxed MWIS primal w.x after every
+    step, computed by the fused reduction on every run.
+    """
+
+    gamma: list = field(default_factory=list)
+    energy: list = field(default_factory=list)
+    pre_energy: list = field(default_factory=list)
+    mass: list = field(default_factory=list)
+    step_inf: list = field(default_factory=list)
+    fallbacks: list = field(default_factory=list)
+    objective: list = field(default_factory=list, repr=False, compare=False)
+
+    @property
+    def total_fallbacks(self) -> int:
+        return sum(self.fallbacks)
+
+    def __len__(self) -> int:
+        return len(self.gamma)
+
+
+def _as_state(g, x) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if x.shape != (g.n,):
+        raise ValueError(f"state has shape {x.shape}, expected ({g.n},)")
+    return x
+
+
+def gn_step(g, x, gamma: float, *, dtype=None, exact=None, device=None) -> np.ndarray:
+    """Apply the weighted regularized normalization map once (dynamics.py:111-119).
+
+    x'_i = x_i / (x_i + gamma * sum_{j ~ i} (v_j / v_i) x_j).  Entries whose
+    denominator is at or below the safe-division threshold are set to the
+    fallback value 0.5 instead of raising.
+    """
+    x = _as_state(g, x)
+    h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
+    out = np.empty(g.n, dtype=np.float64)
+    nfb = ctypes.c_int64(0)
+    flags = E.GN_EXACT if _opt("exact", exact) else 0
+    E.check(E.lib().gn_step(h.handle, E.ptr(x), float(gamma), flags, E.ptr(out), ctypes.byref(nfb)))
+    return out
+
+
+def is_normalizable(g, x) -> bool:
+    """All closed neighborhood sums positive (dynamics.py:122-126)."""
+    x = _as_state(g, x)
+    ok = ctypes.c_int(0)
+    h = device_graph(g)
+    E.check(E.lib().gn_is_normalizable(h.handle, E.ptr(x), ctypes.byref(ok)))
+    return bool(ok.value)
+
+
+_RUN_ERRORS = {
+    E.GN_ERR_NEGATIVE: "state entries must be nonnegative",
+    E.GN_ERR_NOT_NORMALIZABLE: "initial state has a zero closed neighborhood sum",
+}
+
+
+@dataclass
+class RunResult:
+    """Everything one engine run returns (run_wrgn keeps the reference shape)."""
+
+    x: np.ndarray
+    trace: SolveTrace
+    stats: dict
+    history: Optional[np.ndarray] = None
+
+
+def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early_exit: bool = False, *,
+               dtype=None, exact=None, device=None, history: bool = False) -> RunResult:
+    """run_wrgn with the engine's extras (stats, optional per-iteration x)."""
+    x = _as_state(g, x0)
+    h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
+    gam = np.ascontiguousarray(schedule.table())
+    iters = schedule.iterations
+    step_inf = np.zeros(iters, dtype=np.float64)
+    fallbacks = np.zeros(iters, dtype=np.int64)
+    mass = np.zeros(iters, dtype=np.float64)
+    energy = np.zeros(iters, dtype=np.float64) if record_trace else None
+    pre_energy = np.zeros(iters, dtype=np.float64) if record_trace else None
+    hist = np.zeros((iters, g.n), dtype=np.float64) if history else None
+    x_out = np.empty(g.n, dtype=np.float64)
+    ran = ctypes.c_int(0)
+    fail = ctypes.c_int(-1)
+    st = E.RunStats()
+    flags = 0
+    if record_trace:
+        flags |= E.GN_TRACE
+    if early_exit:
+        flags |= E.GN_EARLY_EXIT
+    if _opt("exact", exact):
+        flags |= E.GN_EXACT
+    rc = E.lib().gn_run(h.handle, E.ptr(x), E.ptr(gam), iters, float(schedule.final_gamma), flags,
+                        E.ptr(x_out), E.ptr(step_inf), E.ptr(fallbacks), E.ptr(mass), E.ptr(energy),
+                        E.ptr(pre_energy), E.ptr(hist), ctypes.byref(ran), ctypes.byref(fail),
+                        ctypes.byref(st))
+    if rc in _RUN_ERRORS:
+        raise NormalizationError(_RUN_ERRORS[rc])
+    if rc == E.GN_ERR_NONFINITE:
+        raise NormalizationError(f"non-finite state at iteration {fail.value}")
+    E.check(rc)
+    k = ran.value
+    trace = SolveTrace()
+    trace.gamma = [float(v) for v in gam[:k]]
+    trace.step_inf = [float(v) for v in step_inf[:k]]
+    trace.fallbacks = [int(v) for v in fallbacks[:k]]
+    trace.objective = [float(v) for v in mass[:k]]
+    if record_trace:
+        trace.energy = [float(v) for v in energy[:k]]
+        trace.pre_energy = [float(v) for v in pre_energy[:k]]
+        trace.mass = list(trace.objective)
+    stats = {f: getattr(st, f) for f, _ in E.RunStats._fields_}
+    return RunResult(x_out, trace, stats, hist[:k] if history else None)
+
+
+def run_wrgn(g, x0, schedule: GammaSchedule, record_trace: bool = False, early_exit: bool = False, *,
+             dtype=None, exact=None, device=None) -> tuple[np.ndarray, SolveTrace]:
+    """Iterate the map under a gamma schedule (dynamics.py:129-180).
+
+    Raises NormalizationError if x0 is not normalizable or a non-finite
+    state appears mid-run.  When early_exit is set, stops once gamma has
+    reached its final value and the step infinity-norm falls below 1e-12;
+    otherwise runs the full budget.  Final entries are clamped to [0, 1].
+    """
+    r = run_engine(g, x0, schedule, record_trace, early_exit, dtype=dtype, exact=exact, device=device)
+    return r.x, r.trace
+
+
+def init_random(n: int, seed) -> np.ndarray:
+    """Exponentially sampled start, scaled by its max and clamped to [1e-3, 1].
+
+    Host-side on purpose: it is the seeded input of a run (numpy PCG64
+    stream), identical to dynamics.py:183-191."""
+    if n < 1:
+        raise ValueError("n must be at least 1")
+    rng = np.random.default_rng(seed)
+    u = rng.random(n)
+    e = -np.log(np.maximum(u, np.finfo(np.float64).tiny))
+    x = e / e.max()
+    return np.clip(x, CLAMP_FLOOR, 1.0)
+
+
+def init_warm(values, n: Optional[int] = None) -> np.ndarray:
+    """Clamp an externally supplied fractional vector to [1e-3, 1] (dynamics.py:194-207)."""
+    x = np.asarray(values, dtype=np.float64)
+    if x.ndim != 1:
+        raise ValueError("warm start must be a 1-d vector")
+    if n is not None and len(x) != n:
+        raise ValueError(f"warm start has length {len(x)}, expected {n}")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("warm start contains non-finite entries")
+    return np.clip(x, CLAMP_FLOOR, 1.0)
+
+
+def energy(g, x, gamma: float) -> float:
+    """Quadratic energy (1/2) y'(I + gamma A)y - v'y (dynamics.py:210-219)."""
+    x = _as_state(g, x)
+    out = ctypes.c_double()
+    E.check(E.lib().gn_energy(device_graph(g).handle, E.ptr(x), float(gamma), ctypes.byref(out)))
+    return out.value
+
+
+def weighted_mass(g, x) -> float:
+    """Relaxed objective sum(w_i x_i) (dynamics.py:222-224)."""
+    x = _as_state(g, x)
+    out = ctypes.c_double()
+    E.check(E.lib().gn_weighted_mass(device_graph(g).handle, E.ptr(x), ctypes.byref(out)))
+    return out.value
+
+
+def simplex_state(g, x) -> np.ndarray:
+    """Mass-normalized coordinates p_i = w_i x_i / sum_j w_j x_j (dynamics.py:227-233)."""
+    x = _as_state(g, x)
+    p = np.empty(g.n, dtype=np.float64)
+    rc = E.lib().gn_simplex_state(device_graph(g).handle, E.ptr(x), E.ptr(p))
+    if rc == E.GN_ERR_ZERO_MASS:
+        raise ValueError("weighted mass must be positive")
+    E.check(rc)
+    return p
+
+
+def fitness(g, p, gamma: float) -> tuple[np.ndarray, float]:
+    """Replicator fitness f_i = v_i / ((I + gamma A)(p / v))_i and its average
+    (dynamics.py:236-250)."""
+    p = _as_state(g, p)
+    f = np.empty(g.n, dtype=np.float64)
+    fbar = ctypes.c_double()
+    rc = E.lib().gn_fitness(device_graph(g).handle, E.ptr(p), float(gamma), E.ptr(f), ctypes.byref(fbar))
+    if rc == E.GN_ERR_ZERO_DENOM:
+        raise ValueError("zero denominator in fitness: state not normalizable")
+    E.check(rc)
+    return f, fbar.value
+
+
+def round_result(g, x, *, dtype=None, device=None) -> tuple[np.ndarray, float, bool, bool]:
+    """Device rounding: (0/1 mask, weight, independent, maximal)."""
+    x = _as_state(g, x)
+    h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
+    sel = np.zeros(max(g.n, 1), dtype=np.uint8)
+    weight = ctypes.c_double()
+    ind = ctypes.c_int()
+    mx = ctypes.c_int()
+    cnt = ctypes.c_int64()
+    E.check(E.lib().gn_round(h.handle, E.ptr(x), 0, E.ptr(sel), ctypes.byref(weight), ctypes.byref(ind),
+                             ctypes.byref(mx), ctypes.byref(cnt)))
+    return sel[: g.n], weight.value, bool(ind.value), bool(mx.value)
+
+
+def round_to_mis(g, x) -> MisSolution:
+    """Binarize a state into a maximal independent set (dynamics.py:253-277).
+
+    Thresholds at 0.5, repairs conflicts by dropping the lighter endpoint
+    (ties keep the larger index), then completes greedily by descending
+    weight (ties prefer the smaller index).
+    """
+    sel, weight, ind, mx = round_result(g, x)
+    members = np.flatnonzero(sel)
+    return MisSolution(members=tuple(int(i) for i in members), weight=weight, independent=ind, maximal=mx)
+
+
+__all__ = [
+    "CLAMP_FLOOR",
+    "FALLBACK_VALUE",
+    "SAFE_DIV_THRESHOLD",
+    "GammaSchedule",
+    "NormalizationError",
+    "RunResult",
+    "SolveTrace",
+    "energy",
+    "fitness",
+    "gn_step",
+    "init_random",
+    "init_warm",
+    "is_normalizable",
+    "round_result",
+    "round_to_mis",
+    "run_engine",
+    "run_wrgn",
+    "set_engine_defaults",
+    "simplex_state",
+    "weighted_mass",
+]

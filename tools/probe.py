@@ -1,0 +1,58 @@
+"""Quick engine timing probe (development aid, not the bench contract)."""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+
+import paper_2605_05330_b200 as P  # noqa: E402
+from paper_2605_05330_b200 import generators as G  # noqa: E402
+
+
+def probe(inst, iters=1000, grids=(0,), exact=False, reps=3, dtype=None):
+    g = inst.graph
+    dt = dtype or inst.dtype
+    h = g.device_graph(dt)
+    s = P.GammaSchedule.pursuit(iterations=iters)
+    out = []
+    for grid in grids:
+        h.set_grid(grid)
+        P.run_engine(g, inst.x0, s, dtype=dt, exact=exact)  # warm
+        best = None
+        for _ in range(reps):
+            r = P.run_engine(g, inst.x0, s, dtype=dt, exact=exact)
+            if best is None or r.stats["loop_ms"] < best["loop_ms"]:
+                best = r.stats
+        eus = g.num_edges * iters / (best["loop_ms"] * 1e-3)
+        rec = {"inst": inst.name, "dtype": dt, "exact": exact, "grid": best["grid_blocks"],
+               "loop_ms": round(best["loop_ms"], 3), "us_per_iter": round(best["loop_ms"] * 1e3 / iters, 3),
+               "Geu_s": round(eus / 1e9, 2), "fallbacks": r.trace.total_fallbacks}
+        print(json.dumps(rec), flush=True)
+        out.append(rec)
+    h.set_grid(0)
+    return out
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="C1,C2,C3")
+    args = ap.parse_args()
+    which = args.which.split(",")
+    if "C1" in which:
+        probe(G.c1_er(), grids=(1, 2, 4, 0))
+        probe(G.c1_er(), exact=True, grids=(0,))
+    if "C2" in which:
+        t = time.time(); inst = G.c2_assignment(); print("gen C2", time.time() - t, flush=True)
+        probe(inst, grids=(148, 296, 444, 592, 0))
+        probe(inst, exact=True, grids=(0,), reps=1)
+        probe(inst, dtype="fp64", grids=(0,), reps=1)
+    if "C3" in which:
+        t = time.time(); inst = G.c3_ba(); print("gen C3", time.time() - t, flush=True)
+        probe(inst, grids=(64, 148, 296, 592, 0))
+        probe(inst, exact=True, grids=(0,), reps=1)
+    if "C4" in which:
+        t = time.time(); b = G.c4_batch(1024); print("gen C4", time.time() - t, flush=True)
+        probe(b.instance, grids=(296, 592, 0))
