@@ -11,8 +11,8 @@
  * Conventions
  *   - every function returns int status (GN_OK = 0); gn_last_error() gives a
  *     thread-local message for the last failure on the calling thread;
- *   - host pointers unless GN_DEVICE_IO is set (then x0 / x_out are device
- *     pointers in the graph's dtype);
+ *   - host pointers unless GN_DEVICE_IO is set (then x0 / x_out are fp64
+ *     device pointers, still in the caller's vertex order);
  *   - a gn_graph is immutable after creation and safe for concurrent use by
  *     any number of threads (reference: graph.py:31-33, SPEC "unrestricted
  *     concurrent reads"); each call runs on its own CUDA stream and
@@ -29,9 +29,16 @@ extern "C" {
 
 #define GN_ABI_VERSION 1
 
-/* dtypes of the device state */
+/* dtypes of the device state
+ *   GN_F64       binary64 throughout (the reference arithmetic)
+ *   GN_F32       binary32 gathered values (what each vertex publishes to its
+ *                neighbours, i.e. the bandwidth-bound stream), binary64
+ *                per-vertex state, sums and update.  Keeps every vertex's own
+ *                trajectory out of binary32's denormal range.
+ *   GN_F32_PURE  binary32 throughout (matches the oracle's fp32 bitwise) */
 #define GN_F64 0
 #define GN_F32 1
+#define GN_F32_PURE 2
 
 /* status codes.  NEGATIVE / NOT_NORMALIZABLE / NONFINITE map one-to-one onto
  * the three NormalizationError raises of run_wrgn (dynamics.py:147,149,176). */
@@ -50,7 +57,7 @@ extern "C" {
 #define GN_TRACE 0x1u      /* energy / pre_energy per iteration (record_trace) */
 #define GN_EARLY_EXIT 0x2u /* stop at gamma==final and step_inf < 1e-12 (dynamics.py:177) */
 #define GN_EXACT 0x4u      /* one thread per row, sequential sums: bitwise equal to scipy */
-#define GN_DEVICE_IO 0x8u  /* x0 / x_out are device pointers of the graph dtype */
+#define GN_DEVICE_IO 0x8u  /* x0 / x_out are fp64 device pointers */
 #define GN_NO_CHECK 0x10u  /* skip the x0 checks (gn_step has none: dynamics.py:111-119) */
 #define GN_NO_CLIP 0x20u   /* return the raw state (gn_step) instead of clip(x,0,1) */
 #define GN_NONFINITE_OK 0x40u /* do not stop on a non-finite state (gn_step) */
@@ -76,7 +83,7 @@ int64_t gn_launch_count(void);
 /* WeightedGraph (graph.py:22-75): CSR with sorted, symmetric, deduplicated
  * rows; w > 0.  v = sqrt(w) is formed on the device (IEEE sqrt, bitwise equal
  * to numpy's).  Column indices are int32 (as scipy's csr copy, graph.py:46).
- * block_hint > 0 overrides the persistent grid size (tuning / tests). */
+ * gn_graph_set_grid(g, b > 0) overrides the persistent grid size (tuning). */
 int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices,
                     const double* w, int dtype, int device, gn_graph** out);
 int gn_graph_destroy(gn_graph* g);
@@ -112,8 +119,8 @@ int gn_fitness(gn_graph* g, const double* p, double gamma, double* f_out,
                double* fbar);
 
 /* round_to_mis (dynamics.py:253-277) + MisSolution.from_members
- * (graph.py:178-186).  x is host fp64 (or, with GN_DEVICE_IO, a device array
- * of the graph dtype).  selected: n bytes (0/1).  weight is numpy's pairwise
+ * (graph.py:178-186).  x is host fp64 (or, with GN_DEVICE_IO, a device fp64
+ * array).  selected: n bytes (0/1).  weight is numpy's pairwise
  * sum over members in ascending order (bitwise equal to w[idx].sum()). */
 int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
              double* weight, int* independent, int* maximal, int64_t* count);

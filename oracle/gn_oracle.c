@@ -162,6 +162,58 @@ static void step_f32(int64_t n, const int64_t* indptr, const int32_t* indices,
     *finite = fin;
 }
 
+
+/* Mixed precision (the engine's GN_F32 data path): per-vertex state, sums
+ * and the update in fp64; the value each vertex publishes to its neighbours
+ * is rounded to binary32 (yg = (float)(v*x)).  Same step as step_f64
+ * otherwise. */
+static void step_mixed(int64_t n, const int64_t* indptr, const int32_t* indices,
+                       const double* v, const double* w, const double* x,
+                       const float* yg, double gamma, double* xo, float* ygo,
+                       int64_t* nfb, double* step_inf, int* finite, double* dots) {
+    int64_t fb = 0;
+    double mx = 0.0;
+    int fin = 1;
+    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : fb) reduction(max : mx) reduction(&& : fin) if (!dots)
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
+        double yi = v[i] * x[i];
+        double d = yi + gamma * s;
+        double o;
+        if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++fb; }
+        xo[i] = o;
+        ygo[i] = (float)(v[i] * o);
+        double diff = fabs(o - x[i]);
+        if (diff > mx) mx = diff;
+        fin = fin && isfinite(o);
+        if (dots) {
+            d1 += yi * yi;
+            d2 += yi * s;
+            d3 += w[i] * x[i];
+        }
+    }
+    if (dots) { dots[0] = d1; dots[1] = d2; dots[2] = d3; }
+    *nfb = fb;
+    *step_inf = mx;
+    *finite = fin;
+}
+
+static void dots_mixed(int64_t n, const int64_t* indptr, const int32_t* indices,
+                       const double* v, const double* w, const double* x, const float* yg, double* dots) {
+    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
+        double yi = v[i] * x[i];
+        d1 += yi * yi;
+        d2 += yi * s;
+        d3 += w[i] * x[i];
+    }
+    dots[0] = d1; dots[1] = d2; dots[2] = d3;
+}
+
 /* Sequential dots of a state without stepping (trace tail). */
 static void dots_f64(int64_t n, const int64_t* indptr, const int32_t* indices,
                      const double* w, const double* x, const double* y, double* dots) {
@@ -212,7 +264,8 @@ int gno_step(int64_t n, const int64_t* indptr, const int32_t* indices,
 
 /* ---------------------------------------------------------------------------
  * run_wrgn (dynamics.py:129-180).
- *   dtype 0 = fp64 (the reference arithmetic), 1 = fp32.
+ *   dtype 0 = fp64 (the reference arithmetic), 1 = binary32 throughout,
+ *   2 = mixed (fp64 state and sums, binary32 gathered values).
  *   gammas[k] = schedule.gamma_at(k) precomputed by the caller (bitwise).
  *   x_hist (optional): iters*n fp64, row k = state after step k, unclipped.
  *   mass (optional): w . x_{k+1}, sequential.  energy/pre_energy need TRACE.
@@ -289,6 +342,48 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             x_out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);
         }
         free(v); free(xa); free(ya); free(xb); free(yb);
+    } else if (dtype == 2) {
+        double* v = (double*)malloc(sizeof(double) * nb);
+        double* xa = (double*)malloc(sizeof(double) * nb);
+        double* xb = (double*)malloc(sizeof(double) * nb);
+        float* ya = (float*)malloc(sizeof(float) * nb);
+        float* yb = (float*)malloc(sizeof(float) * nb);
+        for (int64_t i = 0; i < n; ++i) {
+            v[i] = sqrt(w[i]);
+            xa[i] = x0[i];
+            ya[i] = (float)(v[i] * xa[i]);
+        }
+        for (k = 0; k < iters; ++k) {
+            double g = gammas[k], si;
+            int fin;
+            int64_t fb;
+            int want_dots = trace || mass;
+            step_mixed(n, indptr, indices, v, w, xa, ya, g, xb, yb, &fb, &si, &fin,
+                       want_dots ? dots : NULL);
+            if (n == 0) si = 0.0;
+            step_inf[k] = si;
+            fallbacks[k] = fb;
+            if (want_dots) {
+                dots_mixed(n, indptr, indices, v, w, xb, yb, dots_next);
+                if (trace) {
+                    pre_energy[k] = energy_of(dots, g);
+                    energy[k] = energy_of(dots_next, g);
+                }
+                if (mass) mass[k] = dots_next[2];
+            }
+            if (x_hist) memcpy(x_hist + (size_t)k * (size_t)n, xb, sizeof(double) * (size_t)n);
+            double* t = xa; xa = xb; xb = t;
+            float* tf = ya; ya = yb; yb = tf;
+            ran = k + 1;
+            if (!fin) { rc = GNO_ERR_NONFINITE; *fail_iter = k; break; }
+            if (early && g == final_gamma && si < 1e-12) break;
+        }
+        *iters_run = ran;
+        for (int64_t i = 0; i < n; ++i) {
+            double xi = xa[i];
+            x_out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);
+        }
+        free(v); free(xa); free(xb); free(ya); free(yb);
     } else {
         float* v = (float*)malloc(sizeof(float) * nb);
         float* wf = (float*)malloc(sizeof(float) * nb);

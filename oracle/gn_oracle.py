@@ -122,7 +122,8 @@ def run(g, x0, gammas, final_gamma, *, dtype: str = "fp64", trace: bool = False,
     ran = ctypes.c_int(0)
     fail = ctypes.c_int(-1)
     flags = (TRACE if trace else 0) | (EARLY_EXIT if early_exit else 0)
-    rc = lib().gno_run(0 if dtype == "fp64" else 1, g.n, _p(ip), _p(ix), _p(w), _p(x0), _p(gam), iters,
+    code = {"fp64": 0, "fp32_pure": 1, "fp32": 2, "mixed": 2}[dtype]
+    rc = lib().gno_run(code, g.n, _p(ip), _p(ix), _p(w), _p(x0), _p(gam), iters,
                        float(final_gamma), flags, threads, _p(x), _p(si), _p(fb), _p(mass), _p(en), _p(pe),
                        _p(hist), ctypes.byref(ran), ctypes.byref(fail))
     k = ran.value

@@ -19,6 +19,7 @@ LIB_PATH = _HERE / "libgnb200.so"
 
 GN_F64 = 0
 GN_F32 = 1
+GN_F32_PURE = 2
 
 GN_OK = 0
 GN_ERR_ARG = 1

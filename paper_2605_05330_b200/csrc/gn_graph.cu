@@ -61,17 +61,6 @@ int coresident_blocks(const void* kernel, int threads, size_t smem, int device, 
 
 // ---------------------------------------------------------------- kernels
 
-template <typename T>
-__global__ void k_init_weights(int64_t n, const double* __restrict__ w64, T* __restrict__ v,
-                               T* __restrict__ w) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) {
-        double wi = w64[i];
-        v[i] = (T)sqrt(wi);  // graph.py:42 (IEEE sqrt; fp32: the rounding of the fp64 root)
-        w[i] = (T)wi;
-    }
-}
-
 // out = A @ in (fp64), one thread per row, sequential sum (scipy order).
 __global__ void k_spmv_seq(int64_t n, const int32_t* __restrict__ rowptr,
                            const int32_t* __restrict__ col, const double* __restrict__ in,
@@ -210,46 +199,114 @@ static int aux_grid(const gn_graph* g) {
 
 // ---------------------------------------------------------------- planning
 
-static int lanes_for_degree(int32_t d) {
-    if (d <= 4) return 1;
-    if (d <= 8) return 2;
-    if (d <= 16) return 4;
-    if (d <= 32) return 8;
-    if (d <= 64) return 16;
-    if (d <= 8192) return 32;
-    return 0;  // block per row
+// Host-side layout of the loop structures (see gn_graph in gn_internal.cuh).
+struct Layout {
+    std::vector<int32_t> perm, inv;
+    int32_t nhub = 0, nslices = 0, nsplit = 0;
+    std::vector<int64_t> slice_ptr;
+    std::vector<int32_t> row_deg;
+    std::vector<int32_t> hub_ptr, hub_col;
+    std::vector<int32_t> sell32;
+    std::vector<uint16_t> sell16;
+    int idx16 = 0;
+    int32_t maxdeg = 0;
+};
+
+static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indices, Layout& L) {
+    std::vector<int32_t> deg((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        deg[(size_t)i] = (int32_t)(indptr[i + 1] - indptr[i]);
+        L.maxdeg = std::max(L.maxdeg, deg[(size_t)i]);
+    }
+    // hubs: degree-descending (stable)
+    std::vector<int32_t> hubs, regular;
+    for (int64_t i = 0; i < n; ++i) (deg[(size_t)i] > kHubDegree ? hubs : regular).push_back((int32_t)i);
+    std::stable_sort(hubs.begin(), hubs.end(), [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
+    // regular rows: degree-descending inside windows of kSigma (keeps coarse
+    // locality; a uniform-degree graph keeps its numbering)
+    for (size_t w0 = 0; w0 < regular.size(); w0 += kSigma) {
+        size_t w1 = std::min(regular.size(), w0 + (size_t)kSigma);
+        std::stable_sort(regular.begin() + w0, regular.begin() + w1,
+                         [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
+    }
+    // groups of 32 rows; long groups (split over warps) first, the partial
+    // tail group always last
+    const size_t ng = (regular.size() + kSlice - 1) / kSlice;
+    std::vector<int32_t> split_g, whole_g;
+    for (size_t gi = 0; gi < ng; ++gi) {
+        size_t r0 = gi * kSlice, r1 = std::min(regular.size(), r0 + (size_t)kSlice);
+        int32_t len = 0;
+        for (size_t r = r0; r < r1; ++r) len = std::max(len, deg[regular[r]]);
+        bool full = (r1 - r0) == (size_t)kSlice;
+        (full && len >= kSplitLen ? split_g : whole_g).push_back((int32_t)gi);
+    }
+    L.nhub = (int32_t)hubs.size();
+    L.nsplit = (int32_t)split_g.size();
+    L.nslices = (int32_t)ng;
+    L.perm.clear();
+    L.perm.reserve((size_t)n);
+    L.perm.insert(L.perm.end(), hubs.begin(), hubs.end());
+    std::vector<int32_t> order = split_g;
+    order.insert(order.end(), whole_g.begin(), whole_g.end());
+    for (int32_t gi : order) {
+        size_t r0 = (size_t)gi * kSlice, r1 = std::min(regular.size(), r0 + (size_t)kSlice);
+        for (size_t r = r0; r < r1; ++r) L.perm.push_back(regular[r]);
+    }
+    L.inv.assign((size_t)n, 0);
+    for (int64_t r = 0; r < n; ++r) L.inv[(size_t)L.perm[(size_t)r]] = (int32_t)r;
+
+    // hub CSR in new ids, original neighbour order
+    L.hub_ptr.assign((size_t)L.nhub + 1, 0);
+    for (int32_t h = 0; h < L.nhub; ++h) L.hub_ptr[h + 1] = L.hub_ptr[h] + deg[L.perm[h]];
+    L.hub_col.resize((size_t)L.hub_ptr[L.nhub]);
+    for (int32_t h = 0; h < L.nhub; ++h) {
+        int32_t o = L.perm[h];
+        for (int64_t p = indptr[o]; p < indptr[o + 1]; ++p) L.hub_col[(size_t)(L.hub_ptr[h] + (p - indptr[o]))] = L.inv[indices[p]];
+    }
+    // SELL slices, position-major
+    const int64_t nreg = n - L.nhub;
+    L.row_deg.assign((size_t)std::max<int64_t>(nreg, 0), 0);
+    L.slice_ptr.assign((size_t)L.nslices + 1, 0);
+    for (int32_t s = 0; s < L.nslices; ++s) {
+        int32_t len = 0;
+        for (int l = 0; l < kSlice; ++l) {
+            int64_t r = (int64_t)s * kSlice + l;
+            if (r < nreg) {
+                int32_t d = deg[L.perm[(size_t)(L.nhub + r)]];
+                L.row_deg[(size_t)r] = d;
+                len = std::max(len, d);
+            }
+        }
+        L.slice_ptr[s + 1] = L.slice_ptr[s] + (int64_t)len * kSlice;
+    }
+    const int64_t elems = L.slice_ptr[L.nslices];
+    L.idx16 = n <= 65536 ? 1 : 0;
+    if (L.idx16) L.sell16.assign((size_t)elems, 0);
+    else L.sell32.assign((size_t)elems, 0);
+    for (int32_t s = 0; s < L.nslices; ++s) {
+        for (int l = 0; l < kSlice; ++l) {
+            int64_t r = (int64_t)s * kSlice + l;
+            if (r >= nreg) continue;
+            int32_t o = L.perm[(size_t)(L.nhub + r)];
+            for (int64_t p = indptr[o]; p < indptr[o + 1]; ++p) {
+                int64_t at = L.slice_ptr[s] + (p - indptr[o]) * kSlice + l;
+                int32_t nid = L.inv[indices[p]];
+                if (L.idx16) L.sell16[(size_t)at] = (uint16_t)nid;
+                else L.sell32[(size_t)at] = nid;
+            }
+        }
+    }
 }
 
-static int build_plans(gn_graph* g, const int64_t* indptr, std::vector<int32_t>& rows_out) {
-    const int64_t n = g->n;
-    // fixed bin order: block rows first (longest), then G = 32 .. 1
-    const int order[7] = {0, 32, 16, 8, 4, 2, 1};
-    std::vector<std::vector<int32_t>> lists(7);
-    int32_t maxd = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        int32_t d = (int32_t)(indptr[i + 1] - indptr[i]);
-        maxd = std::max(maxd, d);
-        int G = lanes_for_degree(d);
-        for (int b = 0; b < 7; ++b)
-            if (order[b] == G) { lists[b].push_back((int32_t)i); break; }
+template <typename T>
+__global__ void k_init_state_weights(int64_t n, const double* __restrict__ w64, const int32_t* __restrict__ perm,
+                                     T* __restrict__ v, T* __restrict__ w) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) {
+        double wi = w64[perm[r]];
+        v[r] = (T)sqrt(wi);  // graph.py:42 (IEEE sqrt; binary32: rounding of the fp64 root)
+        w[r] = (T)wi;
     }
-    g->max_degree = maxd;
-    rows_out.clear();
-    rows_out.reserve((size_t)n);
-    g->fast.nbins = 0;
-    for (int b = 0; b < 7; ++b) {
-        if (lists[b].empty()) continue;
-        Bin& bin = g->fast.bins[g->fast.nbins++];
-        bin.off = (int32_t)rows_out.size();
-        bin.count = (int32_t)lists[b].size();
-        bin.G = order[b];
-        bin.pad = 0;
-        rows_out.insert(rows_out.end(), lists[b].begin(), lists[b].end());
-    }
-    g->exact.nbins = n > 0 ? 1 : 0;
-    g->exact.bins[0] = Bin{0, (int32_t)n, 1, 0};
-    g->exact.rows = nullptr;
-    return GN_OK;
 }
 
 static void free_graph(gn_graph* g) {
@@ -257,12 +314,9 @@ static void free_graph(gn_graph* g) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
-    cudaFree(g->rowptr);
-    cudaFree(g->col);
-    cudaFree(g->v);
-    cudaFree(g->w);
-    cudaFree(g->w64);
-    cudaFree(g->fast.rows);
+    void* ptrs[] = {g->rowptr, g->col, g->w64, g->perm, g->inv, g->v, g->w,
+                    g->hub_ptr, g->hub_col, g->slice_ptr, g->row_deg, g->sell};
+    for (void* p : ptrs) cudaFree(p);
     if (prev >= 0) cudaSetDevice(prev);
     delete g;
 }
@@ -290,11 +344,11 @@ int gn_device_count(int* count) {
     return GN_OK;
 }
 
-int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* w,
-                    int dtype, int device, gn_graph** out) {
+int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* w, int dtype,
+                    int device, gn_graph** out) {
     *out = nullptr;
     if (n < 0) return fail(GN_ERR_ARG, "vertex count must be nonnegative");
-    if (dtype != GN_F64 && dtype != GN_F32) return fail(GN_ERR_ARG, "dtype must be GN_F64 or GN_F32");
+    if (!valid_dtype(dtype)) return fail(GN_ERR_ARG, "dtype must be GN_F64, GN_F32 or GN_F32_PURE");
     if (n > 0 && (!indptr || !w)) return fail(GN_ERR_ARG, "null graph array");
     const int64_t nnz = n > 0 ? indptr[n] : 0;
     if (nnz >= (int64_t(1) << 31) || n >= (int64_t(1) << 31))
@@ -302,6 +356,8 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     if (n > 0 && indptr[0] != 0) return fail(GN_ERR_ARG, "indptr[0] must be 0");
     for (int64_t i = 0; i < n; ++i)
         if (indptr[i + 1] < indptr[i]) return fail(GN_ERR_ARG, "indptr must be nondecreasing");
+    for (int64_t p = 0; p < nnz; ++p)
+        if (indices[p] < 0 || indices[p] >= n) return fail(GN_ERR_ARG, "column index outside [0,n)");
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -311,11 +367,20 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     }
     if (device < 0 || device >= ndev) return fail(GN_ERR_ARG, "device ordinal out of range");
 
+    Layout L;
+    build_layout(n, indptr, indices, L);
+
     gn_graph* g = new gn_graph();
     g->n = n;
     g->nnz = nnz;
     g->dtype = dtype;
     g->device = device;
+    g->max_degree = L.maxdeg;
+    g->nhub = L.nhub;
+    g->nslices = L.nslices;
+    g->nsplit = L.nsplit;
+    g->idx16 = L.idx16;
+    g->sell_elems = L.slice_ptr.empty() ? 0 : L.slice_ptr.back();
     CallCtx ctx;
     int rc = ctx.open(device);
     if (rc) { delete g; return rc; }
@@ -323,43 +388,58 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
 
     std::vector<int32_t> rowptr32((size_t)n + 1);
     for (int64_t i = 0; i <= n; ++i) rowptr32[(size_t)i] = (int32_t)(n > 0 ? indptr[i] : 0);
-    std::vector<int32_t> rows;
-    build_plans(g, n > 0 ? indptr : nullptr, rows);
 
-    const size_t es = dtype == GN_F64 ? 8 : 4;
+    const size_t es = state_bytes(dtype);
     const size_t nb = (size_t)std::max<int64_t>(n, 1);
+    int64_t bytes = 0;
     auto cleanup = [&](int code) { free_graph(g); return code; };
 #define GN_TRY(expr)                                                              \
     do {                                                                          \
         cudaError_t _e = (expr);                                                  \
         if (_e != cudaSuccess) return cleanup(cuda_fail(_e, #expr, __FILE__, __LINE__)); \
     } while (0)
-    GN_TRY(cudaMalloc(&g->rowptr, sizeof(int32_t) * (nb + 1)));
-    GN_TRY(cudaMalloc(&g->col, sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
+#define GN_UP(dst, src, count, type)                                                              \
+    do {                                                                                          \
+        size_t _b = sizeof(type) * (size_t)std::max<int64_t>((int64_t)(count), 1);                \
+        GN_TRY(cudaMalloc((void**)&(dst), _b));                                                   \
+        bytes += (int64_t)_b;                                                                     \
+        if ((count) > 0)                                                                          \
+            GN_TRY(cudaMemcpyAsync((dst), (src), sizeof(type) * (size_t)(count), cudaMemcpyHostToDevice, ctx.s)); \
+    } while (0)
+    GN_UP(g->rowptr, rowptr32.data(), n + 1, int32_t);
+    GN_UP(g->col, indices, nnz, int32_t);
+    GN_UP(g->w64, w, n, double);
+    GN_UP(g->perm, L.perm.data(), n, int32_t);
+    GN_UP(g->inv, L.inv.data(), n, int32_t);
+    GN_UP(g->hub_ptr, L.hub_ptr.data(), L.nhub + 1, int32_t);
+    GN_UP(g->hub_col, L.hub_col.data(), (int64_t)L.hub_col.size(), int32_t);
+    GN_UP(g->slice_ptr, L.slice_ptr.data(), (int64_t)L.slice_ptr.size(), int64_t);
+    GN_UP(g->row_deg, L.row_deg.data(), (int64_t)L.row_deg.size(), int32_t);
+    if (L.idx16) {
+        uint16_t* p = nullptr;
+        GN_UP(p, L.sell16.data(), (int64_t)L.sell16.size(), uint16_t);
+        g->sell = p;
+    } else {
+        int32_t* p = nullptr;
+        GN_UP(p, L.sell32.data(), (int64_t)L.sell32.size(), int32_t);
+        g->sell = p;
+    }
     GN_TRY(cudaMalloc(&g->v, es * nb));
     GN_TRY(cudaMalloc(&g->w, es * nb));
-    GN_TRY(cudaMalloc(&g->w64, sizeof(double) * nb));
-    GN_TRY(cudaMalloc(&g->fast.rows, sizeof(int32_t) * nb));
-    g->device_bytes = (int64_t)(sizeof(int32_t) * (nb + 1) + sizeof(int32_t) * std::max<int64_t>(nnz, 1) +
-                                2 * es * nb + 8 * nb + 4 * nb);
-    GN_TRY(cudaMemcpyAsync(g->rowptr, rowptr32.data(), sizeof(int32_t) * (size_t)(n + 1),
-                           cudaMemcpyHostToDevice, ctx.s));
-    if (nnz > 0)
-        GN_TRY(cudaMemcpyAsync(g->col, indices, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice, ctx.s));
+    bytes += (int64_t)(2 * es * nb);
+    g->device_bytes = bytes;
     if (n > 0) {
-        GN_TRY(cudaMemcpyAsync(g->w64, w, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, ctx.s));
-        GN_TRY(cudaMemcpyAsync(g->fast.rows, rows.data(), sizeof(int32_t) * (size_t)n,
-                               cudaMemcpyHostToDevice, ctx.s));
         int blocks = grid_for(n, 256);
-        if (dtype == GN_F64)
-            k_init_weights<double><<<blocks, 256, 0, ctx.s>>>(n, g->w64, (double*)g->v, (double*)g->w);
+        if (es == 8)
+            k_init_state_weights<double><<<blocks, 256, 0, ctx.s>>>(n, g->w64, g->perm, (double*)g->v, (double*)g->w);
         else
-            k_init_weights<float><<<blocks, 256, 0, ctx.s>>>(n, g->w64, (float*)g->v, (float*)g->w);
+            k_init_state_weights<float><<<blocks, 256, 0, ctx.s>>>(n, g->w64, g->perm, (float*)g->v, (float*)g->w);
         GN_TRY(cudaGetLastError());
         note_launch();
     }
     GN_TRY(cudaStreamSynchronize(ctx.s));
 #undef GN_TRY
+#undef GN_UP
     *out = g;
     return GN_OK;
 }
@@ -377,7 +457,7 @@ int gn_graph_info(const gn_graph* g, int64_t* n, int64_t* nnz, int* dtype, int* 
     if (dtype) *dtype = g->dtype;
     if (device) *device = g->device;
     if (device_bytes) *device_bytes = g->device_bytes;
-    if (num_bins) *num_bins = g->fast.nbins;
+    if (num_bins) *num_bins = g->nsplit;
     return GN_OK;
 }
 

@@ -15,8 +15,12 @@ namespace gn {
 constexpr double kSafeDiv = 1e-9;
 constexpr double kFallback = 0.5;
 
-constexpr int kMaxBins = 8;
-constexpr int kLoopThreads = 512;  // persistent loop block size
+constexpr int kLoopThreads = 512;  // persistent streaming kernel block
+constexpr int kLoopWarps = kLoopThreads / 32;
+constexpr int kSlice = 32;         // SELL slice height (one row per lane)
+constexpr int kSigma = 4096;       // degree-sort window of the relabeling
+constexpr int kHubDegree = 4096;   // rows above this are processed CTA-wide
+constexpr int kSplitLen = 64;      // slices at least this long are split over warps
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
@@ -37,24 +41,27 @@ void note_launch(int64_t k = 1);
         ::gn::note_launch();                                               \
     } while (0)
 
-// ---------------------------------------------------------------- graph
-// A degree bin: rows [off, off+count) of the bin row list, processed by
-// groups of G lanes per row (G = 1..32) or by a whole block per row (G = 0).
-struct Bin {
-    int32_t off;
-    int32_t count;
-    int32_t G;
-    int32_t pad;
-};
-
-struct Plan {
-    int nbins = 0;
-    Bin bins[kMaxBins];
-    int32_t* rows = nullptr;  // device row list (nullptr => identity order)
-};
+// ---------------------------------------------------------------- dtypes
+// GN_F64:      state, sums and gathered values in binary64 (the reference)
+// GN_F32:      state and sums in binary64, gathered values (the y each vertex
+//              publishes to its neighbours) in binary32 -- halves the gather
+//              bytes and keeps every vertex's own trajectory in fp64 range
+// GN_F32_PURE: binary32 throughout
+inline bool valid_dtype(int d) { return d == GN_F64 || d == GN_F32 || d == GN_F32_PURE; }
+inline size_t state_bytes(int d) { return d == GN_F32_PURE ? 4 : 8; }
+inline size_t gather_bytes(int d) { return d == GN_F64 ? 8 : 4; }
 
 }  // namespace gn
 
+// Device-resident graph.  Two copies of the adjacency:
+//  * the original CSR (ids as the caller numbered them) for rounding, the
+//    checks and the auxiliary fp64 operators;
+//  * the loop layout: vertices relabeled (new id r, perm[r] = old id) so that
+//    hub rows come first and the remaining rows, degree-sorted in windows of
+//    kSigma, form SELL slices of 32 rows stored position-major
+//    (element p of the slice's 32 rows is 32 consecutive indices), which makes
+//    every index load of a warp one coalesced line and lets one thread sum
+//    its row in the reference's sequential order.
 struct gn_graph {
     int64_t n = 0;
     int64_t nnz = 0;
@@ -63,19 +70,33 @@ struct gn_graph {
     int num_sms = 0;
     int grid_override = 0;
     int64_t device_bytes = 0;
-    int32_t* rowptr = nullptr;  // n+1 (nnz < 2^31 enforced)
-    int32_t* col = nullptr;     // nnz
-    void* v = nullptr;          // n, dtype: sqrt(w)
-    void* w = nullptr;          // n, dtype
-    double* w64 = nullptr;      // n fp64 (rounding priorities, MIS weight)
-    gn::Plan fast;              // degree-binned plan
-    gn::Plan exact;             // one thread per row, identity order
     int32_t max_degree = 0;
+
+    // original CSR
+    int32_t* rowptr = nullptr;
+    int32_t* col = nullptr;
+    double* w64 = nullptr;
+
+    // loop layout
+    int32_t* perm = nullptr;  // new -> old
+    int32_t* inv = nullptr;   // old -> new
+    void* v = nullptr;        // sqrt(w) in state precision, new-id order
+    void* w = nullptr;        // w in state precision, new-id order
+    int32_t nhub = 0;         // rows [0, nhub) are hubs
+    int32_t* hub_ptr = nullptr;  // nhub+1, offsets into hub_col
+    int32_t* hub_col = nullptr;  // new ids, original neighbour order
+    int32_t nslices = 0;      // rows [nhub, n) in slices of 32
+    int32_t nsplit = 0;       // slices [0, nsplit) have length >= kSplitLen
+    int64_t* slice_ptr = nullptr;  // nslices+1 element offsets (multiples of 32)
+    int32_t* row_deg = nullptr;    // degree per slice row (n - nhub)
+    void* sell = nullptr;          // int32 or uint16 new ids, position-major
+    int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536)
+    int64_t sell_elems = 0;
 };
 
 namespace gn {
 
-// RAII stream + event helper for one API call.
+// RAII stream for one API call.
 struct CallCtx {
     cudaStream_t s = nullptr;
     int prev_dev = -1;
@@ -84,7 +105,6 @@ struct CallCtx {
     ~CallCtx();
 };
 
-// device-side helpers shared by the kernels
 template <typename T>
 struct Arith;
 
@@ -105,9 +125,9 @@ struct Arith<float> {
 };
 
 // Grid-wide barrier for a co-resident (cooperative) grid.  `target` grows
-// monotonically: barrier number b waits for (b+1)*gridDim.x arrivals.  The
-// gpu-scope fences make every y/x write of the previous phase visible (and
-// invalidate the SM's L1) before any block reads them.
+// monotonically: barrier number b waits for b*gridDim.x arrivals.  The
+// gpu-scope fences publish every x/y write of the phase (and invalidate the
+// SM's L1) before any block reads them.
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {
     __syncthreads();
     if (gridDim.x > 1) {

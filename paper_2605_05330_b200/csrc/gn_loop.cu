@@ -5,21 +5,31 @@
 // step_inf, fallbacks, non-finite stop, early exit, trace), energy 210-219 and
 // weighted_mass 222-224 (fused here as per-iteration dot products).
 //
-// Per iteration k (one pass over the CSR adjacency):
-//   s_i  = sum_{j in N(i)} y_j              gather-sum, degree-binned rows
-//   d_i  = y_i + gamma_k * s_i              (separately rounded, no FMA)
-//   x'_i = d_i > 1e-9 ? y_i / d_i : 0.5     counted fallback
-//   y'_i = v_i * x'_i                       next gather source
-// fused with the per-iteration reductions: max|x'-x| (bitwise: atomicMax on
-// the IEEE bits of a non-negative double), the fallback count, the non-finite
-// flag, and fixed-order fp64 block partials of w.x' (objective) and, in trace
-// mode, y.y, y.s, w.x (the energy terms of the pre-step state).  A grid
-// barrier separates iterations; block 0 folds the partials in block order, so
-// every reduction is deterministic run to run.
+// Per iteration k, one pass over the relabeled adjacency (gn_internal.cuh):
+//   s_r  = sum_{j in N(r)} yg_j          gathered values of step k
+//   y_r  = v_r * x_r                     (bitwise the y the reference forms)
+//   d_r  = y_r + gamma_k * s_r           separately rounded, no FMA
+//   x'_r = d_r > 1e-9 ? y_r / d_r : 0.5  counted fallback
+//   yg'_r = v_r * x'_r                   published for step k+1
+// fused with the per-iteration reductions: max|x'-x| (atomicMax on the IEEE
+// bits of a non-negative double -- order-free, hence deterministic), the
+// fallback count, the first non-finite iteration, and fixed-order fp64 block
+// partials of w.x' (the objective) and, in trace mode, y.y, y.s, w.x (the
+// energy terms of the pre-step state).  Block partials go to a ring that all
+// blocks fold cooperatively every 1024 iterations, off the per-step path.
+//
+// Row work, per iteration:
+//   hub rows (degree > kHubDegree)  one CTA per row (EXACT: one thread per row)
+//   long slices (length >= 64)      the CTA's 16 warps split the positions of a
+//                                   slice; partials folded in warp order
+//   other slices                    one warp per slice, one thread per row,
+//                                   sequential sum = scipy's order (bitwise)
+// A grid barrier separates iterations.
 #include <cuda_runtime.h>
 #include <math.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -27,154 +37,171 @@
 
 namespace gn {
 
-template <typename T>
+constexpr int kRing = 1024;     // iterations of block partials kept before a fold
+constexpr int kSplitSlots = 8;  // long slices buffered per CTA between syncs
+
+template <typename TS, typename TG>
 struct LoopArgs {
     int64_t n;
-    const int32_t* __restrict__ rowptr;
-    const int32_t* __restrict__ col;
-    const T* __restrict__ v;
-    const T* __restrict__ w;
-    const int32_t* __restrict__ rows;  // bin row list; nullptr = identity
-    Bin bins[kMaxBins];
-    int nbins;
-    T* xs[2];
-    T* ys[2];
+    int32_t nhub, nslices, nsplit;
+    int exact;
+    const int32_t* __restrict__ hub_ptr;
+    const int32_t* __restrict__ hub_col;
+    const int64_t* __restrict__ slice_ptr;
+    const int32_t* __restrict__ row_deg;
+    const void* __restrict__ sell;
+    const TS* __restrict__ v;
+    const TS* __restrict__ w;
+    TS* x[2];
+    TG* yg[2];
     const double* __restrict__ gammas;
     int iters;
     double final_gamma;
     int early_exit;
-    int stop_on_nonfinite;
     unsigned long long* step_bits;  // [iters]
     unsigned long long* fb;         // [iters]
-    int* status;                    // [0] nonfinite flag [1] fail iter [2] iters_run
+    int* status;                    // [0] first non-finite iteration (INT_MAX: none) [1] iterations run
     double* dots;                   // [(iters+1)][4]: y.y, y.s, w.x (pre), w.x' (post)
-    double* partials;               // [2][grid][4]
+    double* ring;                   // [kRing][grid][4]
     unsigned int* barrier;
-    T* x_hist;  // optional [iters][n]
+    double* x_hist;                 // optional [iters][n], original order
+    const int32_t* __restrict__ perm;
 };
 
 struct Stats {
     double mx;
     unsigned int fbc;
-    int nonfin;
+    int bad;
     double acc[4];
 };
 
 template <typename T>
 __device__ __forceinline__ T tabs(T v) { return v < T(0) ? -v : v; }
 
-// The elementwise half of _step for one row whose neighbour sum is s.
-template <typename T, bool TRACE>
-__device__ __forceinline__ void update_row(const LoopArgs<T>& a, int row, T s, const T* __restrict__ x,
-                                           const T* __restrict__ y, T* __restrict__ xo, T* __restrict__ yo,
-                                           T g, int k, bool tail, Stats& st) {
-    using A = Arith<T>;
-    const T yi = y[row];
-    const T xi = x[row];
-    const double wi = (double)__ldg(a.w + row);
+// The elementwise half of _step for row r (new id) whose neighbour sum is s.
+template <typename TS, typename TG, bool TRACE>
+__device__ __forceinline__ void update_row(const LoopArgs<TS, TG>& a, int r, TS s, int cur, TS g, int k,
+                                           bool tail, Stats& st) {
+    using A = Arith<TS>;
+    const TS xi = a.x[cur][r];
+    const TS vi = __ldg(a.v + r);
+    const TS yi = A::mul(vi, xi);                    // dynamics.py:104
+    const double wi = (double)__ldg(a.w + r);
     if (TRACE) {
         st.acc[0] = __dadd_rn(st.acc[0], __dmul_rn((double)yi, (double)yi));
         st.acc[1] = __dadd_rn(st.acc[1], __dmul_rn((double)yi, (double)s));
         st.acc[2] = __dadd_rn(st.acc[2], __dmul_rn(wi, (double)xi));
     }
     if (tail) return;
-    const T d = A::add(yi, A::mul(g, s));          // dynamics.py:105
-    const bool ok = (double)d > kSafeDiv;           // dynamics.py:106
-    const T o = ok ? A::div(yi, d) : T(kFallback);  // dynamics.py:107
-    xo[row] = o;
-    yo[row] = A::mul(__ldg(a.v + row), o);          // next y = v * x'
+    const TS d = A::add(yi, A::mul(g, s));          // dynamics.py:105
+    const bool ok = (double)d > kSafeDiv;            // dynamics.py:106
+    const TS o = ok ? A::div(yi, d) : TS(kFallback); // dynamics.py:107
+    a.x[cur ^ 1][r] = o;
+    a.yg[cur ^ 1][r] = (TG)A::mul(vi, o);
     const double diff = (double)tabs(A::sub(o, xi));  // dynamics.py:165
     if (!(diff <= st.mx)) st.mx = diff;
     st.fbc += ok ? 0u : 1u;
-    if (!isfinite(o)) st.nonfin = 1;
-    st.acc[3] = __dadd_rn(st.acc[3], __dmul_rn(wi, (double)o));  // w . x'
-    if (a.x_hist) a.x_hist[(size_t)k * (size_t)a.n + (size_t)row] = o;
+    if (!isfinite((double)o)) st.bad = 1;
+    st.acc[3] = __dadd_rn(st.acc[3], __dmul_rn(wi, (double)o));  // objective w . x'
+    if (a.x_hist) a.x_hist[(size_t)k * (size_t)a.n + (size_t)__ldg(a.perm + r)] = (double)o;
 }
 
-// Rows of one bin, G lanes per row (G in 1..32), 32/G rows per warp task.
-// G == 1 with an in-order walk is the EXACT mode (scipy's sequential sum).
-template <typename T, int G, bool TRACE>
-__device__ __forceinline__ void group_bin(const LoopArgs<T>& a, const Bin& bin, const T* __restrict__ x,
-                                          const T* __restrict__ y, T* __restrict__ xo, T* __restrict__ yo,
-                                          T g, int k, bool tail, int lane, int gwarp, int nwarps, Stats& st) {
-    using A = Arith<T>;
-    constexpr int RPW = 32 / G;
-    const int sub = lane / G, gl = lane % G;
-    const int tasks = (bin.count + RPW - 1) / RPW;
-    for (int t = gwarp; t < tasks; t += nwarps) {
-        const int slot = t * RPW + sub;
-        const bool valid = slot < bin.count;
-        int row = 0, beg = 0, end = 0;
-        if (valid) {
-            row = a.rows ? __ldg(a.rows + bin.off + slot) : bin.off + slot;
-            beg = __ldg(a.rowptr + row);
-            end = __ldg(a.rowptr + row + 1);
-        }
-        T s = T(0);
-        int p = beg + gl;
-        for (; p + 3 * G < end; p += 4 * G) {
-            const int j0 = __ldg(a.col + p), j1 = __ldg(a.col + p + G);
-            const int j2 = __ldg(a.col + p + 2 * G), j3 = __ldg(a.col + p + 3 * G);
-            const T y0 = y[j0], y1 = y[j1], y2 = y[j2], y3 = y[j3];
-            s = A::add(s, y0);
-            s = A::add(s, y1);
-            s = A::add(s, y2);
-            s = A::add(s, y3);
-        }
-        for (; p < end; p += G) s = A::add(s, y[__ldg(a.col + p)]);
+// Sequential sum over positions [pb, pe) of one slice row (lane), masked by
+// the row's degree d.  Loads are issued 8 at a time; the adds stay in order.
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ TS sum_positions(const TI* __restrict__ col, const TG* __restrict__ yg, int lane, int d,
+                                            int pb, int pe) {
+    using A = Arith<TS>;
+    TS s = TS(0);
+    int p = pb;
+    for (; p + 8 <= pe; p += 8) {
+        TI j[8];
+        TG y[8];
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if (valid && gl == 0) update_row<T, TRACE>(a, row, s, x, y, xo, yo, g, k, tail, st);
-    }
-}
-
-// Hub rows: one whole block per row, fixed-order block reduction.
-template <typename T, bool TRACE>
-__device__ __forceinline__ void block_bin(const LoopArgs<T>& a, const Bin& bin, const T* __restrict__ x,
-                                          const T* __restrict__ y, T* __restrict__ xo, T* __restrict__ yo,
-                                          T g, int k, bool tail, Stats& st, T* red) {
-    using A = Arith<T>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int r = blockIdx.x; r < bin.count; r += gridDim.x) {
-        const int row = a.rows ? __ldg(a.rows + bin.off + r) : bin.off + r;
-        const int beg = __ldg(a.rowptr + row), end = __ldg(a.rowptr + row + 1);
-        T s = T(0);
-        for (int p = beg + threadIdx.x; p < end; p += blockDim.x) s = A::add(s, y[__ldg(a.col + p)]);
+        for (int u = 0; u < 8; ++u) j[u] = (p + u < d) ? __ldg(col + (size_t)(p + u) * kSlice + lane) : TI(0);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if (lane == 0) red[warp] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            T tot = T(0);
-            for (int q = 0; q < nw; ++q) tot = A::add(tot, red[q]);
-            update_row<T, TRACE>(a, row, tot, x, y, xo, yo, g, k, tail, st);
-        }
-        __syncthreads();
+        for (int u = 0; u < 8; ++u) y[u] = (p + u < d) ? yg[j[u]] : TG(0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = A::add(s, (TS)y[u]);
     }
+    for (; p < pe; ++p)
+        if (p < d) s = A::add(s, (TS)yg[__ldg(col + (size_t)p * kSlice + lane)]);
+    return s;
 }
 
-template <typename T, bool TRACE>
-__device__ void pass(const LoopArgs<T>& a, int k, bool tail, Stats& st, T* red) {
+template <typename TS, typename TG, typename TI, bool TRACE>
+__device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_part, TS* s_hub) {
+    using A = Arith<TS>;
     const int cur = k & 1;
-    const T* x = a.xs[cur];
-    const T* y = a.ys[cur];
-    T* xo = a.xs[cur ^ 1];
-    T* yo = a.ys[cur ^ 1];
-    const T g = tail ? T(0) : (T)a.gammas[k];
-    const int lane = threadIdx.x & 31;
-    const int gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int b = 0; b < a.nbins; ++b) {
-        const Bin bin = a.bins[b];
-        switch (bin.G) {
-            case 0: block_bin<T, TRACE>(a, bin, x, y, xo, yo, g, k, tail, st, red); break;
-            case 1: group_bin<T, 1, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
-            case 2: group_bin<T, 2, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
-            case 4: group_bin<T, 4, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
-            case 8: group_bin<T, 8, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
-            case 16: group_bin<T, 16, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
-            default: group_bin<T, 32, TRACE>(a, bin, x, y, xo, yo, g, k, tail, lane, gwarp, nwarps, st); break;
+    const TG* __restrict__ yg = a.yg[cur];
+    const TS g = tail ? TS(0) : (TS)a.gammas[k];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = gridDim.x;
+    const TI* __restrict__ sell = (const TI*)a.sell;
+
+    // ---- hub rows
+    if (!a.exact) {
+        for (int h = blockIdx.x; h < a.nhub; h += G) {
+            const int beg = __ldg(a.hub_ptr + h), end = __ldg(a.hub_ptr + h + 1);
+            TS s = TS(0);
+            for (int p = beg + threadIdx.x; p < end; p += blockDim.x) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
+            if (lane == 0) s_hub[warp] = s;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                TS tot = TS(0);
+                for (int q = 0; q < kLoopWarps; ++q) tot = A::add(tot, s_hub[q]);
+                update_row<TS, TG, TRACE>(a, h, tot, cur, g, k, tail, st);
+            }
+            __syncthreads();
         }
+    } else {
+        for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < a.nhub; h += G * blockDim.x) {
+            TS s = TS(0);
+            for (int p = __ldg(a.hub_ptr + h); p < __ldg(a.hub_ptr + h + 1); ++p)
+                s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+            update_row<TS, TG, TRACE>(a, h, s, cur, g, k, tail, st);
+        }
+    }
+
+    // ---- long slices, warps split the positions
+    const int nsplit = a.exact ? 0 : a.nsplit;
+    const int nq = nsplit > (int)blockIdx.x ? (nsplit - 1 - (int)blockIdx.x) / G + 1 : 0;
+    for (int q0 = 0; q0 < nq; q0 += kSplitSlots) {
+        const int qn = min(kSplitSlots, nq - q0);
+        for (int q = 0; q < qn; ++q) {
+            const int s = blockIdx.x + (q0 + q) * G;
+            const int64_t base = __ldg(a.slice_ptr + s);
+            const int L = (int)((__ldg(a.slice_ptr + s + 1) - base) / kSlice);
+            const int r = a.nhub + s * kSlice + lane;
+            const int d = __ldg(a.row_deg + s * kSlice + lane);
+            const int pb = (int)((int64_t)L * warp / kLoopWarps), pe = (int)((int64_t)L * (warp + 1) / kLoopWarps);
+            (void)r;
+            s_part[(q * kLoopWarps + warp) * kSlice + lane] = sum_positions<TS, TG, TI>(sell + base, yg, lane, d, pb, pe);
+        }
+        __syncthreads();
+        for (int q = warp; q < qn; q += kLoopWarps) {
+            const int s = blockIdx.x + (q0 + q) * G;
+            TS tot = TS(0);
+#pragma unroll 4
+            for (int w = 0; w < kLoopWarps; ++w) tot = A::add(tot, s_part[(q * kLoopWarps + w) * kSlice + lane]);
+            update_row<TS, TG, TRACE>(a, a.nhub + s * kSlice + lane, tot, cur, g, k, tail, st);
+        }
+        __syncthreads();
+    }
+
+    // ---- remaining slices: one warp per slice, one thread per row
+    const int first = nsplit;
+    const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
+    for (int s = first + gw; s < a.nslices; s += nw) {
+        const int64_t base = __ldg(a.slice_ptr + s);
+        const int L = (int)((__ldg(a.slice_ptr + s + 1) - base) / kSlice);
+        const int64_t r = (int64_t)a.nhub + (int64_t)s * kSlice + lane;
+        const bool valid = r < a.n;
+        const int d = valid ? __ldg(a.row_deg + (size_t)s * kSlice + lane) : 0;
+        const TS sum = sum_positions<TS, TG, TI>(sell + base, yg, lane, d, 0, L);
+        if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, cur, g, k, tail, st);
     }
 }
 
@@ -185,25 +212,27 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 // Block-level fold of the per-thread stats; thread 0 publishes.
-template <bool TRACE>
-__device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__ partials_cur,
-                        unsigned long long* step_bits, unsigned long long* fb, int* status,
-                        double (*s_acc)[4], double* s_mx, unsigned int* s_fb, int* s_nf) {
+__device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__ ring_slot,
+                        unsigned long long* step_bits, unsigned long long* fb, int* status) {
+    __shared__ double s_acc[kLoopWarps][4];
+    __shared__ double s_mx[kLoopWarps];
+    __shared__ unsigned int s_fb[kLoopWarps];
+    __shared__ int s_bad[kLoopWarps];
     Stats st = st0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         double m = __shfl_xor_sync(0xffffffffu, st.mx, o);
         if (!(m <= st.mx)) st.mx = m;
         st.fbc += __shfl_xor_sync(0xffffffffu, st.fbc, o);
-        st.nonfin |= __shfl_xor_sync(0xffffffffu, st.nonfin, o);
+        st.bad |= __shfl_xor_sync(0xffffffffu, st.bad, o);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) st.acc[q] = warp_sum_d(st.acc[q]);
     if (lane == 0) {
         s_mx[warp] = st.mx;
         s_fb[warp] = st.fbc;
-        s_nf[warp] = st.nonfin;
+        s_bad[warp] = st.bad;
 #pragma unroll
         for (int q = 0; q < 4; ++q) s_acc[warp][q] = st.acc[q];
     }
@@ -211,121 +240,134 @@ __device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__
     if (threadIdx.x == 0) {
         double mx = 0.0, acc[4] = {0.0, 0.0, 0.0, 0.0};
         unsigned int f = 0;
-        int nf = 0;
-        for (int q = 0; q < nw; ++q) {
+        int bad = 0;
+        for (int q = 0; q < kLoopWarps; ++q) {
             if (!(s_mx[q] <= mx)) mx = s_mx[q];
             f += s_fb[q];
-            nf |= s_nf[q];
+            bad |= s_bad[q];
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], s_acc[q][c]);
         }
         if (!tail) {
             if (mx != 0.0) atomicMax(step_bits + k, (unsigned long long)__double_as_longlong(mx));
             if (f) atomicAdd(fb + k, (unsigned long long)f);
-            if (nf) atomicOr(status, 1);
+            if (bad) atomicMin(status, k);
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) partials_cur[blockIdx.x * 4 + c] = acc[c];
+        for (int c = 0; c < 4; ++c) ring_slot[blockIdx.x * 4 + c] = acc[c];
     }
 }
 
-// Block 0, warp 0: fold the block partials of pass k in block order.
-__device__ void fold_partials(const double* __restrict__ partials_cur, int nblocks, double* __restrict__ out) {
-    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+// All blocks: fold ring slots [0, count) (iterations k0..k0+count-1) into
+// dots, one warp per (slot, term), block order fixed.
+__device__ void fold_ring(const double* ring, int count, int k0, double* dots) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = gridDim.x * kLoopWarps;
+    const int G = gridDim.x;
+    for (int t = gw; t < count * 4; t += nw) {
+        const int slot = t >> 2, c = t & 3;
+        const double* src = ring + (size_t)slot * G * 4;
         double s = 0.0;
-        for (int q = lane; q < nblocks; q += 32) s = __dadd_rn(s, __ldcg(partials_cur + q * 4 + c));
+        for (int b = lane; b < G; b += 32) s = __dadd_rn(s, __ldcg(src + b * 4 + c));
         s = warp_sum_d(s);
-        if (lane == 0) out[c] = s;
+        if (lane == 0) dots[(size_t)(k0 + slot) * 4 + c] = s;
     }
 }
 
-template <typename T, bool TRACE>
-__global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<T> a) {
-    __shared__ double s_acc[kLoopThreads / 32][4];
-    __shared__ double s_mx[kLoopThreads / 32];
-    __shared__ unsigned int s_fb[kLoopThreads / 32];
-    __shared__ int s_nf[kLoopThreads / 32];
-    __shared__ T s_red[kLoopThreads / 32];
+template <typename TS, typename TG, typename TI, bool TRACE>
+__global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
+    extern __shared__ unsigned char smem_raw[];
+    TS* s_part = (TS*)smem_raw;
+    __shared__ TS s_hub[kLoopWarps];
     unsigned int bar = 0;
-    int k = 0, ran = 0;
-    bool failed = false;
-    for (k = 0; k < a.iters; ++k) {
+    int ran = 0, k0 = 0;
+    const size_t ring_stride = (size_t)gridDim.x * 4;
+    for (int k = 0; k < a.iters; ++k) {
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<T, TRACE>(a, k, false, st, s_red);
-        double* pc = a.partials + (size_t)(k & 1) * gridDim.x * 4;
-        publish<TRACE>(st, k, false, pc, a.step_bits, a.fb, a.status, s_acc, s_mx, s_fb, s_nf);
+        pass<TS, TG, TI, TRACE>(a, k, false, st, s_part, s_hub);
+        publish(st, k, false, a.ring + (size_t)(k - k0) * ring_stride, a.step_bits, a.fb, a.status);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
-        fold_partials(pc, gridDim.x, a.dots + (size_t)k * 4);
         ran = k + 1;
-        const int nonfin = *(volatile int*)a.status;
-        if (nonfin && a.stop_on_nonfinite) { failed = true; break; }
-        if (a.early_exit && a.gammas[k] == a.final_gamma) {   // dynamics.py:177
+        bool stop = false;
+        if (a.early_exit && a.gammas[k] == a.final_gamma) {  // dynamics.py:177
             const double si = __longlong_as_double(*(volatile long long*)(a.step_bits + k));
-            if (si < 1e-12) break;
+            stop = si < 1e-12;
         }
+        const bool last = stop || ran == a.iters;
+        if (ran - k0 == kRing || (last && !TRACE)) {
+            fold_ring(a.ring, ran - k0, k0, a.dots);
+            grid_barrier(a.barrier, (++bar) * gridDim.x);
+            k0 = ran;
+        }
+        if (stop) break;
     }
-    if (TRACE && !failed) {
-        // energy terms of the final state (reference: energy(g, x_new, gamma))
+    if (TRACE) {
+        // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<T, TRACE>(a, ran, true, st, s_red);
-        double* pc = a.partials + (size_t)(ran & 1) * gridDim.x * 4;
-        publish<TRACE>(st, ran, true, pc, a.step_bits, a.fb, a.status, s_acc, s_mx, s_fb, s_nf);
+        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_part, s_hub);
+        publish(st, ran, true, a.ring + (size_t)(ran - k0) * ring_stride, a.step_bits, a.fb, a.status);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
-        fold_partials(pc, gridDim.x, a.dots + (size_t)ran * 4);
+        fold_ring(a.ring, ran - k0 + 1, k0, a.dots);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.status[1] = failed ? ran - 1 : -1;
-        a.status[2] = ran;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.status[1] = ran;
 }
 
-// x0 (fp64 or T) -> state buffers: x = (T)x0, y = v*x  (dynamics.py:104,145)
-template <typename T, typename TI>
-__global__ void k_prepare(int64_t n, const TI* __restrict__ x0, const T* __restrict__ v, T* __restrict__ x,
-                          T* __restrict__ y) {
+// x0 (original order, fp64) -> state buffers (new order): x = (TS)x0, yg = (TG)(v*x)
+template <typename TS, typename TG>
+__global__ void k_prepare(int64_t n, const double* __restrict__ x0, const int32_t* __restrict__ inv,
+                          const TS* __restrict__ v, TS* __restrict__ x, TG* __restrict__ yg) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
-        T xi = (T)x0[i];
-        x[i] = xi;
-        y[i] = Arith<T>::mul(v[i], xi);
+        const int r = inv[i];
+        const TS xi = (TS)x0[i];
+        x[r] = xi;
+        yg[r] = (TG)Arith<TS>::mul(v[r], xi);
     }
 }
 
-template <typename TI>
-__global__ void k_precheck_any(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                               const TI* __restrict__ x, int* __restrict__ flags) {
+__global__ void k_precheck_f64(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                               const double* __restrict__ x, int* __restrict__ flags) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double xi = (double)x[i];
-    if (xi < 0.0) atomicOr(&flags[0], 1);                 // dynamics.py:146
+    const double xi = x[i];
+    if (xi < 0.0) atomicOr(&flags[0], 1);                   // dynamics.py:146
     double s = 0.0;
-    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = __dadd_rn(s, (double)x[col[p]]);
+    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = __dadd_rn(s, x[col[p]]);
     if (!(__dadd_rn(xi, s) > 0.0)) atomicOr(&flags[1], 1);  // dynamics.py:125
 }
 
-// final state -> output (np.clip(x, 0, 1), dynamics.py:179)
-template <typename T, typename TO>
-__global__ void k_finalize(int64_t n, const T* __restrict__ x, TO* __restrict__ out, int clip) {
+// final state (new order) -> fp64 output (original order), np.clip(x, 0, 1)
+template <typename TS>
+__global__ void k_finalize(int64_t n, const TS* __restrict__ x, const int32_t* __restrict__ inv,
+                           double* __restrict__ out, int clip) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
-        T xi = x[i];
-        if (clip) xi = xi < T(0) ? T(0) : (xi > T(1) ? T(1) : xi);
-        out[i] = (TO)xi;
+        double xi = (double)x[inv[i]];
+        if (clip) xi = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);  // dynamics.py:179
+        out[i] = xi;
     }
-}
-
-template <typename T>
-__global__ void k_hist_to_f64(int64_t total, const T* __restrict__ h, double* __restrict__ out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < total) out[i] = (double)h[i];
 }
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + 255) / 256); }
 
-template <typename T>
+// stream-ordered scratch owned by one call
+struct Workspace {
+    void* p[24] = {};
+    int np = 0;
+    cudaStream_t s = nullptr;
+    template <typename P>
+    cudaError_t alloc(P** out, size_t bytes) {
+        cudaError_t e = cudaMallocAsync((void**)out, std::max<size_t>(bytes, 16), s);
+        if (e == cudaSuccess) p[np++] = (void*)*out;
+        return e;
+    }
+    ~Workspace() {
+        for (int i = 0; i < np; ++i) cudaFreeAsync(p[i], s);
+    }
+};
+
+
+template <typename TS, typename TG, typename TI>
 static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iters, double final_gamma,
                      uint32_t flags, void* x_out, double* step_inf, int64_t* fallbacks, double* mass,
                      double* energy, double* pre_energy, double* x_hist, int* iters_run, int* fail_iter,
@@ -341,170 +383,149 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     cudaStream_t s = ctx.s;
     int64_t h2d = 0, d2h = 0;
 
-    cudaEvent_t e0, e1, e2, e3;
-    GN_CUDA(cudaEventCreate(&e0));
-    GN_CUDA(cudaEventCreate(&e1));
-    GN_CUDA(cudaEventCreate(&e2));
-    GN_CUDA(cudaEventCreate(&e3));
+    cudaEvent_t ev[4];
+    for (auto& e : ev) GN_CUDA(cudaEventCreate(&e));
     struct EvGuard {
-        cudaEvent_t* e[4];
-        ~EvGuard() { for (auto p : e) cudaEventDestroy(*p); }
-    } evg{{&e0, &e1, &e2, &e3}};
-    GN_CUDA(cudaEventRecord(e0, s));
+        cudaEvent_t* e;
+        ~EvGuard() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); }
+    } evg{ev};
+    GN_CUDA(cudaEventRecord(ev[0], s));
 
-    // ---- workspace
-    void* kern = trace ? (void*)k_gn_loop<T, true> : (void*)k_gn_loop<T, false>;
+    // ---- launch geometry
+    void* kern = trace ? (void*)k_gn_loop<TS, TG, TI, true> : (void*)k_gn_loop<TS, TG, TI, false>;
+    const size_t smem = (size_t)kSplitSlots * kLoopWarps * kSlice * sizeof(TS);
+    GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int maxb = 1;
-    if ((rc = coresident_blocks(kern, kLoopThreads, 0, g->device, &maxb))) return rc;
+    if ((rc = coresident_blocks(kern, kLoopThreads, smem, g->device, &maxb))) return rc;
     if (maxb < 1) return fail(GN_ERR_CUDA, "loop kernel cannot be resident");
-    const Plan& plan = (flags & GN_EXACT) ? g->exact : g->fast;
-    int64_t work = g->nnz + 8 * n;
-    int grid = (int)std::min<int64_t>(maxb, std::max<int64_t>(1, (work + 32767) / 32768));
+    const int64_t work = g->sell_elems + 4 * n + (int64_t)g->nhub * 4096;
+    int grid = (int)std::min<int64_t>(maxb, std::max<int64_t>(1, (work + 16383) / 16384));
     if (g->grid_override > 0) grid = std::min(maxb, g->grid_override);
 
-    struct Ws {
-        T *x0 = nullptr, *x1 = nullptr, *y0 = nullptr, *y1 = nullptr, *hist = nullptr;
-        double *xin = nullptr, *dots = nullptr, *part = nullptr, *out64 = nullptr, *hist64 = nullptr;
-        unsigned long long *bits = nullptr, *fb = nullptr;
-        int* status = nullptr;
-        unsigned int* barrier = nullptr;
-        int* chk = nullptr;
-        cudaStream_t s;
-        ~Ws() {
-            void* ptrs[] = {x0, x1, y0, y1, hist, xin, dots, part, out64, hist64, bits, fb, status, barrier, chk};
-            for (void* p : ptrs)
-                if (p) cudaFreeAsync(p, s);
-        }
-    } ws;
+    Workspace ws;
     ws.s = s;
-    const size_t es = sizeof(T);
-    GN_CUDA(cudaMallocAsync((void**)&ws.x0, es * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.x1, es * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.y0, es * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.y1, es * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.bits, 8 * (size_t)iters, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.fb, 8 * (size_t)iters, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.dots, 8 * 4 * (size_t)(iters + 1), s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.part, 8 * 4 * 2 * (size_t)grid, s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.status, 4 * sizeof(int), s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.barrier, sizeof(unsigned int), s));
-    GN_CUDA(cudaMallocAsync((void**)&ws.chk, 2 * sizeof(int), s));
-    GN_CUDA(cudaMemsetAsync(ws.bits, 0, 8 * (size_t)iters, s));
-    GN_CUDA(cudaMemsetAsync(ws.fb, 0, 8 * (size_t)iters, s));
-    GN_CUDA(cudaMemsetAsync(ws.dots, 0, 8 * 4 * (size_t)(iters + 1), s));
-    GN_CUDA(cudaMemsetAsync(ws.status, 0, 4 * sizeof(int), s));
-    GN_CUDA(cudaMemsetAsync(ws.barrier, 0, sizeof(unsigned int), s));
-    GN_CUDA(cudaMemsetAsync(ws.chk, 0, 2 * sizeof(int), s));
-    if (x_hist) GN_CUDA(cudaMallocAsync((void**)&ws.hist, es * nb * (size_t)iters, s));
+    TS *xa, *xb;
+    TG *ya, *yb;
+    double *xin, *dots, *ring, *gam, *out64 = nullptr, *hist = nullptr;
+    unsigned long long *bits, *fbd;
+    int* status;
+    unsigned int* barrier;
+    int* chk;
+    GN_CUDA(ws.alloc(&xa, sizeof(TS) * nb));
+    GN_CUDA(ws.alloc(&xb, sizeof(TS) * nb));
+    GN_CUDA(ws.alloc(&ya, sizeof(TG) * nb));
+    GN_CUDA(ws.alloc(&yb, sizeof(TG) * nb));
+    GN_CUDA(ws.alloc(&bits, 8 * (size_t)iters));
+    GN_CUDA(ws.alloc(&fbd, 8 * (size_t)iters));
+    GN_CUDA(ws.alloc(&dots, 8 * 4 * (size_t)(iters + 1)));
+    GN_CUDA(ws.alloc(&ring, 8 * 4 * (size_t)kRing * grid));
+    GN_CUDA(ws.alloc(&status, 4 * sizeof(int)));
+    GN_CUDA(ws.alloc(&barrier, sizeof(unsigned int)));
+    GN_CUDA(ws.alloc(&chk, 2 * sizeof(int)));
+    GN_CUDA(ws.alloc(&gam, 8 * (size_t)iters));
+    GN_CUDA(cudaMemsetAsync(bits, 0, 8 * (size_t)iters, s));
+    GN_CUDA(cudaMemsetAsync(fbd, 0, 8 * (size_t)iters, s));
+    GN_CUDA(cudaMemsetAsync(dots, 0, 8 * 4 * (size_t)(iters + 1), s));
+    const int status_init[4] = {INT_MAX, 0, 0, 0};
+    GN_CUDA(cudaMemcpyAsync(status, status_init, sizeof(status_init), cudaMemcpyHostToDevice, s));
+    GN_CUDA(cudaMemsetAsync(barrier, 0, sizeof(unsigned int), s));
+    GN_CUDA(cudaMemsetAsync(chk, 0, 2 * sizeof(int), s));
+    if (x_hist) GN_CUDA(ws.alloc(&hist, 8 * nb * (size_t)iters));
+    GN_CUDA(cudaMemcpyAsync(gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice, s));
+    h2d += 8 * iters;
 
     // ---- x0 in, checks (dynamics.py:145-149)
-    const bool check = !(flags & GN_NO_CHECK);
     if (dev_io) {
-        if (n > 0) {
-            if (check) {
-                k_precheck_any<T><<<blocks_for(n), 256, 0, s>>>(n, g->rowptr, g->col, (const T*)x0, ws.chk);
-                GN_LAUNCHED();
-            }
-            k_prepare<T, T><<<blocks_for(n), 256, 0, s>>>(n, (const T*)x0, (const T*)g->v, ws.x0, ws.y0);
-            GN_LAUNCHED();
-        }
+        xin = (double*)x0;
     } else {
-        GN_CUDA(cudaMallocAsync((void**)&ws.xin, 8 * nb, s));
-        if (n > 0) {
-            GN_CUDA(cudaMemcpyAsync(ws.xin, x0, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
-            h2d += 8 * n;
-            if (check) {
-                k_precheck_any<double><<<blocks_for(n), 256, 0, s>>>(n, g->rowptr, g->col, ws.xin, ws.chk);
-                GN_LAUNCHED();
-            }
-            k_prepare<T, double><<<blocks_for(n), 256, 0, s>>>(n, ws.xin, (const T*)g->v, ws.x0, ws.y0);
+        GN_CUDA(ws.alloc(&xin, 8 * nb));
+        if (n > 0) GN_CUDA(cudaMemcpyAsync(xin, x0, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+        h2d += 8 * n;
+    }
+    const bool check = !(flags & GN_NO_CHECK);
+    if (n > 0) {
+        if (check) {
+            k_precheck_f64<<<blocks_for(n), 256, 0, s>>>(n, g->rowptr, g->col, xin, chk);
             GN_LAUNCHED();
         }
+        k_prepare<TS, TG><<<blocks_for(n), 256, 0, s>>>(n, xin, g->inv, (const TS*)g->v, xa, ya);
+        GN_LAUNCHED();
     }
     if (check && n > 0) {
         int hchk[2] = {0, 0};
-        GN_CUDA(cudaMemcpyAsync(hchk, ws.chk, sizeof(hchk), cudaMemcpyDeviceToHost, s));
+        GN_CUDA(cudaMemcpyAsync(hchk, chk, sizeof(hchk), cudaMemcpyDeviceToHost, s));
         GN_CUDA(cudaStreamSynchronize(s));
         if (hchk[0]) return fail(GN_ERR_NEGATIVE, "state entries must be nonnegative");
         if (hchk[1]) return fail(GN_ERR_NOT_NORMALIZABLE, "initial state has a zero closed neighborhood sum");
     }
-    double* dgam = nullptr;
-    GN_CUDA(cudaMallocAsync((void**)&dgam, 8 * (size_t)iters, s));
-    struct GamGuard {
-        double* p;
-        cudaStream_t s;
-        ~GamGuard() { cudaFreeAsync(p, s); }
-    } gg{dgam, s};
-    GN_CUDA(cudaMemcpyAsync(dgam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice, s));
-    h2d += 8 * iters;
 
     // ---- the loop
-    LoopArgs<T> a;
+    LoopArgs<TS, TG> a;
     memset(&a, 0, sizeof(a));
     a.n = n;
-    a.rowptr = g->rowptr;
-    a.col = g->col;
-    a.v = (const T*)g->v;
-    a.w = (const T*)g->w;
-    a.rows = plan.rows;
-    a.nbins = plan.nbins;
-    for (int b = 0; b < plan.nbins; ++b) a.bins[b] = plan.bins[b];
-    a.xs[0] = ws.x0;
-    a.xs[1] = ws.x1;
-    a.ys[0] = ws.y0;
-    a.ys[1] = ws.y1;
-    a.gammas = dgam;
+    a.nhub = g->nhub;
+    a.nslices = g->nslices;
+    a.nsplit = g->nsplit;
+    a.exact = (flags & GN_EXACT) ? 1 : 0;
+    a.hub_ptr = g->hub_ptr;
+    a.hub_col = g->hub_col;
+    a.slice_ptr = g->slice_ptr;
+    a.row_deg = g->row_deg;
+    a.sell = g->sell;
+    a.v = (const TS*)g->v;
+    a.w = (const TS*)g->w;
+    a.x[0] = xa;
+    a.x[1] = xb;
+    a.yg[0] = ya;
+    a.yg[1] = yb;
+    a.gammas = gam;
     a.iters = iters;
     a.final_gamma = final_gamma;
     a.early_exit = (flags & GN_EARLY_EXIT) ? 1 : 0;
-    a.stop_on_nonfinite = (flags & GN_NONFINITE_OK) ? 0 : 1;
-    a.step_bits = ws.bits;
-    a.fb = ws.fb;
-    a.status = ws.status;
-    a.dots = ws.dots;
-    a.partials = ws.part;
-    a.barrier = ws.barrier;
-    a.x_hist = ws.hist;
+    a.step_bits = bits;
+    a.fb = fbd;
+    a.status = status;
+    a.dots = dots;
+    a.ring = ring;
+    a.barrier = barrier;
+    a.x_hist = hist;
+    a.perm = g->perm;
     void* args[] = {&a};
-    GN_CUDA(cudaEventRecord(e1, s));
-    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kLoopThreads), args, 0, s));
+    GN_CUDA(cudaEventRecord(ev[1], s));
+    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kLoopThreads), args, smem, s));
     GN_LAUNCHED();
-    GN_CUDA(cudaEventRecord(e2, s));
+    GN_CUDA(cudaEventRecord(ev[2], s));
 
     // ---- results back
     int hstatus[4];
-    GN_CUDA(cudaMemcpyAsync(hstatus, ws.status, sizeof(hstatus), cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hstatus, status, sizeof(hstatus), cudaMemcpyDeviceToHost, s));
     std::vector<unsigned long long> hbits((size_t)iters), hfb((size_t)iters);
     std::vector<double> hdots(4 * (size_t)(iters + 1));
-    GN_CUDA(cudaMemcpyAsync(hbits.data(), ws.bits, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
-    GN_CUDA(cudaMemcpyAsync(hfb.data(), ws.fb, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
-    GN_CUDA(cudaMemcpyAsync(hdots.data(), ws.dots, 8 * 4 * (size_t)(iters + 1), cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hbits.data(), bits, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hfb.data(), fbd, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hdots.data(), dots, 8 * 4 * (size_t)(iters + 1), cudaMemcpyDeviceToHost, s));
     d2h += 8 * 2 * iters + 8 * 4 * (iters + 1) + 16;
     GN_CUDA(cudaStreamSynchronize(s));
-    const int ran = hstatus[2];
-    const T* xfinal = (ran & 1) ? ws.x1 : ws.x0;
+    const int ran = hstatus[1];
+    const TS* xfinal = (ran & 1) ? xb : xa;
     const int clip = (flags & GN_NO_CLIP) ? 0 : 1;
     if (x_out && n > 0) {
         if (dev_io) {
-            k_finalize<T, T><<<blocks_for(n), 256, 0, s>>>(n, xfinal, (T*)x_out, clip);
+            k_finalize<TS><<<blocks_for(n), 256, 0, s>>>(n, xfinal, g->inv, (double*)x_out, clip);
             GN_LAUNCHED();
         } else {
-            GN_CUDA(cudaMallocAsync((void**)&ws.out64, 8 * nb, s));
-            k_finalize<T, double><<<blocks_for(n), 256, 0, s>>>(n, xfinal, ws.out64, clip);
+            GN_CUDA(ws.alloc(&out64, 8 * nb));
+            k_finalize<TS><<<blocks_for(n), 256, 0, s>>>(n, xfinal, g->inv, out64, clip);
             GN_LAUNCHED();
-            GN_CUDA(cudaMemcpyAsync(x_out, ws.out64, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+            GN_CUDA(cudaMemcpyAsync(x_out, out64, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
             d2h += 8 * n;
         }
     }
     if (x_hist && n > 0 && ran > 0) {
-        const int64_t total = (int64_t)ran * n;
-        GN_CUDA(cudaMallocAsync((void**)&ws.hist64, 8 * (size_t)total, s));
-        k_hist_to_f64<T><<<blocks_for(total), 256, 0, s>>>(total, ws.hist, ws.hist64);
-        GN_LAUNCHED();
-        GN_CUDA(cudaMemcpyAsync(x_hist, ws.hist64, 8 * (size_t)total, cudaMemcpyDeviceToHost, s));
-        d2h += 8 * total;
+        GN_CUDA(cudaMemcpyAsync(x_hist, hist, 8 * (size_t)ran * (size_t)n, cudaMemcpyDeviceToHost, s));
+        d2h += 8 * (int64_t)ran * n;
     }
-    GN_CUDA(cudaEventRecord(e3, s));
+    GN_CUDA(cudaEventRecord(ev[3], s));
     GN_CUDA(cudaStreamSynchronize(s));
 
     for (int k = 0; k < ran; ++k) {
@@ -516,18 +537,19 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
         const double* d1 = &hdots[(size_t)(k + 1) * 4];
         if (mass) mass[k] = d0[3];
         if (trace) {
-            // dynamics.py:219, from the fused dot products of x_k and x_{k+1}
+            // dynamics.py:219 from the fused dot products of x_k and x_{k+1}
             if (pre_energy) pre_energy[k] = 0.5 * (d0[0] + gammas[k] * d0[1]) - d0[2];
             if (energy) energy[k] = 0.5 * (d1[0] + gammas[k] * d1[1]) - d1[2];
         }
     }
+    const int bad = hstatus[0] == INT_MAX ? -1 : hstatus[0];
     if (iters_run) *iters_run = ran;
-    if (fail_iter) *fail_iter = hstatus[1];
+    if (fail_iter) *fail_iter = bad;
     if (stats) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, e1, e2);
+        cudaEventElapsedTime(&ms, ev[1], ev[2]);
         stats->loop_ms = ms;
-        cudaEventElapsedTime(&ms, e0, e3);
+        cudaEventElapsedTime(&ms, ev[0], ev[3]);
         stats->total_ms = ms;
         stats->launches = gn_launch_count() - launches0;
         stats->grid_blocks = grid;
@@ -535,12 +557,24 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
         stats->h2d_bytes = h2d;
         stats->d2h_bytes = d2h;
     }
-    if (hstatus[0] && !(flags & GN_NONFINITE_OK)) {
+    if (bad >= 0 && !(flags & GN_NONFINITE_OK)) {
         char buf[64];
-        snprintf(buf, sizeof(buf), "non-finite state at iteration %d", hstatus[1]);
+        snprintf(buf, sizeof(buf), "non-finite state at iteration %d", bad);
+        if (iters_run) *iters_run = bad + 1;
         return fail(GN_ERR_NONFINITE, buf);
     }
     return GN_OK;
+}
+
+template <typename TS, typename TG>
+static int run_idx(gn_graph* g, const void* x0, const double* gammas, int iters, double final_gamma, uint32_t flags,
+                   void* x_out, double* step_inf, int64_t* fallbacks, double* mass, double* energy,
+                   double* pre_energy, double* x_hist, int* iters_run, int* fail_iter, gn_run_stats* stats) {
+    if (g->idx16)
+        return run_typed<TS, TG, uint16_t>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks,
+                                           mass, energy, pre_energy, x_hist, iters_run, fail_iter, stats);
+    return run_typed<TS, TG, int32_t>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks, mass,
+                                      energy, pre_energy, x_hist, iters_run, fail_iter, stats);
 }
 
 }  // namespace gn
@@ -555,11 +589,17 @@ int gn_run(gn_graph* g, const void* x0, const double* gammas, int iters, double 
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (iters < 1) return fail(GN_ERR_ARG, "iterations must be positive");
     if (!gammas || (g->n > 0 && !x0)) return fail(GN_ERR_ARG, "null input array");
-    if (g->dtype == GN_F64)
-        return run_typed<double>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks, mass,
-                                 energy, pre_energy, x_hist, iters_run, fail_iter, stats);
-    return run_typed<float>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks, mass, energy,
-                            pre_energy, x_hist, iters_run, fail_iter, stats);
+    switch (g->dtype) {
+        case GN_F64:
+            return run_idx<double, double>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks,
+                                           mass, energy, pre_energy, x_hist, iters_run, fail_iter, stats);
+        case GN_F32:
+            return run_idx<double, float>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks,
+                                          mass, energy, pre_energy, x_hist, iters_run, fail_iter, stats);
+        default:
+            return run_idx<float, float>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks, mass,
+                                         energy, pre_energy, x_hist, iters_run, fail_iter, stats);
+    }
 }
 
 int gn_step(gn_graph* g, const double* x, double gamma, uint32_t flags, double* out, int64_t* nfb) {

@@ -330,11 +330,8 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected, doub
     CallCtx ctx;
     int rc = ctx.open(g->device);
     if (rc) return rc;
-    if (flags & GN_DEVICE_IO) {
-        if (g->dtype == GN_F64)
-            return round_impl<double>(g, ctx, (const double*)x, selected, weight, independent, maximal, count);
-        return round_impl<float>(g, ctx, (const float*)x, selected, weight, independent, maximal, count);
-    }
+    if (flags & GN_DEVICE_IO)
+        return round_impl<double>(g, ctx, (const double*)x, selected, weight, independent, maximal, count);
     double* dx = nullptr;
     const size_t nb = (size_t)std::max<int64_t>(g->n, 1);
     GN_CUDA(cudaMallocAsync((void**)&dx, 8 * nb, ctx.s));

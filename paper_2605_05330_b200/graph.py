@@ -26,7 +26,8 @@ class GraphError(ValueError):
 
 
 _DTYPES = {"fp64": E.GN_F64, "float64": E.GN_F64, "f64": E.GN_F64,
-           "fp32": E.GN_F32, "float32": E.GN_F32, "f32": E.GN_F32}
+           "fp32": E.GN_F32, "float32": E.GN_F32, "f32": E.GN_F32, "mixed": E.GN_F32,
+           "fp32_pure": E.GN_F32_PURE, "f32_pure": E.GN_F32_PURE}
 
 
 def dtype_code(dtype) -> int:

@@ -1,0 +1,48 @@
+"""The C-ABI library loads and exports every symbol include/gn_b200.h
+declares; without a device every entry point fails loudly (no CPU path)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, gpu_available
+
+HEADER = ROOT / "include" / "gn_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(gn_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_bound_symbols():
+    from paper_2605_05330_b200 import _engine as E
+
+    assert declared_symbols() == sorted(E.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+
+    from paper_2605_05330_b200 import _engine as E
+
+    lib = ctypes.CDLL(str(E.LIB_PATH))
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.gn_abi_version() == 1
+
+
+def test_no_cpu_fallback_without_device():
+    if gpu_available():
+        pytest.skip("device present: covered by the gpu tests")
+    import paper_2605_05330_b200 as P
+
+    g = P.build_graph(3, [(0, 1), (1, 2)], [1.0, 3.0, 1.0])
+    with pytest.raises(P.EngineUnavailable, match="no CPU fallback"):
+        P.run_wrgn(g, np.array([0.5, 0.5, 0.5]), P.GammaSchedule.pursuit(iterations=10))
+    with pytest.raises(P.EngineUnavailable):
+        P.round_to_mis(g, np.array([1.0, 0.0, 1.0]))
+    with pytest.raises(P.EngineUnavailable):
+        P.gn_step(g, [1, 1, 1], 1.0)

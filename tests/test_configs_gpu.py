@@ -1,0 +1,112 @@
+"""GPU parity on the BASELINE.json configurations (C1, C2, C3, C4, C5) against
+the pinned CPU oracle.
+
+Sizes: C1 and C3 at full size; C2 at full size for a bounded number of
+iterations (the oracle runs at ~60 ms per iteration per core); C4 on a shard
+of graphs; C5 at R-MAT scale 16 (same generator as scale 24).  Full-size runs
+of the long configs are covered by size-independent properties (independence
+and maximality of the rounded set, fp64 weight recomputation, objective
+monotonicity where the theory guarantees it) in test_properties_gpu.py.
+"""
+
+import numpy as np
+import pytest
+
+import gn_oracle as O
+import paper_2605_05330_b200 as P
+from paper_2605_05330_b200 import generators as G
+
+pytestmark = pytest.mark.gpu
+
+THREADS = O.default_threads()
+
+
+def _gates_fp32(inst, ref, r, label):
+    """fp32 (mixed) engine against the fp64 oracle: BASELINE.md section 4."""
+    mass_rel = np.abs(np.array(r.trace.objective) - ref.mass) / np.abs(ref.mass)
+    assert mass_rel.max() <= 1e-4, f"{label}: objective rel {mass_rel.max():.3e}"
+    if r.history is not None:
+        dx = np.abs(r.history - ref.history).max(axis=1)
+        exc = [(int(k), float(dx[k])) for k in np.flatnonzero(dx > 1e-4)]
+        assert not exc, f"{label}: per-iteration |dx| > 1e-4 at {exc[:10]}"
+
+
+def test_c1_full_fp64_bitwise_fast_and_exact():
+    inst = G.c1_er()
+    s = P.GammaSchedule.pursuit()
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, history=True, threads=THREADS)
+    for exact in (False, True):
+        r = P.run_engine(inst.graph, inst.x0, s, exact=exact, history=True)
+        # C1's rows are all short slices: the fast path sums sequentially too
+        np.testing.assert_array_equal(r.history, ref.history)
+        np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
+    sol = P.round_to_mis(inst.graph, r.x)
+    sel, weight, ind, mx = O.round_to_mis(inst.graph, ref.x)
+    assert list(sol.members) == np.flatnonzero(sel).tolist() and sol.weight == weight and ind and mx
+
+
+def test_c2_assignment_fp32_against_oracles():
+    inst = G.c2_assignment()
+    s = P.GammaSchedule.pursuit()
+    short = P.GammaSchedule(0.9, 1.5, 1000, "linear")
+    k = 40  # oracle budget: the first 40 pursuit steps of the full instance
+    tab = short.table()[:k]
+    ref_mixed = O.run(inst.graph, inst.x0, tab, 1.5, dtype="fp32", history=True, threads=THREADS)
+    r = P.run_engine(inst.graph, inst.x0, P.GammaSchedule(0.9, 0.9 + 0.6 * (k - 1) / 999, k, "linear"),
+                     dtype="fp32", exact=True, history=True)
+    np.testing.assert_array_equal(r.trace.gamma, tab)
+    np.testing.assert_array_equal(r.history, ref_mixed.history)
+    ref64 = O.run(inst.graph, inst.x0, tab, 1.5, history=True, threads=THREADS)
+    rf = P.run_engine(inst.graph, inst.x0, P.GammaSchedule(0.9, 0.9 + 0.6 * (k - 1) / 999, k, "linear"),
+                      dtype="fp32", history=True)
+    _gates_fp32(inst, ref64, rf, "C2")
+    # full pursuit on the engine: a valid maximal independent set
+    x, tr = P.run_wrgn(inst.graph, inst.x0, s, dtype="fp32")
+    sol = P.round_to_mis(inst.graph, x)
+    assert sol.independent and sol.maximal and len(sol.members) == 256  # a perfect assignment
+    assert sol.weight == pytest.approx(float(inst.graph.w[list(sol.members)].sum()), rel=0, abs=0)
+
+
+def test_c3_ba_fp64_full_pursuit():
+    inst = G.c3_ba()
+    s = P.GammaSchedule.pursuit()
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, threads=THREADS)
+    r = P.run_engine(inst.graph, inst.x0, s)
+    np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
+    np.testing.assert_allclose(r.x, ref.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(r.trace.step_inf, ref.step_inf, rtol=1e-6, atol=1e-12)
+    sol = P.round_to_mis(inst.graph, r.x)
+    sel, weight, ind, mx = O.round_to_mis(inst.graph, ref.x)
+    assert list(sol.members) == np.flatnonzero(sel).tolist()
+    assert sol.weight == weight and sol.independent and sol.maximal
+    rx = P.run_engine(inst.graph, inst.x0, s, exact=True)
+    np.testing.assert_array_equal(rx.x, ref.x)
+    np.testing.assert_array_equal(rx.trace.step_inf, ref.step_inf)
+
+
+def test_c4_batch_shard_fp32():
+    b = G.c4_batch(graphs=16)
+    inst = b.instance
+    s = P.GammaSchedule.pursuit()
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, history=True, threads=THREADS)
+    r = P.run_engine(inst.graph, inst.x0, s, dtype="fp32", history=True)
+    _gates_fp32(inst, ref, r, "C4")
+    sol = P.round_to_mis(inst.graph, r.x)
+    sel, weight, _, _ = O.round_to_mis(inst.graph, ref.x)
+    assert list(sol.members) == np.flatnonzero(sel).tolist() and sol.weight == weight
+
+
+def test_c5_rmat_scale16_fp32():
+    inst = G.c5_rmat(16)
+    s = P.GammaSchedule.pursuit()
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, threads=THREADS)
+    r = P.run_engine(inst.graph, inst.x0, s, dtype="fp32")
+    mass_rel = np.abs(np.array(r.trace.objective) - ref.mass) / np.abs(ref.mass)
+    assert mass_rel.max() <= 1e-4
+    assert np.abs(r.x - ref.x).max() <= 1e-4
+    rx = P.run_engine(inst.graph, inst.x0, s, dtype="fp64")
+    np.testing.assert_array_equal(rx.trace.fallbacks, ref.fallbacks)
+    np.testing.assert_allclose(rx.x, ref.x, rtol=1e-9, atol=1e-12)
+    sol = P.round_to_mis(inst.graph, rx.x)
+    sel, weight, _, _ = O.round_to_mis(inst.graph, ref.x)
+    assert list(sol.members) == np.flatnonzero(sel).tolist() and sol.weight == weight

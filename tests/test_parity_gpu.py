@@ -101,12 +101,15 @@ def test_fp32_against_fp64_reference_gates():
     assert sol.weight == d["mis_weight"]
 
 
-def test_fp32_exact_is_bitwise_fp32_oracle():
+@pytest.mark.parametrize("dtype", ["fp32", "fp32_pure"])
+def test_fp32_exact_is_bitwise_same_precision_oracle(dtype):
+    """EXACT mode walks every row sequentially, so the engine must equal the
+    oracle carried out in the same precision bit for bit."""
     d = load_golden("c1_er1000_f32inputs_trace")
     g = golden_graph(d)
     s = golden_schedule(d)
-    ref = O.run(g, d["x0"], s.table(), s.final_gamma, dtype="fp32", history=True)
-    r = P.run_engine(g, d["x0"], s, dtype="fp32", exact=True, history=True)
+    ref = O.run(g, d["x0"], s.table(), s.final_gamma, dtype=dtype, history=True)
+    r = P.run_engine(g, d["x0"], s, dtype=dtype, exact=True, history=True)
     np.testing.assert_array_equal(r.history, ref.history)
     np.testing.assert_array_equal(r.trace.step_inf, ref.step_inf)
     np.testing.assert_array_equal(r.x, ref.x)
