@@ -240,6 +240,12 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
         bool full = (r1 - r0) == (size_t)kSlice;
         (full && len >= kSplitLen ? split_g : whole_g).push_back((int32_t)gi);
     }
+    // long slices by length, longest first: the loop deals them out zigzag
+    std::vector<int32_t> glen(ng, 0);
+    for (size_t gi = 0; gi < ng; ++gi)
+        for (size_t r = gi * kSlice; r < std::min(regular.size(), (gi + 1) * (size_t)kSlice); ++r)
+            glen[gi] = std::max(glen[gi], deg[regular[r]]);
+    std::stable_sort(split_g.begin(), split_g.end(), [&](int32_t a, int32_t b) { return glen[a] > glen[b]; });
     L.nhub = (int32_t)hubs.size();
     L.nsplit = (int32_t)split_g.size();
     L.nslices = (int32_t)ng;
@@ -265,6 +271,8 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
     }
     // SELL slices, position-major
     const int64_t nreg = n - L.nhub;
+    L.idx16 = n <= 65536 ? 1 : 0;
+    const int B = L.idx16 ? 8 : 4;  // positions per 16-byte lane vector
     L.row_deg.assign((size_t)std::max<int64_t>(nreg, 0), 0);
     L.slice_ptr.assign((size_t)L.nslices + 1, 0);
     for (int32_t s = 0; s < L.nslices; ++s) {
@@ -277,10 +285,10 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
                 len = std::max(len, d);
             }
         }
+        len = (len + B - 1) / B * B;
         L.slice_ptr[s + 1] = L.slice_ptr[s] + (int64_t)len * kSlice;
     }
     const int64_t elems = L.slice_ptr[L.nslices];
-    L.idx16 = n <= 65536 ? 1 : 0;
     if (L.idx16) L.sell16.assign((size_t)elems, 0);
     else L.sell32.assign((size_t)elems, 0);
     for (int32_t s = 0; s < L.nslices; ++s) {
@@ -289,7 +297,9 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
             if (r >= nreg) continue;
             int32_t o = L.perm[(size_t)(L.nhub + r)];
             for (int64_t p = indptr[o]; p < indptr[o + 1]; ++p) {
-                int64_t at = L.slice_ptr[s] + (p - indptr[o]) * kSlice + l;
+                // block-major: block p/B holds 32 lanes x B consecutive positions
+                const int64_t q = p - indptr[o];
+                int64_t at = L.slice_ptr[s] + (q / B) * (kSlice * B) + (int64_t)l * B + q % B;
                 int32_t nid = L.inv[indices[p]];
                 if (L.idx16) L.sell16[(size_t)at] = (uint16_t)nid;
                 else L.sell32[(size_t)at] = nid;

@@ -58,10 +58,12 @@ inline size_t gather_bytes(int d) { return d == GN_F64 ? 8 : 4; }
 //    checks and the auxiliary fp64 operators;
 //  * the loop layout: vertices relabeled (new id r, perm[r] = old id) so that
 //    hub rows come first and the remaining rows, degree-sorted in windows of
-//    kSigma, form SELL slices of 32 rows stored position-major
-//    (element p of the slice's 32 rows is 32 consecutive indices), which makes
-//    every index load of a warp one coalesced line and lets one thread sum
-//    its row in the reference's sequential order.
+//    kSigma, form SELL slices of 32 rows.  A slice is stored in blocks of B
+//    positions (B = 8 for uint16 ids, 4 for int32): block b holds, lane after
+//    lane, the B consecutive neighbours of each of the 32 rows, so one lane
+//    fetches B indices with one 16-byte load and a warp's loads of a block
+//    cover 512 contiguous bytes.  One thread sums its row in the reference's
+//    sequential order.
 struct gn_graph {
     int64_t n = 0;
     int64_t nnz = 0;
@@ -87,7 +89,7 @@ struct gn_graph {
     int32_t* hub_col = nullptr;  // new ids, original neighbour order
     int32_t nslices = 0;      // rows [nhub, n) in slices of 32
     int32_t nsplit = 0;       // slices [0, nsplit) have length >= kSplitLen
-    int64_t* slice_ptr = nullptr;  // nslices+1 element offsets (multiples of 32)
+    int64_t* slice_ptr = nullptr;  // nslices+1 element offsets (multiples of 32*B)
     int32_t* row_deg = nullptr;    // degree per slice row (n - nhub)
     void* sell = nullptr;          // int32 or uint16 new ids, position-major
     int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536)
@@ -132,13 +134,14 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
     __syncthreads();
     if (gridDim.x > 1) {
         if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(counter, 1u);
+            // release: the block's writes (ordered before us by bar.sync) reach
+            // gpu scope before the arrival; the arrival itself returns nothing
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
             unsigned int seen;
             do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
             } while (seen < target);
-            __threadfence();
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire (invalidates this SM's L1)
         }
         __syncthreads();
     }

@@ -39,6 +39,7 @@ namespace gn {
 
 constexpr int kRing = 1024;     // iterations of block partials kept before a fold
 constexpr int kSplitSlots = 8;  // long slices buffered per CTA between syncs
+constexpr int kRingW = 8;       // per block: 4 dot terms, max|dx|, fallbacks, non-finite flag, pad
 
 template <typename TS, typename TG>
 struct LoopArgs {
@@ -58,14 +59,23 @@ struct LoopArgs {
     int iters;
     double final_gamma;
     int early_exit;
-    unsigned long long* step_bits;  // [iters]
-    unsigned long long* fb;         // [iters]
-    int* status;                    // [0] first non-finite iteration (INT_MAX: none) [1] iterations run
-    double* dots;                   // [(iters+1)][4]: y.y, y.s, w.x (pre), w.x' (post)
-    double* ring;                   // [kRing][grid][4]
+    double* step_inf;  // [iters]   max over blocks of max|x'-x|
+    double* fb;        // [iters]   fallback count (exact in fp64)
+    int* bad;          // [iters]   1 if a non-finite state appeared
+    int* status;       // [0] iterations run
+    double* dots;      // [(iters+1)][4]: y.y, y.s, w.x (pre), w.x' (post)
+    double* ring;      // [kRing][grid][kRingW] per-block partials
     unsigned int* barrier;
     double* x_hist;                 // optional [iters][n], original order
     const int32_t* __restrict__ perm;
+};
+
+struct LoopArgs_common {
+    int iters;
+    double* step_inf;
+    double* fb;
+    int* bad;
+    double* dots;
 };
 
 struct Stats {
@@ -106,26 +116,58 @@ __device__ __forceinline__ void update_row(const LoopArgs<TS, TG>& a, int r, TS 
     if (a.x_hist) a.x_hist[(size_t)k * (size_t)a.n + (size_t)__ldg(a.perm + r)] = (double)o;
 }
 
-// Sequential sum over positions [pb, pe) of one slice row (lane), masked by
-// the row's degree d.  Loads are issued 8 at a time; the adds stay in order.
-template <typename TS, typename TG, typename TI>
-__device__ __forceinline__ TS sum_positions(const TI* __restrict__ col, const TG* __restrict__ yg, int lane, int d,
-                                            int pb, int pe) {
-    using A = Arith<TS>;
-    TS s = TS(0);
-    int p = pb;
-    for (; p + 8 <= pe; p += 8) {
-        TI j[8];
-        TG y[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) j[u] = (p + u < d) ? __ldg(col + (size_t)(p + u) * kSlice + lane) : TI(0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) y[u] = (p + u < d) ? yg[j[u]] : TG(0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = A::add(s, (TS)y[u]);
+// Blocked-SELL lane vectors: one 16-byte load gives B consecutive neighbours.
+template <typename TI>
+struct LaneVec;
+template <>
+struct LaneVec<uint16_t> {
+    static constexpr int B = 8;  // positions per 16-byte vector
+    __device__ static __forceinline__ int get(const uint4& v, int t) {
+        const unsigned w = t < 4 ? (t < 2 ? v.x : v.y) : (t < 6 ? v.z : v.w);
+        return (int)((t & 1) ? (w >> 16) : (w & 0xffffu));
     }
-    for (; p < pe; ++p)
-        if (p < d) s = A::add(s, (TS)yg[__ldg(col + (size_t)p * kSlice + lane)]);
+};
+template <>
+struct LaneVec<int32_t> {
+    static constexpr int B = 4;
+    __device__ static __forceinline__ int get(const uint4& v, int t) {
+        return (int)(t == 0 ? v.x : t == 1 ? v.y : t == 2 ? v.z : v.w);
+    }
+};
+
+// Sequential sum over blocks [bb, be) of one slice row (this lane), masked by
+// the row's degree d.  A batch issues NB vector loads and NB*B gathers before
+// any add; the adds stay in position order (the reference's order).
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ TS sum_blocks(const TI* __restrict__ slice, const TG* __restrict__ yg, int lane, int d,
+                                         int bb, int be) {
+    using A = Arith<TS>;
+    using V = LaneVec<TI>;
+    // 16 four-byte (8 eight-byte) gathers in flight per lane per batch
+    constexpr int B = V::B, NB = (sizeof(TG) == 4 ? 16 : 8) / B > 0 ? (sizeof(TG) == 4 ? 16 : 8) / B : 1;
+    const uint4* __restrict__ base = reinterpret_cast<const uint4*>(slice) + lane;
+    TS s = TS(0);
+    int b = bb;
+    for (; b + NB <= be; b += NB) {
+        uint4 v[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) v[u] = __ldg(base + (size_t)(b + u) * kSlice);
+        TG y[NB * B];
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+#pragma unroll
+            for (int t = 0; t < B; ++t) y[u * B + t] = ((b + u) * B + t < d) ? yg[V::get(v[u], t)] : TG(0);
+#pragma unroll
+        for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
+    }
+    for (; b < be; ++b) {
+        const uint4 v = __ldg(base + (size_t)b * kSlice);
+        TG y[B];
+#pragma unroll
+        for (int t = 0; t < B; ++t) y[t] = (b * B + t < d) ? yg[V::get(v, t)] : TG(0);
+#pragma unroll
+        for (int t = 0; t < B; ++t) s = A::add(s, (TS)y[t]);
+    }
     return s;
 }
 
@@ -166,23 +208,25 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
     }
 
     // ---- long slices, warps split the positions
+    // slices are sorted longest first; round q deals them out in zigzag order
+    // (b, 2G-1-b, 2G+b, ...) so every CTA gets a similar total length
     const int nsplit = a.exact ? 0 : a.nsplit;
-    const int nq = nsplit > (int)blockIdx.x ? (nsplit - 1 - (int)blockIdx.x) / G + 1 : 0;
+    auto split_of = [&](int q) { return q * G + ((q & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x); };
+    int nq = 0;
+    while (split_of(nq) < nsplit) ++nq;
     for (int q0 = 0; q0 < nq; q0 += kSplitSlots) {
         const int qn = min(kSplitSlots, nq - q0);
         for (int q = 0; q < qn; ++q) {
-            const int s = blockIdx.x + (q0 + q) * G;
+            const int s = split_of(q0 + q);
             const int64_t base = __ldg(a.slice_ptr + s);
-            const int L = (int)((__ldg(a.slice_ptr + s + 1) - base) / kSlice);
-            const int r = a.nhub + s * kSlice + lane;
+            const int nblk = (int)((__ldg(a.slice_ptr + s + 1) - base) / (kSlice * LaneVec<TI>::B));
             const int d = __ldg(a.row_deg + s * kSlice + lane);
-            const int pb = (int)((int64_t)L * warp / kLoopWarps), pe = (int)((int64_t)L * (warp + 1) / kLoopWarps);
-            (void)r;
-            s_part[(q * kLoopWarps + warp) * kSlice + lane] = sum_positions<TS, TG, TI>(sell + base, yg, lane, d, pb, pe);
+            const int bb = nblk * warp / kLoopWarps, be = nblk * (warp + 1) / kLoopWarps;
+            s_part[(q * kLoopWarps + warp) * kSlice + lane] = sum_blocks<TS, TG, TI>(sell + base, yg, lane, d, bb, be);
         }
         __syncthreads();
         for (int q = warp; q < qn; q += kLoopWarps) {
-            const int s = blockIdx.x + (q0 + q) * G;
+            const int s = split_of(q0 + q);
             TS tot = TS(0);
 #pragma unroll 4
             for (int w = 0; w < kLoopWarps; ++w) tot = A::add(tot, s_part[(q * kLoopWarps + w) * kSlice + lane]);
@@ -196,11 +240,11 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
     const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
     for (int s = first + gw; s < a.nslices; s += nw) {
         const int64_t base = __ldg(a.slice_ptr + s);
-        const int L = (int)((__ldg(a.slice_ptr + s + 1) - base) / kSlice);
+        const int nblk = (int)((__ldg(a.slice_ptr + s + 1) - base) / (kSlice * LaneVec<TI>::B));
         const int64_t r = (int64_t)a.nhub + (int64_t)s * kSlice + lane;
         const bool valid = r < a.n;
         const int d = valid ? __ldg(a.row_deg + (size_t)s * kSlice + lane) : 0;
-        const TS sum = sum_positions<TS, TG, TI>(sell + base, yg, lane, d, 0, L);
+        const TS sum = sum_blocks<TS, TG, TI>(sell + base, yg, lane, d, 0, nblk);
         if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, cur, g, k, tail, st);
     }
 }
@@ -211,9 +255,10 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-// Block-level fold of the per-thread stats; thread 0 publishes.
-__device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__ ring_slot,
-                        unsigned long long* step_bits, unsigned long long* fb, int* status) {
+// Block-level fold of the per-thread stats; thread 0 stores them (plain
+// stores, no atomics) in this iteration's ring slot.
+template <bool TRACE>
+__device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
     __shared__ double s_acc[kLoopWarps][4];
     __shared__ double s_mx[kLoopWarps];
     __shared__ unsigned int s_fb[kLoopWarps];
@@ -228,7 +273,7 @@ __device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__
         st.bad |= __shfl_xor_sync(0xffffffffu, st.bad, o);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) st.acc[q] = warp_sum_d(st.acc[q]);
+    for (int q = TRACE ? 0 : 3; q < 4; ++q) st.acc[q] = warp_sum_d(st.acc[q]);
     if (lane == 0) {
         s_mx[warp] = st.mx;
         s_fb[warp] = st.fbc;
@@ -246,32 +291,73 @@ __device__ void publish(const Stats& st0, int k, bool tail, double* __restrict__
             f += s_fb[q];
             bad |= s_bad[q];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], s_acc[q][c]);
+            for (int c = TRACE ? 0 : 3; c < 4; ++c) acc[c] = __dadd_rn(acc[c], s_acc[q][c]);
         }
-        if (!tail) {
-            if (mx != 0.0) atomicMax(step_bits + k, (unsigned long long)__double_as_longlong(mx));
-            if (f) atomicAdd(fb + k, (unsigned long long)f);
-            if (bad) atomicMin(status, k);
-        }
+        double* dst = ring_slot + (size_t)blockIdx.x * kRingW;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ring_slot[blockIdx.x * 4 + c] = acc[c];
+        for (int c = 0; c < 4; ++c) dst[c] = acc[c];
+        dst[4] = mx;
+        dst[5] = (double)f;
+        dst[6] = bad ? 1.0 : 0.0;
     }
 }
 
-// All blocks: fold ring slots [0, count) (iterations k0..k0+count-1) into
-// dots, one warp per (slot, term), block order fixed.
-__device__ void fold_ring(const double* ring, int count, int k0, double* dots) {
+// All blocks: fold ring slots [0, count) (iterations k0..k0+count-1), one
+// warp per (slot, quantity), block order fixed.  max|dx| and the non-finite
+// flag are order-free; the sums follow a fixed tree.
+__device__ void fold_ring(const double* ring, int count, int k0, const LoopArgs_common& o) {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = gridDim.x * kLoopWarps;
     const int G = gridDim.x;
-    for (int t = gw; t < count * 4; t += nw) {
-        const int slot = t >> 2, c = t & 3;
-        const double* src = ring + (size_t)slot * G * 4;
-        double s = 0.0;
-        for (int b = lane; b < G; b += 32) s = __dadd_rn(s, __ldcg(src + b * 4 + c));
-        s = warp_sum_d(s);
-        if (lane == 0) dots[(size_t)(k0 + slot) * 4 + c] = s;
+    for (int t = gw; t < count * 7; t += nw) {
+        const int slot = t / 7, c = t % 7;
+        const double* src = ring + (size_t)slot * G * kRingW + c;
+        const int k = k0 + slot;
+        if (c == 4 || c == 6) {
+            double m = 0.0;
+            for (int b = lane; b < G; b += 32) {
+                const double v = __ldcg(src + (size_t)b * kRingW);
+                if (!(v <= m)) m = v;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double v = __shfl_xor_sync(0xffffffffu, m, off);
+                if (!(v <= m)) m = v;
+            }
+            if (lane == 0) {
+                if (c == 4) { if (k < o.iters) o.step_inf[k] = m; }
+                else if (k < o.iters) o.bad[k] = m != 0.0 ? 1 : 0;
+            }
+        } else {
+            double s = 0.0;
+            for (int b = lane; b < G; b += 32) s = __dadd_rn(s, __ldcg(src + (size_t)b * kRingW));
+            s = warp_sum_d(s);
+            if (lane == 0) {
+                if (c == 5) { if (k < o.iters) o.fb[k] = s; }
+                else o.dots[(size_t)k * 4 + c] = s;
+            }
+        }
     }
+}
+
+// Every block computes max|dx| of iteration k from the ring (early exit).
+__device__ double ring_step_inf(const double* ring_slot) {
+    __shared__ double s_m;
+    if (threadIdx.x < 32) {
+        double m = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+            const double v = __ldcg(ring_slot + (size_t)b * kRingW + 4);
+            if (!(v <= m)) m = v;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double v = __shfl_xor_sync(0xffffffffu, m, off);
+            if (!(v <= m)) m = v;
+        }
+        if (threadIdx.x == 0) s_m = m;
+    }
+    __syncthreads();
+    return s_m;
 }
 
 template <typename TS, typename TG, typename TI, bool TRACE>
@@ -279,23 +365,23 @@ __global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
     extern __shared__ unsigned char smem_raw[];
     TS* s_part = (TS*)smem_raw;
     __shared__ TS s_hub[kLoopWarps];
+    const LoopArgs_common oc{a.iters, a.step_inf, a.fb, a.bad, a.dots};
     unsigned int bar = 0;
     int ran = 0, k0 = 0;
-    const size_t ring_stride = (size_t)gridDim.x * 4;
+    const size_t ring_stride = (size_t)gridDim.x * kRingW;
     for (int k = 0; k < a.iters; ++k) {
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
         pass<TS, TG, TI, TRACE>(a, k, false, st, s_part, s_hub);
-        publish(st, k, false, a.ring + (size_t)(k - k0) * ring_stride, a.step_bits, a.fb, a.status);
+        double* slot = a.ring + (size_t)(k - k0) * ring_stride;
+        publish<TRACE>(st, slot);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
         ran = k + 1;
         bool stop = false;
-        if (a.early_exit && a.gammas[k] == a.final_gamma) {  // dynamics.py:177
-            const double si = __longlong_as_double(*(volatile long long*)(a.step_bits + k));
-            stop = si < 1e-12;
-        }
+        if (a.early_exit && a.gammas[k] == a.final_gamma)  // dynamics.py:177
+            stop = ring_step_inf(slot) < 1e-12;
         const bool last = stop || ran == a.iters;
         if (ran - k0 == kRing || (last && !TRACE)) {
-            fold_ring(a.ring, ran - k0, k0, a.dots);
+            fold_ring(a.ring, ran - k0, k0, oc);
             grid_barrier(a.barrier, (++bar) * gridDim.x);
             k0 = ran;
         }
@@ -305,11 +391,11 @@ __global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
         pass<TS, TG, TI, TRACE>(a, ran, true, st, s_part, s_hub);
-        publish(st, ran, true, a.ring + (size_t)(ran - k0) * ring_stride, a.step_bits, a.fb, a.status);
+        publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
-        fold_ring(a.ring, ran - k0 + 1, k0, a.dots);
+        fold_ring(a.ring, ran - k0 + 1, k0, oc);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.status[1] = ran;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.status[0] = ran;
 }
 
 // x0 (original order, fp64) -> state buffers (new order): x = (TS)x0, yg = (TG)(v*x)
@@ -406,28 +492,28 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     ws.s = s;
     TS *xa, *xb;
     TG *ya, *yb;
-    double *xin, *dots, *ring, *gam, *out64 = nullptr, *hist = nullptr;
-    unsigned long long *bits, *fbd;
-    int* status;
+    double *xin, *dots, *ring, *gam, *out64 = nullptr, *hist = nullptr, *dsi, *dfb;
+    int *dbad, *status;
     unsigned int* barrier;
     int* chk;
     GN_CUDA(ws.alloc(&xa, sizeof(TS) * nb));
     GN_CUDA(ws.alloc(&xb, sizeof(TS) * nb));
     GN_CUDA(ws.alloc(&ya, sizeof(TG) * nb));
     GN_CUDA(ws.alloc(&yb, sizeof(TG) * nb));
-    GN_CUDA(ws.alloc(&bits, 8 * (size_t)iters));
-    GN_CUDA(ws.alloc(&fbd, 8 * (size_t)iters));
+    GN_CUDA(ws.alloc(&dsi, 8 * (size_t)iters));
+    GN_CUDA(ws.alloc(&dfb, 8 * (size_t)iters));
+    GN_CUDA(ws.alloc(&dbad, 4 * (size_t)iters));
     GN_CUDA(ws.alloc(&dots, 8 * 4 * (size_t)(iters + 1)));
-    GN_CUDA(ws.alloc(&ring, 8 * 4 * (size_t)kRing * grid));
+    GN_CUDA(ws.alloc(&ring, 8 * (size_t)kRingW * (size_t)std::min(kRing, iters + 1) * grid));
     GN_CUDA(ws.alloc(&status, 4 * sizeof(int)));
     GN_CUDA(ws.alloc(&barrier, sizeof(unsigned int)));
     GN_CUDA(ws.alloc(&chk, 2 * sizeof(int)));
     GN_CUDA(ws.alloc(&gam, 8 * (size_t)iters));
-    GN_CUDA(cudaMemsetAsync(bits, 0, 8 * (size_t)iters, s));
-    GN_CUDA(cudaMemsetAsync(fbd, 0, 8 * (size_t)iters, s));
+    GN_CUDA(cudaMemsetAsync(dsi, 0, 8 * (size_t)iters, s));
+    GN_CUDA(cudaMemsetAsync(dfb, 0, 8 * (size_t)iters, s));
+    GN_CUDA(cudaMemsetAsync(dbad, 0, 4 * (size_t)iters, s));
     GN_CUDA(cudaMemsetAsync(dots, 0, 8 * 4 * (size_t)(iters + 1), s));
-    const int status_init[4] = {INT_MAX, 0, 0, 0};
-    GN_CUDA(cudaMemcpyAsync(status, status_init, sizeof(status_init), cudaMemcpyHostToDevice, s));
+    GN_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), s));
     GN_CUDA(cudaMemsetAsync(barrier, 0, sizeof(unsigned int), s));
     GN_CUDA(cudaMemsetAsync(chk, 0, 2 * sizeof(int), s));
     if (x_hist) GN_CUDA(ws.alloc(&hist, 8 * nb * (size_t)iters));
@@ -482,8 +568,9 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.iters = iters;
     a.final_gamma = final_gamma;
     a.early_exit = (flags & GN_EARLY_EXIT) ? 1 : 0;
-    a.step_bits = bits;
-    a.fb = fbd;
+    a.step_inf = dsi;
+    a.fb = dfb;
+    a.bad = dbad;
     a.status = status;
     a.dots = dots;
     a.ring = ring;
@@ -499,14 +586,16 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     // ---- results back
     int hstatus[4];
     GN_CUDA(cudaMemcpyAsync(hstatus, status, sizeof(hstatus), cudaMemcpyDeviceToHost, s));
-    std::vector<unsigned long long> hbits((size_t)iters), hfb((size_t)iters);
+    std::vector<double> hsi((size_t)iters), hfb((size_t)iters);
+    std::vector<int> hbad((size_t)iters);
     std::vector<double> hdots(4 * (size_t)(iters + 1));
-    GN_CUDA(cudaMemcpyAsync(hbits.data(), bits, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
-    GN_CUDA(cudaMemcpyAsync(hfb.data(), fbd, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hsi.data(), dsi, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hfb.data(), dfb, 8 * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hbad.data(), dbad, 4 * (size_t)iters, cudaMemcpyDeviceToHost, s));
     GN_CUDA(cudaMemcpyAsync(hdots.data(), dots, 8 * 4 * (size_t)(iters + 1), cudaMemcpyDeviceToHost, s));
-    d2h += 8 * 2 * iters + 8 * 4 * (iters + 1) + 16;
+    d2h += 8 * 2 * iters + 4 * iters + 8 * 4 * (iters + 1) + 16;
     GN_CUDA(cudaStreamSynchronize(s));
-    const int ran = hstatus[1];
+    const int ran = hstatus[0];
     const TS* xfinal = (ran & 1) ? xb : xa;
     const int clip = (flags & GN_NO_CLIP) ? 0 : 1;
     if (x_out && n > 0) {
@@ -528,10 +617,11 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     GN_CUDA(cudaEventRecord(ev[3], s));
     GN_CUDA(cudaStreamSynchronize(s));
 
+    int bad = -1;
+    for (int k = 0; k < ran; ++k)
+        if (hbad[(size_t)k]) { bad = k; break; }
     for (int k = 0; k < ran; ++k) {
-        double si;
-        memcpy(&si, &hbits[(size_t)k], 8);
-        if (step_inf) step_inf[k] = si;
+        if (step_inf) step_inf[k] = hsi[(size_t)k];
         if (fallbacks) fallbacks[k] = (int64_t)hfb[(size_t)k];
         const double* d0 = &hdots[(size_t)k * 4];
         const double* d1 = &hdots[(size_t)(k + 1) * 4];
@@ -542,7 +632,6 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
             if (energy) energy[k] = 0.5 * (d1[0] + gammas[k] * d1[1]) - d1[2];
         }
     }
-    const int bad = hstatus[0] == INT_MAX ? -1 : hstatus[0];
     if (iters_run) *iters_run = ran;
     if (fail_iter) *fail_iter = bad;
     if (stats) {

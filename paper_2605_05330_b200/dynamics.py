@@ -177,12 +177,17 @@ class RunResult:
 
 
 def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early_exit: bool = False, *,
-               dtype=None, exact=None, device=None, history: bool = False) -> RunResult:
-    """run_wrgn with the engine's extras (stats, optional per-iteration x)."""
+               dtype=None, exact=None, device=None, history: bool = False,
+               gammas: Optional[np.ndarray] = None) -> RunResult:
+    """run_wrgn with the engine's extras (stats, optional per-iteration x).
+
+    ``gammas`` replaces the schedule's table (e.g. a prefix of a pursuit
+    schedule); the early-exit test still compares with schedule.final_gamma.
+    """
     x = _as_state(g, x0)
     h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
-    gam = np.ascontiguousarray(schedule.table())
-    iters = schedule.iterations
+    gam = np.ascontiguousarray(schedule.table() if gammas is None else np.asarray(gammas, dtype=np.float64))
+    iters = len(gam)
     step_inf = np.zeros(iters, dtype=np.float64)
     fallbacks = np.zeros(iters, dtype=np.int64)
     mass = np.zeros(iters, dtype=np.float64)

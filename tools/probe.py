@@ -39,8 +39,22 @@ def probe(inst, iters=1000, grids=(0,), exact=False, reps=3, dtype=None):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="C1,C2,C3")
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--grid", type=int, default=-1)
+    ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     which = args.which.split(",")
+    if args.grid >= 0:
+        for name in which:
+            if name == "EDGELESS":
+                inst = G.Instance("edgeless", P.from_csr(100000, np.zeros(100001, np.int64), np.zeros(0, np.int32),
+                                                           np.ones(100000)), np.full(100000, 0.5), "fp64")
+            elif name == "C4":
+                inst = G.c4_batch(1024).instance
+            else:
+                inst = G.CONFIGS[name]()
+            probe(inst, iters=args.iters, grids=(args.grid,), reps=args.reps)
+        raise SystemExit(0)
     if "C1" in which:
         probe(G.c1_er(), grids=(1, 2, 4, 0))
         probe(G.c1_er(), exact=True, grids=(0,))
