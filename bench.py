@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""GN engine benchmark: GN edge-updates/s (undirected edges x iterations / s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one run_wrgn over one instance: the reference's default pursuit
+schedule (linear gamma 0.9 -> 1.5, 1000 iterations, dynamics.py:58-63) on the
+workload BASELINE.json's metric is quoted on at one GPU -- configs[1], the
+256x256 assignment conflict graph (C2), fp32 gathered values.  N > 1: one
+process per GPU (torchrun), each rank runs its own replica (C2 does not
+shard: "replicas only"), `value` counts all ranks' edge updates
+over the max-over-ranks device time.  --config C4 shards the C4 batch instead
+(1024 graphs per rank, no collectives).
+
+Printed JSON keys follow the driver contract; see DESIGN.md "Measurement".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "GN edge-updates/sec (edges x iters / s)"
+UNIT = "edge-updates/s"
+
+CONFIG_TEXT = {
+    "C1": "Erdos-Renyi G(n=1000, avg degree 10), w ~ U(0,1], fp64, init_random x0, pursuit 0.9->1.5 x1000",
+    "C2": "assignment-as-MWIS: conflict graph of a 256x256 assignment (65,536 vertices, 16,711,680 edges), "
+          "w ~ U(0,1] fp32, pursuit 0.9->1.5 x1000",
+    "C3": "Barabasi-Albert n=200,000 m=5 (999,975 edges), integer weights U{1..200} fp64, pursuit x1000",
+    "C4": "1024 independent ER graphs n=2000 avg degree 16 per GPU, packed block-diagonal, fp32, pursuit x1000",
+    "C5": "R-MAT scale S edge factor 16 (a=.57,b=c=.19), symmetrised, dedup, fp32, pursuit x1000",
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_instance(config: str, rank: int, scale: int):
+    from paper_2605_05330_b200 import generators as G
+
+    if config == "C1":
+        return G.c1_er()
+    if config == "C2":
+        return G.c2_assignment()
+    if config == "C3":
+        return G.c3_ba()
+    if config == "C4":
+        return G.c4_batch(graphs=1024, first=rank * 1024).instance
+    if config == "C5":
+        return G.c5_rmat(scale)
+    raise SystemExit(f"unknown config {config}")
+
+
+def algorithmic_bytes(n: int, nnz: int, s: int) -> int:
+    """B_iter = 4 nnz + P (n+1) + 3 s n (P = 4 below 2^31 entries)."""
+    p = 4 if nnz < 2**31 else 8
+    return 4 * nnz + p * (n + 1) + 3 * s * n
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def flush_l2(torch, dev):
+    """Write a buffer larger than the 126 MB L2 between timed steps."""
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = flush_l2.buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+
+
+def cpu_reference(inst, seconds: float = 12.0, threads: int | None = None) -> dict:
+    """The CPU path (oracle port of the reference, fp64, all host threads) on
+    a bounded sample of the same workload: the first S pursuit iterations."""
+    import gn_oracle as O
+    from paper_2605_05330_b200 import GammaSchedule
+
+    threads = threads or O.default_threads()
+    tab = GammaSchedule.pursuit().table()
+    t0 = time.perf_counter()
+    O.run(inst.graph, inst.x0, tab[:2], 1.5, threads=threads)
+    per = max((time.perf_counter() - t0) / 2, 1e-6)
+    k = int(min(1000, max(2, seconds / per)))
+    t0 = time.perf_counter()
+    O.run(inst.graph, inst.x0, tab[:k], 1.5, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": inst.m * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {k} of the 1000 pursuit iterations of {inst.name} in fp64 "
+                      f"(oracle/gn_oracle.c, OpenMP row-parallel, bitwise the reference), {dt:.2f} s",
+            "iters": k, "seconds": dt}
+
+
+def ncu_traffic(config: str):
+    """DRAM bytes per loop-kernel launch from the committed ncu summary."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if f.exists():
+        try:
+            d = json.loads(f.read_text())
+            return d.get(config, {}).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    inst = make_instance(args.config, 0, args.scale)
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(inst, seconds=args.ref_seconds)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config + ": " + CONFIG_TEXT[args.config], "n": inst.n, "m": inst.m},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
+                         "sample": base["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--scale", type=int, default=20, help="R-MAT scale for C5")
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+
+    import paper_2605_05330_b200 as P
+    from paper_2605_05330_b200 import _engine as E
+
+    E.load_library()
+    if E.device_count() < 1:
+        raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    inst = make_instance(args.config, rank, args.scale)
+    g = inst.graph
+    dtype = inst.dtype
+    h = g.device_graph(dtype, local)
+    sched = P.GammaSchedule.pursuit(iterations=args.iters)
+    gam = np.ascontiguousarray(sched.table())
+    iters = len(gam)
+    x0_dev = torch.from_numpy(np.ascontiguousarray(inst.x0)).to(dev)
+    x_out = torch.empty(g.n, dtype=torch.float64, device=dev)
+    si = np.zeros(iters)
+    fb = np.zeros(iters, dtype=np.int64)
+    mass = np.zeros(iters)
+    ran = E.ctypes.c_int()
+    fail = E.ctypes.c_int()
+    flags = E.GN_DEVICE_IO
+
+    def device_step():
+        st = E.RunStats()
+        E.check(E.lib().gn_run(h.handle, E.ctypes.c_void_p(x0_dev.data_ptr()), E.ptr(gam), iters, 1.5, flags,
+                               E.ctypes.c_void_p(x_out.data_ptr()), E.ptr(si), E.ptr(fb), E.ptr(mass), None, None,
+                               None, E.ctypes.byref(ran), E.ctypes.byref(fail), E.ctypes.byref(st)))
+        return st
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        flush_l2(torch, dev)
+        device_step()
+    barrier()
+    launches0 = E.launch_count()
+    step_ms, loop_ms = [], []
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(torch, dev)
+            torch.cuda.synchronize()
+            st = device_step()
+            step_ms.append(st.total_ms)
+            loop_ms.append(st.loop_ms)
+    barrier()
+    wall = time.perf_counter() - wall0
+    launches = E.launch_count() - launches0
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    edges_all = inst.m * ws if args.config != "C4" else inst.m * ws
+    value = edges_all * iters * args.steps / (total_ms * 1e-3)
+
+    # ---- e2e through the public API: host x0 in, MIS out, every step
+    x0_host = torch.from_numpy(np.ascontiguousarray(inst.x0)).pin_memory().numpy()
+    e2e_t = []
+    h2d = d2h = 0
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        r = P.run_engine(g, x0_host, sched, dtype=dtype, device=local)
+        sol = P.round_to_mis(g, r.x)
+        barrier()
+        if i >= args.warmup:
+            e2e_t.append(time.perf_counter() - t0)
+            h2d = r.stats["h2d_bytes"] + 8 * g.n          # + the rounding's state upload
+            d2h = r.stats["d2h_bytes"] + g.n + 64         # + membership mask and flags
+    e2e_total = sum(e2e_t)
+    if ws > 1:
+        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = edges_all * iters * args.steps / e2e_total
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peaks = {}
+    pf = ROOT / "MEASURED_PEAKS.json"
+    if pf.exists():
+        peaks = json.loads(pf.read_text())
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    s_bytes = 8 if dtype == "fp64" else 4
+    b_iter = algorithmic_bytes(g.n, 2 * inst.m, s_bytes)
+    loop_avg = statistics.mean(loop_ms)
+    achieved = b_iter * iters / (loop_avg * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config)
+    info = h.info()
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(inst, seconds=args.ref_seconds)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if dtype == "fp64" else "f32-gather/f64-state",
+        "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
+        "config": {
+            "workload": args.config + ": " + CONFIG_TEXT[args.config],
+            "n": g.n, "m": inst.m, "iters": iters, "schedule": "pursuit 0.9->1.5",
+            "parallelism": f"replicas x{ws}" if args.config != "C4" else f"batch shard x{ws}",
+            "l2": "flushed between steps (256 MB write); the 1000 iterations inside a step re-read the graph",
+            "index_format": "uint16" if info["n"] <= 65536 else "int32",
+            "engine_dtype": dtype,
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "paper_2605_05330_b200.run_engine + round_to_mis (host numpy in, MIS out)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "gn::k_gn_loop (persistent, 1 launch = all iterations)",
+                     "bytes_per_launch": b_iter * iters, "b_iter": b_iter, "peak_source": peak_src,
+                     "loop_ms": loop_avg},
+        "cpu_baseline": cpu,
+        "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+        "gpu_launches": int(launches),
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

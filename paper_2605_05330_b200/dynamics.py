@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 from . import _engine as E
-from .graph import MisSolution, device_graph, dtype_code
+from .graph import MisSolution, any_device_graph, device_graph, dtype_code
 
 # dynamics.py:21-24
 SAFE_DIV_THRESHOLD = 1e-9
@@ -155,7 +155,7 @@ def is_normalizable(g, x) -> bool:
     """All closed neighborhood sums positive (dynamics.py:122-126)."""
     x = _as_state(g, x)
     ok = ctypes.c_int(0)
-    h = device_graph(g)
+    h = any_device_graph(g, _opt("device", None))
     E.check(E.lib().gn_is_normalizable(h.handle, E.ptr(x), ctypes.byref(ok)))
     return bool(ok.value)
 
@@ -271,7 +271,7 @@ def energy(g, x, gamma: float) -> float:
     """Quadratic energy (1/2) y'(I + gamma A)y - v'y (dynamics.py:210-219)."""
     x = _as_state(g, x)
     out = ctypes.c_double()
-    E.check(E.lib().gn_energy(device_graph(g).handle, E.ptr(x), float(gamma), ctypes.byref(out)))
+    E.check(E.lib().gn_energy(any_device_graph(g, _opt("device", None)).handle, E.ptr(x), float(gamma), ctypes.byref(out)))
     return out.value
 
 
@@ -279,7 +279,7 @@ def weighted_mass(g, x) -> float:
     """Relaxed objective sum(w_i x_i) (dynamics.py:222-224)."""
     x = _as_state(g, x)
     out = ctypes.c_double()
-    E.check(E.lib().gn_weighted_mass(device_graph(g).handle, E.ptr(x), ctypes.byref(out)))
+    E.check(E.lib().gn_weighted_mass(any_device_graph(g, _opt("device", None)).handle, E.ptr(x), ctypes.byref(out)))
     return out.value
 
 
@@ -287,7 +287,7 @@ def simplex_state(g, x) -> np.ndarray:
     """Mass-normalized coordinates p_i = w_i x_i / sum_j w_j x_j (dynamics.py:227-233)."""
     x = _as_state(g, x)
     p = np.empty(g.n, dtype=np.float64)
-    rc = E.lib().gn_simplex_state(device_graph(g).handle, E.ptr(x), E.ptr(p))
+    rc = E.lib().gn_simplex_state(any_device_graph(g, _opt("device", None)).handle, E.ptr(x), E.ptr(p))
     if rc == E.GN_ERR_ZERO_MASS:
         raise ValueError("weighted mass must be positive")
     E.check(rc)
@@ -300,7 +300,7 @@ def fitness(g, p, gamma: float) -> tuple[np.ndarray, float]:
     p = _as_state(g, p)
     f = np.empty(g.n, dtype=np.float64)
     fbar = ctypes.c_double()
-    rc = E.lib().gn_fitness(device_graph(g).handle, E.ptr(p), float(gamma), E.ptr(f), ctypes.byref(fbar))
+    rc = E.lib().gn_fitness(any_device_graph(g, _opt("device", None)).handle, E.ptr(p), float(gamma), E.ptr(f), ctypes.byref(fbar))
     if rc == E.GN_ERR_ZERO_DENOM:
         raise ValueError("zero denominator in fitness: state not normalizable")
     E.check(rc)
@@ -310,7 +310,8 @@ def fitness(g, p, gamma: float) -> tuple[np.ndarray, float]:
 def round_result(g, x, *, dtype=None, device=None) -> tuple[np.ndarray, float, bool, bool]:
     """Device rounding: (0/1 mask, weight, independent, maximal)."""
     x = _as_state(g, x)
-    h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
+    dev = _opt("device", device)
+    h = device_graph(g, dtype, dev) if dtype is not None else any_device_graph(g, dev)
     sel = np.zeros(max(g.n, 1), dtype=np.uint8)
     weight = ctypes.c_double()
     ind = ctypes.c_int()

@@ -144,6 +144,22 @@ def device_graph(g, dtype=None, device: int = 0) -> E.GraphHandle:
         return h
 
 
+def any_device_graph(g, device: int = 0) -> E.GraphHandle:
+    """An existing handle of g on `device` whatever its dtype (the rounding,
+    checks and fp64 helpers only use the dtype-independent original CSR and
+    fp64 weights), else a new fp64 one."""
+    if isinstance(g, WeightedGraph):
+        for (dt, dev), h in list(g._handles.items()):
+            if dev == device:
+                return h
+        return g.device_graph(None, device)
+    with _FOREIGN_LOCK:
+        for (gid, dt, dev), (obj, h) in list(_FOREIGN_CACHE.items()):
+            if obj is g and dev == device:
+                return h
+    return device_graph(g, None, device)
+
+
 class DeviceAdjacency:
     """Stand-in for the reference's scipy adjacency (graph.py:55-57): only the
     mat-vec the dynamics and tests use, executed by the engine."""
@@ -158,7 +174,7 @@ class DeviceAdjacency:
         if y.shape != (self._g.n,):
             raise ValueError(f"dimension mismatch: {y.shape} vs {self.shape}")
         out = np.empty(self._g.n, dtype=np.float64)
-        h = device_graph(self._g)
+        h = any_device_graph(self._g)
         E.check(E.lib().gn_spmv(h.handle, E.ptr(y), E.ptr(out)))
         return out
 
@@ -254,7 +270,7 @@ def _member_report(g, idx: np.ndarray) -> tuple[float, bool, bool]:
     ind = E.ctypes.c_int()
     mx = E.ctypes.c_int()
     cnt = E.ctypes.c_int64()
-    h = device_graph(g)
+    h = any_device_graph(g)
     E.check(E.lib().gn_check_members(h.handle, E.ptr(mask), E.ctypes.byref(weight), E.ctypes.byref(ind),
                                      E.ctypes.byref(mx), E.ctypes.byref(cnt)))
     return weight.value, bool(ind.value), bool(mx.value)
