@@ -321,6 +321,7 @@ __global__ void k_init_state_weights(int64_t n, const double* __restrict__ w64, 
 
 static void free_graph(gn_graph* g) {
     if (!g) return;
+    release_plans(g);
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);

@@ -15,11 +15,9 @@ namespace gn {
 constexpr double kSafeDiv = 1e-9;
 constexpr double kFallback = 0.5;
 
-constexpr int kLoopThreads = 512;  // persistent streaming kernel block
-constexpr int kLoopWarps = kLoopThreads / 32;
 constexpr int kSlice = 32;         // SELL slice height (one row per lane)
 constexpr int kSigma = 4096;       // degree-sort window of the relabeling
-constexpr int kHubDegree = 4096;   // rows above this are processed CTA-wide
+constexpr int kHubDegree = 512;    // rows above this are processed CTA-wide
 constexpr int kSplitLen = 64;      // slices at least this long are split over warps
 
 // ---------------------------------------------------------------- errors
@@ -148,5 +146,6 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
 }
 
 int coresident_blocks(const void* kernel, int threads, size_t smem, int device, int* out);
+void release_plans(const gn_graph* g);  // gn_loop.cu: cached launch plans of g
 
 }  // namespace gn

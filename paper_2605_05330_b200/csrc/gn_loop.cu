@@ -11,41 +11,57 @@
 //   d_r  = y_r + gamma_k * s_r           separately rounded, no FMA
 //   x'_r = d_r > 1e-9 ? y_r / d_r : 0.5  counted fallback
 //   yg'_r = v_r * x'_r                   published for step k+1
-// fused with the per-iteration reductions: max|x'-x| (atomicMax on the IEEE
-// bits of a non-negative double -- order-free, hence deterministic), the
-// fallback count, the first non-finite iteration, and fixed-order fp64 block
-// partials of w.x' (the objective) and, in trace mode, y.y, y.s, w.x (the
-// energy terms of the pre-step state).  Block partials go to a ring that all
-// blocks fold cooperatively every 1024 iterations, off the per-step path.
+// fused with the per-iteration reductions: max|x'-x|, the fallback count,
+// the non-finite flag and fixed-order fp64 block partials of w.x' (the
+// objective) and, in trace mode, y.y, y.s, w.x (the energy terms of the
+// pre-step state).  Block stats go to a ring (plain stores, no atomics) that
+// all blocks fold cooperatively every kRing iterations.
 //
-// Row work, per iteration:
-//   hub rows (degree > kHubDegree)  one CTA per row (EXACT: one thread per row)
-//   long slices (length >= 64)      the CTA's 16 warps split the positions of a
-//                                   slice; partials folded in warp order
-//   other slices                    one warp per slice, one thread per row,
-//                                   sequential sum = scipy's order (bitwise)
-// A grid barrier separates iterations.
+// Work, decided once per (graph, grid, mode) on the host (build_plan):
+//   CTA items   long slices (the 32 warps split the slice's blocks) and hub
+//               rows (the 32 warps split the row); per-warp partials meet in
+//               shared memory and are folded in warp order
+//   warp items  short slices: one warp per slice, one thread per row,
+//               sequential sum in the reference's order (bitwise)
+// balanced longest-processing-time-first over CTAs and warps.  The index
+// blocks of as many items as fit stay resident in shared memory for the whole
+// run; the rest stream from global memory every iteration.  A grid barrier
+// separates iterations.
 #include <cuda_runtime.h>
 #include <math.h>
 
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <queue>
 #include <vector>
 
 #include "gn_internal.cuh"
 
 namespace gn {
 
-constexpr int kRing = 1024;     // iterations of block partials kept before a fold
-constexpr int kSplitSlots = 8;  // long slices buffered per CTA between syncs
-constexpr int kRingW = 8;       // per block: 4 dot terms, max|dx|, fallbacks, non-finite flag, pad
+constexpr int kThreads = 1024;  // one CTA per SM
+constexpr int kWarps = kThreads / 32;
+constexpr int kSlots = 4;       // CTA items per phase (shared-memory partial slots)
+constexpr int kRing = 1024;     // iterations of block stats kept before a fold
+constexpr int kRingW = 8;       // per block: 4 dot terms, max|dx|, fallbacks, non-finite, pad
+
+enum ItemKind : int32_t { kSplit = 0, kHub = 1, kWhole = 2, kHubSeq = 3 };
+
+// One unit of work.  id: slice (kSplit/kWhole) or first hub row (kHub,
+// kHubSeq); len: blocks (slices) or degree (hub) or row count (kHubSeq);
+// smem: offset of the resident index blocks in 16-byte words, -1 = global.
+struct Item {
+    int32_t id, len, smem, kind;
+};
 
 template <typename TS, typename TG>
 struct LoopArgs {
     int64_t n;
-    int32_t nhub, nslices, nsplit;
-    int exact;
+    int32_t nhub;
     const int32_t* __restrict__ hub_ptr;
     const int32_t* __restrict__ hub_col;
     const int64_t* __restrict__ slice_ptr;
@@ -55,6 +71,11 @@ struct LoopArgs {
     const TS* __restrict__ w;
     TS* x[2];
     TG* yg[2];
+    const int32_t* __restrict__ cta_ptr;   // [G+1] into items (CTA items)
+    const int32_t* __restrict__ warp_ptr;  // [G*kWarps+1] into items (warp items)
+    const Item* __restrict__ items;
+    const int32_t* __restrict__ smem_words;  // [G] resident 16-byte words per CTA
+    int smem_resident_off;                   // byte offset of the resident area
     const double* __restrict__ gammas;
     int iters;
     double final_gamma;
@@ -64,18 +85,10 @@ struct LoopArgs {
     int* bad;          // [iters]   1 if a non-finite state appeared
     int* status;       // [0] iterations run
     double* dots;      // [(iters+1)][4]: y.y, y.s, w.x (pre), w.x' (post)
-    double* ring;      // [kRing][grid][kRingW] per-block partials
+    double* ring;      // [kRing][grid][kRingW]
     unsigned int* barrier;
-    double* x_hist;                 // optional [iters][n], original order
+    double* x_hist;    // optional [iters][n], original order
     const int32_t* __restrict__ perm;
-};
-
-struct LoopArgs_common {
-    int iters;
-    double* step_inf;
-    double* fb;
-    int* bad;
-    double* dots;
 };
 
 struct Stats {
@@ -88,15 +101,27 @@ struct Stats {
 template <typename T>
 __device__ __forceinline__ T tabs(T v) { return v < T(0) ? -v : v; }
 
+// Per-row state, fetched before the row's neighbour sum so its latency hides
+// under the gathers.
+template <typename TS>
+struct RowIn {
+    TS x, v;
+    double w;
+};
+
+template <typename TS, typename TG>
+__device__ __forceinline__ RowIn<TS> row_in(const LoopArgs<TS, TG>& a, int r, int cur) {
+    return RowIn<TS>{a.x[cur][r], __ldg(a.v + r), (double)__ldg(a.w + r)};
+}
+
 // The elementwise half of _step for row r (new id) whose neighbour sum is s.
 template <typename TS, typename TG, bool TRACE>
-__device__ __forceinline__ void update_row(const LoopArgs<TS, TG>& a, int r, TS s, int cur, TS g, int k,
-                                           bool tail, Stats& st) {
+__device__ __forceinline__ void update_row(const LoopArgs<TS, TG>& a, int r, TS s, const RowIn<TS>& in, int cur,
+                                           TS g, int k, bool tail, Stats& st) {
     using A = Arith<TS>;
-    const TS xi = a.x[cur][r];
-    const TS vi = __ldg(a.v + r);
+    const TS xi = in.x, vi = in.v;
+    const double wi = in.w;
     const TS yi = A::mul(vi, xi);                    // dynamics.py:104
-    const double wi = (double)__ldg(a.w + r);
     if (TRACE) {
         st.acc[0] = __dadd_rn(st.acc[0], __dmul_rn((double)yi, (double)yi));
         st.acc[1] = __dadd_rn(st.acc[1], __dmul_rn((double)yi, (double)s));
@@ -121,7 +146,7 @@ template <typename TI>
 struct LaneVec;
 template <>
 struct LaneVec<uint16_t> {
-    static constexpr int B = 8;  // positions per 16-byte vector
+    static constexpr int B = 8;
     __device__ static __forceinline__ int get(const uint4& v, int t) {
         const unsigned w = t < 4 ? (t < 2 ? v.x : v.y) : (t < 6 ? v.z : v.w);
         return (int)((t & 1) ? (w >> 16) : (w & 0xffffu));
@@ -135,33 +160,39 @@ struct LaneVec<int32_t> {
     }
 };
 
+template <bool SMEM>
+__device__ __forceinline__ uint4 load_vec(const uint4* p) {
+    if (SMEM) return *p;
+    return __ldg(p);
+}
+
 // Sequential sum over blocks [bb, be) of one slice row (this lane), masked by
 // the row's degree d.  A batch issues NB vector loads and NB*B gathers before
-// any add; the adds stay in position order (the reference's order).
-template <typename TS, typename TG, typename TI>
-__device__ __forceinline__ TS sum_blocks(const TI* __restrict__ slice, const TG* __restrict__ yg, int lane, int d,
+// any add; the adds stay in position order (the reference's order).  Blocks
+// that lie entirely inside the row skip the mask.
+template <typename TS, typename TG, typename TI, bool SMEM>
+__device__ __forceinline__ TS sum_blocks(const uint4* __restrict__ base, const TG* __restrict__ yg, int d,
                                          int bb, int be) {
     using A = Arith<TS>;
     using V = LaneVec<TI>;
-    // 16 four-byte (8 eight-byte) gathers in flight per lane per batch
-    constexpr int B = V::B, NB = (sizeof(TG) == 4 ? 16 : 8) / B > 0 ? (sizeof(TG) == 4 ? 16 : 8) / B : 1;
-    const uint4* __restrict__ base = reinterpret_cast<const uint4*>(slice) + lane;
+    constexpr int B = V::B;
+    constexpr int NB = (sizeof(TG) == 4 ? 16 : 8) / B > 0 ? (sizeof(TG) == 4 ? 16 : 8) / B : 1;
     TS s = TS(0);
     int b = bb;
-    for (; b + NB <= be; b += NB) {
+    for (; b + NB <= be && (b + NB) * B <= d; b += NB) {
         uint4 v[NB];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) v[u] = __ldg(base + (size_t)(b + u) * kSlice);
+        for (int u = 0; u < NB; ++u) v[u] = load_vec<SMEM>(base + (size_t)(b + u) * kSlice);
         TG y[NB * B];
 #pragma unroll
         for (int u = 0; u < NB; ++u)
 #pragma unroll
-            for (int t = 0; t < B; ++t) y[u * B + t] = ((b + u) * B + t < d) ? yg[V::get(v[u], t)] : TG(0);
+            for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(v[u], t)];
 #pragma unroll
         for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
     }
-    for (; b < be; ++b) {
-        const uint4 v = __ldg(base + (size_t)b * kSlice);
+    for (; b < be && b * B < d; ++b) {
+        const uint4 v = load_vec<SMEM>(base + (size_t)b * kSlice);
         TG y[B];
 #pragma unroll
         for (int t = 0; t < B; ++t) y[t] = (b * B + t < d) ? yg[V::get(v, t)] : TG(0);
@@ -171,82 +202,12 @@ __device__ __forceinline__ TS sum_blocks(const TI* __restrict__ slice, const TG*
     return s;
 }
 
-template <typename TS, typename TG, typename TI, bool TRACE>
-__device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_part, TS* s_hub) {
-    using A = Arith<TS>;
-    const int cur = k & 1;
-    const TG* __restrict__ yg = a.yg[cur];
-    const TS g = tail ? TS(0) : (TS)a.gammas[k];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = gridDim.x;
-    const TI* __restrict__ sell = (const TI*)a.sell;
-
-    // ---- hub rows
-    if (!a.exact) {
-        for (int h = blockIdx.x; h < a.nhub; h += G) {
-            const int beg = __ldg(a.hub_ptr + h), end = __ldg(a.hub_ptr + h + 1);
-            TS s = TS(0);
-            for (int p = beg + threadIdx.x; p < end; p += blockDim.x) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-            if (lane == 0) s_hub[warp] = s;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                TS tot = TS(0);
-                for (int q = 0; q < kLoopWarps; ++q) tot = A::add(tot, s_hub[q]);
-                update_row<TS, TG, TRACE>(a, h, tot, cur, g, k, tail, st);
-            }
-            __syncthreads();
-        }
-    } else {
-        for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < a.nhub; h += G * blockDim.x) {
-            TS s = TS(0);
-            for (int p = __ldg(a.hub_ptr + h); p < __ldg(a.hub_ptr + h + 1); ++p)
-                s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
-            update_row<TS, TG, TRACE>(a, h, s, cur, g, k, tail, st);
-        }
-    }
-
-    // ---- long slices, warps split the positions
-    // slices are sorted longest first; round q deals them out in zigzag order
-    // (b, 2G-1-b, 2G+b, ...) so every CTA gets a similar total length
-    const int nsplit = a.exact ? 0 : a.nsplit;
-    auto split_of = [&](int q) { return q * G + ((q & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x); };
-    int nq = 0;
-    while (split_of(nq) < nsplit) ++nq;
-    for (int q0 = 0; q0 < nq; q0 += kSplitSlots) {
-        const int qn = min(kSplitSlots, nq - q0);
-        for (int q = 0; q < qn; ++q) {
-            const int s = split_of(q0 + q);
-            const int64_t base = __ldg(a.slice_ptr + s);
-            const int nblk = (int)((__ldg(a.slice_ptr + s + 1) - base) / (kSlice * LaneVec<TI>::B));
-            const int d = __ldg(a.row_deg + s * kSlice + lane);
-            const int bb = nblk * warp / kLoopWarps, be = nblk * (warp + 1) / kLoopWarps;
-            s_part[(q * kLoopWarps + warp) * kSlice + lane] = sum_blocks<TS, TG, TI>(sell + base, yg, lane, d, bb, be);
-        }
-        __syncthreads();
-        for (int q = warp; q < qn; q += kLoopWarps) {
-            const int s = split_of(q0 + q);
-            TS tot = TS(0);
-#pragma unroll 4
-            for (int w = 0; w < kLoopWarps; ++w) tot = A::add(tot, s_part[(q * kLoopWarps + w) * kSlice + lane]);
-            update_row<TS, TG, TRACE>(a, a.nhub + s * kSlice + lane, tot, cur, g, k, tail, st);
-        }
-        __syncthreads();
-    }
-
-    // ---- remaining slices: one warp per slice, one thread per row
-    const int first = nsplit;
-    const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
-    for (int s = first + gw; s < a.nslices; s += nw) {
-        const int64_t base = __ldg(a.slice_ptr + s);
-        const int nblk = (int)((__ldg(a.slice_ptr + s + 1) - base) / (kSlice * LaneVec<TI>::B));
-        const int64_t r = (int64_t)a.nhub + (int64_t)s * kSlice + lane;
-        const bool valid = r < a.n;
-        const int d = valid ? __ldg(a.row_deg + (size_t)s * kSlice + lane) : 0;
-        const TS sum = sum_blocks<TS, TG, TI>(sell + base, yg, lane, d, 0, nblk);
-        if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, cur, g, k, tail, st);
-    }
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ TS slice_sum(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
+                                        const TG* __restrict__ yg, int lane, int d, int bb, int be) {
+    if (it.smem >= 0) return sum_blocks<TS, TG, TI, true>(s_res + it.smem + lane, yg, d, bb, be);
+    const uint4* g = reinterpret_cast<const uint4*>((const TI*)a.sell + __ldg(a.slice_ptr + it.id)) + lane;
+    return sum_blocks<TS, TG, TI, false>(g, yg, d, bb, be);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -255,14 +216,102 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = Arith<T>::add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// One pass over this CTA's items.
+template <typename TS, typename TG, typename TI, bool TRACE>
+__device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_part, const uint4* s_res) {
+    using A = Arith<TS>;
+    const int cur = k & 1;
+    const TG* __restrict__ yg = a.yg[cur];
+    const TS g = tail ? TS(0) : (TS)a.gammas[k];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c0 = __ldg(a.cta_ptr + blockIdx.x), c1 = __ldg(a.cta_ptr + blockIdx.x + 1);
+    const int gw = blockIdx.x * kWarps + warp;
+    const int w0 = __ldg(a.warp_ptr + gw), w1 = __ldg(a.warp_ptr + gw + 1);
+    bool warp_done = false;
+    // CTA items in phases of kSlots; the warp items run inside the first
+    // phase, between the partial sums and the barrier that publishes them
+    for (int p0 = c0;; p0 += kSlots) {
+        const int pn = min(kSlots, c1 - p0);
+        for (int q = 0; q < pn; ++q) {
+            const Item it = a.items[p0 + q];
+            if (it.kind == kSplit) {
+                const int d = __ldg(a.row_deg + it.id * kSlice + lane);
+                const int bb = it.len * warp / kWarps, be = it.len * (warp + 1) / kWarps;
+                s_part[(q * kWarps + warp) * kSlice + lane] = slice_sum<TS, TG, TI>(a, it, s_res, yg, lane, d, bb, be);
+            } else {  // kHub: warp w sums elements [w*deg/W, (w+1)*deg/W) of the row
+                const int beg = __ldg(a.hub_ptr + it.id);
+                const int eb = beg + (int)((int64_t)it.len * warp / kWarps);
+                const int ee = beg + (int)((int64_t)it.len * (warp + 1) / kWarps);
+                TS s = TS(0);
+                for (int p = eb + lane; p < ee; p += 32) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+                s = warp_sum(s);
+                if (lane == 0) s_part[(q * kWarps + warp) * kSlice] = s;
+            }
+        }
+        if (!warp_done) {
+            warp_done = true;
+            for (int i = w0; i < w1; ++i) {
+                const Item it = a.items[i];
+                if (it.kind == kWhole) {
+                    const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + lane;
+                    const bool valid = r < a.n;
+                    RowIn<TS> in{};
+                    int d = 0;
+                    if (valid) {
+                        d = __ldg(a.row_deg + (size_t)it.id * kSlice + lane);
+                        in = row_in(a, (int)r, cur);
+                    }
+                    const TS sum = slice_sum<TS, TG, TI>(a, it, s_res, yg, lane, d, 0, it.len);
+                    if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, in, cur, g, k, tail, st);
+                } else {  // kHubSeq (EXACT): one thread per hub row, sequential
+                    if (lane < it.len) {
+                        const int h = it.id + lane;
+                        const RowIn<TS> in = row_in(a, h, cur);
+                        TS s = TS(0);
+                        for (int p = __ldg(a.hub_ptr + h); p < __ldg(a.hub_ptr + h + 1); ++p)
+                            s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+                        update_row<TS, TG, TRACE>(a, h, s, in, cur, g, k, tail, st);
+                    }
+                }
+            }
+        }
+        if (pn <= 0) break;
+        __syncthreads();
+        for (int q = warp; q < pn; q += kWarps) {
+            const Item it = a.items[p0 + q];
+            if (it.kind == kSplit) {
+                const int r = a.nhub + it.id * kSlice + lane;
+                const RowIn<TS> in = row_in(a, r, cur);
+                TS tot = TS(0);
+#pragma unroll 8
+                for (int w = 0; w < kWarps; ++w) tot = A::add(tot, s_part[(q * kWarps + w) * kSlice + lane]);
+                update_row<TS, TG, TRACE>(a, r, tot, in, cur, g, k, tail, st);
+            } else if (lane == 0) {
+                const RowIn<TS> in = row_in(a, it.id, cur);
+                TS tot = TS(0);
+                for (int w = 0; w < kWarps; ++w) tot = A::add(tot, s_part[(q * kWarps + w) * kSlice]);
+                update_row<TS, TG, TRACE>(a, it.id, tot, in, cur, g, k, tail, st);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Block-level fold of the per-thread stats; thread 0 stores them (plain
 // stores, no atomics) in this iteration's ring slot.
 template <bool TRACE>
 __device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
-    __shared__ double s_acc[kLoopWarps][4];
-    __shared__ double s_mx[kLoopWarps];
-    __shared__ unsigned int s_fb[kLoopWarps];
-    __shared__ int s_bad[kLoopWarps];
+    __shared__ double s_acc[kWarps][4];
+    __shared__ double s_mx[kWarps];
+    __shared__ unsigned int s_fb[kWarps];
+    __shared__ int s_bad[kWarps];
     Stats st = st0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -286,7 +335,7 @@ __device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
         double mx = 0.0, acc[4] = {0.0, 0.0, 0.0, 0.0};
         unsigned int f = 0;
         int bad = 0;
-        for (int q = 0; q < kLoopWarps; ++q) {
+        for (int q = 0; q < kWarps; ++q) {
             if (!(s_mx[q] <= mx)) mx = s_mx[q];
             f += s_fb[q];
             bad |= s_bad[q];
@@ -302,12 +351,19 @@ __device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
     }
 }
 
+struct FoldOut {
+    int iters;
+    double* step_inf;
+    double* fb;
+    int* bad;
+    double* dots;
+};
+
 // All blocks: fold ring slots [0, count) (iterations k0..k0+count-1), one
-// warp per (slot, quantity), block order fixed.  max|dx| and the non-finite
-// flag are order-free; the sums follow a fixed tree.
-__device__ void fold_ring(const double* ring, int count, int k0, const LoopArgs_common& o) {
+// warp per (slot, quantity), block order fixed.
+__device__ void fold_ring(const double* ring, int count, int k0, const FoldOut& o) {
     const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = gridDim.x * kLoopWarps;
+    const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
     const int G = gridDim.x;
     for (int t = gw; t < count * 7; t += nw) {
         const int slot = t / 7, c = t % 7;
@@ -324,9 +380,9 @@ __device__ void fold_ring(const double* ring, int count, int k0, const LoopArgs_
                 const double v = __shfl_xor_sync(0xffffffffu, m, off);
                 if (!(v <= m)) m = v;
             }
-            if (lane == 0) {
-                if (c == 4) { if (k < o.iters) o.step_inf[k] = m; }
-                else if (k < o.iters) o.bad[k] = m != 0.0 ? 1 : 0;
+            if (lane == 0 && k < o.iters) {
+                if (c == 4) o.step_inf[k] = m;
+                else o.bad[k] = m != 0.0 ? 1 : 0;
             }
         } else {
             double s = 0.0;
@@ -340,7 +396,7 @@ __device__ void fold_ring(const double* ring, int count, int k0, const LoopArgs_
     }
 }
 
-// Every block computes max|dx| of iteration k from the ring (early exit).
+// Every block computes max|dx| of one iteration from the ring (early exit).
 __device__ double ring_step_inf(const double* ring_slot) {
     __shared__ double s_m;
     if (threadIdx.x < 32) {
@@ -361,17 +417,35 @@ __device__ double ring_step_inf(const double* ring_slot) {
 }
 
 template <typename TS, typename TG, typename TI, bool TRACE>
-__global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
-    extern __shared__ unsigned char smem_raw[];
+__global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     TS* s_part = (TS*)smem_raw;
-    __shared__ TS s_hub[kLoopWarps];
-    const LoopArgs_common oc{a.iters, a.step_inf, a.fb, a.bad, a.dots};
+    uint4* s_res = (uint4*)(smem_raw + a.smem_resident_off);
+    // resident index blocks: copied once, used every iteration
+    {
+        const int nwords = __ldg(a.smem_words + blockIdx.x);
+        if (nwords > 0) {
+            const int c0 = a.cta_ptr[blockIdx.x], c1 = a.cta_ptr[blockIdx.x + 1];
+            const int w0 = a.warp_ptr[blockIdx.x * kWarps], w1 = a.warp_ptr[(blockIdx.x + 1) * kWarps];
+            for (int part = 0; part < 2; ++part) {
+                const int i0 = part ? w0 : c0, i1 = part ? w1 : c1;
+                for (int i = i0; i < i1; ++i) {
+                    const Item it = a.items[i];
+                    if (it.smem < 0 || (it.kind != kSplit && it.kind != kWhole)) continue;
+                    const uint4* src = reinterpret_cast<const uint4*>((const TI*)a.sell + a.slice_ptr[it.id]);
+                    for (int t = threadIdx.x; t < it.len * kSlice; t += blockDim.x) s_res[it.smem + t] = __ldg(src + t);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const FoldOut fo{a.iters, a.step_inf, a.fb, a.bad, a.dots};
     unsigned int bar = 0;
     int ran = 0, k0 = 0;
     const size_t ring_stride = (size_t)gridDim.x * kRingW;
     for (int k = 0; k < a.iters; ++k) {
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE>(a, k, false, st, s_part, s_hub);
+        pass<TS, TG, TI, TRACE>(a, k, false, st, s_part, s_res);
         double* slot = a.ring + (size_t)(k - k0) * ring_stride;
         publish<TRACE>(st, slot);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
@@ -381,7 +455,7 @@ __global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
             stop = ring_step_inf(slot) < 1e-12;
         const bool last = stop || ran == a.iters;
         if (ran - k0 == kRing || (last && !TRACE)) {
-            fold_ring(a.ring, ran - k0, k0, oc);
+            fold_ring(a.ring, ran - k0, k0, fo);
             grid_barrier(a.barrier, (++bar) * gridDim.x);
             k0 = ran;
         }
@@ -390,10 +464,10 @@ __global__ void __launch_bounds__(kLoopThreads) k_gn_loop(LoopArgs<TS, TG> a) {
     if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_part, s_hub);
+        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_part, s_res);
         publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
-        fold_ring(a.ring, ran - k0 + 1, k0, oc);
+        fold_ring(a.ring, ran - k0 + 1, k0, fo);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.status[0] = ran;
 }
@@ -436,6 +510,195 @@ __global__ void k_finalize(int64_t n, const TS* __restrict__ x, const int32_t* _
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + 255) / 256); }
 
+// ------------------------------------------------------------------ plan
+
+// Device plan for one (graph, grid, mode); built on first use and cached
+// (graphs are immutable).
+struct DevicePlan {
+    int grid = 0;
+    int32_t* cta_ptr = nullptr;
+    int32_t* warp_ptr = nullptr;
+    Item* items = nullptr;
+    int32_t* smem_words = nullptr;
+    size_t smem_bytes = 0;  // dynamic shared memory per CTA
+    int resident_off = 0;
+    int64_t resident_words = 0;
+};
+
+struct PlanCache {
+    std::mutex mu;
+    std::map<std::pair<int, int>, DevicePlan> plans;  // (grid, exact) -> plan
+};
+
+static std::mutex g_cache_mu;
+static std::map<const gn_graph*, PlanCache*> g_cache;
+
+void release_plans(const gn_graph* g) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(g);
+    if (it == g_cache.end()) return;
+    for (auto& kv : it->second->plans) {
+        cudaFree(kv.second.cta_ptr);
+        cudaFree(kv.second.warp_ptr);
+        cudaFree(kv.second.items);
+        cudaFree(kv.second.smem_words);
+    }
+    delete it->second;
+    g_cache.erase(it);
+}
+
+// Longest-processing-time-first: CTA items over CTAs, then warp items over
+// all warps (a CTA's share of its CTA items preloads each of its warps).
+static void build_plan(const gn_graph* g, int G, bool exact, size_t part_bytes, size_t smem_cap,
+                       std::vector<int32_t>& cta_ptr, std::vector<int32_t>& warp_ptr, std::vector<Item>& items,
+                       std::vector<int32_t>& smem_words) {
+    const int B = g->idx16 ? 8 : 4;
+    std::vector<int64_t> sp((size_t)g->nslices + 1);
+    cudaMemcpy(sp.data(), g->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
+    std::vector<int32_t> hp((size_t)g->nhub + 1);
+    cudaMemcpy(hp.data(), g->hub_ptr, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost);
+    auto nblk = [&](int s) { return (int32_t)((sp[(size_t)s + 1] - sp[(size_t)s]) / (kSlice * B)); };
+
+    // cost unit ~ one 16-byte block per lane; the fixed term stands for the
+    // per-item round trips
+    const double kFixed = 6.0;
+    std::vector<std::vector<Item>> cta_items((size_t)G);
+    std::vector<double> cta_load((size_t)G, 0.0);
+    std::vector<Item> citems, witems;
+    if (!exact) {
+        for (int h = 0; h < g->nhub; ++h) citems.push_back(Item{h, hp[(size_t)h + 1] - hp[(size_t)h], -1, kHub});
+        for (int s = 0; s < g->nsplit; ++s) citems.push_back(Item{s, nblk(s), -1, kSplit});
+        for (int s = g->nsplit; s < g->nslices; ++s) witems.push_back(Item{s, nblk(s), -1, kWhole});
+    } else {
+        for (int h = 0; h < g->nhub; h += 32) witems.push_back(Item{h, std::min(32, g->nhub - h), -1, kHubSeq});
+        for (int s = 0; s < g->nslices; ++s) witems.push_back(Item{s, nblk(s), -1, kWhole});
+    }
+    auto ccost = [&](const Item& it) {
+        return it.kind == kHub ? kFixed + it.len / (32.0 * kWarps) * 4.0 : kFixed + (double)it.len / kWarps;
+    };
+    auto wcost = [&](const Item& it) {
+        if (it.kind == kHubSeq) {
+            int mx = 0;
+            for (int h = it.id; h < it.id + it.len; ++h) mx = std::max(mx, hp[(size_t)h + 1] - hp[(size_t)h]);
+            return kFixed + mx;
+        }
+        return kFixed + (double)it.len;
+    };
+    using E = std::pair<double, int>;
+    std::stable_sort(citems.begin(), citems.end(), [&](const Item& x, const Item& y) { return ccost(x) > ccost(y); });
+    {
+        std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+        for (int b = 0; b < G; ++b) pq.push({0.0, b});
+        for (const Item& it : citems) {
+            E e = pq.top();
+            pq.pop();
+            cta_items[(size_t)e.second].push_back(it);
+            e.first += ccost(it);
+            cta_load[(size_t)e.second] = e.first;
+            pq.push(e);
+        }
+    }
+    const int W = G * kWarps;
+    std::vector<std::vector<Item>> warp_items((size_t)W);
+    std::stable_sort(witems.begin(), witems.end(), [&](const Item& x, const Item& y) { return wcost(x) > wcost(y); });
+    {
+        std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+        for (int w = 0; w < W; ++w) pq.push({cta_load[(size_t)(w / kWarps)], w});
+        for (const Item& it : witems) {
+            E e = pq.top();
+            pq.pop();
+            warp_items[(size_t)e.second].push_back(it);
+            e.first += wcost(it);
+            pq.push(e);
+        }
+    }
+    // each warp's slices in ascending order (locality of the x / yg rows)
+    for (auto& v : warp_items)
+        std::sort(v.begin(), v.end(), [](const Item& x, const Item& y) { return x.id < y.id; });
+    // shared-memory residency of index blocks, per CTA, within smem_cap
+    smem_words.assign((size_t)G, 0);
+    items.clear();
+    cta_ptr.assign((size_t)G + 1, 0);
+    warp_ptr.assign((size_t)W + 1, 0);
+    const size_t cap_words = smem_cap > part_bytes ? (smem_cap - part_bytes) / 16 : 0;
+    for (int b = 0; b < G; ++b) {
+        size_t used = 0;
+        auto place = [&](Item& it) {
+            if (it.kind != kSplit && it.kind != kWhole) return;
+            const size_t words = (size_t)it.len * kSlice;
+            if (used + words <= cap_words) {
+                it.smem = (int32_t)used;
+                used += words;
+            }
+        };
+        for (Item& it : cta_items[(size_t)b]) place(it);
+        // warp items breadth-first over the CTA's warps so every warp gets some
+        for (size_t depth = 0;; ++depth) {
+            bool any = false;
+            for (int w = 0; w < kWarps; ++w) {
+                auto& v = warp_items[(size_t)b * kWarps + w];
+                if (depth < v.size()) {
+                    any = true;
+                    place(v[depth]);
+                }
+            }
+            if (!any) break;
+        }
+        smem_words[(size_t)b] = (int32_t)used;
+    }
+    for (int b = 0; b < G; ++b) {
+        cta_ptr[(size_t)b] = (int32_t)items.size();
+        items.insert(items.end(), cta_items[(size_t)b].begin(), cta_items[(size_t)b].end());
+    }
+    cta_ptr[(size_t)G] = (int32_t)items.size();
+    for (int w = 0; w < W; ++w) {
+        warp_ptr[(size_t)w] = (int32_t)items.size();
+        items.insert(items.end(), warp_items[(size_t)w].begin(), warp_items[(size_t)w].end());
+    }
+    warp_ptr[(size_t)W] = (int32_t)items.size();
+}
+
+static int get_plan(gn_graph* g, int G, bool exact, size_t part_bytes, size_t smem_cap, const DevicePlan** out) {
+    PlanCache* pc;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto& slot = g_cache[g];
+        if (!slot) slot = new PlanCache();
+        pc = slot;
+    }
+    std::lock_guard<std::mutex> lk(pc->mu);
+    auto key = std::make_pair(G, exact ? 1 : 0);
+    auto it = pc->plans.find(key);
+    if (it != pc->plans.end()) {
+        *out = &it->second;
+        return GN_OK;
+    }
+    std::vector<int32_t> cta_ptr, warp_ptr, smem_words;
+    std::vector<Item> items;
+    build_plan(g, G, exact, part_bytes, smem_cap, cta_ptr, warp_ptr, items, smem_words);
+    DevicePlan p;
+    p.grid = G;
+    GN_CUDA(cudaMalloc(&p.cta_ptr, sizeof(int32_t) * cta_ptr.size()));
+    GN_CUDA(cudaMalloc(&p.warp_ptr, sizeof(int32_t) * warp_ptr.size()));
+    GN_CUDA(cudaMalloc(&p.items, sizeof(Item) * std::max<size_t>(items.size(), 1)));
+    GN_CUDA(cudaMalloc(&p.smem_words, sizeof(int32_t) * smem_words.size()));
+    GN_CUDA(cudaMemcpy(p.cta_ptr, cta_ptr.data(), sizeof(int32_t) * cta_ptr.size(), cudaMemcpyHostToDevice));
+    GN_CUDA(cudaMemcpy(p.warp_ptr, warp_ptr.data(), sizeof(int32_t) * warp_ptr.size(), cudaMemcpyHostToDevice));
+    if (!items.empty())
+        GN_CUDA(cudaMemcpy(p.items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+    GN_CUDA(cudaMemcpy(p.smem_words, smem_words.data(), sizeof(int32_t) * smem_words.size(), cudaMemcpyHostToDevice));
+    int32_t mx = 0;
+    for (int32_t wds : smem_words) {
+        mx = std::max(mx, wds);
+        p.resident_words += wds;
+    }
+    p.resident_off = (int)((part_bytes + 15) / 16 * 16);
+    p.smem_bytes = (size_t)p.resident_off + (size_t)mx * 16;
+    auto res = pc->plans.emplace(key, p);
+    *out = &res.first->second;
+    return GN_OK;
+}
+
 // stream-ordered scratch owned by one call
 struct Workspace {
     void* p[24] = {};
@@ -452,7 +715,6 @@ struct Workspace {
     }
 };
 
-
 template <typename TS, typename TG, typename TI>
 static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iters, double final_gamma,
                      uint32_t flags, void* x_out, double* step_inf, int64_t* fallbacks, double* mass,
@@ -460,6 +722,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
                      gn_run_stats* stats) {
     const bool trace = (flags & GN_TRACE) != 0;
     const bool dev_io = (flags & GN_DEVICE_IO) != 0;
+    const bool exact = (flags & GN_EXACT) != 0;
     const int64_t n = g->n;
     const size_t nb = (size_t)std::max<int64_t>(n, 1);
     const int64_t launches0 = gn_launch_count();
@@ -477,25 +740,30 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     } evg{ev};
     GN_CUDA(cudaEventRecord(ev[0], s));
 
-    // ---- launch geometry
+    // ---- launch geometry and plan
     void* kern = trace ? (void*)k_gn_loop<TS, TG, TI, true> : (void*)k_gn_loop<TS, TG, TI, false>;
-    const size_t smem = (size_t)kSplitSlots * kLoopWarps * kSlice * sizeof(TS);
-    GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int max_optin = 0;
+    GN_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+    const size_t part_bytes = (size_t)kSlots * kWarps * kSlice * sizeof(TS);
+    const size_t static_bytes = 2048;  // publish scratch
+    const size_t smem_cap = (size_t)max_optin - static_bytes;
+    GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
     int maxb = 1;
-    if ((rc = coresident_blocks(kern, kLoopThreads, smem, g->device, &maxb))) return rc;
+    if ((rc = coresident_blocks(kern, kThreads, smem_cap, g->device, &maxb))) return rc;
     if (maxb < 1) return fail(GN_ERR_CUDA, "loop kernel cannot be resident");
-    const int64_t work = g->sell_elems + 4 * n + (int64_t)g->nhub * 4096;
+    const int64_t work = g->sell_elems + 4 * n + (g->nhub ? 32768 : 0);
     int grid = (int)std::min<int64_t>(maxb, std::max<int64_t>(1, (work + 16383) / 16384));
     if (g->grid_override > 0) grid = std::min(maxb, g->grid_override);
+    const DevicePlan* plan = nullptr;
+    if ((rc = get_plan(g, grid, exact, part_bytes, smem_cap, &plan))) return rc;
 
     Workspace ws;
     ws.s = s;
     TS *xa, *xb;
     TG *ya, *yb;
     double *xin, *dots, *ring, *gam, *out64 = nullptr, *hist = nullptr, *dsi, *dfb;
-    int *dbad, *status;
+    int *dbad, *status, *chk;
     unsigned int* barrier;
-    int* chk;
     GN_CUDA(ws.alloc(&xa, sizeof(TS) * nb));
     GN_CUDA(ws.alloc(&xb, sizeof(TS) * nb));
     GN_CUDA(ws.alloc(&ya, sizeof(TG) * nb));
@@ -550,9 +818,6 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     memset(&a, 0, sizeof(a));
     a.n = n;
     a.nhub = g->nhub;
-    a.nslices = g->nslices;
-    a.nsplit = g->nsplit;
-    a.exact = (flags & GN_EXACT) ? 1 : 0;
     a.hub_ptr = g->hub_ptr;
     a.hub_col = g->hub_col;
     a.slice_ptr = g->slice_ptr;
@@ -564,6 +829,11 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.x[1] = xb;
     a.yg[0] = ya;
     a.yg[1] = yb;
+    a.cta_ptr = plan->cta_ptr;
+    a.warp_ptr = plan->warp_ptr;
+    a.items = plan->items;
+    a.smem_words = plan->smem_words;
+    a.smem_resident_off = plan->resident_off;
     a.gammas = gam;
     a.iters = iters;
     a.final_gamma = final_gamma;
@@ -579,7 +849,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.perm = g->perm;
     void* args[] = {&a};
     GN_CUDA(cudaEventRecord(ev[1], s));
-    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kLoopThreads), args, smem, s));
+    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, plan->smem_bytes, s));
     GN_LAUNCHED();
     GN_CUDA(cudaEventRecord(ev[2], s));
 
@@ -642,7 +912,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
         stats->total_ms = ms;
         stats->launches = gn_launch_count() - launches0;
         stats->grid_blocks = grid;
-        stats->block_threads = kLoopThreads;
+        stats->block_threads = kThreads;
         stats->h2d_bytes = h2d;
         stats->d2h_bytes = d2h;
     }
