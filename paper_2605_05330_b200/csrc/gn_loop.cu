@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -40,23 +42,12 @@
 #include <vector>
 
 #include "gn_internal.cuh"
+#include "gn_plan.h"
 
 namespace gn {
 
-constexpr int kThreads = 1024;  // one CTA per SM
-constexpr int kWarps = kThreads / 32;
-constexpr int kSlots = 4;       // CTA items per phase (shared-memory partial slots)
-constexpr int kRing = 1024;     // iterations of block stats kept before a fold
-constexpr int kRingW = 8;       // per block: 4 dot terms, max|dx|, fallbacks, non-finite, pad
-
-enum ItemKind : int32_t { kSplit = 0, kHub = 1, kWhole = 2, kHubSeq = 3 };
-
-// One unit of work.  id: slice (kSplit/kWhole) or first hub row (kHub,
-// kHubSeq); len: blocks (slices) or degree (hub) or row count (kHubSeq);
-// smem: offset of the resident index blocks in 16-byte words, -1 = global.
-struct Item {
-    int32_t id, len, smem, kind;
-};
+constexpr int kRing = 1024;  // iterations of block stats kept before a fold
+constexpr int kRingW = 8;    // per block: 4 dot terms, max|dx|, fallbacks, non-finite, pad
 
 template <typename TS, typename TG>
 struct LoopArgs {
@@ -71,11 +62,14 @@ struct LoopArgs {
     const TS* __restrict__ w;
     TS* x[2];
     TG* yg[2];
-    const int32_t* __restrict__ cta_ptr;   // [G+1] into items (CTA items)
-    const int32_t* __restrict__ warp_ptr;  // [G*kWarps+1] into items (warp items)
+    const int32_t* __restrict__ phase_base;  // [G+1] into phases
+    const int32_t* __restrict__ phase_warp;  // [P*(kWarps+1)] into items
+    const int32_t* __restrict__ phase_comb;  // [P+1] into combs
     const Item* __restrict__ items;
+    const Combine* __restrict__ combs;
     const int32_t* __restrict__ smem_words;  // [G] resident 16-byte words per CTA
-    int smem_resident_off;                   // byte offset of the resident area
+    int hub_slot_off;                        // byte offsets in dynamic shared memory
+    int resident_off;
     const double* __restrict__ gammas;
     int iters;
     double final_gamma;
@@ -89,6 +83,8 @@ struct LoopArgs {
     unsigned int* barrier;
     double* x_hist;    // optional [iters][n], original order
     const int32_t* __restrict__ perm;
+    long long* prof;   // optional timestamps (GN_PROF_ITER): [G][kWarps+4]
+    int prof_iter;
 };
 
 struct Stats {
@@ -100,6 +96,12 @@ struct Stats {
 
 template <typename T>
 __device__ __forceinline__ T tabs(T v) { return v < T(0) ? -v : v; }
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Per-row state, fetched before the row's neighbour sum so its latency hides
 // under the gathers.
@@ -160,54 +162,56 @@ struct LaneVec<int32_t> {
     }
 };
 
-template <bool SMEM>
-__device__ __forceinline__ uint4 load_vec(const uint4* p) {
-    if (SMEM) return *p;
-    return __ldg(p);
-}
-
 // Sequential sum over blocks [bb, be) of one slice row (this lane), masked by
-// the row's degree d.  A batch issues NB vector loads and NB*B gathers before
-// any add; the adds stay in position order (the reference's order).  Blocks
-// that lie entirely inside the row skip the mask.
-template <typename TS, typename TG, typename TI, bool SMEM>
-__device__ __forceinline__ TS sum_blocks(const uint4* __restrict__ base, const TG* __restrict__ yg, int d,
-                                         int bb, int be) {
+// the row's degree d.  `base` (shared or global memory: a generic pointer, so
+// one copy of the loop serves both) addresses block b at base[b * 32].  Each
+// batch issues NB*B gathers before any add, and the next batch's index
+// vectors are requested before this batch's gathers, so a batch costs one
+// memory round trip; the adds stay in position order (the reference's order).
+template <typename TS, typename TG, typename TI>
+__device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ yg, int d, int bb, int be) {
     using A = Arith<TS>;
     using V = LaneVec<TI>;
     constexpr int B = V::B;
     constexpr int NB = (sizeof(TG) == 4 ? 16 : 8) / B > 0 ? (sizeof(TG) == 4 ? 16 : 8) / B : 1;
     TS s = TS(0);
-    int b = bb;
-    for (; b + NB <= be && (b + NB) * B <= d; b += NB) {
-        uint4 v[NB];
+    be = min(be, (d + B - 1) / B);  // blocks past the row's end hold no neighbours
+    if (bb >= be) return s;
+    uint4 v[NB];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) v[u] = load_vec<SMEM>(base + (size_t)(b + u) * kSlice);
-        TG y[NB * B];
+    for (int u = 0; u < NB; ++u)
+        if (bb + u < be) v[u] = base[(size_t)(bb + u) * kSlice];
+    for (int b = bb; b < be; b += NB) {
+        uint4 vn[NB];
 #pragma unroll
         for (int u = 0; u < NB; ++u)
+            if (b + NB + u < be) vn[u] = base[(size_t)(b + NB + u) * kSlice];
+        TG y[NB * B];
+        if (b + NB <= be && (b + NB) * B <= d) {
 #pragma unroll
-            for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(v[u], t)];
+            for (int u = 0; u < NB; ++u)
+#pragma unroll
+                for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(v[u], t)];
+        } else {
+#pragma unroll
+            for (int u = 0; u < NB; ++u)
+#pragma unroll
+                for (int t = 0; t < B; ++t)
+                    y[u * B + t] = (b + u < be && (b + u) * B + t < d) ? yg[V::get(v[u], t)] : TG(0);
+        }
 #pragma unroll
         for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
-    }
-    for (; b < be && b * B < d; ++b) {
-        const uint4 v = load_vec<SMEM>(base + (size_t)b * kSlice);
-        TG y[B];
 #pragma unroll
-        for (int t = 0; t < B; ++t) y[t] = (b * B + t < d) ? yg[V::get(v, t)] : TG(0);
-#pragma unroll
-        for (int t = 0; t < B; ++t) s = A::add(s, (TS)y[t]);
+        for (int u = 0; u < NB; ++u) v[u] = vn[u];
     }
     return s;
 }
 
 template <typename TS, typename TG, typename TI>
-__device__ __forceinline__ TS slice_sum(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
-                                        const TG* __restrict__ yg, int lane, int d, int bb, int be) {
-    if (it.smem >= 0) return sum_blocks<TS, TG, TI, true>(s_res + it.smem + lane, yg, d, bb, be);
-    const uint4* g = reinterpret_cast<const uint4*>((const TI*)a.sell + __ldg(a.slice_ptr + it.id)) + lane;
-    return sum_blocks<TS, TG, TI, false>(g, yg, d, bb, be);
+__device__ __forceinline__ const uint4* slice_base(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
+                                                   int lane) {
+    if (it.smem >= 0) return s_res + it.smem - (ptrdiff_t)it.beg * kSlice + lane;
+    return reinterpret_cast<const uint4*>((const TI*)a.sell + __ldg(a.slice_ptr + it.id)) + lane;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -223,84 +227,88 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// One pass over this CTA's items.
+// One pass over this CTA's items, phase by phase (gn_plan.h).
 template <typename TS, typename TG, typename TI, bool TRACE>
-__device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_part, const uint4* s_res) {
+__device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_slot, TS* s_hslot,
+                     const uint4* s_res) {
     using A = Arith<TS>;
     const int cur = k & 1;
     const TG* __restrict__ yg = a.yg[cur];
     const TS g = tail ? TS(0) : (TS)a.gammas[k];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c0 = __ldg(a.cta_ptr + blockIdx.x), c1 = __ldg(a.cta_ptr + blockIdx.x + 1);
-    const int gw = blockIdx.x * kWarps + warp;
-    const int w0 = __ldg(a.warp_ptr + gw), w1 = __ldg(a.warp_ptr + gw + 1);
-    bool warp_done = false;
-    // CTA items in phases of kSlots; the warp items run inside the first
-    // phase, between the partial sums and the barrier that publishes them
-    for (int p0 = c0;; p0 += kSlots) {
-        const int pn = min(kSlots, c1 - p0);
-        for (int q = 0; q < pn; ++q) {
-            const Item it = a.items[p0 + q];
-            if (it.kind == kSplit) {
-                const int d = __ldg(a.row_deg + it.id * kSlice + lane);
-                const int bb = it.len * warp / kWarps, be = it.len * (warp + 1) / kWarps;
-                s_part[(q * kWarps + warp) * kSlice + lane] = slice_sum<TS, TG, TI>(a, it, s_res, yg, lane, d, bb, be);
-            } else {  // kHub: warp w sums elements [w*deg/W, (w+1)*deg/W) of the row
-                const int beg = __ldg(a.hub_ptr + it.id);
-                const int eb = beg + (int)((int64_t)it.len * warp / kWarps);
-                const int ee = beg + (int)((int64_t)it.len * (warp + 1) / kWarps);
+    const int ph0 = __ldg(a.phase_base + blockIdx.x), ph1 = __ldg(a.phase_base + blockIdx.x + 1);
+    for (int ph = ph0; ph < ph1; ++ph) {
+        const int i0 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp);
+        const int i1 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp + 1);
+        if (a.prof && k == a.prof_iter && lane == 0 && ph == ph0) a.prof[blockIdx.x * (kWarps + 4) + 4 + warp] = gtimer();
+        for (int i = i0; i < i1; ++i) {
+            const Item it = a.items[i];
+            if (it.kind == kWhole || it.kind == kPiece) {
+                const bool whole = it.kind == kWhole;
+                const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + lane;
+                const bool valid = r < a.n;
+                RowIn<TS> in{};
+                int d = 0;
+                if (valid) {
+                    d = __ldg(a.row_deg + (size_t)it.id * kSlice + lane);
+                    if (whole) in = row_in(a, (int)r, cur);
+                }
+                const TS sum = sum_blocks<TS, TG, TI>(slice_base<TS, TG, TI>(a, it, s_res, lane), yg, d, it.beg, it.end);
+                if (!whole) s_slot[it.slot * kSlice + lane] = sum;
+                else if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, in, cur, g, k, tail, st);
+            } else if (it.kind == kHubPiece) {
+                // lanes stride the piece's elements; fixed warp tree
+                const int base = __ldg(a.hub_ptr + it.id);
                 TS s = TS(0);
-                for (int p = eb + lane; p < ee; p += 32) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+                int p = base + it.beg + lane;
+                const int e = base + it.end;
+                for (; p + 3 * 32 < e; p += 4 * 32) {
+                    const int j0 = __ldg(a.hub_col + p), j1 = __ldg(a.hub_col + p + 32);
+                    const int j2 = __ldg(a.hub_col + p + 64), j3 = __ldg(a.hub_col + p + 96);
+                    const TG y0 = yg[j0], y1 = yg[j1], y2 = yg[j2], y3 = yg[j3];
+                    s = A::add(s, (TS)y0);
+                    s = A::add(s, (TS)y1);
+                    s = A::add(s, (TS)y2);
+                    s = A::add(s, (TS)y3);
+                }
+                for (; p < e; p += 32) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
                 s = warp_sum(s);
-                if (lane == 0) s_part[(q * kWarps + warp) * kSlice] = s;
-            }
-        }
-        if (!warp_done) {
-            warp_done = true;
-            for (int i = w0; i < w1; ++i) {
-                const Item it = a.items[i];
-                if (it.kind == kWhole) {
-                    const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + lane;
-                    const bool valid = r < a.n;
-                    RowIn<TS> in{};
-                    int d = 0;
-                    if (valid) {
-                        d = __ldg(a.row_deg + (size_t)it.id * kSlice + lane);
-                        in = row_in(a, (int)r, cur);
-                    }
-                    const TS sum = slice_sum<TS, TG, TI>(a, it, s_res, yg, lane, d, 0, it.len);
-                    if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, in, cur, g, k, tail, st);
-                } else {  // kHubSeq (EXACT): one thread per hub row, sequential
-                    if (lane < it.len) {
-                        const int h = it.id + lane;
-                        const RowIn<TS> in = row_in(a, h, cur);
-                        TS s = TS(0);
-                        for (int p = __ldg(a.hub_ptr + h); p < __ldg(a.hub_ptr + h + 1); ++p)
-                            s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
-                        update_row<TS, TG, TRACE>(a, h, s, in, cur, g, k, tail, st);
-                    }
+                if (lane == 0) s_hslot[it.slot] = s;
+            } else {  // kHubSeq (EXACT): one thread per hub row, sequential
+                if (lane < it.end - it.beg) {
+                    const int h = it.id + lane;
+                    const RowIn<TS> in = row_in(a, h, cur);
+                    TS s = TS(0);
+                    for (int p = __ldg(a.hub_ptr + h); p < __ldg(a.hub_ptr + h + 1); ++p)
+                        s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+                    update_row<TS, TG, TRACE>(a, h, s, in, cur, g, k, tail, st);
                 }
             }
         }
-        if (pn <= 0) break;
-        __syncthreads();
-        for (int q = warp; q < pn; q += kWarps) {
-            const Item it = a.items[p0 + q];
-            if (it.kind == kSplit) {
-                const int r = a.nhub + it.id * kSlice + lane;
-                const RowIn<TS> in = row_in(a, r, cur);
-                TS tot = TS(0);
-#pragma unroll 8
-                for (int w = 0; w < kWarps; ++w) tot = A::add(tot, s_part[(q * kWarps + w) * kSlice + lane]);
-                update_row<TS, TG, TRACE>(a, r, tot, in, cur, g, k, tail, st);
-            } else if (lane == 0) {
-                const RowIn<TS> in = row_in(a, it.id, cur);
-                TS tot = TS(0);
-                for (int w = 0; w < kWarps; ++w) tot = A::add(tot, s_part[(q * kWarps + w) * kSlice]);
-                update_row<TS, TG, TRACE>(a, it.id, tot, in, cur, g, k, tail, st);
-            }
+        if (a.prof && k == a.prof_iter && ph == ph0) {
+            __syncwarp();
+            if (lane == 0) a.prof[blockIdx.x * (kWarps + 4) + 4 + warp] = gtimer() - a.prof[blockIdx.x * (kWarps + 4) + 4 + warp];
         }
-        __syncthreads();
+        const int c0 = __ldg(a.phase_comb + ph), c1 = __ldg(a.phase_comb + ph + 1);
+        if (c1 > c0) {
+            __syncthreads();
+            for (int c = c0 + warp; c < c1; c += kWarps) {
+                const Combine cb = a.combs[c];
+                if (cb.kind == 0) {
+                    const int r = a.nhub + cb.id * kSlice + lane;
+                    const RowIn<TS> in = row_in(a, r, cur);
+                    TS tot = TS(0);
+                    for (int q = 0; q < cb.nslot; ++q) tot = A::add(tot, s_slot[(cb.slot + q) * kSlice + lane]);
+                    update_row<TS, TG, TRACE>(a, r, tot, in, cur, g, k, tail, st);
+                } else if (lane == 0) {
+                    const RowIn<TS> in = row_in(a, cb.id, cur);
+                    TS tot = TS(0);
+                    for (int q = 0; q < cb.nslot; ++q) tot = A::add(tot, s_hslot[cb.slot + q]);
+                    update_row<TS, TG, TRACE>(a, cb.id, tot, in, cur, g, k, tail, st);
+                }
+            }
+            if (ph + 1 < ph1) __syncthreads();
+        }
     }
 }
 
@@ -419,36 +427,39 @@ __device__ double ring_step_inf(const double* ring_slot) {
 template <typename TS, typename TG, typename TI, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TS* s_part = (TS*)smem_raw;
-    uint4* s_res = (uint4*)(smem_raw + a.smem_resident_off);
+    TS* s_slot = (TS*)smem_raw;
+    TS* s_hslot = (TS*)(smem_raw + a.hub_slot_off);
+    uint4* s_res = (uint4*)(smem_raw + a.resident_off);
     // resident index blocks: copied once, used every iteration
-    {
-        const int nwords = __ldg(a.smem_words + blockIdx.x);
-        if (nwords > 0) {
-            const int c0 = a.cta_ptr[blockIdx.x], c1 = a.cta_ptr[blockIdx.x + 1];
-            const int w0 = a.warp_ptr[blockIdx.x * kWarps], w1 = a.warp_ptr[(blockIdx.x + 1) * kWarps];
-            for (int part = 0; part < 2; ++part) {
-                const int i0 = part ? w0 : c0, i1 = part ? w1 : c1;
-                for (int i = i0; i < i1; ++i) {
-                    const Item it = a.items[i];
-                    if (it.smem < 0 || (it.kind != kSplit && it.kind != kWhole)) continue;
-                    const uint4* src = reinterpret_cast<const uint4*>((const TI*)a.sell + a.slice_ptr[it.id]);
-                    for (int t = threadIdx.x; t < it.len * kSlice; t += blockDim.x) s_res[it.smem + t] = __ldg(src + t);
-                }
-            }
+    if (__ldg(a.smem_words + blockIdx.x) > 0) {
+        const int ph0 = a.phase_base[blockIdx.x], ph1 = a.phase_base[blockIdx.x + 1];
+        const int i0 = a.phase_warp[ph0 * (kWarps + 1)], i1 = a.phase_warp[(ph1 - 1) * (kWarps + 1) + kWarps];
+        for (int i = i0; i < i1; ++i) {
+            const Item it = a.items[i];
+            if (it.smem < 0) continue;
+            const uint4* src = reinterpret_cast<const uint4*>((const TI*)a.sell + a.slice_ptr[it.id]) +
+                               (size_t)it.beg * kSlice;
+            const int words = (it.end - it.beg) * kSlice;
+            for (int t = threadIdx.x; t < words; t += blockDim.x) s_res[it.smem + t] = __ldg(src + t);
         }
-        __syncthreads();
     }
+    __syncthreads();
     const FoldOut fo{a.iters, a.step_inf, a.fb, a.bad, a.dots};
     unsigned int bar = 0;
     int ran = 0, k0 = 0;
     const size_t ring_stride = (size_t)gridDim.x * kRingW;
     for (int k = 0; k < a.iters; ++k) {
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE>(a, k, false, st, s_part, s_res);
+        const bool pr = a.prof && k == a.prof_iter && threadIdx.x == 0;
+        long long* pp = a.prof ? a.prof + blockIdx.x * (kWarps + 4) : nullptr;
+        if (pr) pp[0] = gtimer();
+        pass<TS, TG, TI, TRACE>(a, k, false, st, s_slot, s_hslot, s_res);
+        if (pr) pp[1] = gtimer();
         double* slot = a.ring + (size_t)(k - k0) * ring_stride;
         publish<TRACE>(st, slot);
+        if (pr) pp[2] = gtimer();
         grid_barrier(a.barrier, (++bar) * gridDim.x);
+        if (pr) pp[3] = gtimer();
         ran = k + 1;
         bool stop = false;
         if (a.early_exit && a.gammas[k] == a.final_gamma)  // dynamics.py:177
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
     if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_part, s_res);
+        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_slot, s_hslot, s_res);
         publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
         fold_ring(a.ring, ran - k0 + 1, k0, fo);
@@ -512,16 +523,16 @@ static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + 255) / 
 
 // ------------------------------------------------------------------ plan
 
-// Device plan for one (graph, grid, mode); built on first use and cached
-// (graphs are immutable).
+// Device copy of one HostPlan; built on first use and cached per (graph,
+// grid, mode) -- graphs are immutable.
 struct DevicePlan {
-    int grid = 0;
-    int32_t* cta_ptr = nullptr;
-    int32_t* warp_ptr = nullptr;
+    int32_t* phase_base = nullptr;
+    int32_t* phase_warp = nullptr;
+    int32_t* phase_comb = nullptr;
     Item* items = nullptr;
+    Combine* combs = nullptr;
     int32_t* smem_words = nullptr;
-    size_t smem_bytes = 0;  // dynamic shared memory per CTA
-    int resident_off = 0;
+    int max_slots = 0, max_hub_slots = 0, max_words = 0;
     int64_t resident_words = 0;
 };
 
@@ -538,127 +549,22 @@ void release_plans(const gn_graph* g) {
     auto it = g_cache.find(g);
     if (it == g_cache.end()) return;
     for (auto& kv : it->second->plans) {
-        cudaFree(kv.second.cta_ptr);
-        cudaFree(kv.second.warp_ptr);
-        cudaFree(kv.second.items);
-        cudaFree(kv.second.smem_words);
+        void* ptrs[] = {kv.second.phase_base, kv.second.phase_warp, kv.second.phase_comb, kv.second.items,
+                        kv.second.combs, kv.second.smem_words};
+        for (void* p : ptrs) cudaFree(p);
     }
     delete it->second;
     g_cache.erase(it);
 }
 
-// Longest-processing-time-first: CTA items over CTAs, then warp items over
-// all warps (a CTA's share of its CTA items preloads each of its warps).
-static void build_plan(const gn_graph* g, int G, bool exact, size_t part_bytes, size_t smem_cap,
-                       std::vector<int32_t>& cta_ptr, std::vector<int32_t>& warp_ptr, std::vector<Item>& items,
-                       std::vector<int32_t>& smem_words) {
-    const int B = g->idx16 ? 8 : 4;
-    std::vector<int64_t> sp((size_t)g->nslices + 1);
-    cudaMemcpy(sp.data(), g->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost);
-    std::vector<int32_t> hp((size_t)g->nhub + 1);
-    cudaMemcpy(hp.data(), g->hub_ptr, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost);
-    auto nblk = [&](int s) { return (int32_t)((sp[(size_t)s + 1] - sp[(size_t)s]) / (kSlice * B)); };
-
-    // cost unit ~ one 16-byte block per lane; the fixed term stands for the
-    // per-item round trips
-    const double kFixed = 6.0;
-    std::vector<std::vector<Item>> cta_items((size_t)G);
-    std::vector<double> cta_load((size_t)G, 0.0);
-    std::vector<Item> citems, witems;
-    if (!exact) {
-        for (int h = 0; h < g->nhub; ++h) citems.push_back(Item{h, hp[(size_t)h + 1] - hp[(size_t)h], -1, kHub});
-        for (int s = 0; s < g->nsplit; ++s) citems.push_back(Item{s, nblk(s), -1, kSplit});
-        for (int s = g->nsplit; s < g->nslices; ++s) witems.push_back(Item{s, nblk(s), -1, kWhole});
-    } else {
-        for (int h = 0; h < g->nhub; h += 32) witems.push_back(Item{h, std::min(32, g->nhub - h), -1, kHubSeq});
-        for (int s = 0; s < g->nslices; ++s) witems.push_back(Item{s, nblk(s), -1, kWhole});
-    }
-    auto ccost = [&](const Item& it) {
-        return it.kind == kHub ? kFixed + it.len / (32.0 * kWarps) * 4.0 : kFixed + (double)it.len / kWarps;
-    };
-    auto wcost = [&](const Item& it) {
-        if (it.kind == kHubSeq) {
-            int mx = 0;
-            for (int h = it.id; h < it.id + it.len; ++h) mx = std::max(mx, hp[(size_t)h + 1] - hp[(size_t)h]);
-            return kFixed + mx;
-        }
-        return kFixed + (double)it.len;
-    };
-    using E = std::pair<double, int>;
-    std::stable_sort(citems.begin(), citems.end(), [&](const Item& x, const Item& y) { return ccost(x) > ccost(y); });
-    {
-        std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
-        for (int b = 0; b < G; ++b) pq.push({0.0, b});
-        for (const Item& it : citems) {
-            E e = pq.top();
-            pq.pop();
-            cta_items[(size_t)e.second].push_back(it);
-            e.first += ccost(it);
-            cta_load[(size_t)e.second] = e.first;
-            pq.push(e);
-        }
-    }
-    const int W = G * kWarps;
-    std::vector<std::vector<Item>> warp_items((size_t)W);
-    std::stable_sort(witems.begin(), witems.end(), [&](const Item& x, const Item& y) { return wcost(x) > wcost(y); });
-    {
-        std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
-        for (int w = 0; w < W; ++w) pq.push({cta_load[(size_t)(w / kWarps)], w});
-        for (const Item& it : witems) {
-            E e = pq.top();
-            pq.pop();
-            warp_items[(size_t)e.second].push_back(it);
-            e.first += wcost(it);
-            pq.push(e);
-        }
-    }
-    // each warp's slices in ascending order (locality of the x / yg rows)
-    for (auto& v : warp_items)
-        std::sort(v.begin(), v.end(), [](const Item& x, const Item& y) { return x.id < y.id; });
-    // shared-memory residency of index blocks, per CTA, within smem_cap
-    smem_words.assign((size_t)G, 0);
-    items.clear();
-    cta_ptr.assign((size_t)G + 1, 0);
-    warp_ptr.assign((size_t)W + 1, 0);
-    const size_t cap_words = smem_cap > part_bytes ? (smem_cap - part_bytes) / 16 : 0;
-    for (int b = 0; b < G; ++b) {
-        size_t used = 0;
-        auto place = [&](Item& it) {
-            if (it.kind != kSplit && it.kind != kWhole) return;
-            const size_t words = (size_t)it.len * kSlice;
-            if (used + words <= cap_words) {
-                it.smem = (int32_t)used;
-                used += words;
-            }
-        };
-        for (Item& it : cta_items[(size_t)b]) place(it);
-        // warp items breadth-first over the CTA's warps so every warp gets some
-        for (size_t depth = 0;; ++depth) {
-            bool any = false;
-            for (int w = 0; w < kWarps; ++w) {
-                auto& v = warp_items[(size_t)b * kWarps + w];
-                if (depth < v.size()) {
-                    any = true;
-                    place(v[depth]);
-                }
-            }
-            if (!any) break;
-        }
-        smem_words[(size_t)b] = (int32_t)used;
-    }
-    for (int b = 0; b < G; ++b) {
-        cta_ptr[(size_t)b] = (int32_t)items.size();
-        items.insert(items.end(), cta_items[(size_t)b].begin(), cta_items[(size_t)b].end());
-    }
-    cta_ptr[(size_t)G] = (int32_t)items.size();
-    for (int w = 0; w < W; ++w) {
-        warp_ptr[(size_t)w] = (int32_t)items.size();
-        items.insert(items.end(), warp_items[(size_t)w].begin(), warp_items[(size_t)w].end());
-    }
-    warp_ptr[(size_t)W] = (int32_t)items.size();
+template <typename T>
+static int upload(const std::vector<T>& h, T** d) {
+    GN_CUDA(cudaMalloc((void**)d, sizeof(T) * std::max<size_t>(h.size(), 1)));
+    if (!h.empty()) GN_CUDA(cudaMemcpy(*d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return GN_OK;
 }
 
-static int get_plan(gn_graph* g, int G, bool exact, size_t part_bytes, size_t smem_cap, const DevicePlan** out) {
+static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const DevicePlan** out) {
     PlanCache* pc;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -673,27 +579,23 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t part_bytes, size_t sm
         *out = &it->second;
         return GN_OK;
     }
-    std::vector<int32_t> cta_ptr, warp_ptr, smem_words;
-    std::vector<Item> items;
-    build_plan(g, G, exact, part_bytes, smem_cap, cta_ptr, warp_ptr, items, smem_words);
+    std::vector<int64_t> sp((size_t)g->nslices + 1);
+    GN_CUDA(cudaMemcpy(sp.data(), g->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> hp((size_t)g->nhub + 1);
+    GN_CUDA(cudaMemcpy(hp.data(), g->hub_ptr, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
+    PlanInput in{g->n, g->nhub, g->nslices, g->nsplit, g->idx16 ? 8 : 4, &sp, &hp};
+    HostPlan hpn;
+    build_plan(in, G, exact, resident_cap, hpn);
     DevicePlan p;
-    p.grid = G;
-    GN_CUDA(cudaMalloc(&p.cta_ptr, sizeof(int32_t) * cta_ptr.size()));
-    GN_CUDA(cudaMalloc(&p.warp_ptr, sizeof(int32_t) * warp_ptr.size()));
-    GN_CUDA(cudaMalloc(&p.items, sizeof(Item) * std::max<size_t>(items.size(), 1)));
-    GN_CUDA(cudaMalloc(&p.smem_words, sizeof(int32_t) * smem_words.size()));
-    GN_CUDA(cudaMemcpy(p.cta_ptr, cta_ptr.data(), sizeof(int32_t) * cta_ptr.size(), cudaMemcpyHostToDevice));
-    GN_CUDA(cudaMemcpy(p.warp_ptr, warp_ptr.data(), sizeof(int32_t) * warp_ptr.size(), cudaMemcpyHostToDevice));
-    if (!items.empty())
-        GN_CUDA(cudaMemcpy(p.items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
-    GN_CUDA(cudaMemcpy(p.smem_words, smem_words.data(), sizeof(int32_t) * smem_words.size(), cudaMemcpyHostToDevice));
-    int32_t mx = 0;
-    for (int32_t wds : smem_words) {
-        mx = std::max(mx, wds);
-        p.resident_words += wds;
-    }
-    p.resident_off = (int)((part_bytes + 15) / 16 * 16);
-    p.smem_bytes = (size_t)p.resident_off + (size_t)mx * 16;
+    int rc;
+    if ((rc = upload(hpn.phase_base, &p.phase_base)) || (rc = upload(hpn.phase_warp, &p.phase_warp)) ||
+        (rc = upload(hpn.phase_comb, &p.phase_comb)) || (rc = upload(hpn.items, &p.items)) ||
+        (rc = upload(hpn.combs, &p.combs)) || (rc = upload(hpn.smem_words, &p.smem_words)))
+        return rc;
+    p.max_slots = hpn.max_slots;
+    p.max_hub_slots = hpn.max_hub_slots;
+    for (int32_t w : hpn.smem_words) p.max_words = std::max(p.max_words, w);
+    p.resident_words = hpn.resident_words;
     auto res = pc->plans.emplace(key, p);
     *out = &res.first->second;
     return GN_OK;
@@ -744,9 +646,14 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     void* kern = trace ? (void*)k_gn_loop<TS, TG, TI, true> : (void*)k_gn_loop<TS, TG, TI, false>;
     int max_optin = 0;
     GN_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    const size_t part_bytes = (size_t)kSlots * kWarps * kSlice * sizeof(TS);
+    const size_t slot_bytes = (size_t)kMaxSlots * kSlice * sizeof(TS) + (size_t)kMaxHubSlots * sizeof(TS);
     const size_t static_bytes = 2048;  // publish scratch
-    const size_t smem_cap = (size_t)max_optin - static_bytes;
+    // index residency budget: what is left after the partial slots, capped so
+    // the L1 keeps room for the gathers (GN_SMEM_RES_KB overrides)
+    size_t res_cap = 96 * 1024;
+    if (const char* e = getenv("GN_SMEM_RES_KB")) res_cap = (size_t)atoi(e) * 1024;
+    res_cap = std::min(res_cap, (size_t)max_optin - static_bytes - slot_bytes);
+    const size_t smem_cap = slot_bytes + res_cap;
     GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
     int maxb = 1;
     if ((rc = coresident_blocks(kern, kThreads, smem_cap, g->device, &maxb))) return rc;
@@ -755,7 +662,10 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     int grid = (int)std::min<int64_t>(maxb, std::max<int64_t>(1, (work + 16383) / 16384));
     if (g->grid_override > 0) grid = std::min(maxb, g->grid_override);
     const DevicePlan* plan = nullptr;
-    if ((rc = get_plan(g, grid, exact, part_bytes, smem_cap, &plan))) return rc;
+    if ((rc = get_plan(g, grid, exact, res_cap, &plan))) return rc;
+    const int hub_slot_off = (int)((size_t)kMaxSlots * kSlice * sizeof(TS));
+    const int resident_off = (int)((slot_bytes + 15) / 16 * 16);
+    const size_t dyn_smem = (size_t)resident_off + (size_t)plan->max_words * 16;
 
     Workspace ws;
     ws.s = s;
@@ -829,11 +739,14 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.x[1] = xb;
     a.yg[0] = ya;
     a.yg[1] = yb;
-    a.cta_ptr = plan->cta_ptr;
-    a.warp_ptr = plan->warp_ptr;
+    a.phase_base = plan->phase_base;
+    a.phase_warp = plan->phase_warp;
+    a.phase_comb = plan->phase_comb;
     a.items = plan->items;
+    a.combs = plan->combs;
     a.smem_words = plan->smem_words;
-    a.smem_resident_off = plan->resident_off;
+    a.hub_slot_off = hub_slot_off;
+    a.resident_off = resident_off;
     a.gammas = gam;
     a.iters = iters;
     a.final_gamma = final_gamma;
@@ -847,9 +760,17 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.barrier = barrier;
     a.x_hist = hist;
     a.perm = g->perm;
+    long long* dprof = nullptr;
+    const char* prof_env = getenv("GN_PROF_ITER");
+    if (prof_env) {
+        a.prof_iter = atoi(prof_env);
+        GN_CUDA(ws.alloc(&dprof, sizeof(long long) * (size_t)grid * (kWarps + 4)));
+        GN_CUDA(cudaMemsetAsync(dprof, 0, sizeof(long long) * (size_t)grid * (kWarps + 4), s));
+        a.prof = dprof;
+    }
     void* args[] = {&a};
     GN_CUDA(cudaEventRecord(ev[1], s));
-    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, plan->smem_bytes, s));
+    GN_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, dyn_smem, s));
     GN_LAUNCHED();
     GN_CUDA(cudaEventRecord(ev[2], s));
 
@@ -886,6 +807,25 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     }
     GN_CUDA(cudaEventRecord(ev[3], s));
     GN_CUDA(cudaStreamSynchronize(s));
+    if (dprof) {
+        std::vector<long long> hp((size_t)grid * (kWarps + 4));
+        GN_CUDA(cudaMemcpy(hp.data(), dprof, sizeof(long long) * hp.size(), cudaMemcpyDeviceToHost));
+        const char* path = getenv("GN_PROF_OUT");
+        FILE* f = fopen(path ? path : "gn_prof.txt", "a");
+        if (f) {
+            long long t0 = LLONG_MAX;
+            for (int b = 0; b < grid; ++b) t0 = std::min(t0, hp[(size_t)b * (kWarps + 4)]);
+            fprintf(f, "# grid %d iter %d: cta pass_start pass_end publish_end barrier_end | warp item ns\n", grid,
+                    a.prof_iter);
+            for (int b = 0; b < grid; ++b) {
+                const long long* q = &hp[(size_t)b * (kWarps + 4)];
+                fprintf(f, "%d %lld %lld %lld %lld |", b, q[0] - t0, q[1] - t0, q[2] - t0, q[3] - t0);
+                for (int w = 0; w < kWarps; ++w) fprintf(f, " %lld", q[4 + w]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
 
     int bad = -1;
     for (int k = 0; k < ran; ++k)
