@@ -210,7 +210,15 @@ struct Layout {
     std::vector<uint16_t> sell16;
     int idx16 = 0;
     int32_t maxdeg = 0;
+    std::vector<uint64_t> sig;  // per slice: MinHash of the 128-byte lines it gathers
 };
+
+static inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
 
 static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indices, Layout& L) {
     std::vector<int32_t> deg((size_t)n);
@@ -287,6 +295,20 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
         }
         len = (len + B - 1) / B * B;
         L.slice_ptr[s + 1] = L.slice_ptr[s] + (int64_t)len * kSlice;
+    }
+    // MinHash over the 128-byte lines (16 fp64 ids) a slice gathers: slices
+    // with overlapping neighbourhoods get equal signatures w.p. = Jaccard, and
+    // the plan places equal signatures on the same SM so its L1 serves them
+    L.sig.assign((size_t)L.nslices, ~0ull);
+    for (int32_t s = 0; s < L.nslices; ++s) {
+        uint64_t m = ~0ull;
+        for (int l = 0; l < kSlice; ++l) {
+            int64_t r = (int64_t)s * kSlice + l;
+            if (r >= nreg) continue;
+            int32_t o = L.perm[(size_t)(L.nhub + r)];
+            for (int64_t p = indptr[o]; p < indptr[o + 1]; ++p) m = std::min(m, mix64((uint64_t)(L.inv[indices[p]] >> 4)));
+        }
+        L.sig[(size_t)s] = m;
     }
     const int64_t elems = L.slice_ptr[L.nslices];
     if (L.idx16) L.sell16.assign((size_t)elems, 0);
@@ -392,6 +414,7 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     g->nsplit = L.nsplit;
     g->idx16 = L.idx16;
     g->sell_elems = L.slice_ptr.empty() ? 0 : L.slice_ptr.back();
+    g->slice_sig = std::move(L.sig);
     CallCtx ctx;
     int rc = ctx.open(device);
     if (rc) { delete g; return rc; }

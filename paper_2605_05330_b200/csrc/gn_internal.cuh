@@ -92,6 +92,7 @@ struct gn_graph {
     void* sell = nullptr;          // int32 or uint16 new ids, position-major
     int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536)
     int64_t sell_elems = 0;
+    std::vector<uint64_t> slice_sig;  // host: per-slice MinHash (gn_graph.cu, used by the plan)
 };
 
 namespace gn {

@@ -3,10 +3,13 @@
 // The kernel runs the same work every iteration, so who does what is decided
 // once per (graph, grid, mode) on the host and cached with the graph:
 //
-//   level 1  every unit (short slice, long slice, hub row) goes to a CTA,
-//            longest-processing-time-first on its total gather count: a
-//            CTA's warps share one SM's L1/LSU, the resource random gathers
-//            saturate, so CTAs (not warps) are what must be balanced;
+//   level 1  every unit (short slice, long slice, hub row) goes to a CTA.
+//            A CTA's warps share one SM's L1/LSU -- the resource gathers
+//            saturate -- so CTAs (not warps) are balanced on total gather
+//            count: hub rows first, longest-processing-time-first, then the
+//            slices in MinHash-signature order as contiguous runs that fill
+//            every CTA to the mean, so slices with overlapping neighbourhoods
+//            share an SM and its L1;
 //   level 2  inside a CTA, long slices and hub rows are cut into fixed-size
 //            pieces (8 blocks of a slice, <= 1024 elements of a hub row:
 //            independent of the grid, so the summation tree -- and every bit
@@ -28,9 +31,9 @@ namespace gn {
 
 constexpr int kThreads = 1024;  // one CTA per SM
 constexpr int kWarps = kThreads / 32;
-constexpr int kPieceBlocks = 8;      // blocks per piece of a long slice
+constexpr int kPieceBlocks = 4;      // blocks per piece of a long slice
 constexpr int kHubPieceElems = 1024; // elements per piece of a hub row (at least)
-constexpr int kMaxSlots = 64;        // slice-piece slots per phase (32 partials each)
+constexpr int kMaxSlots = 256;       // slice-piece slots per phase (32 partials each)
 constexpr int kMaxHubSlots = 512;    // hub-piece slots per phase (1 partial each)
 
 enum ItemKind : int32_t { kWhole = 0, kPiece = 1, kHubPiece = 2, kHubSeq = 3 };
@@ -67,6 +70,7 @@ struct PlanInput {
     int B;                              // positions per block (8 or 4)
     const std::vector<int64_t>* slice_ptr;
     const std::vector<int32_t>* hub_ptr;
+    const std::vector<uint64_t>* sig;   // per-slice neighbourhood signature (may be empty)
 };
 
 void build_plan(const PlanInput& in, int G, bool exact, size_t resident_cap_bytes, HostPlan& out);

@@ -42,6 +42,7 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--grid", type=int, default=-1)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--dtypes", default="")
     args = ap.parse_args()
     which = args.which.split(",")
     if args.grid >= 0:
@@ -53,7 +54,8 @@ if __name__ == "__main__":
                 inst = G.c4_batch(1024).instance
             else:
                 inst = G.CONFIGS[name]()
-            probe(inst, iters=args.iters, grids=(args.grid,), reps=args.reps)
+            for dt in (args.dtypes.split(",") if args.dtypes else [None]):
+                probe(inst, iters=args.iters, grids=(args.grid,), reps=args.reps, dtype=dt)
         raise SystemExit(0)
     if "C1" in which:
         probe(G.c1_er(), grids=(1, 2, 4, 0))
