@@ -583,7 +583,8 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const D
     GN_CUDA(cudaMemcpy(sp.data(), g->slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost));
     std::vector<int32_t> hp((size_t)g->nhub + 1);
     GN_CUDA(cudaMemcpy(hp.data(), g->hub_ptr, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
-    PlanInput in{g->n, g->nhub, g->nslices, g->nsplit, g->idx16 ? 8 : 4, &sp, &hp, &g->slice_sig};
+    PlanInput in{g->n, g->nhub, g->nslices, g->nsplit, g->idx16 ? 8 : 4, &sp, &hp, &g->slice_sig,
+                 getenv("GN_PLAN_COLOCATE") != nullptr};
     HostPlan hpn;
     build_plan(in, G, exact, resident_cap, hpn);
     DevicePlan p;

@@ -57,15 +57,17 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
         for (int s = in.nsplit; s < in.nslices; ++s) units.push_back({0, s, kFixed + (double)nblk(s) * B});
     }
 
-    // ---- level 1: units -> CTAs.  Hub rows (the big units) LPT, then slices
-    // in signature order, as contiguous runs filling each CTA to the mean.
+    // ---- level 1: units -> CTAs, longest-processing-time-first on total
+    // cost.  With `colocate` the slices are instead taken in signature order
+    // as contiguous runs filling each CTA to the mean (neighbourhood-sharing
+    // slices on one SM); measured slower on C2/C3, kept for experiments.
     std::vector<std::vector<Unit>> per_cta((size_t)G);
     std::vector<double> load((size_t)G, 0.0);
     double total = 0.0;
     for (const Unit& u : units) total += u.cost;
     const double target = total / G;
     std::vector<Unit> big, small;
-    for (const Unit& u : units) (u.kind == 2 || u.kind == 3 ? big : small).push_back(u);
+    for (const Unit& u : units) (!in.colocate || u.kind == 2 || u.kind == 3 ? big : small).push_back(u);
     std::stable_sort(big.begin(), big.end(), [](const Unit& a, const Unit& b) { return a.cost > b.cost; });
     {
         MinHeap pq;
@@ -79,29 +81,24 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
             pq.push(e);
         }
     }
-    const auto& sig = *in.sig;
-    if (!sig.empty())
-        std::stable_sort(small.begin(), small.end(), [&](const Unit& a, const Unit& b) {
-            return sig[(size_t)a.id] != sig[(size_t)b.id] ? sig[(size_t)a.id] < sig[(size_t)b.id] : a.id < b.id;
-        });
-    {
-        // fill CTA b up to the running target; leftovers go to the least loaded
+    if (!small.empty()) {
+        const auto& sig = *in.sig;
+        if (!sig.empty())
+            std::stable_sort(small.begin(), small.end(), [&](const Unit& a, const Unit& b) {
+                return sig[(size_t)a.id] != sig[(size_t)b.id] ? sig[(size_t)a.id] < sig[(size_t)b.id] : a.id < b.id;
+            });
         size_t i = 0;
-        double placed = 0.0;
-        for (const Unit& u : small) placed += u.cost;
-        for (int b = 0; b < G && i < small.size(); ++b) {
+        for (int b = 0; b < G && i < small.size(); ++b)
             while (i < small.size() && load[(size_t)b] + small[i].cost * 0.5 <= target) {
                 per_cta[(size_t)b].push_back(small[i]);
                 load[(size_t)b] += small[i].cost;
                 ++i;
             }
-        }
         for (; i < small.size(); ++i) {
             int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
             per_cta[(size_t)b].push_back(small[i]);
             load[(size_t)b] += small[i].cost;
         }
-        (void)placed;
     }
 
     // ---- level 2: per CTA, phases of pieces (+ the short slices in phase 0)

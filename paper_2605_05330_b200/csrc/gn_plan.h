@@ -3,13 +3,10 @@
 // The kernel runs the same work every iteration, so who does what is decided
 // once per (graph, grid, mode) on the host and cached with the graph:
 //
-//   level 1  every unit (short slice, long slice, hub row) goes to a CTA.
-//            A CTA's warps share one SM's L1/LSU -- the resource gathers
-//            saturate -- so CTAs (not warps) are balanced on total gather
-//            count: hub rows first, longest-processing-time-first, then the
-//            slices in MinHash-signature order as contiguous runs that fill
-//            every CTA to the mean, so slices with overlapping neighbourhoods
-//            share an SM and its L1;
+//   level 1  every unit (short slice, long slice, hub row) goes to a CTA,
+//            longest-processing-time-first on its total gather count: a
+//            CTA's warps share one SM's L1/LSU, the resource gathers
+//            saturate, so CTAs (not warps) are what must be balanced;
 //   level 2  inside a CTA, long slices and hub rows are cut into fixed-size
 //            pieces (8 blocks of a slice, <= 1024 elements of a hub row:
 //            independent of the grid, so the summation tree -- and every bit
@@ -71,6 +68,7 @@ struct PlanInput {
     const std::vector<int64_t>* slice_ptr;
     const std::vector<int32_t>* hub_ptr;
     const std::vector<uint64_t>* sig;   // per-slice neighbourhood signature (may be empty)
+    bool colocate;                      // level 1 by signature runs instead of LPT
 };
 
 void build_plan(const PlanInput& in, int G, bool exact, size_t resident_cap_bytes, HostPlan& out);
