@@ -129,6 +129,27 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
 int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight,
                      int* independent, int* maximal, int64_t* count);
 
+/* ---- batches of independent graphs (BASELINE config C4) ----
+ * B graphs packed block-diagonally: graph b owns vertices
+ * [offsets[b], offsets[b+1]) and no edge leaves it.  Each graph runs its own
+ * run_wrgn (per-graph checks, early exit, non-finite stop) -- bitwise what
+ * gn_run gives graph by graph -- on one CTA with the graph resident in shared
+ * memory.  Graphs must have <= 4096 vertices and fit in shared memory.
+ * Outputs are per graph: step_inf / fallbacks / mass are [B][iters],
+ * iters_run / status (GN_OK or the gn_run error code) / fail_iter are [B]. */
+typedef struct gn_batch gn_batch;
+int gn_batch_create(int64_t num_graphs, const int64_t* offsets, int64_t n,
+                    const int64_t* indptr, const int32_t* indices,
+                    const double* w, int dtype, int device, gn_batch** out);
+int gn_batch_destroy(gn_batch* b);
+int gn_batch_info(const gn_batch* b, int64_t* num_graphs, int64_t* n,
+                  int64_t* device_bytes, int64_t* smem_bytes);
+int gn_batch_run(gn_batch* b, const void* x0, const double* gammas, int iters,
+                 double final_gamma, uint32_t flags, void* x_out,
+                 double* step_inf, int64_t* fallbacks, double* mass,
+                 int* iters_run, int* status, int* fail_iter,
+                 gn_run_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

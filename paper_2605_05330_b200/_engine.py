@@ -60,6 +60,10 @@ EXPORTED = (
     "gn_fitness",
     "gn_round",
     "gn_check_members",
+    "gn_batch_create",
+    "gn_batch_destroy",
+    "gn_batch_info",
+    "gn_batch_run",
 )
 
 
@@ -119,6 +123,13 @@ _SIGNATURES = {
     "gn_fitness": (_I32, [_P, _P, _D, _P, _PD]),
     "gn_round": (_I32, [_P, _P, _U32, _P, _PD, _PI, _PI, _PI64]),
     "gn_check_members": (_I32, [_P, _P, _PD, _PI, _PI, _PI64]),
+    "gn_batch_create": (_I32, [_I64, _P, _I64, _P, _P, _P, _I32, _I32, ctypes.POINTER(_P)]),
+    "gn_batch_destroy": (_I32, [_P]),
+    "gn_batch_info": (_I32, [_P, _PI64, _PI64, _PI64, _PI64]),
+    "gn_batch_run": (
+        _I32,
+        [_P, _P, _P, _I32, _D, _U32, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(RunStats)],
+    ),
 }
 
 _lib = None

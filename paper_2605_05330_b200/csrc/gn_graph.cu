@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -344,6 +345,7 @@ __global__ void k_init_state_weights(int64_t n, const double* __restrict__ w64, 
 static void free_graph(gn_graph* g) {
     if (!g) return;
     release_plans(g);
+    if (g->resident) batch_destroy(g->resident);
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
@@ -474,6 +476,18 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     GN_TRY(cudaStreamSynchronize(ctx.s));
 #undef GN_TRY
 #undef GN_UP
+    // small graphs also get the shared-memory-resident (CTA-per-graph) layout
+    if (n > 0 && n <= 4096 && !getenv("GN_NO_RESIDENT")) {
+        const int64_t offs[2] = {0, n};
+        gn_batch* r = nullptr;
+        if (batch_create(1, offs, n, indptr, indices, w, dtype, device, &r) == GN_OK) {
+            int max_optin = 0;
+            cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+            if (batch_smem_bytes(r) + 4096 <= (size_t)max_optin) g->resident = r;
+            else batch_destroy(r);
+        }
+        set_error("");
+    }
     *out = g;
     return GN_OK;
 }

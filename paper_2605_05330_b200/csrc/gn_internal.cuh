@@ -93,6 +93,7 @@ struct gn_graph {
     int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536)
     int64_t sell_elems = 0;
     std::vector<uint64_t> slice_sig;  // host: per-slice MinHash (gn_graph.cu, used by the plan)
+    gn_batch* resident = nullptr;     // small graphs: the whole-graph-in-shared-memory kernel
 };
 
 namespace gn {
@@ -148,5 +149,14 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
 
 int coresident_blocks(const void* kernel, int threads, size_t smem, int device, int* out);
 void release_plans(const gn_graph* g);  // gn_loop.cu: cached launch plans of g
+
+// gn_batch.cu: the resident (CTA-per-graph) kernel
+int batch_create(int64_t B, const int64_t* offsets, int64_t n, const int64_t* indptr, const int32_t* indices,
+                 const double* w, int dtype, int device, gn_batch** out);
+void batch_destroy(gn_batch* b);
+size_t batch_smem_bytes(const gn_batch* b);
+int batch_run(gn_batch* b, const void* x0, const double* gammas, int iters, double final_gamma, uint32_t flags,
+              void* x_out, double* step_inf, int64_t* fallbacks, double* mass, double* energy, double* pre_energy,
+              double* x_hist, int* iters_run, int* status, int* fail_iter, gn_run_stats* stats);
 
 }  // namespace gn

@@ -889,6 +889,14 @@ int gn_run(gn_graph* g, const void* x0, const double* gammas, int iters, double 
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (iters < 1) return fail(GN_ERR_ARG, "iterations must be positive");
     if (!gammas || (g->n > 0 && !x0)) return fail(GN_ERR_ARG, "null input array");
+    if (g->resident && !getenv("GN_NO_RESIDENT")) {
+        int st = GN_OK, fi = -1, ran = 0;
+        int rc = batch_run(g->resident, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks, mass,
+                           energy, pre_energy, x_hist, &ran, &st, &fi, stats);
+        if (iters_run) *iters_run = ran;
+        if (fail_iter) *fail_iter = fi;
+        return rc;
+    }
     switch (g->dtype) {
         case GN_F64:
             return run_idx<double, double>(g, x0, gammas, iters, final_gamma, flags, x_out, step_inf, fallbacks,
