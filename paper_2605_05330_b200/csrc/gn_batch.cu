@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -539,7 +540,11 @@ static int batch_run_typed(gn_batch* bt, const void* x0, const double* gammas, i
     a.smem_y_off = (int)(((size_t)bt->max_idx * 2 + 15) / 16 * 16);
     void* kern = trace ? (void*)k_gn_batch<TS, TG, true> : (void*)k_gn_batch<TS, TG, false>;
     GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int threads = (int)std::min<int64_t>(kBatchThreads, std::max<int64_t>(32, ((bt->max_n + kRowsPerThread - 1) / kRowsPerThread + 31) / 32 * 32));
+    // rows per thread: as few as the 1024-thread block allows (more warps to
+    // hide the dependent per-row add chains); GN_BATCH_THREADS overrides
+    int threads = (int)std::min<int64_t>(kBatchThreads, std::max<int64_t>(32, (bt->max_n + 31) / 32 * 32));
+    if (const char* e = getenv("GN_BATCH_THREADS")) threads = std::max(32, std::min(kBatchThreads, atoi(e)));
+    threads = std::max<int>(threads, (int)((bt->max_n + kRowsPerThread - 1) / kRowsPerThread + 31) / 32 * 32);
     GN_CUDA(cudaEventRecord(ev[1], s));
     if (B > 0 && n > 0) {
         void* args[] = {&a};
