@@ -252,15 +252,26 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
         slot[5] = (double)fbc;
         slot[6] = nf ? 1.0 : 0.0;
     }
-    __syncthreads();
-    for (int c = 0; c < 7; ++c) tot[c] = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-        const double* sl = s_red[k & 1][q];
+    __syncthreads();  // also publishes yn
+    // warp 0 folds the warp partials (fixed shuffle tree); only it holds tot
+    if (warp == 0) {
+        const int nw = (int)(blockDim.x >> 5);
+        const double* sl = s_red[k & 1][lane];
+        double t[7];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tot[c] = __dadd_rn(tot[c], sl[c]);
-        if (!(sl[4] <= tot[4])) tot[4] = sl[4];
-        tot[5] += sl[5];
-        if (sl[6] != 0.0) tot[6] = 1.0;
+        for (int c = 0; c < 7; ++c) t[c] = lane < nw ? sl[c] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) t[c] = __dadd_rn(t[c], __shfl_xor_sync(0xffffffffu, t[c], o));
+            const double m = __shfl_xor_sync(0xffffffffu, t[4], o);
+            if (!(m <= t[4])) t[4] = m;
+            t[5] += __shfl_xor_sync(0xffffffffu, t[5], o);
+            const double f = __shfl_xor_sync(0xffffffffu, t[6], o);
+            if (f != 0.0) t[6] = 1.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 7; ++c) tot[c] = t[c];
     }
 }
 
@@ -309,22 +320,28 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_gn_batch(BatchArgs<TS, TG>
     double* out_si = a.step_inf + b * a.iters;
     double* out_fb = a.fb + b * a.iters;
     double* out_dots = a.dots + b * (int64_t)(a.iters + 1) * 4;
-    int ran = 0, bad = -1;
+    __shared__ int s_stop;
+    int ran = 0, bad = -1;  // bad: tracked by thread 0
     double tot[7];
     for (int k = 0; k < a.iters; ++k) {
         batch_pass<TS, TG, TRACE>(a, R, s_idx, s_y, nb, k & 1, (TS)a.gammas[k], false, k, v0, s_red, tot);
+        ran = k + 1;
         if (threadIdx.x == 0) {
             out_si[k] = tot[4];
             out_fb[k] = tot[5];
 #pragma unroll
             for (int c = 0; c < 4; ++c) out_dots[(size_t)k * 4 + c] = tot[c];
+            if (tot[6] != 0.0 && bad < 0) bad = k;  // a non-finite state: reported, run continues
         }
-        ran = k + 1;
-        if (tot[6] != 0.0 && bad < 0) bad = k;
-        if (bad >= 0 && a.stop_nonfinite) break;
-        if (a.early_exit && a.gammas[k] == a.final_gamma && tot[4] < 1e-12) break;  // dynamics.py:177
+        if (a.early_exit && a.gammas[k] == a.final_gamma) {  // dynamics.py:177
+            if (threadIdx.x == 0) s_stop = tot[4] < 1e-12;
+            __syncthreads();
+            const int stop = s_stop;
+            __syncthreads();
+            if (stop) break;
+        }
     }
-    if (TRACE && !(bad >= 0 && a.stop_nonfinite)) {
+    if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         batch_pass<TS, TG, TRACE>(a, R, s_idx, s_y, nb, ran & 1, TS(0), true, ran, v0, s_red, tot);
         if (threadIdx.x == 0)
