@@ -150,6 +150,33 @@ int gn_batch_run(gn_batch* b, const void* x0, const double* gammas, int iters,
                  int* iters_run, int* status, int* fail_iter,
                  gn_run_stats* stats);
 
+/* ---- one vertex-range partition of a graph ----
+ * Owned vertices [0, n_own) and ghosts [n_own, n_own + n_ghost) (grouped by
+ * owning peer); indptr/indices: the owned rows over local ids, neighbour
+ * order as in the global graph; w: n_own + n_ghost weights.  Per iteration k
+ * on `stream` (0 = the partition's own stream): gn_part_step, then the halo:
+ * gn_part_pack (owned values at d_idx -> contiguous device buffer), the
+ * caller's exchange (NCCL send/recv on the same stream), gn_part_unpack
+ * (device buffer -> ghost slots [ghost_first, ghost_first + count)).
+ * gn_part_end returns x (clipped) and the owned rows' per-iteration stats
+ * (max|dx|, fallbacks, w.x'); the caller reduces them over partitions. */
+typedef struct gn_part gn_part;
+int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr,
+                   const int32_t* indices, const double* w, int dtype,
+                   int device, gn_part** out);
+int gn_part_destroy(gn_part* p);
+int gn_part_info(const gn_part* p, int64_t* n_own, int64_t* n_ghost, int64_t* nnz);
+int gn_part_elem_bytes(const gn_part* p);
+int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
+                  uint32_t flags);
+int gn_part_step(gn_part* p, int k, uintptr_t stream);
+int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count,
+                 void* d_out, uintptr_t stream);
+int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first,
+                   int64_t count, uintptr_t stream);
+int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf,
+                int64_t* fallbacks, double* mass, int* bad);
+
 #ifdef __cplusplus
 }
 #endif

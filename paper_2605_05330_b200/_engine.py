@@ -64,6 +64,15 @@ EXPORTED = (
     "gn_batch_destroy",
     "gn_batch_info",
     "gn_batch_run",
+    "gn_part_create",
+    "gn_part_destroy",
+    "gn_part_info",
+    "gn_part_elem_bytes",
+    "gn_part_begin",
+    "gn_part_step",
+    "gn_part_pack",
+    "gn_part_unpack",
+    "gn_part_end",
 )
 
 
@@ -130,6 +139,15 @@ _SIGNATURES = {
         _I32,
         [_P, _P, _P, _I32, _D, _U32, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(RunStats)],
     ),
+    "gn_part_create": (_I32, [_I64, _I64, _P, _P, _P, _I32, _I32, ctypes.POINTER(_P)]),
+    "gn_part_destroy": (_I32, [_P]),
+    "gn_part_info": (_I32, [_P, _PI64, _PI64, _PI64]),
+    "gn_part_elem_bytes": (_I32, [_P]),
+    "gn_part_begin": (_I32, [_P, _P, _P, _I32, _U32]),
+    "gn_part_step": (_I32, [_P, _I32, ctypes.c_size_t]),
+    "gn_part_pack": (_I32, [_P, _I32, _P, _I64, _P, ctypes.c_size_t]),
+    "gn_part_unpack": (_I32, [_P, _I32, _P, _I64, _I64, ctypes.c_size_t]),
+    "gn_part_end": (_I32, [_P, _I32, _P, _P, _P, _P, _PI]),
 }
 
 _lib = None

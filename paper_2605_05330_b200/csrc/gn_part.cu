@@ -1,0 +1,387 @@
+// gn_part.cu -- one vertex-range partition of a graph too large for one GPU
+// (BASELINE config C5): the owned rows' GN steps, with the
+// published values of ghost vertices supplied by a halo exchange between
+// iterations.
+//
+// Local numbering: owned vertices [0, n_own) (in the caller's order), ghosts
+// [n_own, n_own + n_ghost) grouped by owning peer.  Neighbour lists keep the
+// reference's order (ascending global id), so each owned row sums exactly as
+// the unpartitioned graph does and a partitioned run equals the single-GPU
+// run bit for bit.
+//
+// Per iteration k, on the caller's stream: gn_part_step (sums + updates of the
+// owned rows, one thread per row, sequential sums; per-block fixed-order stats
+// partials), then gn_part_pack (owned values -> contiguous send buffers), the
+// exchange (NCCL grouped send/recv, issued by the caller on the same stream),
+// gn_part_unpack (receive buffers -> ghost slots).  gn_part_end folds the
+// per-iteration stats in block order.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gn_internal.cuh"
+
+struct gn_part {
+    int64_t n_own = 0, n_ghost = 0, nnz = 0;
+    int dtype = GN_F64;
+    int device = 0;
+    int32_t* rowptr = nullptr;  // n_own+1
+    int32_t* col = nullptr;     // local ids
+    double* w64 = nullptr;      // n_own + n_ghost
+    // run state
+    int iters = 0;
+    uint32_t flags = 0;
+    void* x[2] = {nullptr, nullptr};   // state precision, n_own
+    void* yg[2] = {nullptr, nullptr};  // gathered precision, n_own + n_ghost
+    void* v = nullptr;                 // state precision, n_own + n_ghost
+    double* gam = nullptr;
+    double* part = nullptr;  // [iters][nblocks][4]: max|dx|, fallbacks, w.x', non-finite
+    int nblocks = 0;
+    cudaStream_t own_stream = nullptr;
+};
+
+namespace gn {
+
+constexpr int kPartThreads = 256;
+
+template <typename TS, typename TG>
+__global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __restrict__ x0,
+                               const double* __restrict__ w64, TS* __restrict__ x, TS* __restrict__ v,
+                               TG* __restrict__ yg) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n_all) return;
+    const TS vi = (TS)sqrt(w64[i]);  // graph.py:42
+    const TS xi = (TS)x0[i];
+    v[i] = vi;
+    yg[i] = (TG)Arith<TS>::mul(vi, xi);
+    if (i < n_own) x[i] = xi;
+}
+
+template <typename TS, typename TG>
+__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, const int32_t* __restrict__ rowptr,
+                                                            const int32_t* __restrict__ col,
+                                                            const double* __restrict__ w64, const TS* __restrict__ v,
+                                                            const TS* __restrict__ x, TS* __restrict__ xo,
+                                                            const TG* __restrict__ yg, TG* __restrict__ ygo,
+                                                            const double* __restrict__ gam, int k,
+                                                            double* __restrict__ part) {
+    using A = Arith<TS>;
+    const TS g = (TS)gam[k];
+    double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_own;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        TS s = TS(0);
+        for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = A::add(s, (TS)yg[col[p]]);  // scipy order
+        const TS xi = x[i], vi = v[i];
+        const TS yi = A::mul(vi, xi);
+        const TS d = A::add(yi, A::mul(g, s));          // dynamics.py:105
+        const bool ok = (double)d > kSafeDiv;            // dynamics.py:106
+        const TS o = ok ? A::div(yi, d) : TS(kFallback); // dynamics.py:107
+        xo[i] = o;
+        ygo[i] = (TG)A::mul(vi, o);
+        const TS dx = A::sub(o, xi);
+        const double diff = (double)(dx < TS(0) ? -dx : dx);
+        if (!(diff <= mx)) mx = diff;
+        fb += ok ? 0.0 : 1.0;
+        if (!isfinite((double)o)) nf = 1.0;
+        ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
+    }
+    __shared__ double red[kPartThreads / 32][4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double m = __shfl_xor_sync(0xffffffffu, mx, o);
+        if (!(m <= mx)) mx = m;
+        fb += __shfl_xor_sync(0xffffffffu, fb, o);
+        ob = __dadd_rn(ob, __shfl_xor_sync(0xffffffffu, ob, o));
+        nf = fmax(nf, __shfl_xor_sync(0xffffffffu, nf, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5][0] = mx;
+        red[threadIdx.x >> 5][1] = fb;
+        red[threadIdx.x >> 5][2] = ob;
+        red[threadIdx.x >> 5][3] = nf;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < kPartThreads / 32; ++q) {
+            if (!(red[q][0] <= t[0])) t[0] = red[q][0];
+            t[1] += red[q][1];
+            t[2] = __dadd_rn(t[2], red[q][2]);
+            t[3] = fmax(t[3], red[q][3]);
+        }
+        double* dst = part + ((size_t)k * gridDim.x + blockIdx.x) * 4;
+        dst[0] = t[0];
+        dst[1] = t[1];
+        dst[2] = t[2];
+        dst[3] = t[3];
+    }
+}
+
+// fold per-block stats of every iteration in block order (one warp per iteration)
+__global__ void k_part_fold(const double* __restrict__ part, int nblocks, int iters, double* __restrict__ out) {
+    const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= iters) return;
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = lane; b < nblocks; b += 32) {
+        const double* s = part + ((size_t)k * nblocks + b) * 4;
+        if (!(s[0] <= t[0])) t[0] = s[0];
+        t[1] += s[1];
+        t[2] = __dadd_rn(t[2], s[2]);
+        t[3] = fmax(t[3], s[3]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double m = __shfl_xor_sync(0xffffffffu, t[0], o);
+        if (!(m <= t[0])) t[0] = m;
+        t[1] += __shfl_xor_sync(0xffffffffu, t[1], o);
+        t[2] = __dadd_rn(t[2], __shfl_xor_sync(0xffffffffu, t[2], o));
+        t[3] = fmax(t[3], __shfl_xor_sync(0xffffffffu, t[3], o));
+    }
+    if (lane == 0)
+        for (int c = 0; c < 4; ++c) out[(size_t)k * 4 + c] = t[c];
+}
+
+template <typename TG>
+__global__ void k_part_pack(const TG* __restrict__ yg, const int32_t* __restrict__ idx, int64_t count,
+                            TG* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) out[i] = yg[idx[i]];
+}
+
+template <typename TG>
+__global__ void k_part_unpack(TG* __restrict__ yg, int64_t first, const TG* __restrict__ in, int64_t count) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) yg[first + i] = in[i];
+}
+
+template <typename TS, typename TOut>
+__global__ void k_part_out(int64_t n, const TS* __restrict__ x, TOut* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        double xi = (double)x[i];
+        out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);  // dynamics.py:179
+    }
+}
+
+static int pblocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kPartThreads - 1) / kPartThreads, 1 << 16)); }
+
+static void part_free_run(gn_part* p) {
+    void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
+    p->gam = p->part = nullptr;
+}
+
+}  // namespace gn
+
+using namespace gn;
+
+extern "C" {
+
+int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const int32_t* indices, const double* w,
+                   int dtype, int device, gn_part** out) {
+    *out = nullptr;
+    if (n_own < 0 || n_ghost < 0) return fail(GN_ERR_ARG, "bad partition sizes");
+    if (!valid_dtype(dtype)) return fail(GN_ERR_ARG, "dtype must be GN_F64, GN_F32 or GN_F32_PURE");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(GN_ERR_NODEV, "no CUDA device visible: the GN engine has no CPU fallback");
+    }
+    const int64_t nnz = n_own > 0 ? indptr[n_own] : 0;
+    if (nnz >= (int64_t(1) << 31)) return fail(GN_ERR_ARG, "partition too large");
+    for (int64_t p = 0; p < nnz; ++p)
+        if (indices[p] < 0 || indices[p] >= n_own + n_ghost) return fail(GN_ERR_ARG, "local column id out of range");
+    gn_part* P = new gn_part();
+    P->n_own = n_own;
+    P->n_ghost = n_ghost;
+    P->nnz = nnz;
+    P->dtype = dtype;
+    P->device = device;
+    CallCtx ctx;
+    int rc = ctx.open(device);
+    if (rc) { delete P; return rc; }
+    std::vector<int32_t> rp((size_t)n_own + 1);
+    for (int64_t i = 0; i <= n_own; ++i) rp[(size_t)i] = (int32_t)(n_own > 0 ? indptr[i] : 0);
+    const int64_t nall = n_own + n_ghost;
+    cudaError_t ce;
+    if ((ce = cudaMalloc(&P->rowptr, 4 * ((size_t)n_own + 1))) != cudaSuccess ||
+        (ce = cudaMalloc(&P->col, 4 * (size_t)std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+        (ce = cudaMalloc(&P->w64, 8 * (size_t)std::max<int64_t>(nall, 1))) != cudaSuccess) {
+        delete P;
+        return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
+    }
+    cudaMemcpy(P->rowptr, rp.data(), 4 * rp.size(), cudaMemcpyHostToDevice);
+    if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
+    if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
+    GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
+    *out = P;
+    return GN_OK;
+}
+
+int gn_part_destroy(gn_part* p) {
+    if (!p) return GN_OK;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    part_free_run(p);
+    cudaFree(p->rowptr);
+    cudaFree(p->col);
+    cudaFree(p->w64);
+    if (p->own_stream) cudaStreamDestroy(p->own_stream);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete p;
+    return GN_OK;
+}
+
+int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters, uint32_t flags) {
+    if (!p || iters < 1 || !gammas) return fail(GN_ERR_ARG, "bad gn_part_begin arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    part_free_run(p);
+    const int64_t nall = p->n_own + p->n_ghost;
+    const size_t es = state_bytes(p->dtype), gs = gather_bytes(p->dtype);
+    const size_t nb = (size_t)std::max<int64_t>(nall, 1);
+    p->iters = iters;
+    p->flags = flags;
+    p->nblocks = pblocks(p->n_own);
+    GN_CUDA(cudaMalloc(&p->x[0], es * nb));
+    GN_CUDA(cudaMalloc(&p->x[1], es * nb));
+    GN_CUDA(cudaMalloc(&p->yg[0], gs * nb));
+    GN_CUDA(cudaMalloc(&p->yg[1], gs * nb));
+    GN_CUDA(cudaMalloc(&p->v, es * nb));
+    GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
+    GN_CUDA(cudaMalloc((void**)&p->part, 32 * (size_t)iters * p->nblocks));
+    GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
+    double* dx0 = nullptr;
+    GN_CUDA(cudaMalloc((void**)&dx0, 8 * nb));
+    if (nall) GN_CUDA(cudaMemcpy(dx0, x0, 8 * (size_t)nall, cudaMemcpyHostToDevice));
+    if (nall > 0) {
+        const int blocks = pblocks(nall);
+        switch (p->dtype) {
+            case GN_F64:
+                k_part_prepare<double, double><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (double*)p->x[0],
+                                                                          (double*)p->v, (double*)p->yg[0]);
+                break;
+            case GN_F32:
+                k_part_prepare<double, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (double*)p->x[0],
+                                                                         (double*)p->v, (float*)p->yg[0]);
+                break;
+            default:
+                k_part_prepare<float, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (float*)p->x[0],
+                                                                        (float*)p->v, (float*)p->yg[0]);
+        }
+        GN_LAUNCHED();
+        // the ghost slots of the other buffer are filled by unpack before they are read
+        GN_CUDA(cudaMemcpy(p->yg[1], p->yg[0], gs * (size_t)nall, cudaMemcpyDeviceToDevice));
+    }
+    GN_CUDA(cudaDeviceSynchronize());
+    cudaFree(dx0);
+    return GN_OK;
+}
+
+int gn_part_step(gn_part* p, int k, uintptr_t stream) {
+    if (!p || k < 0 || k >= p->iters) return fail(GN_ERR_ARG, "iteration out of range");
+    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    const int cur = k & 1;
+    const int nb = p->nblocks;
+    switch (p->dtype) {
+        case GN_F64:
+            k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
+                p->n_own, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
+                (double*)p->x[cur ^ 1], (const double*)p->yg[cur], (double*)p->yg[cur ^ 1], p->gam, k, p->part);
+            break;
+        case GN_F32:
+            k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
+                p->n_own, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
+                (double*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
+            break;
+        default:
+            k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
+                p->n_own, p->rowptr, p->col, p->w64, (const float*)p->v, (const float*)p->x[cur],
+                (float*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
+    }
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+int gn_part_elem_bytes(const gn_part* p) { return p ? (int)gather_bytes(p->dtype) : 0; }
+
+// pack owned published values after step k (i.e. the values step k+1 reads)
+int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count, void* d_out, uintptr_t stream) {
+    if (!p || count < 0) return fail(GN_ERR_ARG, "bad pack arguments");
+    if (count == 0) return GN_OK;
+    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    const void* src = p->yg[(k & 1) ^ 1];
+    const int blocks = (int)((count + 255) / 256);
+    if (gather_bytes(p->dtype) == 8)
+        k_part_pack<double><<<blocks, 256, 0, s>>>((const double*)src, d_idx, count, (double*)d_out);
+    else
+        k_part_pack<float><<<blocks, 256, 0, s>>>((const float*)src, d_idx, count, (float*)d_out);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first, int64_t count, uintptr_t stream) {
+    if (!p || count < 0 || ghost_first < 0 || ghost_first + count > p->n_ghost) return fail(GN_ERR_ARG, "bad unpack");
+    if (count == 0) return GN_OK;
+    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    void* dst = p->yg[(k & 1) ^ 1];
+    const int blocks = (int)((count + 255) / 256);
+    if (gather_bytes(p->dtype) == 8)
+        k_part_unpack<double><<<blocks, 256, 0, s>>>((double*)dst, p->n_own + ghost_first, (const double*)d_in, count);
+    else
+        k_part_unpack<float><<<blocks, 256, 0, s>>>((float*)dst, p->n_own + ghost_first, (const float*)d_in, count);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+// stats of the owned rows after `done` iterations, x clipped
+int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* fallbacks, double* mass, int* bad) {
+    if (!p || done < 0 || done > p->iters) return fail(GN_ERR_ARG, "bad gn_part_end arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    GN_CUDA(cudaDeviceSynchronize());
+    double *dout = nullptr, *dx = nullptr;
+    GN_CUDA(cudaMalloc((void**)&dout, 32 * (size_t)std::max(done, 1)));
+    GN_CUDA(cudaMalloc((void**)&dx, 8 * (size_t)std::max<int64_t>(p->n_own, 1)));
+    if (done > 0) {
+        k_part_fold<<<(done + 7) / 8, 256>>>(p->part, p->nblocks, done, dout);
+        GN_LAUNCHED();
+    }
+    if (p->n_own > 0) {
+        if (state_bytes(p->dtype) == 8)
+            k_part_out<double, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const double*)p->x[done & 1], dx);
+        else
+            k_part_out<float, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const float*)p->x[done & 1], dx);
+        GN_LAUNCHED();
+    }
+    std::vector<double> h(4 * (size_t)std::max(done, 1));
+    GN_CUDA(cudaMemcpy(h.data(), dout, 32 * (size_t)done, cudaMemcpyDeviceToHost));
+    if (x_out && p->n_own) GN_CUDA(cudaMemcpy(x_out, dx, 8 * (size_t)p->n_own, cudaMemcpyDeviceToHost));
+    cudaFree(dout);
+    cudaFree(dx);
+    if (bad) *bad = -1;
+    for (int k = 0; k < done; ++k) {
+        if (step_inf) step_inf[k] = h[(size_t)k * 4];
+        if (fallbacks) fallbacks[k] = (int64_t)h[(size_t)k * 4 + 1];
+        if (mass) mass[k] = h[(size_t)k * 4 + 2];
+        if (bad && *bad < 0 && h[(size_t)k * 4 + 3] != 0.0) *bad = k;
+    }
+    return GN_OK;
+}
+
+int gn_part_info(const gn_part* p, int64_t* n_own, int64_t* n_ghost, int64_t* nnz) {
+    if (!p) return fail(GN_ERR_ARG, "null partition");
+    if (n_own) *n_own = p->n_own;
+    if (n_ghost) *n_ghost = p->n_ghost;
+    if (nnz) *nnz = p->nnz;
+    return GN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+"""Vertex-range partitioning of one graph over several GPUs.
+
+Each partition owns a contiguous range of vertices, chosen so every part
+holds about the same number of adjacency entries (R-MAT concentrates its hubs
+at low ids, so equal vertex counts would be badly imbalanced).  A part's
+neighbours outside its range are its ghosts, sorted by global id -- which
+groups them by owning peer, since ranges are contiguous.  Every iteration:
+
+    step     each part updates its owned rows (csrc/gn_part.cu), reading the
+             published values of owned vertices and ghosts
+    halo     each part packs the published values its peers hold as ghosts
+             and sends them; received buffers are unpacked into ghost slots
+
+Neighbour lists keep the global (reference) order, so a partitioned run is
+bitwise the single-GPU run.  Exchanges: LocalExchange (all parts in one
+process, e.g. one GPU, for tests) and DistExchange (one part per rank,
+torch.distributed send/recv: NCCL over NVLink on GPUs, gloo on CPU tests).
+The compute backend is pluggable; EngineBackend is the CUDA engine.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .dynamics import GammaSchedule
+
+
+@dataclass
+class PartSpec:
+    """Local view of partition p."""
+
+    p: int
+    parts: int
+    lo: int
+    hi: int
+    ghosts: np.ndarray        # global ids, ascending
+    ghost_ptr: np.ndarray     # [parts+1]: ghosts owned by peer q are ghosts[ghost_ptr[q]:ghost_ptr[q+1]]
+    indptr: np.ndarray        # owned rows, local column ids
+    indices: np.ndarray       # int32 in [0, n_own + n_ghost)
+    w: np.ndarray             # n_own + n_ghost
+    send_idx: dict = field(default_factory=dict)  # peer q -> local owned ids q holds as ghosts (q's order)
+
+    @property
+    def n_own(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def n_ghost(self) -> int:
+        return len(self.ghosts)
+
+    def local_x0(self, x0_global: np.ndarray) -> np.ndarray:
+        return np.concatenate([x0_global[self.lo:self.hi], x0_global[self.ghosts]]).astype(np.float64)
+
+
+def partition_ranges(indptr: np.ndarray, parts: int) -> np.ndarray:
+    """Contiguous vertex ranges with about equal adjacency entries (+1 per
+    vertex so empty rows still count): [parts+1] boundaries."""
+    n = len(indptr) - 1
+    if parts < 1:
+        raise ValueError("parts must be positive")
+    cost = np.diff(np.asarray(indptr, dtype=np.int64)) + 1
+    cum = np.concatenate([[0], np.cumsum(cost)])
+    targets = cum[-1] * np.arange(1, parts) / parts
+    cuts = np.searchsorted(cum, targets, side="left")
+    bounds = np.concatenate([[0], np.clip(cuts, 0, n), [n]]).astype(np.int64)
+    return np.maximum.accumulate(bounds)
+
+
+def build_partitions(g, parts: int, bounds: Optional[np.ndarray] = None) -> list[PartSpec]:
+    """Local views of every partition of g (host-side setup, done once)."""
+    indptr = np.asarray(g.indptr, dtype=np.int64)
+    indices = np.asarray(g.indices, dtype=np.int64)
+    w = np.asarray(g.w, dtype=np.float64)
+    bounds = partition_ranges(indptr, parts) if bounds is None else np.asarray(bounds, dtype=np.int64)
+    specs = []
+    for p in range(parts):
+        lo, hi = int(bounds[p]), int(bounds[p + 1])
+        cols = indices[indptr[lo]:indptr[hi]]
+        ghosts = np.unique(cols[(cols < lo) | (cols >= hi)])
+        owner = np.searchsorted(bounds, ghosts, side="right") - 1
+        ghost_ptr = np.searchsorted(owner, np.arange(parts + 1), side="left").astype(np.int64)
+        local = np.where((cols >= lo) & (cols < hi), cols - lo,
+                         (hi - lo) + np.searchsorted(ghosts, cols)).astype(np.int32)
+        specs.append(PartSpec(p, parts, lo, hi, ghosts, ghost_ptr, indptr[lo:hi + 1] - indptr[lo], local,
+                              np.concatenate([w[lo:hi], w[ghosts]])))
+    for p, sp in enumerate(specs):
+        for q, sq in enumerate(specs):
+            if q == p:
+                continue
+            need = sq.ghosts[sq.ghost_ptr[p]:sq.ghost_ptr[p + 1]]  # q's ghosts owned by p
+            if len(need):
+                sp.send_idx[q] = (need - sp.lo).astype(np.int32)
+    return specs
+
+
+# ---------------------------------------------------------------- backends
+
+class EngineBackend:
+    """One partition on the CUDA engine (gn_part_*)."""
+
+    def __init__(self, spec: PartSpec, dtype="fp64", device: int = 0):
+        import torch
+
+        from . import _engine as E
+        from .graph import dtype_code
+
+        self.E, self.torch, self.spec = E, torch, spec
+        self.device = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        E.check(E.lib().gn_part_create(spec.n_own, spec.n_ghost, E.ptr(np.ascontiguousarray(spec.indptr)),
+                                       E.ptr(np.ascontiguousarray(spec.indices)), E.ptr(np.ascontiguousarray(spec.w)),
+                                       dtype_code(dtype), device, ctypes.byref(h)))
+        self.h = h
+        self.elem = E.lib().gn_part_elem_bytes(h)
+        self.tdtype = torch.float64 if self.elem == 8 else torch.float32
+        self.send_idx = {q: torch.from_numpy(v).to(self.device) for q, v in spec.send_idx.items()}
+
+    def _stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def begin(self, x0_local: np.ndarray, gammas: np.ndarray) -> None:
+        E = self.E
+        self.gam = np.ascontiguousarray(gammas, dtype=np.float64)
+        E.check(E.lib().gn_part_begin(self.h, E.ptr(np.ascontiguousarray(x0_local, dtype=np.float64)),
+                                      E.ptr(self.gam), len(self.gam), 0))
+
+    def step(self, k: int) -> None:
+        self.E.check(self.E.lib().gn_part_step(self.h, k, self._stream()))
+
+    def empty(self, count: int):
+        return self.torch.empty(count, dtype=self.tdtype, device=self.device)
+
+    def pack(self, k: int, q: int):
+        idx = self.send_idx[q]
+        buf = self.empty(len(idx))
+        self.E.check(self.E.lib().gn_part_pack(self.h, k, ctypes.c_void_p(idx.data_ptr()), len(idx),
+                                               ctypes.c_void_p(buf.data_ptr()), self._stream()))
+        return buf
+
+    def unpack(self, k: int, q: int, buf) -> None:
+        first = int(self.spec.ghost_ptr[q])
+        self.E.check(self.E.lib().gn_part_unpack(self.h, k, ctypes.c_void_p(buf.data_ptr()), first, buf.numel(),
+                                                 self._stream()))
+
+    def end(self, done: int):
+        E = self.E
+        x = np.empty(self.spec.n_own)
+        si = np.zeros(max(done, 1))
+        fb = np.zeros(max(done, 1), dtype=np.int64)
+        ms = np.zeros(max(done, 1))
+        bad = ctypes.c_int(-1)
+        E.check(E.lib().gn_part_end(self.h, done, E.ptr(x), E.ptr(si), E.ptr(fb), E.ptr(ms), ctypes.byref(bad)))
+        return x, si[:done], fb[:done], ms[:done], bad.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None) is not None:
+            self.E.lib().gn_part_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- exchanges
+
+class LocalExchange:
+    """All partitions in this process: the halo is a buffer hand-over."""
+
+    def __init__(self, backends: Sequence):
+        self.backends = list(backends)
+
+    def halo(self, k: int) -> None:
+        outgoing = {}
+        for p, b in enumerate(self.backends):
+            for q in b.spec.send_idx:
+                outgoing[(p, q)] = b.pack(k, q)
+        for (p, q), buf in outgoing.items():
+            self.backends[q].unpack(k, p, buf)
+
+
+class DistExchange:
+    """One partition per rank; grouped point-to-point sends/receives
+    (torch.distributed: NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, backend, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.b, self.group = dist, backend, group
+        spec = backend.spec
+        self.recv_from = [q for q in range(spec.parts) if q != spec.p and spec.ghost_ptr[q + 1] > spec.ghost_ptr[q]]
+
+    def halo(self, k: int) -> None:
+        dist, b = self.dist, self.b
+        spec = b.spec
+        ops, recvs = [], []
+        for q in self.recv_from:
+            buf = b.empty(int(spec.ghost_ptr[q + 1] - spec.ghost_ptr[q]))
+            recvs.append((q, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, q, self.group))
+        for q in spec.send_idx:
+            ops.append(dist.P2POp(dist.isend, b.pack(k, q), q, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for q, buf in recvs:
+            b.unpack(k, q, buf)
+
+
+@dataclass
+class PartResult:
+    x: np.ndarray            # owned entries (clipped)
+    step_inf: np.ndarray     # this part's per-iteration max|dx|
+    fallbacks: np.ndarray
+    mass: np.ndarray         # this part's w.x'
+    bad: int
+
+
+def run_partition(backend, exchange, x0_local: np.ndarray, schedule: GammaSchedule) -> PartResult:
+    """The pursuit on one partition (all ranks call this together)."""
+    gam = schedule.table()
+    backend.begin(x0_local, gam)
+    for k in range(len(gam)):
+        backend.step(k)
+        exchange.halo(k)
+    x, si, fb, ms, bad = backend.end(len(gam))
+    return PartResult(x, si, fb, ms, bad)
+
+
+def run_local_partitions(g, x0: np.ndarray, schedule: GammaSchedule, parts: int, make_backend) -> dict:
+    """All parts of g in this process (e.g. on one GPU): returns the global x
+    and the combined per-iteration trace (max / sum / sum over parts)."""
+    specs = build_partitions(g, parts)
+    backends = [make_backend(s) for s in specs]
+    ex = LocalExchange(backends)
+    gam = schedule.table()
+    for b, s in zip(backends, specs):
+        b.begin(s.local_x0(x0), gam)
+    for k in range(len(gam)):
+        for b in backends:
+            b.step(k)
+        ex.halo(k)
+    outs = [b.end(len(gam)) for b in backends]
+    x = np.concatenate([o[0] for o in outs])
+    return {"x": x, "step_inf": np.max([o[1] for o in outs], axis=0), "fallbacks": np.sum([o[2] for o in outs], axis=0),
+            "mass": np.sum([o[3] for o in outs], axis=0), "specs": specs}

@@ -1,0 +1,155 @@
+"""Vertex-range partitioning (C5 path): host-side partition/halo logic and the
+multi-rank protocol, on CPU.  The 2-rank test runs the real DistExchange over
+torch.distributed (gloo, 127.0.0.1) with a numpy stand-in for the per-part
+GPU compute (test infrastructure, scipy's sequential csr_matvec = the
+reference order), and checks the assembled trajectory bitwise against the
+unpartitioned oracle."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import gn_oracle as O
+import paper_2605_05330_b200 as P
+from paper_2605_05330_b200 import generators as G
+from paper_2605_05330_b200.partition import (DistExchange, LocalExchange, build_partitions, partition_ranges,
+                                             run_partition)
+
+
+class NumpyBackend:
+    """CPU stand-in for EngineBackend (tests only): same step, fp64."""
+
+    def __init__(self, spec):
+        import scipy.sparse as sp
+        import torch
+
+        self.torch, self.spec = torch, spec
+        self.A = sp.csr_matrix((np.ones(len(spec.indices)), spec.indices, spec.indptr),
+                               shape=(spec.n_own, spec.n_own + spec.n_ghost))
+        self.v = np.sqrt(spec.w)
+
+    def begin(self, x0_local, gammas):
+        self.gam = gammas
+        self.x = x0_local[: self.spec.n_own].copy()
+        self.y = [self.v * x0_local, self.v * x0_local]
+        self.si, self.fb, self.ms = [], [], []
+
+    def step(self, k):
+        yc = self.y[k & 1]
+        s = self.A @ yc
+        yi = self.v[: self.spec.n_own] * self.x
+        d = yi + self.gam[k] * s
+        ok = d > 1e-9
+        o = np.where(ok, yi / np.where(ok, d, 1.0), 0.5)
+        self.si.append(float(np.max(np.abs(o - self.x))) if len(o) else 0.0)
+        self.fb.append(int(len(o) - np.count_nonzero(ok)))
+        self.x = o
+        self.y[(k & 1) ^ 1][: self.spec.n_own] = self.v[: self.spec.n_own] * o
+
+    def empty(self, count):
+        return self.torch.empty(count, dtype=self.torch.float64)
+
+    def pack(self, k, q):
+        return self.torch.from_numpy(self.y[(k & 1) ^ 1][self.spec.send_idx[q]].copy())
+
+    def unpack(self, k, q, buf):
+        first = self.spec.n_own + int(self.spec.ghost_ptr[q])
+        self.y[(k & 1) ^ 1][first:first + buf.numel()] = buf.numpy()
+
+    def end(self, done):
+        return np.clip(self.x, 0, 1), np.array(self.si), np.array(self.fb), np.zeros(done), -1
+
+
+def _graph():
+    return G.c5_rmat(11)
+
+
+def test_partition_ranges_balance_and_cover():
+    g = _graph().graph
+    for parts in (1, 2, 3, 8):
+        b = partition_ranges(g.indptr, parts)
+        assert b[0] == 0 and b[-1] == g.n and np.all(np.diff(b) >= 0)
+        cost = np.diff(g.indptr) + 1
+        loads = [cost[b[p]:b[p + 1]].sum() for p in range(parts)]
+        assert max(loads) <= cost.sum() / parts + cost.max()
+
+
+def test_local_views_reproduce_global_rows_and_halo_lists():
+    g = _graph().graph
+    specs = build_partitions(g, 3)
+    for s in specs:
+        glob = np.concatenate([np.arange(s.lo, s.hi), s.ghosts])
+        for r in range(s.n_own):
+            row = glob[s.indices[s.indptr[r]:s.indptr[r + 1]]]
+            np.testing.assert_array_equal(row, g.neighbors(s.lo + r))  # same order
+        for q, t in enumerate(specs):
+            if q == s.p:
+                continue
+            owned_by_q = s.ghosts[s.ghost_ptr[q]:s.ghost_ptr[q + 1]]
+            sent = t.send_idx.get(s.p, np.zeros(0, np.int32)) + t.lo
+            np.testing.assert_array_equal(owned_by_q, sent)
+
+
+def test_local_exchange_protocol_is_bitwise_unpartitioned():
+    inst = _graph()
+    s = P.GammaSchedule.pursuit(iterations=200)
+    specs = build_partitions(inst.graph, 4)
+    backends = [NumpyBackend(sp) for sp in specs]
+    ex = LocalExchange(backends)
+    gam = s.table()
+    for b, sp in zip(backends, specs):
+        b.begin(sp.local_x0(inst.x0), gam)
+    for k in range(len(gam)):
+        for b in backends:
+            b.step(k)
+        ex.halo(k)
+    x = np.concatenate([b.end(len(gam))[0] for b in backends])
+    ref = O.run(inst.graph, inst.x0, gam, s.final_gamma)
+    np.testing.assert_array_equal(x, ref.x)
+    np.testing.assert_array_equal(np.max([b.si for b in backends], axis=0), ref.step_inf)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst = _graph()
+        s = P.GammaSchedule.pursuit(iterations=150)
+        spec = build_partitions(inst.graph, world)[rank]
+        be = NumpyBackend(spec)
+        res = run_partition(be, DistExchange(be), spec.local_x0(inst.x0), s)
+        out = [None] * world
+        dist.all_gather_object(out, (spec.lo, res.x, res.step_inf, res.fallbacks))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_halo_exchange_is_bitwise_unpartitioned():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    x = np.concatenate([o[1] for o in out])
+    inst = _graph()
+    s = P.GammaSchedule.pursuit(iterations=150)
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma)
+    np.testing.assert_array_equal(x, ref.x)
+    np.testing.assert_array_equal(np.max([o[2] for o in out], axis=0), ref.step_inf)
+    np.testing.assert_array_equal(np.sum([o[3] for o in out], axis=0), ref.fallbacks)
