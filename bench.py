@@ -246,7 +246,7 @@ def main():
         kernel_name = "gn::k_gn_batch (one CTA per graph, graph resident in shared memory)"
 
         def device_step():
-            r = gb.run(None, sched, device_x0=x0_dev.data_ptr(), device_x_out=x_out.data_ptr())
+            r = gb.run(None, sched, device_x0=x0_dev.data_ptr(), device_x_out=x_out.data_ptr(), traces=False)
             st = E.RunStats()
             for f, _ in E.RunStats._fields_:
                 setattr(st, f, r.stats[f])

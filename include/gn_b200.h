@@ -154,7 +154,7 @@ int gn_batch_run(gn_batch* b, const void* x0, const double* gammas, int iters,
  * Owned vertices [0, n_own) and ghosts [n_own, n_own + n_ghost) (grouped by
  * owning peer); indptr/indices: the owned rows over local ids, neighbour
  * order as in the global graph; w: n_own + n_ghost weights.  Per iteration k
- * on `stream` (0 = the partition's own stream): gn_part_step, then the halo:
+ * on `stream` (a cudaStream_t; 0 = the legacy default stream): gn_part_step, then the halo:
  * gn_part_pack (owned values at d_idx -> contiguous device buffer), the
  * caller's exchange (NCCL send/recv on the same stream), gn_part_unpack
  * (device buffer -> ghost slots [ghost_first, ghost_first + count)).

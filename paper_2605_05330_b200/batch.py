@@ -77,7 +77,7 @@ class GraphBatch:
         return {"graphs": B.value, "n": n.value, "device_bytes": db.value, "smem_bytes_per_graph_cta": sm.value}
 
     def run(self, x0, schedule: GammaSchedule, early_exit: bool = False, *, raise_on_error: bool = False,
-            device_x0=None, device_x_out=None) -> BatchResult:
+            device_x0=None, device_x_out=None, traces: bool = True) -> BatchResult:
         """run_wrgn on every graph.  x0 is the packed start (host numpy), or
         device_x0/device_x_out are fp64 CUDA pointers (inputs already in HBM)."""
         iters = schedule.iterations
@@ -100,9 +100,9 @@ class GraphBatch:
                 raise ValueError(f"x0 has shape {xh.shape}, expected ({self.graph.n},)")
             x = np.empty(self.graph.n)
             xin, xout = E.ptr(xh), E.ptr(x)
+        tr = (E.ptr(si), E.ptr(fb), E.ptr(ob)) if traces else (None, None, None)
         rc = self._lib.gn_batch_run(self._h, xin, E.ptr(gam), iters, float(schedule.final_gamma), flags, xout,
-                                    E.ptr(si), E.ptr(fb), E.ptr(ob), E.ptr(ran), E.ptr(status), E.ptr(fail),
-                                    ctypes.byref(st))
+                                    *tr, E.ptr(ran), E.ptr(status), E.ptr(fail), ctypes.byref(st))
         if rc not in (E.GN_OK, E.GN_ERR_NEGATIVE, E.GN_ERR_NOT_NORMALIZABLE, E.GN_ERR_NONFINITE):
             E.check(rc)
         if raise_on_error and rc != E.GN_OK:

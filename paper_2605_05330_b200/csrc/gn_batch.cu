@@ -571,13 +571,17 @@ static int batch_run_typed(gn_batch* bt, const void* x0, const double* gammas, i
     GN_CUDA(cudaEventRecord(ev[2], s));
     std::vector<double> hsi((size_t)B * iters), hfb((size_t)B * iters), hd(4 * (size_t)B * (iters + 1));
     std::vector<int> hran((size_t)B, 0), hbad((size_t)B, -1);
+    const bool want_trace = step_inf || fallbacks || mass || energy || pre_energy;
     if (n > 0) {
-        GN_CUDA(cudaMemcpyAsync(hsi.data(), dsi, 8 * hsi.size(), cudaMemcpyDeviceToHost, s));
-        GN_CUDA(cudaMemcpyAsync(hfb.data(), dfb, 8 * hfb.size(), cudaMemcpyDeviceToHost, s));
-        GN_CUDA(cudaMemcpyAsync(hd.data(), dd, 8 * hd.size(), cudaMemcpyDeviceToHost, s));
+        if (want_trace) {  // per-graph traces only when asked for (B x iters values each)
+            GN_CUDA(cudaMemcpyAsync(hsi.data(), dsi, 8 * hsi.size(), cudaMemcpyDeviceToHost, s));
+            GN_CUDA(cudaMemcpyAsync(hfb.data(), dfb, 8 * hfb.size(), cudaMemcpyDeviceToHost, s));
+            GN_CUDA(cudaMemcpyAsync(hd.data(), dd, 8 * hd.size(), cudaMemcpyDeviceToHost, s));
+            d2h += 8 * (int64_t)(hsi.size() + hfb.size() + hd.size());
+        }
         GN_CUDA(cudaMemcpyAsync(hran.data(), dran, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
         GN_CUDA(cudaMemcpyAsync(hbad.data(), dbad, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
-        d2h += 8 * (int64_t)(hsi.size() + hfb.size() + hd.size()) + 8 * B;
+        d2h += 8 * B;
         if (x_out && !dev_io) {
             GN_CUDA(cudaMemcpyAsync(x_out, xout, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
             d2h += 8 * n;

@@ -173,7 +173,9 @@ __device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ 
     using A = Arith<TS>;
     using V = LaneVec<TI>;
     constexpr int B = V::B;
-    constexpr int NB = (sizeof(TG) == 4 ? 16 : 8) / B > 0 ? (sizeof(TG) == 4 ? 16 : 8) / B : 1;
+    // gathers in flight per lane: 32 four-byte or 16 eight-byte values
+    constexpr int GIF = sizeof(TG) == 4 ? 32 : 16;
+    constexpr int NB = GIF / B > 0 ? GIF / B : 1;
     TS s = TS(0);
     be = min(be, (d + B - 1) / B);  // blocks past the row's end hold no neighbours
     if (bb >= be) return s;

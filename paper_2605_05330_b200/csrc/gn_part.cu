@@ -288,7 +288,7 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
 
 int gn_part_step(gn_part* p, int k, uintptr_t stream) {
     if (!p || k < 0 || k >= p->iters) return fail(GN_ERR_ARG, "iteration out of range");
-    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0: the legacy default stream (orders with torch's)
     const int cur = k & 1;
     const int nb = p->nblocks;
     switch (p->dtype) {
@@ -317,7 +317,7 @@ int gn_part_elem_bytes(const gn_part* p) { return p ? (int)gather_bytes(p->dtype
 int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count, void* d_out, uintptr_t stream) {
     if (!p || count < 0) return fail(GN_ERR_ARG, "bad pack arguments");
     if (count == 0) return GN_OK;
-    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0: the legacy default stream (orders with torch's)
     const void* src = p->yg[(k & 1) ^ 1];
     const int blocks = (int)((count + 255) / 256);
     if (gather_bytes(p->dtype) == 8)
@@ -331,7 +331,7 @@ int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count, void* d
 int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first, int64_t count, uintptr_t stream) {
     if (!p || count < 0 || ghost_first < 0 || ghost_first + count > p->n_ghost) return fail(GN_ERR_ARG, "bad unpack");
     if (count == 0) return GN_OK;
-    cudaStream_t s = stream ? (cudaStream_t)stream : p->own_stream;
+    cudaStream_t s = (cudaStream_t)stream;  // 0: the legacy default stream (orders with torch's)
     void* dst = p->yg[(k & 1) ^ 1];
     const int blocks = (int)((count + 255) / 256);
     if (gather_bytes(p->dtype) == 8)

@@ -26,9 +26,9 @@
 
 namespace gn {
 
-constexpr int kThreads = 1024;  // one CTA per SM
+constexpr int kThreads = 512;   // one CTA per SM; 128 registers per thread for deep gather batches
 constexpr int kWarps = kThreads / 32;
-constexpr int kPieceBlocks = 4;      // blocks per piece of a long slice
+constexpr int kPieceBlocks = 8;      // blocks per piece of a long slice
 constexpr int kHubPieceElems = 1024; // elements per piece of a hub row (at least)
 constexpr int kMaxSlots = 256;       // slice-piece slots per phase (32 partials each)
 constexpr int kMaxHubSlots = 512;    // hub-piece slots per phase (1 partial each)
