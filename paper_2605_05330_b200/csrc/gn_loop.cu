@@ -85,6 +85,8 @@ struct LoopArgs {
     const int32_t* __restrict__ perm;
     long long* prof;   // optional timestamps (GN_PROF_ITER): [G][kWarps+4]
     int prof_iter;
+    int dbg;           // GN_DEBUG_GATHER (timing experiments only; results are wrong when set):
+                       // 1 = gathers read a fixed element, 2 = no index loads
 };
 
 struct Stats {
@@ -169,7 +171,7 @@ struct LaneVec<int32_t> {
 // vectors are requested before this batch's gathers, so a batch costs one
 // memory round trip; the adds stay in position order (the reference's order).
 template <typename TS, typename TG, typename TI>
-__device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ yg, int d, int bb, int be) {
+__device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ yg, int d, int bb, int be, int dbg) {
     using A = Arith<TS>;
     using V = LaneVec<TI>;
     constexpr int B = V::B;
@@ -180,14 +182,20 @@ __device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ 
     be = min(be, (d + B - 1) / B);  // blocks past the row's end hold no neighbours
     if (bb >= be) return s;
     uint4 v[NB];
+    const uint4 fake = make_uint4(threadIdx.x, threadIdx.x * 3, threadIdx.x * 5, threadIdx.x * 7);
 #pragma unroll
     for (int u = 0; u < NB; ++u)
-        if (bb + u < be) v[u] = base[(size_t)(bb + u) * kSlice];
+        if (bb + u < be) v[u] = dbg == 2 ? fake : base[(size_t)(bb + u) * kSlice];
+    if (dbg == 1) yg = yg + 0;
     for (int b = bb; b < be; b += NB) {
         uint4 vn[NB];
 #pragma unroll
         for (int u = 0; u < NB; ++u)
-            if (b + NB + u < be) vn[u] = base[(size_t)(b + NB + u) * kSlice];
+            if (b + NB + u < be) vn[u] = dbg == 2 ? fake : base[(size_t)(b + NB + u) * kSlice];
+        if (dbg == 1) {
+#pragma unroll
+            for (int u = 0; u < NB; ++u) v[u] = make_uint4(0, 0, 0, 0);
+        }
         TG y[NB * B];
         if (b + NB <= be && (b + NB) * B <= d) {
 #pragma unroll
@@ -214,6 +222,88 @@ __device__ __forceinline__ const uint4* slice_base(const LoopArgs<TS, TG>& a, co
                                                    int lane) {
     if (it.smem >= 0) return s_res + it.smem - (ptrdiff_t)it.beg * kSlice + lane;
     return reinterpret_cast<const uint4*>((const TI*)a.sell + __ldg(a.slice_ptr + it.id)) + lane;
+}
+
+// ---- software-pipelined slice items -----------------------------------
+// A warp walks its slice items (short slices and pieces of long slices) with
+// a two-deep pipeline: while item i's gathers are in flight, item i+1's
+// degree, row state and first index vectors are already loading, and item
+// i+2's descriptor too.  Each item costs about one memory round trip instead
+// of four dependent ones.
+template <typename TG>
+struct GatherDepth {
+    static constexpr int value = sizeof(TG) == 4 ? 32 : 16;  // gathers in flight per lane
+};
+
+template <typename TS, typename TI, typename TG>
+struct SlicePre {
+    static constexpr int B = LaneVec<TI>::B;
+    // index vectors per batch, at most 4 (two batches of them are live at once)
+    static constexpr int NB = GatherDepth<TG>::value / B > 4 ? 4 : (GatherDepth<TG>::value / B > 0 ? GatherDepth<TG>::value / B : 1);
+    const uint4* base;  // block `beg` of the item, this lane
+    int beg, nb, d, row;
+    bool whole, valid;
+    RowIn<TS> in;
+    uint4 v[NB];
+};
+
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
+                                               int lane, int cur, SlicePre<TS, TI, TG>& p) {
+    using SP = SlicePre<TS, TI, TG>;
+    p.whole = it.kind == kWhole;
+    p.beg = it.beg;
+    p.nb = it.end - it.beg;
+    const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + lane;
+    p.valid = r < a.n;
+    p.row = (int)r;
+    // Item.pad0/pad1: 16-byte-word offset of block `beg` in the global index array
+    const int64_t goff = ((int64_t)(uint32_t)it.pad1 << 32) | (uint32_t)it.pad0;
+    p.base = (it.smem >= 0 ? s_res + it.smem : reinterpret_cast<const uint4*>(a.sell) + goff) + lane;
+    p.d = p.valid ? __ldg(a.row_deg + (size_t)it.id * kSlice + lane) : 0;
+    if (p.whole && p.valid) p.in = row_in(a, p.row, cur);
+#pragma unroll
+    for (int u = 0; u < SP::NB; ++u)
+        if (u < p.nb) p.v[u] = p.base[(size_t)u * kSlice];
+}
+
+// Sequential sum of one lane's row over the item's blocks; p.v holds the
+// first batch of index vectors.
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const TG* __restrict__ yg) {
+    using A = Arith<TS>;
+    using V = LaneVec<TI>;
+    using SP = SlicePre<TS, TI, TG>;
+    constexpr int B = SP::B, NB = SP::NB;
+    TS s = TS(0);
+    const int d = p.d;
+    // local blocks that hold any of this row's neighbours
+    const int be = min(p.nb, max(0, (d - p.beg * B + B - 1) / B));
+    for (int b = 0; b < be; b += NB) {
+        uint4 vn[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+            if (b + NB + u < be) vn[u] = p.base[(size_t)(b + NB + u) * kSlice];
+        TG y[NB * B];
+        const int pos0 = (p.beg + b) * B;
+        if (b + NB <= be && pos0 + NB * B <= d) {
+#pragma unroll
+            for (int u = 0; u < NB; ++u)
+#pragma unroll
+                for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(p.v[u], t)];
+        } else {
+#pragma unroll
+            for (int u = 0; u < NB; ++u)
+#pragma unroll
+                for (int t = 0; t < B; ++t)
+                    y[u * B + t] = (b + u < be && pos0 + u * B + t < d) ? yg[V::get(p.v[u], t)] : TG(0);
+        }
+#pragma unroll
+        for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
+#pragma unroll
+        for (int u = 0; u < NB; ++u) p.v[u] = vn[u];
+    }
+    return s;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -243,21 +333,36 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
         const int i0 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp);
         const int i1 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp + 1);
         if (a.prof && k == a.prof_iter && lane == 0 && ph == ph0) a.prof[blockIdx.x * (kWarps + 4) + 4 + warp] = gtimer();
-        for (int i = i0; i < i1; ++i) {
+        // slice items first (the plan sorts each warp's list by kind), pipelined
+        int i = i0;
+        {
+            SlicePre<TS, TI, TG> pc, pn;
+            Item nxt2;
+            bool have = i < i1 && a.items[i].kind <= kPiece;
+            if (have) {
+                const Item it0 = a.items[i];
+                slice_prefetch<TS, TG, TI>(a, it0, s_res, lane, cur, pc);
+            }
+            bool have2 = have && i + 1 < i1;
+            if (have2) nxt2 = a.items[i + 1];
+            while (have) {
+                const Item curit = a.items[i];  // L1 hit: loaded one step ago
+                const bool more = have2 && nxt2.kind <= kPiece;
+                if (more) slice_prefetch<TS, TG, TI>(a, nxt2, s_res, lane, cur, pn);
+                if (more && i + 2 < i1) nxt2 = a.items[i + 2];
+                const TS sum = slice_consume<TS, TG, TI>(pc, yg);
+                if (!pc.whole) s_slot[curit.slot * kSlice + lane] = sum;
+                else if (pc.valid) update_row<TS, TG, TRACE>(a, pc.row, sum, pc.in, cur, g, k, tail, st);
+                ++i;
+                have = more;
+                have2 = more && i + 1 < i1;
+                if (more) pc = pn;
+            }
+        }
+        for (; i < i1; ++i) {
             const Item it = a.items[i];
             if (it.kind == kWhole || it.kind == kPiece) {
-                const bool whole = it.kind == kWhole;
-                const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + lane;
-                const bool valid = r < a.n;
-                RowIn<TS> in{};
-                int d = 0;
-                if (valid) {
-                    d = __ldg(a.row_deg + (size_t)it.id * kSlice + lane);
-                    if (whole) in = row_in(a, (int)r, cur);
-                }
-                const TS sum = sum_blocks<TS, TG, TI>(slice_base<TS, TG, TI>(a, it, s_res, lane), yg, d, it.beg, it.end);
-                if (!whole) s_slot[it.slot * kSlice + lane] = sum;
-                else if (valid) update_row<TS, TG, TRACE>(a, (int)r, sum, in, cur, g, k, tail, st);
+                // not reached: slice items precede hub items in every warp list
             } else if (it.kind == kHubPiece) {
                 // lanes stride the piece's elements; fixed warp tree
                 const int base = __ldg(a.hub_ptr + it.id);
@@ -763,6 +868,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.barrier = barrier;
     a.x_hist = hist;
     a.perm = g->perm;
+    if (const char* e = getenv("GN_DEBUG_GATHER")) a.dbg = atoi(e);
     long long* dprof = nullptr;
     const char* prof_env = getenv("GN_PROF_ITER");
     if (prof_env) {

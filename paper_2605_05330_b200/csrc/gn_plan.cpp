@@ -194,7 +194,15 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
             }
             for (int w = 0; w < kWarps; ++w) {
                 out.phase_warp.push_back((int32_t)out.items.size());
-                out.items.insert(out.items.end(), wl[(size_t)w].begin(), wl[(size_t)w].end());
+                for (Item it : wl[(size_t)w]) {
+                    if (it.kind == kWhole || it.kind == kPiece) {
+                        // 16-byte-word offset of block `beg`: slice start (elements) * elem size / 16 + 32 per block
+                        const int64_t words = sp[(size_t)it.id] / B + (int64_t)it.beg * 32;
+                        it.pad0 = (int32_t)(uint32_t)(words & 0xffffffffll);
+                        it.pad1 = (int32_t)(uint32_t)(words >> 32);
+                    }
+                    out.items.push_back(it);
+                }
             }
             out.phase_warp.push_back((int32_t)out.items.size());
             out.combs.insert(out.combs.end(), ph.combs.begin(), ph.combs.end());

@@ -39,7 +39,8 @@ enum ItemKind : int32_t { kWhole = 0, kPiece = 1, kHubPiece = 2, kHubSeq = 3 };
 // kPiece:    id = slice, [beg, end) = blocks of the piece, slot = slice slot
 // kHubPiece: id = hub row, [beg, end) = element offsets in the row, slot = hub slot
 // kHubSeq:   id = first hub row, end - beg = rows (EXACT mode, one thread per row)
-// smem: 16-byte-word offset of the resident copy of blocks [beg, end), -1 = global
+// smem: 16-byte-word offset of the resident copy of blocks [beg, end), -1 = global;
+// pad0/pad1: low/high 32 bits of the 16-byte-word offset of block beg in the global index array
 struct Item {
     int32_t kind, id, beg, end, slot, smem, pad0, pad1;
 };
