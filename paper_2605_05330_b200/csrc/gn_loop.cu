@@ -153,7 +153,8 @@ struct LaneVec<uint16_t> {
     static constexpr int B = 8;
     __device__ static __forceinline__ int get(const uint4& v, int t) {
         const unsigned w = t < 4 ? (t < 2 ? v.x : v.y) : (t < 6 ? v.z : v.w);
-        return (int)((t & 1) ? (w >> 16) : (w & 0xffffu));
+        // one PRMT (low half) or SHF (high half); the address is then one IMAD.WIDE.U32
+        return (int)((t & 1) ? (w >> 16) : __byte_perm(w, 0u, 0x4410));
     }
 };
 template <>
@@ -333,31 +334,26 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
         const int i0 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp);
         const int i1 = __ldg(a.phase_warp + ph * (kWarps + 1) + warp + 1);
         if (a.prof && k == a.prof_iter && lane == 0 && ph == ph0) a.prof[blockIdx.x * (kWarps + 4) + 4 + warp] = gtimer();
-        // slice items first (the plan sorts each warp's list by kind), pipelined
+        // slice items first (the plan sorts each warp's list by kind), two at
+        // a time: both items' loads are issued before either is consumed
         int i = i0;
-        {
-            SlicePre<TS, TI, TG> pc, pn;
-            Item nxt2;
-            bool have = i < i1 && a.items[i].kind <= kPiece;
-            if (have) {
-                const Item it0 = a.items[i];
-                slice_prefetch<TS, TG, TI>(a, it0, s_res, lane, cur, pc);
+        while (i < i1) {
+            const Item it0 = a.items[i];
+            if (it0.kind > kPiece) break;
+            const bool two = i + 1 < i1 && a.items[i + 1].kind <= kPiece;
+            const Item it1 = two ? a.items[i + 1] : it0;
+            SlicePre<TS, TI, TG> p0, p1;
+            slice_prefetch<TS, TG, TI>(a, it0, s_res, lane, cur, p0);
+            if (two) slice_prefetch<TS, TG, TI>(a, it1, s_res, lane, cur, p1);
+            const TS s0 = slice_consume<TS, TG, TI>(p0, yg);
+            if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
+            else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
+            if (two) {
+                const TS s1 = slice_consume<TS, TG, TI>(p1, yg);
+                if (!p1.whole) s_slot[it1.slot * kSlice + lane] = s1;
+                else if (p1.valid) update_row<TS, TG, TRACE>(a, p1.row, s1, p1.in, cur, g, k, tail, st);
             }
-            bool have2 = have && i + 1 < i1;
-            if (have2) nxt2 = a.items[i + 1];
-            while (have) {
-                const Item curit = a.items[i];  // L1 hit: loaded one step ago
-                const bool more = have2 && nxt2.kind <= kPiece;
-                if (more) slice_prefetch<TS, TG, TI>(a, nxt2, s_res, lane, cur, pn);
-                if (more && i + 2 < i1) nxt2 = a.items[i + 2];
-                const TS sum = slice_consume<TS, TG, TI>(pc, yg);
-                if (!pc.whole) s_slot[curit.slot * kSlice + lane] = sum;
-                else if (pc.valid) update_row<TS, TG, TRACE>(a, pc.row, sum, pc.in, cur, g, k, tail, st);
-                ++i;
-                have = more;
-                have2 = more && i + 1 < i1;
-                if (more) pc = pn;
-            }
+            i += two ? 2 : 1;
         }
         for (; i < i1; ++i) {
             const Item it = a.items[i];
