@@ -307,8 +307,12 @@ def main():
             r = gb.run(x0_host, sched)
         else:
             r = P.run_engine(g, x0_host, sched, dtype=dtype, device=local)
+        t1 = time.perf_counter()
         sol = P.round_to_mis(g, r.x)
         barrier()
+        if os.environ.get("GN_BENCH_VERBOSE"):
+            print(f"e2e step {i}: run {1e3 * (t1 - t0):.2f} ms, round {1e3 * (time.perf_counter() - t1):.2f} ms, "
+                  f"call {r.stats['total_ms']:.2f} ms", file=sys.stderr, flush=True)
         if i >= args.warmup:
             e2e_t.append(time.perf_counter() - t0)
             h2d = r.stats["h2d_bytes"] + 8 * g.n          # + the rounding's state upload
