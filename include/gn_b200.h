@@ -177,6 +177,16 @@ int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first,
 int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf,
                 int64_t* fallbacks, double* mass, int* bad);
 
+/* ---- graph generation on the device (BASELINE config C5) ----
+ * R-MAT with 2^scale vertices and edge_factor * 2^scale samples, quadrant
+ * probabilities (a, b, c, 1-a-b-c); self-loops dropped, symmetrised,
+ * deduplicated; the same counter-based stream as generators.rmat_pairs.
+ * Returns a canonical CSR in host arrays the caller frees with gn_free_host. */
+int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c,
+                uint64_t seed, int device, int64_t* nnz, int64_t** indptr,
+                int32_t** indices);
+void gn_free_host(void* p);
+
 #ifdef __cplusplus
 }
 #endif

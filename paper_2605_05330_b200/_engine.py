@@ -73,6 +73,8 @@ EXPORTED = (
     "gn_part_pack",
     "gn_part_unpack",
     "gn_part_end",
+    "gn_gen_rmat",
+    "gn_free_host",
 )
 
 
@@ -148,6 +150,9 @@ _SIGNATURES = {
     "gn_part_pack": (_I32, [_P, _I32, _P, _I64, _P, ctypes.c_size_t]),
     "gn_part_unpack": (_I32, [_P, _I32, _P, _I64, _I64, ctypes.c_size_t]),
     "gn_part_end": (_I32, [_P, _I32, _P, _P, _P, _P, _PI]),
+    "gn_gen_rmat": (_I32, [_I32, _I32, _D, _D, _D, ctypes.c_uint64, _I32, _PI64, ctypes.POINTER(_P),
+                           ctypes.POINTER(_P)]),
+    "gn_free_host": (None, [_P]),
 }
 
 _lib = None

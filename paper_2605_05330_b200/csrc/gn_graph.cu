@@ -300,8 +300,8 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
     // MinHash over the 128-byte lines (16 fp64 ids) a slice gathers: slices
     // with overlapping neighbourhoods get equal signatures w.p. = Jaccard, and
     // the plan places equal signatures on the same SM so its L1 serves them
-    L.sig.assign((size_t)L.nslices, ~0ull);
-    for (int32_t s = 0; s < L.nslices; ++s) {
+    L.sig.assign(getenv("GN_PLAN_COLOCATE") ? (size_t)L.nslices : 0, ~0ull);
+    for (int32_t s = 0; s < (int32_t)L.sig.size(); ++s) {
         uint64_t m = ~0ull;
         for (int l = 0; l < kSlice; ++l) {
             int64_t r = (int64_t)s * kSlice + l;

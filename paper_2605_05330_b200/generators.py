@@ -296,6 +296,41 @@ def c5_rmat(scale: int = 16, edge_factor: int = 16, seed: int = 2605_0005) -> In
                      "sampled_edges": int(len(s)), "unique_edges": int(len(indices) // 2)})
 
 
+def rmat_csr_gpu(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+                 seed: int = 2605_0005, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """The R-MAT of rmat_pairs + _canonical, generated, deduplicated and
+    turned into CSR on the GPU (csrc/gn_gen.cu); bitwise the CPU result."""
+    import ctypes
+
+    from . import _engine as E
+
+    nnz = ctypes.c_int64()
+    pp, pc = ctypes.c_void_p(), ctypes.c_void_p()
+    E.check(E.lib().gn_gen_rmat(scale, edge_factor, a, b, c, seed, device, ctypes.byref(nnz), ctypes.byref(pp),
+                                ctypes.byref(pc)))
+    n = 1 << scale
+    try:
+        indptr = np.ctypeslib.as_array(ctypes.cast(pp, ctypes.POINTER(ctypes.c_int64)), shape=(n + 1,)).copy()
+        indices = (np.ctypeslib.as_array(ctypes.cast(pc, ctypes.POINTER(ctypes.c_int32)), shape=(nnz.value,)).copy()
+                   if nnz.value else np.zeros(0, np.int32))
+    finally:
+        E.lib().gn_free_host(pp)
+        E.lib().gn_free_host(pc)
+    return indptr, indices
+
+
+def c5_rmat_gpu(scale: int = 24, edge_factor: int = 16, seed: int = 2605_0005, device: int = 0) -> Instance:
+    """C5 at full scale: the graph of c5_rmat(scale) built on the GPU."""
+    n = 1 << scale
+    indptr, indices = rmat_csr_gpu(scale, edge_factor, seed=seed, device=device)
+    w = 1.0 - hash_uniform_f32(seed, n, 1)
+    x0 = f32_exact(init_random(n, [seed, 1]))
+    g = WeightedGraph(n, indptr, indices, w)
+    return Instance(f"C5-rmat{scale}", g, x0, "fp32",
+                    {"scale": scale, "edge_factor": edge_factor, "seed": seed, "sampled_edges": n * edge_factor,
+                     "unique_edges": int(len(indices) // 2), "generated_on": "gpu"})
+
+
 CONFIGS = {
     "C1": c1_er,
     "C2": c2_assignment,
