@@ -42,7 +42,7 @@ CONFIG_TEXT = {
           "w ~ U(0,1] fp32, pursuit 0.9->1.5 x1000",
     "C3": "Barabasi-Albert n=200,000 m=5 (999,975 edges), integer weights U{1..200} fp64, pursuit x1000",
     "C4": "1024 independent ER graphs n=2000 avg degree 16 per GPU, packed block-diagonal, fp32, pursuit x1000",
-    "C5": "R-MAT scale S edge factor 16 (a=.57,b=c=.19), symmetrised, dedup, fp32, pursuit x1000",
+    "C5": "R-MAT edge factor 16 (a=.57,b=c=.19), symmetrised, dedup, fp32, pursuit x1000 (scale in config.scale)",
 }
 
 
@@ -65,7 +65,7 @@ def make_instance(config: str, rank: int, scale: int):
     if config == "C4":
         return G.c4_batch(graphs=1024, first=rank * 1024).instance
     if config == "C5":
-        return G.c5_rmat(scale)
+        return G.c5_rmat_gpu(scale) if scale >= 18 else G.c5_rmat(scale)
     raise SystemExit(f"unknown config {config}")
 
 
@@ -193,7 +193,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
-    ap.add_argument("--scale", type=int, default=20, help="R-MAT scale for C5")
+    ap.add_argument("--scale", type=int, default=24, help="R-MAT scale for C5 (BASELINE: 24)")
     ap.add_argument("--dtype", default=None, help="engine dtype (default: fp64 for C1-C3, fp32 for C4/C5)")
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
@@ -365,6 +365,7 @@ def main():
         "config": {
             "workload": args.config + ": " + CONFIG_TEXT[args.config],
             "n": g.n, "m": inst.m, "iters": iters, "schedule": "pursuit 0.9->1.5",
+            "scale": args.scale if args.config == "C5" else None,
             "parallelism": f"replicas x{ws}" if args.config != "C4" else f"batch shard x{ws} (1024 graphs/rank)",
             "l2": "flushed between steps (256 MB write); the 1000 iterations inside a step re-read the graph",
             "index_format": "uint16" if info["n"] <= 65536 else "int32",

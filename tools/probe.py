@@ -52,6 +52,13 @@ if __name__ == "__main__":
                                                            np.ones(100000)), np.full(100000, 0.5), "fp64")
             elif name == "C4":
                 inst = G.c4_batch(1024).instance
+            elif name.startswith("C5S"):
+                t = time.time()
+                inst = G.c5_rmat_gpu(int(name[3:]))
+                print("gen", name, time.time() - t, inst.graph, flush=True)
+                t = time.time()
+                inst.graph.device_graph(inst.dtype)
+                print("graph create", time.time() - t, flush=True)
             else:
                 inst = G.CONFIGS[name]()
             for dt in (args.dtypes.split(",") if args.dtypes else [None]):
