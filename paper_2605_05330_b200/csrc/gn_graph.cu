@@ -221,7 +221,7 @@ static inline uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indices, Layout& L) {
+static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indices, bool global_sort, Layout& L) {
     std::vector<int32_t> deg((size_t)n);
     for (int64_t i = 0; i < n; ++i) {
         deg[(size_t)i] = (int32_t)(indptr[i + 1] - indptr[i]);
@@ -232,9 +232,12 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
     for (int64_t i = 0; i < n; ++i) (deg[(size_t)i] > kHubDegree ? hubs : regular).push_back((int32_t)i);
     std::stable_sort(hubs.begin(), hubs.end(), [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
     // regular rows: degree-descending inside windows of kSigma (keeps coarse
-    // locality; a uniform-degree graph keeps its numbering)
-    for (size_t w0 = 0; w0 < regular.size(); w0 += kSigma) {
-        size_t w1 = std::min(regular.size(), w0 + (size_t)kSigma);
+    // locality; a uniform-degree graph keeps its numbering) -- or globally,
+    // when the hot-vertex cache is on, so the smallest new ids (the cached
+    // ones) are the most gathered vertices
+    const size_t win = global_sort ? std::max<size_t>(regular.size(), 1) : (size_t)kSigma;
+    for (size_t w0 = 0; w0 < regular.size(); w0 += win) {
+        size_t w1 = std::min(regular.size(), w0 + win);
         std::stable_sort(regular.begin() + w0, regular.begin() + w1,
                          [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
     }
@@ -402,8 +405,14 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     }
     if (device < 0 || device >= ndev) return fail(GN_ERR_ARG, "device ordinal out of range");
 
+    // hot-vertex cache: for large graphs the values of the first `hot` new ids
+    // (the most gathered vertices) are mirrored in shared memory each
+    // iteration (128 KB); GN_HOT=0 disables it
+    const int64_t hot_cap = (int64_t)(131072 / gather_bytes(dtype));
+    int64_t hot = n >= 8 * hot_cap ? hot_cap : 0;
+    if (const char* e = getenv("GN_HOT")) hot = atoi(e) ? std::min<int64_t>(hot_cap, n) : 0;
     Layout L;
-    build_layout(n, indptr, indices, L);
+    build_layout(n, indptr, indices, hot > 0, L);
 
     gn_graph* g = new gn_graph();
     g->n = n;
@@ -417,6 +426,7 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     g->idx16 = L.idx16;
     g->sell_elems = L.slice_ptr.empty() ? 0 : L.slice_ptr.back();
     g->slice_sig = std::move(L.sig);
+    g->hot = L.idx16 ? 0 : (int32_t)hot;
     CallCtx ctx;
     int rc = ctx.open(device);
     if (rc) { delete g; return rc; }

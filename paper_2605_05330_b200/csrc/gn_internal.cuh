@@ -94,6 +94,7 @@ struct gn_graph {
     int64_t sell_elems = 0;
     std::vector<uint64_t> slice_sig;  // host: per-slice MinHash (gn_graph.cu, used by the plan)
     gn_batch* resident = nullptr;     // small graphs: the whole-graph-in-shared-memory kernel
+    int32_t hot = 0;                  // new ids [0, hot) are mirrored in shared memory (0: off)
 };
 
 namespace gn {

@@ -69,7 +69,9 @@ struct LoopArgs {
     const Combine* __restrict__ combs;
     const int32_t* __restrict__ smem_words;  // [G] resident 16-byte words per CTA
     int hub_slot_off;                        // byte offsets in dynamic shared memory
+    int hot_off;
     int resident_off;
+    int hot;                                 // new ids [0, hot) mirrored in shared memory
     const double* __restrict__ gammas;
     int iters;
     double final_gamma;
@@ -225,6 +227,19 @@ __device__ __forceinline__ const uint4* slice_base(const LoopArgs<TS, TG>& a, co
     return reinterpret_cast<const uint4*>((const TI*)a.sell + __ldg(a.slice_ptr + it.id)) + lane;
 }
 
+// Where gathered values come from: global memory, or -- for the hottest
+// vertices (new ids < hot) -- their shared-memory mirror.
+template <typename TG, bool HOT>
+struct GSrc {
+    const TG* __restrict__ yg;
+    const TG* s_hot;
+    int hot;
+    __device__ __forceinline__ TG operator[](int j) const {
+        if (HOT) return j < hot ? s_hot[j] : yg[j];
+        return yg[j];
+    }
+};
+
 // ---- software-pipelined slice items -----------------------------------
 // A warp walks its slice items (short slices and pieces of long slices) with
 // a two-deep pipeline: while item i's gathers are in flight, item i+1's
@@ -270,8 +285,8 @@ __device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const 
 
 // Sequential sum of one lane's row over the item's blocks; p.v holds the
 // first batch of index vectors.
-template <typename TS, typename TG, typename TI>
-__device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const TG* __restrict__ yg) {
+template <typename TS, typename TG, typename TI, bool HOT>
+__device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<TG, HOT>& yg) {
     using A = Arith<TS>;
     using V = LaneVec<TI>;
     using SP = SlicePre<TS, TI, TG>;
@@ -321,12 +336,21 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // One pass over this CTA's items, phase by phase (gn_plan.h).
-template <typename TS, typename TG, typename TI, bool TRACE>
+template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
 __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_slot, TS* s_hslot,
-                     const uint4* s_res) {
+                     const uint4* s_res, TG* s_hot) {
     using A = Arith<TS>;
     const int cur = k & 1;
-    const TG* __restrict__ yg = a.yg[cur];
+    if (HOT) {
+        // mirror the hottest vertices' published values (written by all CTAs
+        // before the last grid barrier) into shared memory
+        const uint4* src = reinterpret_cast<const uint4*>(a.yg[cur]);
+        uint4* dst = reinterpret_cast<uint4*>(s_hot);
+        const int words = (int)((size_t)a.hot * sizeof(TG) / 16);
+        for (int t = threadIdx.x; t < words; t += blockDim.x) dst[t] = __ldcg(src + t);
+        __syncthreads();
+    }
+    const GSrc<TG, HOT> yg{a.yg[cur], s_hot, a.hot};
     const TS g = tail ? TS(0) : (TS)a.gammas[k];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ph0 = __ldg(a.phase_base + blockIdx.x), ph1 = __ldg(a.phase_base + blockIdx.x + 1);
@@ -345,11 +369,11 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
             SlicePre<TS, TI, TG> p0, p1;
             slice_prefetch<TS, TG, TI>(a, it0, s_res, lane, cur, p0);
             if (two) slice_prefetch<TS, TG, TI>(a, it1, s_res, lane, cur, p1);
-            const TS s0 = slice_consume<TS, TG, TI>(p0, yg);
+            const TS s0 = slice_consume<TS, TG, TI, HOT>(p0, yg);
             if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
             else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
             if (two) {
-                const TS s1 = slice_consume<TS, TG, TI>(p1, yg);
+                const TS s1 = slice_consume<TS, TG, TI, HOT>(p1, yg);
                 if (!p1.whole) s_slot[it1.slot * kSlice + lane] = s1;
                 else if (p1.valid) update_row<TS, TG, TRACE>(a, p1.row, s1, p1.in, cur, g, k, tail, st);
             }
@@ -527,11 +551,12 @@ __device__ double ring_step_inf(const double* ring_slot) {
     return s_m;
 }
 
-template <typename TS, typename TG, typename TI, bool TRACE>
+template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
 __global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TS* s_slot = (TS*)smem_raw;
     TS* s_hslot = (TS*)(smem_raw + a.hub_slot_off);
+    TG* s_hot = (TG*)(smem_raw + a.hot_off);
     uint4* s_res = (uint4*)(smem_raw + a.resident_off);
     // resident index blocks: copied once, used every iteration
     if (__ldg(a.smem_words + blockIdx.x) > 0) {
@@ -556,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
         const bool pr = a.prof && k == a.prof_iter && threadIdx.x == 0;
         long long* pp = a.prof ? a.prof + blockIdx.x * (kWarps + 4) : nullptr;
         if (pr) pp[0] = gtimer();
-        pass<TS, TG, TI, TRACE>(a, k, false, st, s_slot, s_hslot, s_res);
+        pass<TS, TG, TI, TRACE, HOT>(a, k, false, st, s_slot, s_hslot, s_res, s_hot);
         if (pr) pp[1] = gtimer();
         double* slot = a.ring + (size_t)(k - k0) * ring_stride;
         publish<TRACE>(st, slot);
@@ -578,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
     if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE>(a, ran, true, st, s_slot, s_hslot, s_res);
+        pass<TS, TG, TI, TRACE, HOT>(a, ran, true, st, s_slot, s_hslot, s_res, s_hot);
         publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
         fold_ring(a.ring, ran - k0 + 1, k0, fo);
@@ -747,10 +772,14 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     GN_CUDA(cudaEventRecord(ev[0], s));
 
     // ---- launch geometry and plan
-    void* kern = trace ? (void*)k_gn_loop<TS, TG, TI, true> : (void*)k_gn_loop<TS, TG, TI, false>;
+    const bool hot = g->hot > 0 && sizeof(TI) == 4;
+    void* kern;
+    if (hot) kern = trace ? (void*)k_gn_loop<TS, TG, TI, true, true> : (void*)k_gn_loop<TS, TG, TI, false, true>;
+    else kern = trace ? (void*)k_gn_loop<TS, TG, TI, true, false> : (void*)k_gn_loop<TS, TG, TI, false, false>;
     int max_optin = 0;
     GN_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    const size_t slot_bytes = (size_t)kMaxSlots * kSlice * sizeof(TS) + (size_t)kMaxHubSlots * sizeof(TS);
+    const size_t hot_bytes = hot ? (size_t)g->hot * sizeof(TG) : 0;
+    const size_t slot_bytes = (size_t)kMaxSlots * kSlice * sizeof(TS) + (size_t)kMaxHubSlots * sizeof(TS) + hot_bytes;
     const size_t static_bytes = 2048;  // publish scratch
     // index residency budget: what is left after the partial slots, capped so
     // the L1 keeps room for the gathers (GN_SMEM_RES_KB overrides)
@@ -768,6 +797,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     const DevicePlan* plan = nullptr;
     if ((rc = get_plan(g, grid, exact, res_cap, &plan))) return rc;
     const int hub_slot_off = (int)((size_t)kMaxSlots * kSlice * sizeof(TS));
+    const int hot_off = (int)(((size_t)hub_slot_off + (size_t)kMaxHubSlots * sizeof(TS) + 15) / 16 * 16);
     const int resident_off = (int)((slot_bytes + 15) / 16 * 16);
     const size_t dyn_smem = (size_t)resident_off + (size_t)plan->max_words * 16;
 
@@ -850,6 +880,8 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.combs = plan->combs;
     a.smem_words = plan->smem_words;
     a.hub_slot_off = hub_slot_off;
+    a.hot_off = hot_off;
+    a.hot = hot ? g->hot : 0;
     a.resident_off = resident_off;
     a.gammas = gam;
     a.iters = iters;

@@ -115,3 +115,19 @@ def test_c5_rmat_scale16_fp32():
     sol = P.round_to_mis(inst.graph, rx.x)
     sel, weight, _, _ = O.round_to_mis(inst.graph, ref.x)
     assert list(sol.members) == np.flatnonzero(sel).tolist() and sol.weight == weight
+
+
+def test_c5_scale18_hot_cache_exact_bitwise():
+    """n = 2^18 enables the shared-memory hot-vertex cache (fp32 gathers):
+    EXACT mode must still equal the same-precision oracle bit for bit, and
+    the fast mode must pass the fp32 gates."""
+    inst = G.c5_rmat(18)
+    s = P.GammaSchedule.pursuit()
+    tab = s.table()[:60]
+    ref = O.run(inst.graph, inst.x0, tab, 1.5, dtype="fp32", threads=THREADS)
+    r = P.run_engine(inst.graph, inst.x0, s, dtype="fp32", exact=True, gammas=tab)
+    np.testing.assert_array_equal(r.x, ref.x)
+    np.testing.assert_array_equal(r.trace.step_inf, ref.step_inf)
+    rf = P.run_engine(inst.graph, inst.x0, s, dtype="fp32", gammas=tab)
+    np.testing.assert_allclose(rf.x, ref.x, rtol=0, atol=1e-5)
+    assert np.array_equal(np.array(rf.trace.fallbacks), ref.fallbacks)
