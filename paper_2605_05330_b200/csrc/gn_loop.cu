@@ -247,8 +247,8 @@ struct GSrc {
 // i+2's descriptor too.  Each item costs about one memory round trip instead
 // of four dependent ones.
 template <typename TG>
-struct GatherDepth {
-    static constexpr int value = sizeof(TG) == 4 ? 32 : 16;  // gathers in flight per lane
+struct GatherDepth {  // gathers in flight per lane (register budget: 64K / (kThreads * kCtasPerSm))
+    static constexpr int value = (sizeof(TG) == 4 ? 32 : 16) / kCtasPerSm;
 };
 
 template <typename TS, typename TI, typename TG>
@@ -552,7 +552,7 @@ __device__ double ring_step_inf(const double* ring_slot) {
 }
 
 template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
-__global__ void __launch_bounds__(kThreads, 1) k_gn_loop(LoopArgs<TS, TG> a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, TG> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TS* s_slot = (TS*)smem_raw;
     TS* s_hslot = (TS*)(smem_raw + a.hub_slot_off);
@@ -785,7 +785,10 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     // the L1 keeps room for the gathers (GN_SMEM_RES_KB overrides)
     size_t res_cap = 96 * 1024;
     if (const char* e = getenv("GN_SMEM_RES_KB")) res_cap = (size_t)atoi(e) * 1024;
-    res_cap = std::min(res_cap, (size_t)max_optin - static_bytes - slot_bytes);
+    int smem_sm = 0;
+    GN_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g->device));
+    const size_t per_cta = std::min<size_t>((size_t)max_optin, (size_t)smem_sm / kCtasPerSm - 1024);
+    res_cap = std::min(res_cap, per_cta > static_bytes + slot_bytes ? per_cta - static_bytes - slot_bytes : 0);
     const size_t smem_cap = slot_bytes + res_cap;
     GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
     int maxb = 1;
