@@ -166,7 +166,7 @@ def load_library(path: os.PathLike | str | None = None) -> ctypes.CDLL:
     with _lib_lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else Path(os.environ.get("GN_LIB", LIB_PATH))
+        p = Path(path) if path else Path(os.environ.get("GN_LIB") or LIB_PATH)
         try:
             lib = ctypes.CDLL(str(p))
         except OSError as exc:

@@ -44,6 +44,10 @@
 #include "gn_internal.cuh"
 #include "gn_plan.h"
 
+#ifndef GN_DBG_GATHER
+#define GN_DBG_GATHER 0  // timing experiments only (results are wrong when set)
+#endif
+
 namespace gn {
 
 constexpr int kRing = 1024;  // iterations of block stats kept before a fold
@@ -87,8 +91,6 @@ struct LoopArgs {
     const int32_t* __restrict__ perm;
     long long* prof;   // optional timestamps (GN_PROF_ITER): [G][kWarps+4]
     int prof_iter;
-    int dbg;           // GN_DEBUG_GATHER (timing experiments only; results are wrong when set):
-                       // 1 = gathers read a fixed element, 2 = no index loads
 };
 
 struct Stats {
@@ -166,59 +168,6 @@ struct LaneVec<int32_t> {
         return (int)(t == 0 ? v.x : t == 1 ? v.y : t == 2 ? v.z : v.w);
     }
 };
-
-// Sequential sum over blocks [bb, be) of one slice row (this lane), masked by
-// the row's degree d.  `base` (shared or global memory: a generic pointer, so
-// one copy of the loop serves both) addresses block b at base[b * 32].  Each
-// batch issues NB*B gathers before any add, and the next batch's index
-// vectors are requested before this batch's gathers, so a batch costs one
-// memory round trip; the adds stay in position order (the reference's order).
-template <typename TS, typename TG, typename TI>
-__device__ __noinline__ TS sum_blocks(const uint4* base, const TG* __restrict__ yg, int d, int bb, int be, int dbg) {
-    using A = Arith<TS>;
-    using V = LaneVec<TI>;
-    constexpr int B = V::B;
-    // gathers in flight per lane: 32 four-byte or 16 eight-byte values
-    constexpr int GIF = sizeof(TG) == 4 ? 32 : 16;
-    constexpr int NB = GIF / B > 0 ? GIF / B : 1;
-    TS s = TS(0);
-    be = min(be, (d + B - 1) / B);  // blocks past the row's end hold no neighbours
-    if (bb >= be) return s;
-    uint4 v[NB];
-    const uint4 fake = make_uint4(threadIdx.x, threadIdx.x * 3, threadIdx.x * 5, threadIdx.x * 7);
-#pragma unroll
-    for (int u = 0; u < NB; ++u)
-        if (bb + u < be) v[u] = dbg == 2 ? fake : base[(size_t)(bb + u) * kSlice];
-    if (dbg == 1) yg = yg + 0;
-    for (int b = bb; b < be; b += NB) {
-        uint4 vn[NB];
-#pragma unroll
-        for (int u = 0; u < NB; ++u)
-            if (b + NB + u < be) vn[u] = dbg == 2 ? fake : base[(size_t)(b + NB + u) * kSlice];
-        if (dbg == 1) {
-#pragma unroll
-            for (int u = 0; u < NB; ++u) v[u] = make_uint4(0, 0, 0, 0);
-        }
-        TG y[NB * B];
-        if (b + NB <= be && (b + NB) * B <= d) {
-#pragma unroll
-            for (int u = 0; u < NB; ++u)
-#pragma unroll
-                for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(v[u], t)];
-        } else {
-#pragma unroll
-            for (int u = 0; u < NB; ++u)
-#pragma unroll
-                for (int t = 0; t < B; ++t)
-                    y[u * B + t] = (b + u < be && (b + u) * B + t < d) ? yg[V::get(v[u], t)] : TG(0);
-        }
-#pragma unroll
-        for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
-#pragma unroll
-        for (int u = 0; u < NB; ++u) v[u] = vn[u];
-    }
-    return s;
-}
 
 template <typename TS, typename TG, typename TI>
 __device__ __forceinline__ const uint4* slice_base(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
@@ -300,13 +249,23 @@ __device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<
 #pragma unroll
         for (int u = 0; u < NB; ++u)
             if (b + NB + u < be) vn[u] = p.base[(size_t)(b + NB + u) * kSlice];
+#if GN_DBG_GATHER == 1  // timing experiment: gathers hit a few cached lines
+#pragma unroll
+        for (int u = 0; u < NB; ++u) p.v[u] = make_uint4(threadIdx.x & 31, 32 + (threadIdx.x & 31), 64, 96);
+#endif
         TG y[NB * B];
         const int pos0 = (p.beg + b) * B;
         if (b + NB <= be && pos0 + NB * B <= d) {
 #pragma unroll
             for (int u = 0; u < NB; ++u)
 #pragma unroll
-                for (int t = 0; t < B; ++t) y[u * B + t] = yg[V::get(p.v[u], t)];
+                for (int t = 0; t < B; ++t) {
+#if GN_DBG_GATHER == 3  // timing experiment: no gathers
+                    y[u * B + t] = (TG)V::get(p.v[u], t);
+#else
+                    y[u * B + t] = yg[V::get(p.v[u], t)];
+#endif
+                }
         } else {
 #pragma unroll
             for (int u = 0; u < NB; ++u)
@@ -899,7 +858,6 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.barrier = barrier;
     a.x_hist = hist;
     a.perm = g->perm;
-    if (const char* e = getenv("GN_DEBUG_GATHER")) a.dbg = atoi(e);
     long long* dprof = nullptr;
     const char* prof_env = getenv("GN_PROF_ITER");
     if (prof_env) {

@@ -29,7 +29,10 @@ namespace gn {
 #ifndef GN_LOOP_CTAS_PER_SM
 #define GN_LOOP_CTAS_PER_SM 1
 #endif
-constexpr int kThreads = 512;   // per CTA; one CTA per SM -> 128 registers per thread for deep gather batches
+#ifndef GN_LOOP_THREADS
+#define GN_LOOP_THREADS 512
+#endif
+constexpr int kThreads = GN_LOOP_THREADS;  // per CTA; one CTA per SM -> 128 registers per thread for deep gather batches
 constexpr int kCtasPerSm = GN_LOOP_CTAS_PER_SM;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPieceBlocks = 8;      // blocks per piece of a long slice
