@@ -129,6 +129,23 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
 int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight,
                      int* independent, int* maximal, int64_t* count);
 
+/* ---- several starts on one graph (solver.py:100-153) ----
+ * num_starts trajectories of run_wrgn on the same graph and schedule,
+ * advanced together (state stored start-minor, so one contiguous read per
+ * neighbour serves every start).  x0 / x_out are [num_starts][n] fp64,
+ * original order.  Each start is bitwise its own gn_run(GN_EXACT) run: per
+ * start checks (status GN_ERR_NEGATIVE / GN_ERR_NOT_NORMALIZABLE: not run),
+ * non-finite stop (GN_ERR_NONFINITE, fail_iter) and early exit.  Outputs
+ * step_inf / fallbacks are [num_starts][iters] (entries past iters_run[b]
+ * untouched); iters_run / status / fail_iter are [num_starts].  Returns
+ * GN_OK, or the first failing start's code.  1 <= num_starts <= 64.
+ * Flags: GN_EARLY_EXIT, GN_NO_CHECK, GN_NO_CLIP, GN_NONFINITE_OK. */
+int gn_multi_run(gn_graph* g, int num_starts, const double* x0,
+                 const double* gammas, int iters, double final_gamma,
+                 uint32_t flags, double* x_out, double* step_inf,
+                 int64_t* fallbacks, int* iters_run, int* status,
+                 int* fail_iter, gn_run_stats* stats);
+
 /* ---- batches of independent graphs (BASELINE config C4) ----
  * B graphs packed block-diagonally: graph b owns vertices
  * [offsets[b], offsets[b+1]) and no edge leaves it.  Each graph runs its own

@@ -60,6 +60,7 @@ EXPORTED = (
     "gn_fitness",
     "gn_round",
     "gn_check_members",
+    "gn_multi_run",
     "gn_batch_create",
     "gn_batch_destroy",
     "gn_batch_info",
@@ -134,6 +135,10 @@ _SIGNATURES = {
     "gn_fitness": (_I32, [_P, _P, _D, _P, _PD]),
     "gn_round": (_I32, [_P, _P, _U32, _P, _PD, _PI, _PI, _PI64]),
     "gn_check_members": (_I32, [_P, _P, _PD, _PI, _PI, _PI64]),
+    "gn_multi_run": (
+        _I32,
+        [_P, _I32, _P, _P, _I32, _D, _U32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(RunStats)],
+    ),
     "gn_batch_create": (_I32, [_I64, _P, _I64, _P, _P, _P, _I32, _I32, ctypes.POINTER(_P)]),
     "gn_batch_destroy": (_I32, [_P]),
     "gn_batch_info": (_I32, [_P, _PI64, _PI64, _PI64, _PI64]),

@@ -348,6 +348,7 @@ __global__ void k_init_state_weights(int64_t n, const double* __restrict__ w64, 
 static void free_graph(gn_graph* g) {
     if (!g) return;
     release_plans(g);
+    release_multi_plans(g);
     if (g->resident) batch_destroy(g->resident);
     int prev = -1;
     cudaGetDevice(&prev);

@@ -150,6 +150,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
 
 int coresident_blocks(const void* kernel, int threads, size_t smem, int device, int* out);
 void release_plans(const gn_graph* g);  // gn_loop.cu: cached launch plans of g
+void release_multi_plans(const gn_graph* g);  // gn_multi.cu: cached multi-start plans of g
 
 // gn_batch.cu: the resident (CTA-per-graph) kernel
 int batch_create(int64_t B, const int64_t* offsets, int64_t n, const int64_t* indptr, const int32_t* indices,

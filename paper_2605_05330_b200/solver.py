@@ -6,8 +6,9 @@ graphnorm.io.make_result (io.py:260-280).  Where the reference fans the
 starts out over a thread pool, the engine runs them together: graphs small
 enough for the resident kernel (<= 4096 vertices) run all starts at once, one
 CTA per start (the graph replicated B times in a batch, csrc/gn_batch.cu --
-bitwise the per-start runs); larger graphs run the starts back to back, each
-one already using the whole GPU.  Rounding and the MisSolution checks run on
+bitwise the per-start runs); larger graphs run all starts in one multi-start
+engine call (the states stored start-minor, csrc/gn_multi.cu -- bitwise the
+per-start EXACT runs).  Rounding and the MisSolution checks run on
 the GPU per start.
 """
 
@@ -22,6 +23,7 @@ import numpy as np
 from .batch import GraphBatch
 from .dynamics import GammaSchedule, NormalizationError, init_random, init_warm, round_to_mis, run_engine
 from .graph import WeightedGraph, csr_from_edges, from_csr
+from .multistart import MAX_STARTS, run_multi
 
 FORMAT_VERSION = "1.0"
 
@@ -149,6 +151,22 @@ def solve_instance(g, instance_name: str, config: RunConfig, warm_starts: Option
             stats.fallback_events += int(res.fallbacks[b, : res.iters_run[b]].sum())
             records.append(StartRecord(start_id, sol.weight, sol.independent, sol.maximal, int(res.iters_run[b]),
                                        elapsed))
+    elif len(tasks) > 1 and not config.trace:
+        # all starts in one engine call (csrc/gn_multi.cu), up to 64 at a time
+        for c0 in range(0, len(tasks), MAX_STARTS):
+            chunk = tasks[c0:c0 + MAX_STARTS]
+            t0 = time.perf_counter()
+            res = run_multi(g, np.stack([x for _, x in chunk]), schedule, dtype=dtype, device=device)
+            elapsed = (time.perf_counter() - t0) * 1000.0
+            for b, (start_id, _) in enumerate(chunk):
+                if res.status[b] != 0:
+                    records.append(StartRecord(start_id, 0.0, False, False, 0, elapsed))
+                    stats.aborted_starts += 1
+                    continue
+                sol = round_to_mis(g, res.x[b])
+                stats.fallback_events += int(res.fallbacks[b, : res.iters_run[b]].sum())
+                records.append(StartRecord(start_id, sol.weight, sol.independent, sol.maximal,
+                                           int(res.iters_run[b]), elapsed))
     else:
         for start_id, x0 in tasks:
             t0 = time.perf_counter()
