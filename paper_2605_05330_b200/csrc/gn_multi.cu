@@ -34,6 +34,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "gn_internal.cuh"
@@ -62,16 +63,22 @@ struct Pack<float> {
     }
 };
 
+// A row as the kernel walks it: original id, CSR offset, degree.
+struct RowDesc {
+    int32_t r, rb, deg, pad;
+};
+
 template <typename TS, typename TG>
 struct MultiArgs {
     int64_t n;
     int B, Bp;
-    const int32_t* __restrict__ rowptr;  // original CSR
-    const int32_t* __restrict__ col;
-    const int32_t* __restrict__ order;   // rows in processing order (original ids)
-    const int32_t* __restrict__ wbeg;    // [G * kMWarps + 1] ranges of `order` per warp
+    const int32_t* __restrict__ col;     // original CSR column indices
+    const int4* __restrict__ rdesc;      // regular rows in processing order (RowDesc)
+    const int32_t* __restrict__ wbeg;    // [G * kMWarps + 1] ranges of rdesc per warp
+    const int32_t* __restrict__ wmid;    // [G * kMWarps]: rows [wbeg, wmid) are warp rows (fast mode)
+    const int4* __restrict__ hdesc;      // split rows (fast mode), grouped by CTA
+    const int32_t* __restrict__ hbeg;    // [G + 1] ranges of hdesc per CTA
     const TS* __restrict__ v;            // original order
-    const TS* __restrict__ w;
     TS* x[2];                            // [n][Bp]
     TG* yg[2];                           // [n][Bp]
     const double* __restrict__ gammas;
@@ -86,30 +93,169 @@ struct MultiArgs {
     unsigned int* barrier;
 };
 
+template <int T>
+struct TeamIdx {
+    static constexpr int NI = (kMU + T - 1) / T;  // index registers per lane
+    // positions q + i*T + t (i*T + t < kMU) of a segment of length len
+    __device__ static __forceinline__ void load(const int32_t* __restrict__ colp, int q, int len, int t,
+                                                int (&idx)[NI]) {
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int pos = q + i * T + t;
+            idx[i] = (i * T + t < kMU && pos < len) ? __ldg(colp + pos) : 0;
+        }
+    }
+};
+
+// Sequential sum, for the lane's S starts, of positions [0, len) of one row
+// segment (colp = its first column index); idx holds the first index chunk.
+// lmax / lmin: the warp's longest / shortest segment (all teams step together).
 template <typename TS, typename TG, int T>
-__global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) {
+__device__ __forceinline__ void team_sum(const int32_t* __restrict__ colp, int len, int lmax, int lmin,
+                                         int (&idx)[TeamIdx<T>::NI], const TG* __restrict__ ybase, int Bp,
+                                         int tbase, int t, TS (&acc)[Pack<TG>::S]) {
     using A = Arith<TS>;
     using P = Pack<TG>;
     using PT = typename P::T;
-    constexpr int S = P::S;
-    constexpr int NI = (kMU + T - 1) / T;  // index registers per lane
+    constexpr int S = P::S, NI = TeamIdx<T>::NI;
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = TS(0);
+    for (int q = 0; q < lmax; q += kMU) {
+        int nidx[NI];
+        TeamIdx<T>::load(colp, q + kMU, len, t, nidx);
+        PT val[kMU];
+        if (q + kMU <= lmin) {
+#pragma unroll
+            for (int u = 0; u < kMU; ++u) {
+                const int j = __shfl_sync(0xffffffffu, idx[u / T], tbase + (u & (T - 1)));
+                val[u] = __ldg(reinterpret_cast<const PT*>(ybase + (size_t)j * Bp));
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kMU; ++u) {
+                const int j = __shfl_sync(0xffffffffu, idx[u / T], tbase + (u & (T - 1)));
+                if (q + u < len) val[u] = __ldg(reinterpret_cast<const PT*>(ybase + (size_t)j * Bp));
+                else val[u] = PT();
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kMU; ++u)
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] = A::add(acc[s], (TS)P::at(val[u], s));
+#pragma unroll
+        for (int i = 0; i < NI; ++i) idx[i] = nidx[i];
+    }
+}
+
+// dynamics.py:104-107 for one (row, start); stats of that start
+template <typename TS, typename TG>
+__device__ __forceinline__ void update_one(TS xi, TS vi, TS sum, TS g, TS* xn, TG* yn, double& mx, unsigned int& fbc,
+                                           int& bd) {
+    using A = Arith<TS>;
+    const TS yi = A::mul(vi, xi);
+    const TS d = A::add(yi, A::mul(g, sum));
+    const bool ok = (double)d > kSafeDiv;
+    const TS o = ok ? A::div(yi, d) : TS(kFallback);
+    *xn = o;
+    *yn = (TG)A::mul(vi, o);
+    TS df = A::sub(o, xi);  // dynamics.py:165
+    df = df < TS(0) ? -df : df;
+    if (!((double)df <= mx)) mx = (double)df;
+    fbc += ok ? 0u : 1u;
+    if (!isfinite((double)o)) bd = 1;
+}
+
+// Sum of a value over the warp's teams (lanes with equal t), the same fixed
+// butterfly on every lane (IEEE addition is commutative: all lanes agree).
+template <typename TS, int T>
+__device__ __forceinline__ TS fold_teams(TS v) {
+#pragma unroll
+    for (int o = T; o < 32; o <<= 1) v = Arith<TS>::add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ RowDesc row_at(const int4* __restrict__ d, int i, int end) {
+    if (i < end) {
+        const int4 q = __ldg(d + i);
+        return RowDesc{q.x, q.y, q.z, 0};
+    }
+    return RowDesc{-1, 0, 0, 0};
+}
+
+// Position in a warp's step stream (see k_gn_multi).
+constexpr int kStepCta = 0, kStepWarp = 1, kStepTeam = 2, kStepDone = 3;
+struct StepPos {
+    int ph, i;
+};
+
+__device__ __forceinline__ StepPos first_step(int h0, int h1, int p0, int pm, int p1) {
+    if (h0 < h1) return StepPos{kStepCta, h0};
+    if (p0 < pm) return StepPos{kStepWarp, p0};
+    if (pm < p1) return StepPos{kStepTeam, pm};
+    return StepPos{kStepDone, 0};
+}
+
+__device__ __forceinline__ StepPos next_step(StepPos q, int rpw, int h1, int p0, int pm, int p1) {
+    if (q.ph == kStepCta && q.i + 1 < h1) return StepPos{kStepCta, q.i + 1};
+    if (q.ph == kStepCta && p0 < pm) return StepPos{kStepWarp, p0};
+    if (q.ph == kStepWarp && q.i + 1 < pm) return StepPos{kStepWarp, q.i + 1};
+    if ((q.ph == kStepCta || q.ph == kStepWarp) && pm < p1) return StepPos{kStepTeam, pm};
+    if (q.ph == kStepTeam && q.i + rpw < p1) return StepPos{kStepTeam, q.i + rpw};
+    return StepPos{kStepDone, 0};
+}
+
+template <typename TS, typename TG>
+__device__ __forceinline__ RowDesc step_desc(const MultiArgs<TS, TG>& a, StepPos q, int team, int h1, int pm, int p1) {
+    if (q.ph == kStepCta) return row_at(a.hdesc, q.i, h1);
+    if (q.ph == kStepWarp) return row_at(a.rdesc, q.i, pm);
+    if (q.ph == kStepTeam) return row_at(a.rdesc, q.i + team, p1);
+    return RowDesc{-1, 0, 0, 0};
+}
+
+// this team's segment [beg, beg + len) of the step's row
+template <int RPW, int NT>
+__device__ __forceinline__ void step_segment(StepPos q, const RowDesc& d, int team, int tau, int& beg, int& len) {
+    int parts = 1, part = 0;
+    if (q.ph == kStepCta) {
+        parts = NT;
+        part = tau;
+    } else if (q.ph == kStepWarp) {
+        parts = RPW;
+        part = team;
+    }
+    beg = (int)((int64_t)d.deg * part / parts);
+    len = (int)((int64_t)d.deg * (part + 1) / parts) - beg;
+}
+
+template <typename TS, typename TG, int T>
+__global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) {
+    using A = Arith<TS>;
+    using TI = TeamIdx<T>;
+    constexpr int S = Pack<TG>::S, NI = TI::NI;
+    constexpr int RPW = 32 / T;              // rows a warp works at once
+    constexpr int NT = kMWarps * RPW;        // teams per CTA
     __shared__ unsigned char s_frozen[kMaxStarts];
     __shared__ double s_mx[kMWarps][kMaxStarts];
     __shared__ unsigned int s_fb[kMWarps][kMaxStarts];
     __shared__ int s_bad[kMWarps][kMaxStarts];
+    __shared__ double s_hmx[kMaxStarts];
+    __shared__ unsigned int s_hfb[kMaxStarts];
+    __shared__ int s_hbad[kMaxStarts];
+    __shared__ TS s_part[kMWarps * T * S];   // per-warp partials of a CTA row
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tbase = lane & ~(T - 1), t = lane & (T - 1);
+    const int tbase = lane & ~(T - 1), t = lane & (T - 1), team = lane / T;
+    const int tau = warp * RPW + team;
     const int B = a.B, Bp = a.Bp;
     if (threadIdx.x < kMaxStarts) s_frozen[threadIdx.x] = (threadIdx.x >= B || a.skip[threadIdx.x]) ? 1 : 0;
     __syncthreads();
     const int gw = blockIdx.x * kMWarps + warp;
-    const int p0 = __ldg(a.wbeg + gw), p1 = __ldg(a.wbeg + gw + 1);
+    const int p0 = __ldg(a.wbeg + gw), pm = __ldg(a.wmid + gw), p1 = __ldg(a.wbeg + gw + 1);
+    const int h0 = __ldg(a.hbeg + blockIdx.x), h1 = __ldg(a.hbeg + blockIdx.x + 1);
     unsigned int bar = 0;
-    int k = 0;
-    for (; k < a.iters; ++k) {
+    for (int k = 0; k < a.iters; ++k) {
         const int cur = k & 1;
         const TS g = (TS)a.gammas[k];
-        const TG* __restrict__ yg = a.yg[cur];
+        const TG* __restrict__ ybase = a.yg[cur] + t * S;
         double mx[S];
         unsigned int fbc[S];
         int bd[S];
@@ -119,80 +265,90 @@ __global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) 
             fbc[s] = 0u;
             bd[s] = 0;
         }
-        for (int p = p0; p < p1; p += 32 / T) {
-            const int pi = p + lane / T;
-            const bool has = pi < p1;
-            const int r = has ? __ldg(a.order + pi) : 0;
-            const int rb = has ? __ldg(a.rowptr + r) : 0;
-            const int deg = has ? __ldg(a.rowptr + r + 1) - rb : 0;
-            const int dmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)deg);
-            const int dmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)deg);
-            TS acc[S];
+        if (threadIdx.x < kMaxStarts) {
+            s_hmx[threadIdx.x] = 0.0;
+            s_hfb[threadIdx.x] = 0u;
+            s_hbad[threadIdx.x] = 0;
+        }
+        // ---- the warp's work as one stream of steps: CTA rows (fast mode:
+        // every team of the CTA sums one piece; per-warp folds meet in shared
+        // memory), then warp rows (the warp's teams split one row, folded by a
+        // fixed shuffle tree), then team rows (one team per row).  Step i+2's
+        // descriptor and step i+1's first index chunk load under step i's gathers.
+        StepPos q0 = first_step(h0, h1, p0, pm, p1);
+        RowDesc d0 = step_desc(a, q0, team, h1, pm, p1);
+        StepPos q1 = next_step(q0, RPW, h1, p0, pm, p1);
+        RowDesc d1 = step_desc(a, q1, team, h1, pm, p1);
+        int b0, l0;
+        step_segment<RPW, NT>(q0, d0, team, tau, b0, l0);
+        int idx[NI];
+        TI::load(a.col + d0.rb + b0, 0, l0, t, idx);
+        while (q0.ph != kStepDone) {
+            const StepPos q2 = next_step(q1, RPW, h1, p0, pm, p1);
+            const RowDesc d2 = step_desc(a, q2, team, h1, pm, p1);
+            TS xs[S];
+            TS vi = TS(0);
+            const size_t off = (size_t)(d0.r < 0 ? 0 : d0.r) * Bp + t * S;
+            if (q0.ph != kStepCta && d0.r >= 0) {
+                vi = __ldg(a.v + d0.r);
 #pragma unroll
-            for (int s = 0; s < S; ++s) acc[s] = TS(0);
-            int idx[NI];
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                const int pos = i * T + t;
-                idx[i] = (pos < kMU && pos < deg) ? __ldg(a.col + rb + pos) : 0;
+                for (int s = 0; s < S; ++s) xs[s] = a.x[cur][off + s];
             }
-            const TG* __restrict__ ybase = yg + t * S;
-            for (int q = 0; q < dmax; q += kMU) {
-                int nidx[NI];
+            int b1, l1;
+            step_segment<RPW, NT>(q1, d1, team, tau, b1, l1);
+            int ridx[NI];
+            TI::load(a.col + d1.rb + b1, 0, l1, t, ridx);
+            const int lmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)l0);
+            const int lmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)l0);
+            TS acc[S];
+            team_sum<TS, TG, T>(a.col + d0.rb + b0, l0, lmax, lmin, idx, ybase, Bp, tbase, t, acc);
+            if (q0.ph == kStepTeam) {
+                if (d0.r >= 0) {
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const int pos = q + kMU + i * T + t;
-                    nidx[i] = (i * T + t < kMU && pos < deg) ? __ldg(a.col + rb + pos) : 0;
+                    for (int s = 0; s < S; ++s) {
+                        if (s_frozen[t * S + s]) continue;
+                        update_one<TS, TG>(xs[s], vi, acc[s], g, a.x[cur ^ 1] + off + s, a.yg[cur ^ 1] + off + s,
+                                           mx[s], fbc[s], bd[s]);
+                    }
                 }
-                PT val[kMU];
-                if (q + kMU <= dmin) {
+            } else {
 #pragma unroll
-                    for (int u = 0; u < kMU; ++u) {
-                        const int j = __shfl_sync(0xffffffffu, idx[u / T], tbase + (u & (T - 1)));
-                        val[u] = __ldg(reinterpret_cast<const PT*>(ybase + (size_t)j * Bp));
+                for (int s = 0; s < S; ++s) acc[s] = fold_teams<TS, T>(acc[s]);
+                if (q0.ph == kStepWarp) {
+                    if (lane < T) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) {
+                            if (s_frozen[t * S + s]) continue;
+                            update_one<TS, TG>(xs[s], vi, acc[s], g, a.x[cur ^ 1] + off + s,
+                                               a.yg[cur ^ 1] + off + s, mx[s], fbc[s], bd[s]);
+                        }
                     }
                 } else {
+                    if (lane < T)
 #pragma unroll
-                    for (int u = 0; u < kMU; ++u) {
-                        const int j = __shfl_sync(0xffffffffu, idx[u / T], tbase + (u & (T - 1)));
-                        if (q + u < deg) val[u] = __ldg(reinterpret_cast<const PT*>(ybase + (size_t)j * Bp));
-                        else val[u] = PT();
+                        for (int s = 0; s < S; ++s) s_part[warp * T * S + t * S + s] = acc[s];
+                    __syncthreads();
+                    if (threadIdx.x < B && !s_frozen[threadIdx.x]) {
+                        const int b = threadIdx.x;
+                        TS tot = TS(0);
+                        for (int w = 0; w < kMWarps; ++w) tot = A::add(tot, s_part[w * T * S + b]);
+                        const size_t hoff = (size_t)d0.r * Bp + b;
+                        update_one<TS, TG>(a.x[cur][hoff], __ldg(a.v + d0.r), tot, g, a.x[cur ^ 1] + hoff,
+                                           a.yg[cur ^ 1] + hoff, s_hmx[b], s_hfb[b], s_hbad[b]);
                     }
+                    __syncthreads();
                 }
-#pragma unroll
-                for (int u = 0; u < kMU; ++u)
-#pragma unroll
-                    for (int s = 0; s < S; ++s) acc[s] = A::add(acc[s], (TS)P::at(val[u], s));
-#pragma unroll
-                for (int i = 0; i < NI; ++i) idx[i] = nidx[i];
             }
-            if (!has) continue;
-            // dynamics.py:104-107 for this row and the lane's starts
-            const TS vi = __ldg(a.v + r);
-            const size_t off = (size_t)r * Bp + t * S;
-            const TS* xc = a.x[cur] + off;
-            TS* xn = a.x[cur ^ 1] + off;
-            TG* yn = a.yg[cur ^ 1] + off;
+            q0 = q1;
+            d0 = d1;
+            b0 = b1;
+            l0 = l1;
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int b = t * S + s;
-                if (s_frozen[b]) continue;
-                const TS xi = xc[s];
-                const TS yi = A::mul(vi, xi);
-                const TS d = A::add(yi, A::mul(g, acc[s]));
-                const bool ok = (double)d > kSafeDiv;
-                const TS o = ok ? A::div(yi, d) : TS(kFallback);
-                xn[s] = o;
-                yn[s] = (TG)A::mul(vi, o);
-                TS df = A::sub(o, xi);  // dynamics.py:165
-                df = df < TS(0) ? -df : df;
-                const double diff = (double)df;
-                if (!(diff <= mx[s])) mx[s] = diff;
-                fbc[s] += ok ? 0u : 1u;
-                if (!isfinite((double)o)) bd[s] = 1;
-            }
+            for (int i = 0; i < NI; ++i) idx[i] = ridx[i];
+            q1 = q2;
+            d1 = d2;
         }
-        // per start: fold the warp's teams (lanes with equal t), then the CTA
+        // ---- per start: fold the warp's teams (lanes with equal t), then the CTA
 #pragma unroll
         for (int o = T; o < 32; o <<= 1) {
 #pragma unroll
@@ -217,9 +373,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) 
         __syncthreads();
         if (threadIdx.x < B && !s_frozen[threadIdx.x]) {
             const int b = threadIdx.x;
-            double m = 0.0;
-            unsigned int f = 0;
-            int bb = 0;
+            double m = s_hmx[b];
+            unsigned int f = s_hfb[b];
+            int bb = s_hbad[b];
             for (int q = 0; q < kMWarps; ++q) {
                 if (!(s_mx[q][b] <= m)) m = s_mx[q][b];
                 f += s_fb[q][b];
@@ -298,18 +454,30 @@ __global__ void k_multi_precheck(int64_t n, const int32_t* __restrict__ rowptr, 
     if (!(__dadd_rn(xi, s) > 0.0)) atomicOr(&flags[1], 1);  // dynamics.py:125
 }
 
-// ---- host plan: contiguous ranges of the relabel order per warp, balanced by gathers
+// ---- host plan (cached per graph, grid and mode) -------------------------
+// Fast mode splits rows longer than one warp's fair share over all teams of a
+// CTA (LPT over CTAs); the remaining rows, in the relabel order (degree-sorted:
+// a warp's concurrent rows have similar lengths), are cut into contiguous
+// per-warp ranges so that every CTA carries the same gathers in total.
 struct MultiPlan {
+    int4* rdesc = nullptr;
     int32_t* wbeg = nullptr;
+    int32_t* wmid = nullptr;
+    int4* hdesc = nullptr;
+    int32_t* hbeg = nullptr;
 };
 static std::mutex g_mplan_mu;
-static std::map<std::pair<const gn_graph*, int>, MultiPlan> g_mplans;
+static std::map<std::tuple<const gn_graph*, int, int, int>, MultiPlan> g_mplans;
 
 void release_multi_plans(const gn_graph* g) {
     std::lock_guard<std::mutex> lk(g_mplan_mu);
     for (auto it = g_mplans.begin(); it != g_mplans.end();) {
-        if (it->first.first == g) {
+        if (std::get<0>(it->first) == g) {
+            cudaFree(it->second.rdesc);
             cudaFree(it->second.wbeg);
+            cudaFree(it->second.wmid);
+            cudaFree(it->second.hdesc);
+            cudaFree(it->second.hbeg);
             it = g_mplans.erase(it);
         } else {
             ++it;
@@ -317,12 +485,19 @@ void release_multi_plans(const gn_graph* g) {
     }
 }
 
-static int multi_plan(gn_graph* g, int G, const int32_t** out) {
+template <typename V>
+static int upload_vec(const std::vector<V>& h, V** d) {
+    GN_CUDA(cudaMalloc((void**)d, sizeof(V) * std::max<size_t>(h.size(), 1)));
+    if (!h.empty()) GN_CUDA(cudaMemcpy(*d, h.data(), sizeof(V) * h.size(), cudaMemcpyHostToDevice));
+    return GN_OK;
+}
+
+static int multi_plan(gn_graph* g, int G, bool exact, int rpw, const MultiPlan** out) {
     std::lock_guard<std::mutex> lk(g_mplan_mu);
-    auto key = std::make_pair((const gn_graph*)g, G);
+    auto key = std::make_tuple((const gn_graph*)g, G, exact ? 1 : 0, rpw);
     auto it = g_mplans.find(key);
     if (it != g_mplans.end()) {
-        *out = it->second.wbeg;
+        *out = &it->second;
         return GN_OK;
     }
     const int64_t n = g->n;
@@ -330,23 +505,75 @@ static int multi_plan(gn_graph* g, int G, const int32_t** out) {
     GN_CUDA(cudaMemcpy(rp.data(), g->rowptr, sizeof(int32_t) * rp.size(), cudaMemcpyDeviceToHost));
     if (n > 0) GN_CUDA(cudaMemcpy(perm.data(), g->perm, sizeof(int32_t) * perm.size(), cudaMemcpyDeviceToHost));
     const int nw = G * kMWarps;
-    // cost of a row: its gathers plus a fixed per-row share (index fetch, update)
-    constexpr double kRowCost = 8.0;
+    constexpr double kRowCost = 8.0;  // per-row share of the index fetch and the update, in gathers
+    auto deg = [&](int32_t r) { return rp[(size_t)r + 1] - rp[(size_t)r]; };
     double total = 0.0;
-    for (int64_t i = 0; i < n; ++i) total += (double)(rp[(size_t)perm[(size_t)i] + 1] - rp[(size_t)perm[(size_t)i]]) + kRowCost;
-    std::vector<int32_t> wb((size_t)nw + 1, (int32_t)n);
-    wb[0] = 0;
-    double acc = 0.0;
-    int w = 1;
-    for (int64_t i = 0; i < n && w < nw; ++i) {
-        acc += (double)(rp[(size_t)perm[(size_t)i] + 1] - rp[(size_t)perm[(size_t)i]]) + kRowCost;
-        while (w < nw && acc >= total * w / nw) wb[(size_t)w++] = (int32_t)(i + 1);
+    for (int64_t i = 0; i < n; ++i) total += (double)deg(perm[(size_t)i]) + kRowCost;
+    const double share = total / nw;  // one warp's fair share
+    // fast mode: rows longer than a warp's share (and 2048) are split over a
+    // CTA; rows whose walk would outlast a team's share are split over a warp
+    const double cta_min = std::max(2048.0, share), warp_min = std::max(2.0 * kMU, share / rpw);
+    std::vector<int32_t> split, wrows, trows;
+    trows.reserve((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t r = perm[(size_t)i];
+        const double d = deg(r);
+        (exact || d <= warp_min ? trows : (d <= cta_min ? wrows : split)).push_back(r);
     }
-    int32_t* d = nullptr;
-    GN_CUDA(cudaMalloc(&d, sizeof(int32_t) * wb.size()));
-    GN_CUDA(cudaMemcpy(d, wb.data(), sizeof(int32_t) * wb.size(), cudaMemcpyHostToDevice));
-    g_mplans[key].wbeg = d;
-    *out = d;
+    std::vector<int32_t> regular = wrows;
+    regular.insert(regular.end(), trows.begin(), trows.end());
+    std::vector<double> load((size_t)G, 0.0);
+    std::vector<std::vector<int32_t>> per_cta((size_t)G);
+    for (int32_t r : split) {  // degree-descending already (hubs lead the relabel order)
+        const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        per_cta[(size_t)c].push_back(r);
+        load[(size_t)c] += (double)deg(r) + kRowCost;
+    }
+    std::vector<int4> hd;
+    std::vector<int32_t> hb((size_t)G + 1, 0);
+    for (int c = 0; c < G; ++c) {
+        for (int32_t r : per_cta[(size_t)c]) hd.push_back(make_int4(r, rp[(size_t)r], deg(r), 0));
+        hb[(size_t)c + 1] = (int32_t)hd.size();
+    }
+    // regular rows: CTA c gets (total / G - load[c]) of them, cut evenly over its warps
+    std::vector<int4> rd;
+    rd.reserve(regular.size());
+    std::vector<double> pre(regular.size() + 1, 0.0);
+    for (size_t i = 0; i < regular.size(); ++i) {
+        const int32_t r = regular[i];
+        rd.push_back(make_int4(r, rp[(size_t)r], deg(r), 0));
+        pre[i + 1] = pre[i] + (double)deg(r) + kRowCost;
+    }
+    std::vector<double> bound((size_t)nw + 1, 0.0);  // target prefix cost at each warp boundary
+    double acc = 0.0;
+    const double reg_total = pre.back();
+    double want_total = 0.0;
+    for (int c = 0; c < G; ++c) want_total += std::max(0.0, total / G - load[(size_t)c]);
+    for (int c = 0; c < G; ++c) {
+        const double want = want_total > 0 ? std::max(0.0, total / G - load[(size_t)c]) * reg_total / want_total : 0.0;
+        for (int w = 0; w < kMWarps; ++w) {
+            acc += want / kMWarps;
+            bound[(size_t)c * kMWarps + w + 1] = acc;
+        }
+    }
+    std::vector<int32_t> wb((size_t)nw + 1, (int32_t)regular.size());
+    wb[0] = 0;
+    size_t i = 0;
+    for (int w = 1; w < nw; ++w) {
+        while (i < regular.size() && pre[i + 1] <= bound[(size_t)w]) ++i;
+        wb[(size_t)w] = (int32_t)i;
+    }
+    std::vector<int32_t> wm((size_t)nw);
+    for (int w = 0; w < nw; ++w)
+        wm[(size_t)w] = std::min(std::max((int32_t)wrows.size(), wb[(size_t)w]), wb[(size_t)w + 1]);
+    MultiPlan mp;
+    int rc;
+    if ((rc = upload_vec(rd, &mp.rdesc)) || (rc = upload_vec(wb, &mp.wbeg)) || (rc = upload_vec(wm, &mp.wmid)) ||
+        (rc = upload_vec(hd, &mp.hdesc)) ||
+        (rc = upload_vec(hb, &mp.hbeg)))
+        return rc;
+    auto res = g_mplans.emplace(key, mp);
+    *out = &res.first->second;
     return GN_OK;
 }
 
@@ -358,7 +585,6 @@ static void* multi_kernel() {
 template <typename TS, typename TG>
 static void* pick_kernel(int T) {
     switch (T) {
-        case 1: return multi_kernel<TS, TG, 1>();
         case 2: return multi_kernel<TS, TG, 2>();
         case 4: return multi_kernel<TS, TG, 4>();
         case 8: return multi_kernel<TS, TG, 8>();
@@ -391,7 +617,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     const int64_t n = g->n;
     const int64_t launches0 = gn_launch_count();
     constexpr int S = Pack<TG>::S;
-    int Bp = S;
+    int Bp = 2 * S;  // teams of at least 2 lanes (one-lane teams would need 16 index registers per chunk)
     while (Bp < B) Bp *= 2;
     const int T = Bp / S;
     CallCtx ctx;
@@ -471,20 +697,21 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     const int64_t rows_per_cta = (int64_t)kMWarps * (32 / T);
     int grid = (int)std::min<int64_t>(maxb, std::max<int64_t>(1, (n + rows_per_cta - 1) / rows_per_cta));
     if (g->grid_override > 0) grid = std::min(maxb, g->grid_override);
-    const int32_t* wbeg = nullptr;
-    if ((rc = multi_plan(g, grid, &wbeg))) return rc;
+    const MultiPlan* plan = nullptr;
+    if ((rc = multi_plan(g, grid, (flags & GN_EXACT) != 0, 32 / T, &plan))) return rc;
 
     MultiArgs<TS, TG> a;
     memset(&a, 0, sizeof(a));
     a.n = n;
     a.B = B;
     a.Bp = Bp;
-    a.rowptr = g->rowptr;
     a.col = g->col;
-    a.order = g->perm;
-    a.wbeg = wbeg;
+    a.rdesc = plan->rdesc;
+    a.wbeg = plan->wbeg;
+    a.wmid = plan->wmid;
+    a.hdesc = plan->hdesc;
+    a.hbeg = plan->hbeg;
     a.v = v;
-    a.w = w;
     a.x[0] = xa;
     a.x[1] = xa + nn * Bp;
     a.yg[0] = ya;

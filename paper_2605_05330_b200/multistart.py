@@ -3,9 +3,10 @@
 solver.py:100-153).
 
 The engine keeps the B states start-minor (x[v][b]) so that one contiguous
-read per neighbour serves every start (csrc/gn_multi.cu).  Each start's
-trajectory is bitwise its own ``run_wrgn(..., exact=True)`` run: the same
-per-row sequential sums, per-start checks, non-finite stop and early exit.
+read per neighbour serves every start (csrc/gn_multi.cu).  In EXACT mode each
+start's trajectory is bitwise its own ``run_wrgn(..., exact=True)`` run: the
+same per-row sequential sums, per-start checks, non-finite stop and early
+exit.  The fast mode differs only in the rows it splits (hubs).
 """
 
 from __future__ import annotations
@@ -56,13 +57,16 @@ class MultiResult:
         return t
 
 
-def run_multi(g, x0s, schedule: GammaSchedule, early_exit: bool = False, *, dtype=None, device=None,
-              clip: bool = True) -> MultiResult:
+def run_multi(g, x0s, schedule: GammaSchedule, early_exit: bool = False, *, dtype=None, exact=None,
+              device=None, clip: bool = True) -> MultiResult:
     """run_wrgn(g, x0s[b], schedule) for every start b, in one engine call.
 
     ``x0s`` is [B, n] (1 <= B <= 64).  Starts that fail the initial checks or
     reach a non-finite state are reported in ``status`` (they do not stop the
     others); ``MultiResult.error(b)`` gives run_wrgn's message for them.
+    With ``exact`` every start is bitwise its own ``run_wrgn(exact=True)``;
+    otherwise rows longer than a warp's share of the work are summed in
+    pieces (fixed piece order: deterministic, within the fp64 tolerance).
     """
     X = np.ascontiguousarray(np.asarray(x0s, dtype=np.float64))
     if X.ndim != 2 or X.shape[1] != g.n:
@@ -81,6 +85,8 @@ def run_multi(g, x0s, schedule: GammaSchedule, early_exit: bool = False, *, dtyp
     fail = np.full(B, -1, dtype=np.int32)
     st = E.RunStats()
     flags = (E.GN_EARLY_EXIT if early_exit else 0) | (0 if clip else E.GN_NO_CLIP)
+    if _opt("exact", exact):
+        flags |= E.GN_EXACT
     rc = E.lib().gn_multi_run(h.handle, B, E.ptr(X), E.ptr(gam), iters, float(schedule.final_gamma), flags,
                               E.ptr(x), E.ptr(si), E.ptr(fb), E.ptr(ran), E.ptr(status), E.ptr(fail),
                               ctypes.byref(st))

@@ -18,7 +18,7 @@ def _starts(n, B, seed=11):
 
 
 def _same_as_single(g, X, sched, dtype, early_exit=False):
-    res = P.run_multi(g, X, sched, early_exit=early_exit, dtype=dtype)
+    res = P.run_multi(g, X, sched, early_exit=early_exit, dtype=dtype, exact=True)
     for b in range(X.shape[0]):
         r = P.run_engine(g, X[b], sched, early_exit=early_exit, dtype=dtype, exact=True)
         k = len(r.trace)
@@ -74,7 +74,7 @@ def test_failing_starts_do_not_stop_the_others():
     X = _starts(g.n, 4)
     X[1, 7] = -0.25              # negative entry
     X[2, :] = 0.0                # zero closed-neighbourhood sums
-    res = P.run_multi(g, X, s, dtype="fp64")
+    res = P.run_multi(g, X, s, dtype="fp64", exact=True)
     assert res.error(1) == "state entries must be nonnegative"
     assert res.error(2) == "initial state has a zero closed neighborhood sum"
     assert res.iters_run[1] == 0 and res.iters_run[2] == 0
@@ -106,3 +106,23 @@ def test_solver_uses_multistart_for_large_graphs():
         assert rec.start == f"seed-4.{i}" and rec.objective == w and rec.valid and rec.maximal
         assert rec.iterations == 200
     assert stats.aborted_starts == 0
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_fast_mode_split_hubs_within_tolerance(dtype):
+    # BA n=200k: the hubs exceed a warp's share and are summed in pieces
+    inst = G.c3_ba()
+    s = P.GammaSchedule.pursuit(iterations=200)
+    X = _starts(inst.n, 4, seed=3)
+    res = P.run_multi(inst.graph, X, s, dtype=dtype)
+    ex = P.run_multi(inst.graph, X, s, dtype=dtype, exact=True)
+    for b in range(4):
+        ref = O.run(inst.graph, X[b], s.table(), s.final_gamma, threads=O.default_threads())
+        tol = 1e-9 if dtype == "fp64" else 1e-3
+        assert np.max(np.abs(res.x[b] - ref.x)) <= tol
+        assert np.array_equal(res.fallbacks[b], ref.fallbacks)
+        if dtype == "fp64":
+            assert np.array_equal(ex.x[b], ref.x)  # EXACT stays bitwise
+            assert np.allclose(res.step_inf[b], ref.step_inf, rtol=1e-6, atol=1e-12)
+    again = P.run_multi(inst.graph, X, s, dtype=dtype)
+    assert np.array_equal(again.x, res.x)  # deterministic piece order
