@@ -18,6 +18,7 @@ Printed JSON keys follow the driver contract; see DESIGN.md "Measurement".
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -198,6 +199,8 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--starts", type=int, default=1,
+                    help="starts per instance (SURVEY 8f f1): >1 runs them together through gn_multi_run")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":
@@ -237,8 +240,10 @@ def main():
     sched = P.GammaSchedule.pursuit(iterations=args.iters)
     gam = np.ascontiguousarray(sched.table())
     iters = len(gam)
-    x0_dev = torch.from_numpy(np.ascontiguousarray(inst.x0)).to(dev)
-    x_out = torch.empty(g.n, dtype=torch.float64, device=dev)
+    starts = max(1, args.starts) if batch is None else 1
+    x0s = inst.x0[None, :] if starts == 1 else np.stack([P.init_random(g.n, [2605, b]) for b in range(starts)])
+    x0_dev = torch.from_numpy(np.ascontiguousarray(x0s)).to(dev)
+    x_out = torch.empty((starts, g.n), dtype=torch.float64, device=dev)
     si = np.zeros(iters)
     fb = np.zeros(iters, dtype=np.int64)
     mass = np.zeros(iters)
@@ -254,6 +259,21 @@ def main():
             st = E.RunStats()
             for f, _ in E.RunStats._fields_:
                 setattr(st, f, r.stats[f])
+            return st
+    elif starts > 1:
+        h = g.device_graph(dtype, local)
+        kernel_name = "gn::k_gn_multi (persistent, all starts and iterations in 1 launch)"
+        msi = np.zeros((starts, iters))
+        mfb = np.zeros((starts, iters), dtype=np.int64)
+        mran = np.zeros(starts, dtype=np.int32)
+        mst = np.zeros(starts, dtype=np.int32)
+        mfail = np.zeros(starts, dtype=np.int32)
+
+        def device_step():
+            st = E.RunStats()
+            E.check(E.lib().gn_multi_run(h.handle, starts, E.ctypes.c_void_p(x0_dev.data_ptr()), E.ptr(gam), iters,
+                                         1.5, flags, E.ctypes.c_void_p(x_out.data_ptr()), E.ptr(msi), E.ptr(mfb),
+                                         E.ptr(mran), E.ptr(mst), E.ptr(mfail), E.ctypes.byref(st)))
             return st
     else:
         h = g.device_graph(dtype, local)
@@ -293,10 +313,14 @@ def main():
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    edges_all = inst.m * ws if args.config != "C4" else inst.m * ws
+    edges_all = inst.m * ws * starts
     value = edges_all * iters * args.steps / (total_ms * 1e-3)
 
-    # ---- e2e through the public API: host x0 in, MIS out, every step
+    # ---- e2e through the public API: host x0 in, MIS out, every step.
+    # The harness has torch loaded (millions of tracked objects): move them
+    # out of the collector's way so a full collection cannot land in a step.
+    gc.collect()
+    gc.freeze()
     x0_host = torch.from_numpy(np.ascontiguousarray(inst.x0)).pin_memory().numpy()
     e2e_t = []
     h2d = d2h = 0
@@ -305,18 +329,20 @@ def main():
         t0 = time.perf_counter()
         if batch is not None:
             r = gb.run(x0_host, sched)
+        elif starts > 1:
+            r = P.run_multi(g, x0s, sched, dtype=dtype, device=local)
         else:
             r = P.run_engine(g, x0_host, sched, dtype=dtype, device=local)
         t1 = time.perf_counter()
-        sol = P.round_to_mis(g, r.x)
+        sol = [P.round_to_mis(g, xb) for xb in r.x] if starts > 1 else P.round_to_mis(g, r.x)
         barrier()
         if os.environ.get("GN_BENCH_VERBOSE"):
             print(f"e2e step {i}: run {1e3 * (t1 - t0):.2f} ms, round {1e3 * (time.perf_counter() - t1):.2f} ms, "
-                  f"call {r.stats['total_ms']:.2f} ms", file=sys.stderr, flush=True)
+                  f"call {r.stats['total_ms']:.2f} ms loop {r.stats['loop_ms']:.2f} ms", file=sys.stderr, flush=True)
         if i >= args.warmup:
             e2e_t.append(time.perf_counter() - t0)
-            h2d = r.stats["h2d_bytes"] + 8 * g.n          # + the rounding's state upload
-            d2h = r.stats["d2h_bytes"] + g.n + 64         # + membership mask and flags
+            h2d = r.stats["h2d_bytes"] + 8 * g.n * starts          # + the rounding's state upload
+            d2h = r.stats["d2h_bytes"] + (g.n + 64) * starts       # + membership mask and flags
     del sol
     e2e_total = sum(e2e_t)
     if ws > 1:
@@ -337,10 +363,12 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     s_bytes = 8 if dtype == "fp64" else 4  # s = element size of the state vectors
-    b_iter = algorithmic_bytes(g.n, 2 * inst.m, s_bytes)
+    # SURVEY 8(d) per iteration; with several starts the index stream is read
+    # once for all of them and the state streams once per start
+    b_iter = algorithmic_bytes(g.n, 2 * inst.m, s_bytes) + 3 * s_bytes * g.n * (starts - 1)
     loop_avg = statistics.mean(loop_ms)
     achieved = b_iter * iters / (loop_avg * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config) if starts == 1 else None
     info = {"n": g.n}
 
     cpu = None
@@ -363,7 +391,7 @@ def main():
         "dtype": {"fp64": "f64", "fp32": "f32-gather/f64-state", "fp32_pure": "f32"}[dtype],
         "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
         "config": {
-            "workload": args.config + ": " + CONFIG_TEXT[args.config],
+            "workload": args.config + ": " + CONFIG_TEXT[args.config] + (f"; {starts} starts per call" if starts > 1 else ""),
             "n": g.n, "m": inst.m, "iters": iters, "schedule": "pursuit 0.9->1.5",
             "scale": args.scale if args.config == "C5" else None,
             "parallelism": f"replicas x{ws}" if args.config != "C4" else f"batch shard x{ws} (1024 graphs/rank)",
@@ -371,9 +399,11 @@ def main():
             "index_format": "uint16" if info["n"] <= 65536 else "int32",
             "inputs": "w and x0 binary32-representable (BASELINE configs[1]: fp32 weights)",
             "engine_dtype": dtype,
+            "starts": starts,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "api": "paper_2605_05330_b200.run_engine + round_to_mis (host numpy in, MIS out)"},
+                "api": ("paper_2605_05330_b200.run_multi + round_to_mis per start" if starts > 1 else
+                        "paper_2605_05330_b200.run_engine + round_to_mis") + " (host numpy in, MIS out)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_name,

@@ -139,7 +139,9 @@ int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight,
  * step_inf / fallbacks are [num_starts][iters] (entries past iters_run[b]
  * untouched); iters_run / status / fail_iter are [num_starts].  Returns
  * GN_OK, or the first failing start's code.  1 <= num_starts <= 64.
- * Flags: GN_EARLY_EXIT, GN_NO_CHECK, GN_NO_CLIP, GN_NONFINITE_OK. */
+ * Flags: GN_EXACT (no row splitting: bitwise per start), GN_EARLY_EXIT,
+ * GN_NO_CHECK, GN_NO_CLIP, GN_NONFINITE_OK, GN_DEVICE_IO (x0 / x_out are
+ * device fp64 arrays). */
 int gn_multi_run(gn_graph* g, int num_starts, const double* x0,
                  const double* gammas, int iters, double final_gamma,
                  uint32_t flags, double* x_out, double* step_inf,

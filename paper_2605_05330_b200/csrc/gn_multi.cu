@@ -646,7 +646,9 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     GN_CUDA(ws.get(&ya, 2 * sizeof(TG) * nn * Bp));
     GN_CUDA(ws.get(&v, sizeof(TS) * nn));
     GN_CUDA(ws.get(&w, sizeof(TS) * nn));
-    GN_CUDA(ws.get(&xin, 8 * nn * B));
+    const bool dev_io = (flags & GN_DEVICE_IO) != 0;
+    if (dev_io) xin = const_cast<double*>(x0);
+    else GN_CUDA(ws.get(&xin, 8 * nn * B));
     GN_CUDA(ws.get(&gam, 8 * (size_t)iters));
     GN_CUDA(ws.get(&sinf, 8 * (size_t)iters * B));
     GN_CUDA(ws.get(&fb, 4 * (size_t)iters * B));
@@ -655,7 +657,8 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     GN_CUDA(ws.get(&skip, 4 * (size_t)B));
     GN_CUDA(ws.get(&chk, 8 * (size_t)B));
     GN_CUDA(ws.get(&barrier, 4));
-    GN_CUDA(ws.get(&out64, 8 * nn * B));
+    if (dev_io) out64 = x_out;
+    else GN_CUDA(ws.get(&out64, 8 * nn * B));
     GN_CUDA(cudaMemsetAsync(sinf, 0, 8 * (size_t)iters * B, s));
     GN_CUDA(cudaMemsetAsync(fb, 0, 4 * (size_t)iters * B, s));
     GN_CUDA(cudaMemsetAsync(bad, 0, 4 * (size_t)iters * B, s));
@@ -663,8 +666,8 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     GN_CUDA(cudaMemsetAsync(chk, 0, 8 * (size_t)B, s));
     GN_CUDA(cudaMemsetAsync(barrier, 0, 4, s));
     GN_CUDA(cudaMemcpyAsync(gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice, s));
-    if (n > 0) GN_CUDA(cudaMemcpyAsync(xin, x0, 8 * (size_t)n * B, cudaMemcpyHostToDevice, s));
-    int64_t h2d = 8 * (int64_t)iters + 8 * n * B, d2h = 0;
+    if (n > 0 && !dev_io) GN_CUDA(cudaMemcpyAsync(xin, x0, 8 * (size_t)n * B, cudaMemcpyHostToDevice, s));
+    int64_t h2d = 8 * (int64_t)iters + (dev_io ? 0 : 8 * n * B), d2h = 0;
 
     // checks per start (dynamics.py:145-149)
     std::vector<int> hchk(2 * (size_t)B, 0), hskip((size_t)B, 0);
@@ -746,8 +749,10 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
         k_multi_finalize<TS><<<blocks_of(n * B), 256, 0, s>>>(n, B, Bp, a.x[0], a.x[1], run, out64,
                                                              (flags & GN_NO_CLIP) ? 0 : 1);
         GN_LAUNCHED();
-        GN_CUDA(cudaMemcpyAsync(x_out, out64, 8 * (size_t)n * B, cudaMemcpyDeviceToHost, s));
-        d2h += 8 * n * B;
+        if (!dev_io) {
+            GN_CUDA(cudaMemcpyAsync(x_out, out64, 8 * (size_t)n * B, cudaMemcpyDeviceToHost, s));
+            d2h += 8 * n * B;
+        }
     }
     GN_CUDA(cudaEventRecord(ev[3], s));
     GN_CUDA(cudaStreamSynchronize(s));
