@@ -13,8 +13,8 @@
 // lists (local uint16 ids, the reference's neighbour order) stored
 // position-major in pairs so a lane fetches positions p, p+1 with one 32-bit
 // shared load and a warp's fetch is 128 contiguous bytes.  Each thread owns
-// up to kRowsPerThread rows whose x, v, w stay in registers for the whole
-// run; only the published values yg live in shared memory (ping-pong).
+// up to kRowsPerThread rows (dealt snake-wise over the degree order) whose
+// x, v, w stay in registers for the whole run; only the published values yg live in shared memory (ping-pong).
 // Per iteration: sequential per-row sums (the reference's order: bitwise),
 // the update, and one block reduction (step_inf, fallbacks, non-finite,
 // objective and the trace dots) whose single __syncthreads also publishes
@@ -162,6 +162,14 @@ __device__ __forceinline__ double bwarp_sum(double v) {
     return v;
 }
 
+// Row q of this thread.  Rows are degree-descending; a snake deal (t, then
+// 2*blockDim-1-t, ...) gives every thread a long and a short row, so the
+// per-iteration barrier does not wait for the threads holding the hubs.
+__device__ __forceinline__ int own_row(int q) {
+    const int t = (q & 1) ? (int)blockDim.x - 1 - (int)threadIdx.x : (int)threadIdx.x;
+    return q * (int)blockDim.x + t;
+}
+
 // Per-thread row state (registers for the whole run).
 template <typename TS>
 struct OwnRows {
@@ -186,7 +194,7 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
     int nf = 0;
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = threadIdx.x + q * blockDim.x;
+        const int r = own_row(q);
         if (r >= nb) continue;
         // sequential neighbour sum in the reference's order; a 32-bit shared
         // load fetches positions p, p+1
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_gn_batch(BatchArgs<TS, TG>
     OwnRows<TS> R;
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = threadIdx.x + q * blockDim.x;
+        const int r = own_row(q);
         R.deg[q] = 0;
         R.x[q] = TS(0);
         R.v[q] = TS(0);
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_gn_batch(BatchArgs<TS, TG>
     }
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = threadIdx.x + q * blockDim.x;
+        const int r = own_row(q);
         if (r < nb) {
             double xo = (double)R.x[q];
             if (a.clip) xo = xo < 0.0 ? 0.0 : (xo > 1.0 ? 1.0 : xo);
