@@ -91,6 +91,7 @@ struct LoopArgs {
     const int32_t* __restrict__ perm;
     long long* prof;   // optional timestamps (GN_PROF_ITER): [G][kWarps+4]
     int prof_iter;
+    const int* chk;    // [2] x0 check flags (k_precheck_f64): set -> the run does not start
 };
 
 struct Stats {
@@ -513,6 +514,10 @@ __device__ double ring_step_inf(const double* ring_slot) {
 template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, TG> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (__ldcg(a.chk) | __ldcg(a.chk + 1)) {  // x0 failed its checks (dynamics.py:146-149)
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.status[0] = 0;
+        return;
+    }
     TS* s_slot = (TS*)smem_raw;
     TS* s_hslot = (TS*)(smem_raw + a.hub_slot_off);
     TG* s_hot = (TG*)(smem_raw + a.hot_off);
@@ -811,13 +816,8 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
         k_prepare<TS, TG><<<blocks_for(n), 256, 0, s>>>(n, xin, g->inv, (const TS*)g->v, xa, ya);
         GN_LAUNCHED();
     }
-    if (check && n > 0) {
-        int hchk[2] = {0, 0};
-        GN_CUDA(cudaMemcpyAsync(hchk, chk, sizeof(hchk), cudaMemcpyDeviceToHost, s));
-        GN_CUDA(cudaStreamSynchronize(s));
-        if (hchk[0]) return fail(GN_ERR_NEGATIVE, "state entries must be nonnegative");
-        if (hchk[1]) return fail(GN_ERR_NOT_NORMALIZABLE, "initial state has a zero closed neighborhood sum");
-    }
+    // the check flags are read by the loop kernel itself (it exits at once
+    // when one is set) and by the host with the results: no sync here
 
     // ---- the loop
     LoopArgs<TS, TG> a;
@@ -858,6 +858,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.barrier = barrier;
     a.x_hist = hist;
     a.perm = g->perm;
+    a.chk = chk;
     long long* dprof = nullptr;
     const char* prof_env = getenv("GN_PROF_ITER");
     if (prof_env) {
@@ -873,8 +874,9 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     GN_CUDA(cudaEventRecord(ev[2], s));
 
     // ---- results back
-    int hstatus[4];
+    int hstatus[4], hchk[2] = {0, 0};
     GN_CUDA(cudaMemcpyAsync(hstatus, status, sizeof(hstatus), cudaMemcpyDeviceToHost, s));
+    GN_CUDA(cudaMemcpyAsync(hchk, chk, sizeof(hchk), cudaMemcpyDeviceToHost, s));
     std::vector<double> hsi((size_t)iters), hfb((size_t)iters);
     std::vector<int> hbad((size_t)iters);
     std::vector<double> hdots(4 * (size_t)(iters + 1));
@@ -884,6 +886,8 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     GN_CUDA(cudaMemcpyAsync(hdots.data(), dots, 8 * 4 * (size_t)(iters + 1), cudaMemcpyDeviceToHost, s));
     d2h += 8 * 2 * iters + 4 * iters + 8 * 4 * (iters + 1) + 16;
     GN_CUDA(cudaStreamSynchronize(s));
+    if (hchk[0]) return fail(GN_ERR_NEGATIVE, "state entries must be nonnegative");             // dynamics.py:147
+    if (hchk[1]) return fail(GN_ERR_NOT_NORMALIZABLE, "initial state has a zero closed neighborhood sum");  // :149
     const int ran = hstatus[0];
     const TS* xfinal = (ran & 1) ? xb : xa;
     const int clip = (flags & GN_NO_CLIP) ? 0 : 1;
