@@ -331,7 +331,7 @@ def round_to_mis(g, x) -> MisSolution:
     """
     sel, weight, ind, mx = round_result(g, x)
     members = np.flatnonzero(sel)
-    return MisSolution(members=tuple(int(i) for i in members), weight=weight, independent=ind, maximal=mx)
+    return MisSolution(members=tuple(members.tolist()), weight=weight, independent=ind, maximal=mx)
 
 
 __all__ = [

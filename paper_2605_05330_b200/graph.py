@@ -309,7 +309,7 @@ class MisSolution:
     def from_members(cls, g, members: Iterable[int]) -> "MisSolution":
         idx = _check_members(g, members)
         weight, ind, mx = _member_report(g, idx)
-        return cls(members=tuple(int(i) for i in idx), weight=weight, independent=ind, maximal=mx)
+        return cls(members=tuple(np.asarray(idx, dtype=np.int64).tolist()), weight=weight, independent=ind, maximal=mx)
 
 
 def erdos_renyi(
