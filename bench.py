@@ -187,6 +187,111 @@ def run_reference(args, ws, rank):
     return 0
 
 
+def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
+    """C5 as BASELINE names it: the graph vertex-range partitioned over the N
+    ranks (partition.py), each rank stepping its owned rows (gn_part_step) and
+    exchanging boundary values with its peers every iteration (NCCL
+    point-to-point through torch.distributed).  Strong scaling: the graph is
+    the same at every N.  Timed with CUDA events on the stream the engine and
+    NCCL share, max over ranks."""
+    from paper_2605_05330_b200.partition import DistExchange, EngineBackend, build_partitions
+
+    dtype = args.dtype or inst.dtype
+    sched = P.GammaSchedule.pursuit(iterations=args.iters)
+    gam = sched.table()
+    iters = len(gam)
+    spec = build_partitions(inst.graph, ws)[rank]
+    be = EngineBackend(spec, dtype=dtype, device=local)
+    ex = DistExchange(be) if ws > 1 else None
+    x0l = spec.local_x0(inst.x0)
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+
+    def step():
+        be.begin(x0l, gam)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(iters):
+            be.step(k)
+            if ex is not None:
+                ex.halo(k)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        flush_l2(torch, dev)
+        step()
+    launches0 = E.launch_count()
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(torch, dev)
+            barrier()
+            times.append(step())
+    launches = E.launch_count() - launches0
+    total_ms = float(sum(times))
+    # e2e: host x0 in, the owned x out, every step (begin .. end)
+    e2e = []
+    for _ in range(args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        be.begin(x0l, gam)
+        for k in range(iters):
+            be.step(k)
+            if ex is not None:
+                ex.halo(k)
+        be.end(iters)
+        barrier()
+        e2e.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e)
+    if ws > 1:
+        t = torch.tensor([total_ms, e2e_total], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, e2e_total = float(t[0].item()), float(t[1].item())
+    if rank == 0:
+        m, n = inst.m, inst.graph.n
+        value = m * iters * args.steps / (total_ms * 1e-3)
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        s_bytes = 8 if dtype == "fp64" else 4
+        b_iter = algorithmic_bytes(n, 2 * m, s_bytes)
+        achieved = b_iter * iters * args.steps / (total_ms * 1e-3) / 1e9
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": {"fp64": "f64", "fp32": "f32-gather/f64-state", "fp32_pure": "f32"}[dtype],
+            "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
+            "config": {"workload": "C5: " + CONFIG_TEXT["C5"] + f"; vertex-range partitioned over {ws} GPU(s)",
+                       "n": n, "m": m, "iters": iters, "scale": args.scale, "parallelism": f"partition x{ws}",
+                       "ghosts_rank0": spec.n_ghost, "owned_rank0": spec.n_own,
+                       "l2": "flushed between steps (256 MB write)", "engine_dtype": dtype},
+            "e2e": {"value": m * iters * args.steps / e2e_total, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * (spec.n_own + spec.n_ghost) + 8 * iters,
+                    "d2h_bytes_per_step": 8 * spec.n_own + 32 * iters,
+                    "api": "partition.EngineBackend begin/step/halo/end (host x0 in, owned x out), rank 0 shown"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
+                         "frac": achieved / (peak * ws), "traffic": None,
+                         "kernel": "gn::k_part_step (one launch per iteration and part) + NCCL halo",
+                         "b_iter": b_iter, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs) x n_gpus"},
+            "cpu_baseline": None,
+            "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    be.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -199,6 +304,8 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="C5: vertex-range partitioned engine (the default for C5 under torchrun, N>1)")
     ap.add_argument("--starts", type=int, default=1,
                     help="starts per instance (SURVEY 8f f1): >1 runs them together through gn_multi_run")
     args = ap.parse_args()
@@ -233,6 +340,8 @@ def main():
         inst = make_instance(args.config, rank, args.scale)
         batch = None
     g = inst.graph
+    if args.config == "C5" and (ws > 1 or args.partition):
+        return run_partitioned(args, ws, rank, local, inst, torch, P, E)
     # C2's graph stays in L2, so binary64 gathers cost no bandwidth and avoid
     # the fp32->fp64 conversions of the mixed dtype: run it in the reference's
     # own arithmetic

@@ -10,7 +10,8 @@
 // run bit for bit.
 //
 // Per iteration k, on the caller's stream: gn_part_step (sums + updates of the
-// owned rows, one thread per row, sequential sums; per-block fixed-order stats
+// owned rows -- one thread per row in degree order, sequential sums; in fast
+// mode the longest rows split over a warp -- with per-block fixed-order stats
 // partials), then gn_part_pack (owned values -> contiguous send buffers), the
 // exchange (NCCL grouped send/recv, issued by the caller on the same stream),
 // gn_part_unpack (receive buffers -> ghost slots).  gn_part_end folds the
@@ -30,6 +31,9 @@ struct gn_part {
     int device = 0;
     int32_t* rowptr = nullptr;  // n_own+1
     int32_t* col = nullptr;     // local ids
+    int32_t* order = nullptr;   // owned rows, degree-descending (stable)
+    int64_t n_long = 0;         // order[0, n_long): rows split over a warp (fast mode)
+    int64_t n_long_fast = 0;    // rows above kPartLongDegree
     double* w64 = nullptr;      // n_own + n_ghost
     // run state
     int iters = 0;
@@ -39,7 +43,8 @@ struct gn_part {
     void* v = nullptr;                 // state precision, n_own + n_ghost
     double* gam = nullptr;
     double* part = nullptr;  // [iters][nblocks][4]: max|dx|, fallbacks, w.x', non-finite
-    int nblocks = 0;
+    int nblocks = 0;       // blocks per step (stats partials per iteration)
+    int nblocks_long = 0;  // of which the first handle the split rows
     cudaStream_t own_stream = nullptr;
 };
 
@@ -60,8 +65,42 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
     if (i < n_own) x[i] = xi;
 }
 
+constexpr int kPartLongDegree = 512;
+#ifndef GN_PART_UNROLL
+#define GN_PART_UNROLL 8
+#endif
+constexpr int kPartUnroll = GN_PART_UNROLL;  // gathers in flight per thread  // fast mode: longer rows are split over a warp
+
+// dynamics.py:104-107 for owned row i with neighbour sum s; stats of the thread
 template <typename TS, typename TG>
-__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, const int32_t* __restrict__ rowptr,
+__device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double* __restrict__ w64,
+                                            const TS* __restrict__ v, const TS* __restrict__ x, TS* __restrict__ xo,
+                                            TG* __restrict__ ygo, double& mx, double& fb, double& ob, double& nf) {
+    using A = Arith<TS>;
+    const TS xi = x[i], vi = v[i];
+    const TS yi = A::mul(vi, xi);
+    const TS d = A::add(yi, A::mul(g, s));          // dynamics.py:105
+    const bool ok = (double)d > kSafeDiv;            // dynamics.py:106
+    const TS o = ok ? A::div(yi, d) : TS(kFallback); // dynamics.py:107
+    xo[i] = o;
+    ygo[i] = (TG)A::mul(vi, o);
+    const TS dx = A::sub(o, xi);
+    const double diff = (double)(dx < TS(0) ? -dx : dx);
+    if (!(diff <= mx)) mx = diff;
+    fb += ok ? 0.0 : 1.0;
+    if (!isfinite((double)o)) nf = 1.0;
+    ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
+}
+
+// One step of the owned rows.  Blocks [0, nbl) split the n_long longest rows
+// over warps (lanes stride the positions, fixed butterfly fold: fast mode
+// only); the other blocks give one thread to each remaining row, rows taken
+// in degree-descending order so a warp's rows have similar lengths, summed
+// sequentially in the reference's order (bitwise) with 8 gathers in flight.
+template <typename TS, typename TG>
+__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, int64_t n_long, int nbl,
+                                                            const int32_t* __restrict__ order,
+                                                            const int32_t* __restrict__ rowptr,
                                                             const int32_t* __restrict__ col,
                                                             const double* __restrict__ w64, const TS* __restrict__ v,
                                                             const TS* __restrict__ x, TS* __restrict__ xo,
@@ -70,24 +109,45 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, const
                                                             double* __restrict__ part) {
     using A = Arith<TS>;
     const TS g = (TS)gam[k];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_own;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        TS s = TS(0);
-        for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = A::add(s, (TS)yg[col[p]]);  // scipy order
-        const TS xi = x[i], vi = v[i];
-        const TS yi = A::mul(vi, xi);
-        const TS d = A::add(yi, A::mul(g, s));          // dynamics.py:105
-        const bool ok = (double)d > kSafeDiv;            // dynamics.py:106
-        const TS o = ok ? A::div(yi, d) : TS(kFallback); // dynamics.py:107
-        xo[i] = o;
-        ygo[i] = (TG)A::mul(vi, o);
-        const TS dx = A::sub(o, xi);
-        const double diff = (double)(dx < TS(0) ? -dx : dx);
-        if (!(diff <= mx)) mx = diff;
-        fb += ok ? 0.0 : 1.0;
-        if (!isfinite((double)o)) nf = 1.0;
-        ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
+    if ((int)blockIdx.x < nbl) {
+        for (int64_t q = (int64_t)blockIdx.x * kWarpsPerBlock + warp; q < n_long; q += (int64_t)nbl * kWarpsPerBlock) {
+            const int64_t i = order[q];
+            const int32_t rb = rowptr[i], re = rowptr[i + 1];
+            TS s = TS(0);
+            int32_t p = rb + lane;
+            for (; p + 3 * 32 < re; p += 4 * 32) {
+                const TG y0 = yg[col[p]], y1 = yg[col[p + 32]], y2 = yg[col[p + 64]], y3 = yg[col[p + 96]];
+                s = A::add(s, (TS)y0);
+                s = A::add(s, (TS)y1);
+                s = A::add(s, (TS)y2);
+                s = A::add(s, (TS)y3);
+            }
+            for (; p < re; p += 32) s = A::add(s, (TS)yg[col[p]]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
+            if (lane == 0) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+        }
+    } else {
+        const int64_t nrest = n_own - n_long;
+        for (int64_t q = (int64_t)(blockIdx.x - nbl) * blockDim.x + threadIdx.x; q < nrest;
+             q += (int64_t)(gridDim.x - nbl) * blockDim.x) {
+            const int64_t i = order[n_long + q];
+            const int32_t rb = rowptr[i], re = rowptr[i + 1];
+            TS s = TS(0);
+            int32_t p = rb;
+            for (; p + kPartUnroll <= re; p += kPartUnroll) {  // scipy order, loads before the adds
+                TG y[kPartUnroll];
+#pragma unroll
+                for (int u = 0; u < kPartUnroll; ++u) y[u] = __ldg(yg + __ldg(col + p + u));
+#pragma unroll
+                for (int u = 0; u < kPartUnroll; ++u) s = A::add(s, (TS)y[u]);
+            }
+            for (; p < re; ++p) s = A::add(s, (TS)yg[col[p]]);
+            part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+        }
     }
     __shared__ double red[kPartThreads / 32][4];
 #pragma unroll
@@ -219,6 +279,19 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
         return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
     }
     cudaMemcpy(P->rowptr, rp.data(), 4 * rp.size(), cudaMemcpyHostToDevice);
+    // owned rows by degree, descending (stable): balanced warps, long rows first
+    std::vector<int32_t> order((size_t)n_own);
+    for (int64_t i = 0; i < n_own; ++i) order[(size_t)i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return rp[(size_t)a + 1] - rp[(size_t)a] > rp[(size_t)b + 1] - rp[(size_t)b]; });
+    while (P->n_long_fast < n_own &&
+           rp[(size_t)order[(size_t)P->n_long_fast] + 1] - rp[(size_t)order[(size_t)P->n_long_fast]] > kPartLongDegree)
+        ++P->n_long_fast;
+    if ((ce = cudaMalloc(&P->order, 4 * (size_t)std::max<int64_t>(n_own, 1))) != cudaSuccess) {
+        delete P;
+        return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
+    }
+    if (n_own) cudaMemcpy(P->order, order.data(), 4 * (size_t)n_own, cudaMemcpyHostToDevice);
     if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
     if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
     GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
@@ -234,6 +307,7 @@ int gn_part_destroy(gn_part* p) {
     part_free_run(p);
     cudaFree(p->rowptr);
     cudaFree(p->col);
+    cudaFree(p->order);
     cudaFree(p->w64);
     if (p->own_stream) cudaStreamDestroy(p->own_stream);
     if (prev >= 0) cudaSetDevice(prev);
@@ -250,7 +324,11 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     const size_t nb = (size_t)std::max<int64_t>(nall, 1);
     p->iters = iters;
     p->flags = flags;
-    p->nblocks = pblocks(p->n_own);
+    // GN_EXACT: every row summed sequentially (bitwise the reference); else the
+    // longest rows are split over warps
+    p->n_long = (flags & GN_EXACT) ? 0 : p->n_long_fast;
+    p->nblocks_long = p->n_long ? (int)std::min<int64_t>((p->n_long + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
+    p->nblocks = p->nblocks_long + pblocks(p->n_own - p->n_long);
     GN_CUDA(cudaMalloc(&p->x[0], es * nb));
     GN_CUDA(cudaMalloc(&p->x[1], es * nb));
     GN_CUDA(cudaMalloc(&p->yg[0], gs * nb));
@@ -294,17 +372,17 @@ int gn_part_step(gn_part* p, int k, uintptr_t stream) {
     switch (p->dtype) {
         case GN_F64:
             k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
+                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
                 (double*)p->x[cur ^ 1], (const double*)p->yg[cur], (double*)p->yg[cur ^ 1], p->gam, k, p->part);
             break;
         case GN_F32:
             k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
+                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
                 (double*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
             break;
         default:
             k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->rowptr, p->col, p->w64, (const float*)p->v, (const float*)p->x[cur],
+                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const float*)p->v, (const float*)p->x[cur],
                 (float*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
     }
     GN_LAUNCHED();

@@ -11,8 +11,8 @@ groups them by owning peer, since ranges are contiguous.  Every iteration:
     halo     each part packs the published values its peers hold as ghosts
              and sends them; received buffers are unpacked into ghost slots
 
-Neighbour lists keep the global (reference) order, so a partitioned run is
-bitwise the single-GPU run.  Exchanges: LocalExchange (all parts in one
+Neighbour lists keep the global (reference) order, so a partitioned EXACT run
+is bitwise the single-GPU EXACT run (and the reference).  Exchanges: LocalExchange (all parts in one
 process, e.g. one GPU, for tests) and DistExchange (one part per rank,
 torch.distributed send/recv: NCCL over NVLink on GPUs, gloo on CPU tests).
 The compute backend is pluggable; EngineBackend is the CUDA engine.
@@ -102,8 +102,10 @@ def build_partitions(g, parts: int, bounds: Optional[np.ndarray] = None) -> list
 class EngineBackend:
     """One partition on the CUDA engine (gn_part_*)."""
 
-    def __init__(self, spec: PartSpec, dtype="fp64", device: int = 0):
+    def __init__(self, spec: PartSpec, dtype="fp64", device: int = 0, exact: Optional[bool] = None):
         import torch
+
+        from .dynamics import _opt
 
         from . import _engine as E
         from .graph import dtype_code
@@ -115,6 +117,9 @@ class EngineBackend:
                                        E.ptr(np.ascontiguousarray(spec.indices)), E.ptr(np.ascontiguousarray(spec.w)),
                                        dtype_code(dtype), device, ctypes.byref(h)))
         self.h = h
+        # exact: every row summed sequentially (bitwise the single-GPU EXACT run);
+        # otherwise rows longer than 512 are split over a warp
+        self.flags = E.GN_EXACT if _opt("exact", exact) else 0
         self.elem = E.lib().gn_part_elem_bytes(h)
         self.tdtype = torch.float64 if self.elem == 8 else torch.float32
         self.send_idx = {q: torch.from_numpy(v).to(self.device) for q, v in spec.send_idx.items()}
@@ -126,7 +131,7 @@ class EngineBackend:
         E = self.E
         self.gam = np.ascontiguousarray(gammas, dtype=np.float64)
         E.check(E.lib().gn_part_begin(self.h, E.ptr(np.ascontiguousarray(x0_local, dtype=np.float64)),
-                                      E.ptr(self.gam), len(self.gam), 0))
+                                      E.ptr(self.gam), len(self.gam), self.flags))
 
     def step(self, k: int) -> None:
         self.E.check(self.E.lib().gn_part_step(self.h, k, self._stream()))

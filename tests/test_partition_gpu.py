@@ -16,9 +16,24 @@ pytestmark = pytest.mark.gpu
 def test_partitioned_engine_bitwise(dtype, parts):
     inst = G.c5_rmat(13)
     s = P.GammaSchedule.pursuit(iterations=300)
-    out = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype=dtype))
+    out = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype=dtype, exact=True))
     ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, dtype=dtype)
     np.testing.assert_array_equal(out["x"], ref.x)
     np.testing.assert_array_equal(out["step_inf"], ref.step_inf)
     np.testing.assert_array_equal(out["fallbacks"], ref.fallbacks)
     np.testing.assert_allclose(out["mass"], ref.mass, rtol=1e-12)
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_partitioned_fast_mode_within_tolerance(parts):
+    # R-MAT hubs (degree > 512) are split over warps: fixed fold order
+    inst = G.c5_rmat(14)
+    assert np.diff(inst.graph.indptr).max() > 512
+    s = P.GammaSchedule.pursuit(iterations=300)
+    out = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"))
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma)
+    assert np.max(np.abs(out["x"] - ref.x)) <= 1e-9
+    np.testing.assert_array_equal(out["fallbacks"], ref.fallbacks)
+    np.testing.assert_allclose(out["step_inf"], ref.step_inf, rtol=1e-6, atol=1e-12)
+    again = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"))
+    np.testing.assert_array_equal(again["x"], out["x"])
