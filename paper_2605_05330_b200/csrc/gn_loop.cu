@@ -75,6 +75,7 @@ struct LoopArgs {
     int hub_slot_off;                        // byte offsets in dynamic shared memory
     int hot_off;
     int resident_off;
+    int item_cache_off;                      // > 0: the CTA's items and lane degrees copied to shared memory here
     int hot;                                 // new ids [0, hot) mirrored in shared memory
     const double* __restrict__ gammas;
     int iters;
@@ -213,9 +214,19 @@ struct SlicePre {
     uint4 v[NB];
 };
 
+// Where a CTA reads its item descriptors and slice-row degrees: a shared
+// memory copy made once per run (when they fit) -- every iteration then
+// starts its items without a global round trip -- or global memory.
+struct ItemSrc {
+    const Item* it;       // items, indexed from `base`
+    const int32_t* deg;   // [item - base][32] lane degrees of slice items, or nullptr (global row_deg)
+    int base;
+    __device__ __forceinline__ Item at(int i) const { return it[i - base]; }
+};
+
 template <typename TS, typename TG, typename TI>
-__device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const Item& it, const uint4* s_res,
-                                               int lane, int cur, SlicePre<TS, TI, TG>& p) {
+__device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const Item& it, const ItemSrc& src, int i,
+                                               const uint4* s_res, int lane, int cur, SlicePre<TS, TI, TG>& p) {
     using SP = SlicePre<TS, TI, TG>;
     p.whole = it.kind == kWhole;
     p.beg = it.beg;
@@ -226,7 +237,8 @@ __device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const 
     // Item.pad0/pad1: 16-byte-word offset of block `beg` in the global index array
     const int64_t goff = ((int64_t)(uint32_t)it.pad1 << 32) | (uint32_t)it.pad0;
     p.base = (it.smem >= 0 ? s_res + it.smem : reinterpret_cast<const uint4*>(a.sell) + goff) + lane;
-    p.d = p.valid ? __ldg(a.row_deg + (size_t)it.id * kSlice + lane) : 0;
+    p.d = src.deg ? src.deg[(i - src.base) * kSlice + lane]
+                  : (p.valid ? __ldg(a.row_deg + (size_t)it.id * kSlice + lane) : 0);
     if (p.whole && p.valid) p.in = row_in(a, p.row, cur);
 #pragma unroll
     for (int u = 0; u < SP::NB; ++u)
@@ -298,7 +310,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // One pass over this CTA's items, phase by phase (gn_plan.h).
 template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
 __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_slot, TS* s_hslot,
-                     const uint4* s_res, TG* s_hot) {
+                     const uint4* s_res, TG* s_hot, const ItemSrc& src) {
     using A = Arith<TS>;
     const int cur = k & 1;
     if (HOT) {
@@ -322,13 +334,13 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
         // a time: both items' loads are issued before either is consumed
         int i = i0;
         while (i < i1) {
-            const Item it0 = a.items[i];
+            const Item it0 = src.at(i);
             if (it0.kind > kPiece) break;
-            const bool two = i + 1 < i1 && a.items[i + 1].kind <= kPiece;
-            const Item it1 = two ? a.items[i + 1] : it0;
+            const bool two = i + 1 < i1 && src.at(i + 1).kind <= kPiece;
+            const Item it1 = two ? src.at(i + 1) : it0;
             SlicePre<TS, TI, TG> p0, p1;
-            slice_prefetch<TS, TG, TI>(a, it0, s_res, lane, cur, p0);
-            if (two) slice_prefetch<TS, TG, TI>(a, it1, s_res, lane, cur, p1);
+            slice_prefetch<TS, TG, TI>(a, it0, src, i, s_res, lane, cur, p0);
+            if (two) slice_prefetch<TS, TG, TI>(a, it1, src, i + 1, s_res, lane, cur, p1);
             const TS s0 = slice_consume<TS, TG, TI, HOT>(p0, yg);
             if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
             else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
@@ -340,7 +352,7 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
             i += two ? 2 : 1;
         }
         for (; i < i1; ++i) {
-            const Item it = a.items[i];
+            const Item it = src.at(i);
             if (it.kind == kWhole || it.kind == kPiece) {
                 // not reached: slice items precede hub items in every warp list
             } else if (it.kind == kHubPiece) {
@@ -522,6 +534,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
     TS* s_hslot = (TS*)(smem_raw + a.hub_slot_off);
     TG* s_hot = (TG*)(smem_raw + a.hot_off);
     uint4* s_res = (uint4*)(smem_raw + a.resident_off);
+    ItemSrc src{a.items, nullptr, 0};
+    if (a.item_cache_off > 0) {
+        const int ph0 = a.phase_base[blockIdx.x], ph1 = a.phase_base[blockIdx.x + 1];
+        const int i0 = a.phase_warp[ph0 * (kWarps + 1)], i1 = a.phase_warp[(ph1 - 1) * (kWarps + 1) + kWarps];
+        Item* s_items = (Item*)(smem_raw + a.item_cache_off);
+        int32_t* s_deg = (int32_t*)(s_items + (i1 - i0));
+        for (int t = threadIdx.x; t < (i1 - i0) * 8; t += blockDim.x)
+            reinterpret_cast<int32_t*>(s_items)[t] = __ldg(reinterpret_cast<const int32_t*>(a.items + i0) + t);
+        for (int t = threadIdx.x; t < (i1 - i0) * kSlice; t += blockDim.x) {
+            const Item it = a.items[i0 + t / kSlice];
+            const int64_t r = (int64_t)a.nhub + (int64_t)it.id * kSlice + (t % kSlice);
+            s_deg[t] = (it.kind <= kPiece && r < a.n) ? __ldg(a.row_deg + (size_t)it.id * kSlice + (t % kSlice)) : 0;
+        }
+        src = ItemSrc{s_items, s_deg, i0};
+    }
     // resident index blocks: copied once, used every iteration
     if (__ldg(a.smem_words + blockIdx.x) > 0) {
         const int ph0 = a.phase_base[blockIdx.x], ph1 = a.phase_base[blockIdx.x + 1];
@@ -545,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
         const bool pr = a.prof && k == a.prof_iter && threadIdx.x == 0;
         long long* pp = a.prof ? a.prof + blockIdx.x * (kWarps + 4) : nullptr;
         if (pr) pp[0] = gtimer();
-        pass<TS, TG, TI, TRACE, HOT>(a, k, false, st, s_slot, s_hslot, s_res, s_hot);
+        pass<TS, TG, TI, TRACE, HOT>(a, k, false, st, s_slot, s_hslot, s_res, s_hot, src);
         if (pr) pp[1] = gtimer();
         double* slot = a.ring + (size_t)(k - k0) * ring_stride;
         publish<TRACE>(st, slot);
@@ -567,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
     if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE, HOT>(a, ran, true, st, s_slot, s_hslot, s_res, s_hot);
+        pass<TS, TG, TI, TRACE, HOT>(a, ran, true, st, s_slot, s_hslot, s_res, s_hot, src);
         publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
         fold_ring(a.ring, ran - k0 + 1, k0, fo);
@@ -625,6 +652,7 @@ struct DevicePlan {
     Combine* combs = nullptr;
     int32_t* smem_words = nullptr;
     int max_slots = 0, max_hub_slots = 0, max_words = 0;
+    int max_cta_items = 0;  // most items any CTA holds
     int64_t resident_words = 0;
 };
 
@@ -688,6 +716,12 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const D
     p.max_slots = hpn.max_slots;
     p.max_hub_slots = hpn.max_hub_slots;
     for (int32_t w : hpn.smem_words) p.max_words = std::max(p.max_words, w);
+    for (int b = 0; b < G; ++b) {
+        const int ph0 = hpn.phase_base[(size_t)b], ph1 = hpn.phase_base[(size_t)b + 1];
+        if (ph1 > ph0)
+            p.max_cta_items = std::max(p.max_cta_items, hpn.phase_warp[(size_t)(ph1 - 1) * (kWarps + 1) + kWarps] -
+                                                            hpn.phase_warp[(size_t)ph0 * (kWarps + 1)]);
+    }
     p.resident_words = hpn.resident_words;
     auto res = pc->plans.emplace(key, p);
     *out = &res.first->second;
@@ -766,7 +800,19 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     const int hub_slot_off = (int)((size_t)kMaxSlots * kSlice * sizeof(TS));
     const int hot_off = (int)(((size_t)hub_slot_off + (size_t)kMaxHubSlots * sizeof(TS) + 15) / 16 * 16);
     const int resident_off = (int)((slot_bytes + 15) / 16 * 16);
-    const size_t dyn_smem = (size_t)resident_off + (size_t)plan->max_words * 16;
+    size_t dyn_smem = (size_t)resident_off + (size_t)plan->max_words * 16;
+    // the CTA's item descriptors and slice-row degrees, when they fit
+    int item_cache_off = 0;
+    {
+        const size_t off = (dyn_smem + 15) / 16 * 16;
+        const size_t bytes = (size_t)plan->max_cta_items * (sizeof(Item) + kSlice * sizeof(int32_t));
+        if (!getenv("GN_NO_ITEM_CACHE") && plan->max_cta_items > 0 && off + bytes + static_bytes <= per_cta) {
+            item_cache_off = (int)off;
+            dyn_smem = off + bytes;
+            GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max(dyn_smem, smem_cap)));
+        }
+    }
 
     Workspace ws;
     ws.s = s;
@@ -845,6 +891,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.hot_off = hot_off;
     a.hot = hot ? g->hot : 0;
     a.resident_off = resident_off;
+    a.item_cache_off = item_cache_off;
     a.gammas = gam;
     a.iters = iters;
     a.final_gamma = final_gamma;
