@@ -148,6 +148,27 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
     }
 }
 
+// The same barrier in two halves, so a CTA can do barrier-independent work
+// (loads of static data and of its own rows) while the others arrive.
+__device__ __forceinline__ void grid_arrive(unsigned int* counter) {
+    __syncthreads();
+    if (gridDim.x > 1 && threadIdx.x == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+}
+
+__device__ __forceinline__ void grid_wait(unsigned int* counter, unsigned int target) {
+    if (gridDim.x > 1) {
+        if (threadIdx.x == 0) {
+            unsigned int seen;
+            do {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+            } while (seen < target);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+    }
+}
+
 int coresident_blocks(const void* kernel, int threads, size_t smem, int device, int* out);
 void release_plans(const gn_graph* g);  // gn_loop.cu: cached launch plans of g
 void release_multi_plans(const gn_graph* g);  // gn_multi.cu: cached multi-start plans of g

@@ -245,6 +245,38 @@ __device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const 
         if (u < p.nb) p.v[u] = p.base[(size_t)u * kSlice];
 }
 
+// The storage of a warp's item pair.  The first pair of an iteration is
+// prefetched while the grid barrier before it is still pending: it reads
+// only static data (indices, degrees, v, w) and rows this CTA itself wrote.
+template <typename TS, typename TI, typename TG>
+struct ItemPair {
+    SlicePre<TS, TI, TG> p0, p1;
+    int n;  // > 0: the first pair of phase ph0 is already prefetched (n items)
+};
+
+template <typename TS, typename TG, typename TI>
+__device__ __forceinline__ void prefetch_first(const LoopArgs<TS, TG>& a, int k, const ItemSrc& src,
+                                               const uint4* s_res, ItemPair<TS, TI, TG>& pr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pr.n = 0;
+    const int ph0 = __ldg(a.phase_base + blockIdx.x);
+    if (ph0 >= __ldg(a.phase_base + blockIdx.x + 1)) return;
+    const int i0 = __ldg(a.phase_warp + ph0 * (kWarps + 1) + warp);
+    const int i1 = __ldg(a.phase_warp + ph0 * (kWarps + 1) + warp + 1);
+    if (i0 >= i1) return;
+    const Item it0 = src.at(i0);
+    if (it0.kind > kPiece) return;
+    slice_prefetch<TS, TG, TI>(a, it0, src, i0, s_res, lane, k & 1, pr.p0);
+    pr.n = 1;
+    if (i0 + 1 < i1) {
+        const Item it1 = src.at(i0 + 1);
+        if (it1.kind <= kPiece) {
+            slice_prefetch<TS, TG, TI>(a, it1, src, i0 + 1, s_res, lane, k & 1, pr.p1);
+            pr.n = 2;
+        }
+    }
+}
+
 // Sequential sum of one lane's row over the item's blocks; p.v holds the
 // first batch of index vectors.
 template <typename TS, typename TG, typename TI, bool HOT>
@@ -310,7 +342,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // One pass over this CTA's items, phase by phase (gn_plan.h).
 template <typename TS, typename TG, typename TI, bool TRACE, bool HOT>
 __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS* s_slot, TS* s_hslot,
-                     const uint4* s_res, TG* s_hot, const ItemSrc& src) {
+                     const uint4* s_res, TG* s_hot, const ItemSrc& src, ItemPair<TS, TI, TG>& pr) {
     using A = Arith<TS>;
     const int cur = k & 1;
     if (HOT) {
@@ -333,14 +365,19 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
         // slice items first (the plan sorts each warp's list by kind), two at
         // a time: both items' loads are issued before either is consumed
         int i = i0;
+        bool ready = ph == ph0 && pr.n > 0;  // the first pair came prefetched
+        SlicePre<TS, TI, TG>& p0 = pr.p0;
+        SlicePre<TS, TI, TG>& p1 = pr.p1;
         while (i < i1) {
             const Item it0 = src.at(i);
             if (it0.kind > kPiece) break;
             const bool two = i + 1 < i1 && src.at(i + 1).kind <= kPiece;
             const Item it1 = two ? src.at(i + 1) : it0;
-            SlicePre<TS, TI, TG> p0, p1;
-            slice_prefetch<TS, TG, TI>(a, it0, src, i, s_res, lane, cur, p0);
-            if (two) slice_prefetch<TS, TG, TI>(a, it1, src, i + 1, s_res, lane, cur, p1);
+            if (!ready) {
+                slice_prefetch<TS, TG, TI>(a, it0, src, i, s_res, lane, cur, p0);
+                if (two) slice_prefetch<TS, TG, TI>(a, it1, src, i + 1, s_res, lane, cur, p1);
+            }
+            ready = false;
             const TS s0 = slice_consume<TS, TG, TI, HOT>(p0, yg);
             if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
             else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
@@ -567,17 +604,27 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
     unsigned int bar = 0;
     int ran = 0, k0 = 0;
     const size_t ring_stride = (size_t)gridDim.x * kRingW;
+    // early first pairs pay on the uint16-index graphs (C2: -2%); with int32
+    // indices the pair held across the barrier costs spills (C3: +4%)
+    constexpr bool kEarly = sizeof(TI) == 2;
+    ItemPair<TS, TI, TG> ipair;
+    ipair.n = 0;
+    if (kEarly) prefetch_first<TS, TG, TI>(a, 0, src, s_res, ipair);
     for (int k = 0; k < a.iters; ++k) {
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
         const bool pr = a.prof && k == a.prof_iter && threadIdx.x == 0;
         long long* pp = a.prof ? a.prof + blockIdx.x * (kWarps + 4) : nullptr;
         if (pr) pp[0] = gtimer();
-        pass<TS, TG, TI, TRACE, HOT>(a, k, false, st, s_slot, s_hslot, s_res, s_hot, src);
+        pass<TS, TG, TI, TRACE, HOT>(a, k, false, st, s_slot, s_hslot, s_res, s_hot, src, ipair);
         if (pr) pp[1] = gtimer();
         double* slot = a.ring + (size_t)(k - k0) * ring_stride;
         publish<TRACE>(st, slot);
         if (pr) pp[2] = gtimer();
-        grid_barrier(a.barrier, (++bar) * gridDim.x);
+        ++bar;
+        grid_arrive(a.barrier);
+        // the next iteration's first items load while the other CTAs arrive
+        if (kEarly && k + 1 < a.iters) prefetch_first<TS, TG, TI>(a, k + 1, src, s_res, ipair);
+        grid_wait(a.barrier, bar * gridDim.x);
         if (pr) pp[3] = gtimer();
         ran = k + 1;
         bool stop = false;
@@ -594,7 +641,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
     if (TRACE) {
         // energy terms of the final state (the reference's energy(g, x_new, gamma))
         Stats st{0.0, 0u, 0, {0.0, 0.0, 0.0, 0.0}};
-        pass<TS, TG, TI, TRACE, HOT>(a, ran, true, st, s_slot, s_hslot, s_res, s_hot, src);
+        ipair.n = 0;
+        if (kEarly) prefetch_first<TS, TG, TI>(a, ran, src, s_res, ipair);
+        pass<TS, TG, TI, TRACE, HOT>(a, ran, true, st, s_slot, s_hslot, s_res, s_hot, src, ipair);
         publish<TRACE>(st, a.ring + (size_t)(ran - k0) * ring_stride);
         grid_barrier(a.barrier, (++bar) * gridDim.x);
         fold_ring(a.ring, ran - k0 + 1, k0, fo);
