@@ -6,6 +6,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <mutex>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -44,6 +45,18 @@ int CallCtx::open(int device) {
     GN_CUDA(cudaGetDevice(&prev_dev));
     if (prev_dev != device) GN_CUDA(cudaSetDevice(device));
     GN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // per-call workspaces come from the device's default pool: keep what it
+    // has mapped instead of returning it to the driver at every sync
+    static std::once_flag pool_once[64];
+    if (device >= 0 && device < 64)
+        std::call_once(pool_once[device], [device]() {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+        });
     return GN_OK;
 }
 
