@@ -223,6 +223,7 @@ struct Layout {
     std::vector<int32_t> sell32;
     std::vector<uint16_t> sell16;
     int idx16 = 0;
+    int sentinel = 0;  // 1: padding positions hold id n (a vertex whose published value is always 0)
     int32_t maxdeg = 0;
     std::vector<uint64_t> sig;  // per slice: MinHash of the 128-byte lines it gathers
 };
@@ -328,8 +329,13 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
         L.sig[(size_t)s] = m;
     }
     const int64_t elems = L.slice_ptr[L.nslices];
-    if (L.idx16) L.sell16.assign((size_t)elems, 0);
-    else L.sell32.assign((size_t)elems, 0);
+    // int32 ids: padding is id n, the zero-valued dummy vertex, so a lane runs
+    // its slice's full length without degree masks (adding +0.0 leaves a sum's
+    // bits unchanged).  uint16 layouts keep the degree masks (the id n may not
+    // fit, and on their dense rows the masks are rare)
+    L.sentinel = L.idx16 ? 0 : 1;
+    if (L.idx16) L.sell16.assign((size_t)elems, L.sentinel ? (uint16_t)n : (uint16_t)0);
+    else L.sell32.assign((size_t)elems, L.sentinel ? (int32_t)n : 0);
     for (int32_t s = 0; s < L.nslices; ++s) {
         for (int l = 0; l < kSlice; ++l) {
             int64_t r = (int64_t)s * kSlice + l;

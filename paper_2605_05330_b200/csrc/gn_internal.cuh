@@ -90,7 +90,7 @@ struct gn_graph {
     int64_t* slice_ptr = nullptr;  // nslices+1 element offsets (multiples of 32*B)
     int32_t* row_deg = nullptr;    // degree per slice row (n - nhub)
     void* sell = nullptr;          // int32 or uint16 new ids, position-major
-    int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536)
+    int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536); else int32 ids, padding = id n
     int64_t sell_elems = 0;
     std::vector<uint64_t> slice_sig;  // host: per-slice MinHash (gn_graph.cu, used by the plan)
     gn_batch* resident = nullptr;     // small graphs: the whole-graph-in-shared-memory kernel

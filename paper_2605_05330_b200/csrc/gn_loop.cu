@@ -210,6 +210,8 @@ struct SlicePre {
     const uint4* base;  // block `beg` of the item, this lane
     int beg, nb, d, row;
     bool whole, valid;
+    // int32-id layouts pad with the zero-valued vertex n (gn_graph.cu): no degree masks
+    static constexpr bool kSent = sizeof(TI) == 4;
     RowIn<TS> in;
     uint4 v[NB];
 };
@@ -237,8 +239,9 @@ __device__ __forceinline__ void slice_prefetch(const LoopArgs<TS, TG>& a, const 
     // Item.pad0/pad1: 16-byte-word offset of block `beg` in the global index array
     const int64_t goff = ((int64_t)(uint32_t)it.pad1 << 32) | (uint32_t)it.pad0;
     p.base = (it.smem >= 0 ? s_res + it.smem : reinterpret_cast<const uint4*>(a.sell) + goff) + lane;
-    p.d = src.deg ? src.deg[(i - src.base) * kSlice + lane]
-                  : (p.valid ? __ldg(a.row_deg + (size_t)it.id * kSlice + lane) : 0);
+    p.d = SlicePre<TS, TI, TG>::kSent ? 0
+                 : (src.deg ? src.deg[(i - src.base) * kSlice + lane]
+                            : (p.valid ? __ldg(a.row_deg + (size_t)it.id * kSlice + lane) : 0));
     if (p.whole && p.valid) p.in = row_in(a, p.row, cur);
 #pragma unroll
     for (int u = 0; u < SP::NB; ++u)
@@ -287,8 +290,9 @@ __device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<
     constexpr int B = SP::B, NB = SP::NB;
     TS s = TS(0);
     const int d = p.d;
-    // local blocks that hold any of this row's neighbours
-    const int be = min(p.nb, max(0, (d - p.beg * B + B - 1) / B));
+    // local blocks that hold any of this row's neighbours (all of the item's
+    // blocks when padding names the zero vertex: the warp stays converged)
+    const int be = SP::kSent ? p.nb : min(p.nb, max(0, (d - p.beg * B + B - 1) / B));
     for (int b = 0; b < be; b += NB) {
         uint4 vn[NB];
 #pragma unroll
@@ -300,7 +304,7 @@ __device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<
 #endif
         TG y[NB * B];
         const int pos0 = (p.beg + b) * B;
-        if (b + NB <= be && pos0 + NB * B <= d) {
+        if (b + NB <= be && (SP::kSent || pos0 + NB * B <= d)) {
 #pragma unroll
             for (int u = 0; u < NB; ++u)
 #pragma unroll
@@ -316,7 +320,7 @@ __device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<
             for (int u = 0; u < NB; ++u)
 #pragma unroll
                 for (int t = 0; t < B; ++t)
-                    y[u * B + t] = (b + u < be && pos0 + u * B + t < d) ? yg[V::get(p.v[u], t)] : TG(0);
+                    y[u * B + t] = (b + u < be && (SP::kSent || pos0 + u * B + t < d)) ? yg[V::get(p.v[u], t)] : TG(0);
         }
 #pragma unroll
         for (int q = 0; q < NB * B; ++q) s = A::add(s, (TS)y[q]);
@@ -758,6 +762,27 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const D
                  getenv("GN_PLAN_COLOCATE") != nullptr};
     HostPlan hpn;
     build_plan(in, G, exact, resident_cap, hpn);
+    if (getenv("GN_PLAN_DUMP")) {  // diagnosis: items per warp by kind, phases, residency
+        std::vector<int> per_kind(4, 0);
+        int max_items = 0, max_phases = 0;
+        double sum_items = 0;
+        for (int b = 0; b < G; ++b) {
+            const int ph0 = hpn.phase_base[(size_t)b], ph1 = hpn.phase_base[(size_t)b + 1];
+            max_phases = std::max(max_phases, ph1 - ph0);
+            for (int ph = ph0; ph < ph1; ++ph)
+                for (int w = 0; w < kWarps; ++w) {
+                    const int i0 = hpn.phase_warp[(size_t)ph * (kWarps + 1) + w];
+                    const int i1 = hpn.phase_warp[(size_t)ph * (kWarps + 1) + w + 1];
+                    max_items = std::max(max_items, i1 - i0);
+                    sum_items += i1 - i0;
+                    for (int i = i0; i < i1; ++i) per_kind[(size_t)hpn.items[(size_t)i].kind]++;
+                }
+        }
+        fprintf(stderr, "[plan] G=%d nhub=%d nslices=%d nsplit=%d items: whole=%d piece=%d hubpiece=%d hubseq=%d "
+                        "per-warp mean=%.2f max=%d phases/CTA max=%d combines=%zu resident=%.1f MB\n",
+                G, g->nhub, g->nslices, g->nsplit, per_kind[0], per_kind[1], per_kind[2], per_kind[3],
+                sum_items / (G * kWarps), max_items, max_phases, hpn.combs.size(), hpn.resident_words * 16 / 1e6);
+    }
     DevicePlan p;
     int rc;
     if ((rc = upload(hpn.phase_base, &p.phase_base)) || (rc = upload(hpn.phase_warp, &p.phase_warp)) ||
@@ -873,8 +898,11 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     unsigned int* barrier;
     GN_CUDA(ws.alloc(&xa, sizeof(TS) * nb));
     GN_CUDA(ws.alloc(&xb, sizeof(TS) * nb));
-    GN_CUDA(ws.alloc(&ya, sizeof(TG) * nb));
-    GN_CUDA(ws.alloc(&yb, sizeof(TG) * nb));
+    // published values, each buffer with the zero vertex n at its end (SELL padding ids point there)
+    GN_CUDA(ws.alloc(&ya, sizeof(TG) * (nb + 1)));
+    GN_CUDA(ws.alloc(&yb, sizeof(TG) * (nb + 1)));
+    GN_CUDA(cudaMemsetAsync(ya + n, 0, sizeof(TG), s));
+    GN_CUDA(cudaMemsetAsync(yb + n, 0, sizeof(TG), s));
     GN_CUDA(ws.alloc(&dsi, 8 * (size_t)iters));
     GN_CUDA(ws.alloc(&dfb, 8 * (size_t)iters));
     GN_CUDA(ws.alloc(&dbad, 4 * (size_t)iters));
