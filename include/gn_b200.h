@@ -124,6 +124,12 @@ int gn_fitness(gn_graph* g, const double* p, double gamma, double* f_out,
  * sum over members in ascending order (bitwise equal to w[idx].sum()). */
 int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
              double* weight, int* independent, int* maximal, int64_t* count);
+/* round_to_mis of num_states states (x: [num_states][n] fp64, host or, with
+ * GN_DEVICE_IO, device) with one synchronisation: selected [num_states][n]
+ * (may be NULL), weight / independent / maximal / count [num_states]. */
+int gn_round_many(gn_graph* g, int num_states, const void* x, uint32_t flags,
+                  uint8_t* selected, double* weight, int* independent,
+                  int* maximal, int64_t* count);
 /* is_independent / is_maximal_independent / set_weight (graph.py:134-162)
  * on a 0/1 membership mask. */
 int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight,

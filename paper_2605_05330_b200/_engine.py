@@ -59,6 +59,7 @@ EXPORTED = (
     "gn_simplex_state",
     "gn_fitness",
     "gn_round",
+    "gn_round_many",
     "gn_check_members",
     "gn_multi_run",
     "gn_batch_create",
@@ -134,6 +135,7 @@ _SIGNATURES = {
     "gn_simplex_state": (_I32, [_P, _P, _P]),
     "gn_fitness": (_I32, [_P, _P, _D, _P, _PD]),
     "gn_round": (_I32, [_P, _P, _U32, _P, _PD, _PI, _PI, _PI64]),
+    "gn_round_many": (_I32, [_P, _I32, _P, _U32, _P, _P, _P, _P, _P]),
     "gn_check_members": (_I32, [_P, _P, _PD, _PI, _PI, _PI64]),
     "gn_multi_run": (
         _I32,

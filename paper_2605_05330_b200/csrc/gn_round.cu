@@ -216,105 +216,144 @@ __global__ void k_pairwise(const double* __restrict__ a, const int* __restrict__
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kRoundThreads - 1) / kRoundThreads); }
 
-// shared tail of gn_round and gn_check_members: flags, compaction, weight
-static int check_and_weigh(gn_graph* g, CallCtx& ctx, uint8_t* dsel, double* weight, int* independent,
-                           int* maximal, int64_t* count, uint8_t* sel_out) {
-    cudaStream_t s = ctx.s;
-    const int64_t n = g->n;
-    const size_t nb = (size_t)std::max<int64_t>(n, 1);
-    int* flags = nullptr;
-    int* dcount = nullptr;
-    double *mw = nullptr, *res = nullptr, *scratch = nullptr;
-    void* tmp = nullptr;
+// Device scratch of one rounding, reused by the rounds of a batch.
+struct RoundScratch {
+    uint8_t *conf = nullptr, *cand = nullptr, *join = nullptr;
+    int32_t* list = nullptr;
+    int *dm = nullptr, *counters = nullptr;
+    unsigned int* barrier = nullptr;
+    double *mw = nullptr, *scratch = nullptr;
+    void *tmp = nullptr;
     size_t tmp_bytes = 0;
-    GN_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, g->w64, dsel, (double*)nullptr, (int*)nullptr,
-                                       (int)n, s));
-    // scratch for two pairwise levels: 2 * 2^D with 2^D <= 2 * ceil(n/64) + 2
-    const int64_t half = 2 * ((int64_t)nb / 64 + 2);
-    GN_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), s));
-    GN_CUDA(cudaMallocAsync((void**)&flags, 2 * sizeof(int), s));
-    GN_CUDA(cudaMallocAsync((void**)&dcount, sizeof(int), s));
-    GN_CUDA(cudaMallocAsync((void**)&mw, 8 * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&res, 8, s));
-    GN_CUDA(cudaMallocAsync((void**)&scratch, 8 * 2 * (size_t)half, s));
-    GN_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
-    GN_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int), s));
+    int64_t half = 0;
+    cudaStream_t s = nullptr;
+    int open(gn_graph* g, cudaStream_t st) {
+        s = st;
+        const int64_t n = g->n;
+        const size_t nb = (size_t)std::max<int64_t>(n, 1);
+        thrust::counting_iterator<int32_t> ids(0);
+        size_t t1 = 0, t2 = 0;
+        GN_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, ids, conf, list, dm, (int)n, s));
+        GN_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, g->w64, conf, (double*)nullptr, (int*)nullptr, (int)n, s));
+        tmp_bytes = std::max<size_t>(std::max(t1, t2), 16);
+        // scratch for two pairwise levels: 2 * 2^D with 2^D <= 2 * ceil(n/64) + 2
+        half = 2 * ((int64_t)nb / 64 + 2);
+        GN_CUDA(cudaMallocAsync((void**)&conf, nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&cand, nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&join, nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&list, 4 * nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&dm, sizeof(int), s));
+        GN_CUDA(cudaMallocAsync((void**)&counters, 2 * sizeof(int), s));
+        GN_CUDA(cudaMallocAsync((void**)&barrier, sizeof(unsigned int), s));
+        GN_CUDA(cudaMallocAsync((void**)&mw, 8 * nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&scratch, 8 * 2 * (size_t)half, s));
+        GN_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+        return GN_OK;
+    }
+    ~RoundScratch() {
+        void* ptrs[] = {conf, cand, join, list, dm, counters, barrier, mw, scratch, tmp};
+        for (void* p : ptrs)
+            if (p) cudaFreeAsync(p, s);
+    }
+};
+
+// Enqueue flags (independent, maximal), member count and the pairwise member
+// weight of the 0/1 mask dsel into out[0..1], cnt[0], wout[0] (device).
+static int enqueue_check(gn_graph* g, RoundScratch& R, const uint8_t* dsel, int* out, int* cnt, double* wout) {
+    cudaStream_t s = R.s;
+    const int64_t n = g->n;
+    GN_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(int), s));
+    GN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), s));
     if (n > 0) {
-        k_check<<<blocks_for(n), kRoundThreads, 0, s>>>(n, g->rowptr, g->col, dsel, flags);
+        k_check<<<blocks_for(n), kRoundThreads, 0, s>>>(n, g->rowptr, g->col, dsel, out);
         GN_LAUNCHED();
-        GN_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, g->w64, dsel, mw, dcount, (int)n, s));
+        size_t tb = R.tmp_bytes;
+        GN_CUDA(cub::DeviceSelect::Flagged(R.tmp, tb, g->w64, dsel, R.mw, cnt, (int)n, s));
         note_launch();
     }
-    k_pairwise<<<1, 1024, 0, s>>>(mw, dcount, scratch, 2 * half, res);
+    k_pairwise<<<1, 1024, 0, s>>>(R.mw, cnt, R.scratch, 2 * R.half, wout);
     GN_LAUNCHED();
-    int hflags[2];
-    int hcount = 0;
-    GN_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
-    GN_CUDA(cudaMemcpyAsync(&hcount, dcount, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GN_CUDA(cudaMemcpyAsync(weight, res, sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (sel_out && n > 0) GN_CUDA(cudaMemcpyAsync(sel_out, dsel, (size_t)n, cudaMemcpyDeviceToHost, s));
-    void* ptrs[] = {tmp, flags, dcount, mw, res, scratch};
-    for (void* p : ptrs) cudaFreeAsync(p, s);
-    GN_CUDA(cudaStreamSynchronize(s));
-    *independent = hflags[0] == 0;
-    *maximal = hflags[0] == 0 && hflags[1] == 0;
-    if (count) *count = hcount;
     return GN_OK;
 }
 
+// Enqueue round_to_mis of the device state dx into the mask sel (device).
 template <typename TI>
-static int round_impl(gn_graph* g, CallCtx& ctx, const TI* dx, uint8_t* selected, double* weight,
-                      int* independent, int* maximal, int64_t* count) {
+static int enqueue_round(gn_graph* g, RoundScratch& R, const TI* dx, uint8_t* sel) {
+    cudaStream_t s = R.s;
+    const int64_t n = g->n;
+    if (n == 0) return GN_OK;
+    GN_CUDA(cudaMemsetAsync(R.dm, 0, sizeof(int), s));
+    GN_CUDA(cudaMemsetAsync(R.counters, 0, 2 * sizeof(int), s));
+    GN_CUDA(cudaMemsetAsync(R.barrier, 0, sizeof(unsigned int), s));
+    k_threshold<TI><<<blocks_for(n), kRoundThreads, 0, s>>>(n, dx, sel);
+    GN_LAUNCHED();
+    k_conflicts<<<blocks_for(n), kRoundThreads, 0, s>>>(n, g->rowptr, g->col, sel, R.conf);
+    GN_LAUNCHED();
+    thrust::counting_iterator<int32_t> ids(0);
+    size_t tb = R.tmp_bytes;
+    GN_CUDA(cub::DeviceSelect::Flagged(R.tmp, tb, ids, R.conf, R.list, R.dm, (int)n, s));
+    note_launch();
+    k_repair<<<1, 32, 0, s>>>(R.list, R.dm, g->rowptr, g->col, g->w64, sel);
+    GN_LAUNCHED();
+    int maxb = 1, rc;
+    if ((rc = coresident_blocks((const void*)k_greedy, kRoundThreads, 0, g->device, &maxb))) return rc;
+    int grid = (int)std::min<int64_t>(maxb, blocks_for(n));
+    int64_t nn = n;
+    const int32_t* rp = g->rowptr;
+    const int32_t* cc = g->col;
+    const double* ww = g->w64;
+    void* args[] = {&nn, &rp, &cc, &ww, &sel, &R.cand, &R.join, &R.counters, &R.barrier};
+    GN_CUDA(cudaLaunchCooperativeKernel((const void*)k_greedy, dim3(grid), dim3(kRoundThreads), args, 0, s));
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+// B roundings (states x[b], host or device fp64) with one synchronisation.
+static int round_batch(gn_graph* g, int B, const double* x, bool dev_x, uint8_t* selected, double* weight,
+                       int* independent, int* maximal, int64_t* count) {
+    CallCtx ctx;
+    int rc = ctx.open(g->device);
+    if (rc) return rc;
     cudaStream_t s = ctx.s;
     const int64_t n = g->n;
     const size_t nb = (size_t)std::max<int64_t>(n, 1);
-    uint8_t *sel = nullptr, *conf = nullptr, *cand = nullptr, *join = nullptr;
-    int32_t* list = nullptr;
-    int* dm = nullptr;
-    int* counters = nullptr;
-    unsigned int* barrier = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    thrust::counting_iterator<int32_t> ids(0);
-    GN_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, ids, conf, list, dm, (int)n, s));
-    GN_CUDA(cudaMallocAsync((void**)&sel, nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&conf, nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&cand, nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&join, nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&list, 4 * nb, s));
-    GN_CUDA(cudaMallocAsync((void**)&dm, sizeof(int), s));
-    GN_CUDA(cudaMallocAsync((void**)&counters, 2 * sizeof(int), s));
-    GN_CUDA(cudaMallocAsync((void**)&barrier, sizeof(unsigned int), s));
-    GN_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), s));
-    GN_CUDA(cudaMemsetAsync(dm, 0, sizeof(int), s));
-    GN_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), s));
-    GN_CUDA(cudaMemsetAsync(barrier, 0, sizeof(unsigned int), s));
-    int rc = GN_OK;
-    if (n > 0) {
-        k_threshold<TI><<<blocks_for(n), kRoundThreads, 0, s>>>(n, dx, sel);
-        GN_LAUNCHED();
-        k_conflicts<<<blocks_for(n), kRoundThreads, 0, s>>>(n, g->rowptr, g->col, sel, conf);
-        GN_LAUNCHED();
-        GN_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, ids, conf, list, dm, (int)n, s));
-        note_launch();
-        k_repair<<<1, 32, 0, s>>>(list, dm, g->rowptr, g->col, g->w64, sel);
-        GN_LAUNCHED();
-        int maxb = 1;
-        if ((rc = coresident_blocks((const void*)k_greedy, kRoundThreads, 0, g->device, &maxb))) return rc;
-        int grid = (int)std::min<int64_t>(maxb, blocks_for(n));
-        int64_t nn = n;
-        const int32_t* rp = g->rowptr;
-        const int32_t* cc = g->col;
-        const double* ww = g->w64;
-        void* args[] = {&nn, &rp, &cc, &ww, &sel, &cand, &join, &counters, &barrier};
-        GN_CUDA(cudaLaunchCooperativeKernel((const void*)k_greedy, dim3(grid), dim3(kRoundThreads), args, 0, s));
-        GN_LAUNCHED();
+    RoundScratch R;
+    if ((rc = R.open(g, s))) return rc;
+    uint8_t* sel = nullptr;
+    double *dx = nullptr, *dw = nullptr;
+    int* dflags = nullptr;
+    GN_CUDA(cudaMallocAsync((void**)&sel, nb * B, s));
+    GN_CUDA(cudaMallocAsync((void**)&dw, 8 * (size_t)B, s));
+    GN_CUDA(cudaMallocAsync((void**)&dflags, 3 * sizeof(int) * (size_t)B, s));
+    if (!dev_x) {
+        GN_CUDA(cudaMallocAsync((void**)&dx, 8 * nb * B, s));
+        if (n > 0) GN_CUDA(cudaMemcpyAsync(dx, x, 8 * (size_t)n * B, cudaMemcpyHostToDevice, s));
     }
-    rc = check_and_weigh(g, ctx, sel, weight, independent, maximal, count, selected);
-    void* ptrs[] = {sel, conf, cand, join, list, dm, counters, barrier, tmp};
-    for (void* p : ptrs) cudaFreeAsync(p, s);
-    cudaStreamSynchronize(s);
-    return rc;
+    const double* xs = dev_x ? x : dx;
+    for (int b = 0; b < B && rc == GN_OK; ++b) {
+        rc = enqueue_round<double>(g, R, xs + (size_t)b * n, sel + nb * b);
+        if (rc == GN_OK) rc = enqueue_check(g, R, sel + nb * b, dflags + 3 * b, dflags + 3 * b + 2, dw + b);
+    }
+    std::vector<int> hf(3 * (size_t)B);
+    if (rc == GN_OK) {
+        cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(weight, dw, 8 * (size_t)B, cudaMemcpyDeviceToHost, s);
+        if (selected && n > 0)
+            for (int b = 0; b < B; ++b)
+                cudaMemcpyAsync(selected + (size_t)n * b, sel + nb * b, (size_t)n, cudaMemcpyDeviceToHost, s);
+    }
+    void* ptrs[] = {sel, dx, dw, dflags};
+    for (void* p : ptrs)
+        if (p) cudaFreeAsync(p, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (rc != GN_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "round sync", __FILE__, __LINE__);
+    for (int b = 0; b < B; ++b) {
+        independent[b] = hf[3 * (size_t)b] == 0;
+        maximal[b] = hf[3 * (size_t)b] == 0 && hf[3 * (size_t)b + 1] == 0;
+        if (count) count[b] = hf[3 * (size_t)b + 2];
+    }
+    return GN_OK;
 }
 
 }  // namespace gn
@@ -327,19 +366,17 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected, doub
              int* maximal, int64_t* count) {
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (g->n > 0 && !x) return fail(GN_ERR_ARG, "null state");
-    CallCtx ctx;
-    int rc = ctx.open(g->device);
-    if (rc) return rc;
-    if (flags & GN_DEVICE_IO)
-        return round_impl<double>(g, ctx, (const double*)x, selected, weight, independent, maximal, count);
-    double* dx = nullptr;
-    const size_t nb = (size_t)std::max<int64_t>(g->n, 1);
-    GN_CUDA(cudaMallocAsync((void**)&dx, 8 * nb, ctx.s));
-    if (g->n > 0) GN_CUDA(cudaMemcpyAsync(dx, x, 8 * (size_t)g->n, cudaMemcpyHostToDevice, ctx.s));
-    rc = round_impl<double>(g, ctx, dx, selected, weight, independent, maximal, count);
-    cudaFreeAsync(dx, ctx.s);
-    cudaStreamSynchronize(ctx.s);
-    return rc;
+    return round_batch(g, 1, (const double*)x, (flags & GN_DEVICE_IO) != 0, selected, weight, independent, maximal,
+                       count);
+}
+
+int gn_round_many(gn_graph* g, int num_states, const void* x, uint32_t flags, uint8_t* selected, double* weight,
+                  int* independent, int* maximal, int64_t* count) {
+    if (!g) return fail(GN_ERR_ARG, "null graph");
+    if (num_states < 1 || !weight || !independent || !maximal) return fail(GN_ERR_ARG, "bad gn_round_many arguments");
+    if (g->n > 0 && !x) return fail(GN_ERR_ARG, "null state");
+    return round_batch(g, num_states, (const double*)x, (flags & GN_DEVICE_IO) != 0, selected, weight, independent,
+                       maximal, count);
 }
 
 int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight, int* independent, int* maximal,
@@ -348,14 +385,32 @@ int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight, int* inde
     CallCtx ctx;
     int rc = ctx.open(g->device);
     if (rc) return rc;
-    uint8_t* dsel = nullptr;
+    cudaStream_t s = ctx.s;
     const size_t nb = (size_t)std::max<int64_t>(g->n, 1);
-    GN_CUDA(cudaMallocAsync((void**)&dsel, nb, ctx.s));
-    if (g->n > 0) GN_CUDA(cudaMemcpyAsync(dsel, mask, (size_t)g->n, cudaMemcpyHostToDevice, ctx.s));
-    rc = check_and_weigh(g, ctx, dsel, weight, independent, maximal, count, nullptr);
-    cudaFreeAsync(dsel, ctx.s);
-    cudaStreamSynchronize(ctx.s);
-    return rc;
+    RoundScratch R;
+    if ((rc = R.open(g, s))) return rc;
+    uint8_t* dsel = nullptr;
+    int* dflags = nullptr;
+    double* dw = nullptr;
+    GN_CUDA(cudaMallocAsync((void**)&dsel, nb, s));
+    GN_CUDA(cudaMallocAsync((void**)&dflags, 3 * sizeof(int), s));
+    GN_CUDA(cudaMallocAsync((void**)&dw, 8, s));
+    if (g->n > 0) GN_CUDA(cudaMemcpyAsync(dsel, mask, (size_t)g->n, cudaMemcpyHostToDevice, s));
+    rc = enqueue_check(g, R, dsel, dflags, dflags + 2, dw);
+    int hf[3] = {0, 0, 0};
+    if (rc == GN_OK) {
+        cudaMemcpyAsync(hf, dflags, sizeof(hf), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(weight, dw, 8, cudaMemcpyDeviceToHost, s);
+    }
+    void* ptrs[] = {dsel, dflags, dw};
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (rc != GN_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "check sync", __FILE__, __LINE__);
+    *independent = hf[0] == 0;
+    *maximal = hf[0] == 0 && hf[1] == 0;
+    if (count) *count = hf[2];
+    return GN_OK;
 }
 
 }  // extern "C"

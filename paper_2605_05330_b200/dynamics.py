@@ -322,6 +322,27 @@ def round_result(g, x, *, dtype=None, device=None) -> tuple[np.ndarray, float, b
     return sel[: g.n], weight.value, bool(ind.value), bool(mx.value)
 
 
+def round_many(g, xs, *, device=None) -> list[MisSolution]:
+    """round_to_mis of every row of xs ([B, n]) in one engine call (the
+    rounding kernels of all states are queued back to back, one sync)."""
+    X = np.ascontiguousarray(np.asarray(xs, dtype=np.float64))
+    if X.ndim != 2 or X.shape[1] != g.n:
+        raise ValueError(f"states have shape {X.shape}, expected (B, {g.n})")
+    B = X.shape[0]
+    if B == 0:
+        return []
+    h = any_device_graph(g, _opt("device", device))
+    sel = np.zeros((B, max(g.n, 1)), dtype=np.uint8)
+    weight = np.zeros(B)
+    ind = np.zeros(B, dtype=np.int32)
+    mx = np.zeros(B, dtype=np.int32)
+    cnt = np.zeros(B, dtype=np.int64)
+    E.check(E.lib().gn_round_many(h.handle, B, E.ptr(X), 0, E.ptr(sel), E.ptr(weight), E.ptr(ind), E.ptr(mx),
+                                  E.ptr(cnt)))
+    return [MisSolution(members=tuple(np.flatnonzero(sel[b, : g.n]).tolist()), weight=float(weight[b]),
+                        independent=bool(ind[b]), maximal=bool(mx[b])) for b in range(B)]
+
+
 def round_to_mis(g, x) -> MisSolution:
     """Binarize a state into a maximal independent set (dynamics.py:253-277).
 
@@ -348,6 +369,7 @@ __all__ = [
     "init_random",
     "init_warm",
     "is_normalizable",
+    "round_many",
     "round_result",
     "round_to_mis",
     "run_engine",

@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 from .batch import GraphBatch
-from .dynamics import GammaSchedule, NormalizationError, init_random, init_warm, round_to_mis, run_engine
+from .dynamics import GammaSchedule, NormalizationError, init_random, init_warm, round_many, round_to_mis, run_engine
 from .graph import WeightedGraph, csr_from_edges, from_csr
 from .multistart import MAX_STARTS, run_multi
 
@@ -158,12 +158,14 @@ def solve_instance(g, instance_name: str, config: RunConfig, warm_starts: Option
             t0 = time.perf_counter()
             res = run_multi(g, np.stack([x for _, x in chunk]), schedule, dtype=dtype, device=device)
             elapsed = (time.perf_counter() - t0) * 1000.0
+            ok = [b for b in range(len(chunk)) if res.status[b] == 0]
+            sols = dict(zip(ok, round_many(g, res.x[ok], device=device)))
             for b, (start_id, _) in enumerate(chunk):
                 if res.status[b] != 0:
                     records.append(StartRecord(start_id, 0.0, False, False, 0, elapsed))
                     stats.aborted_starts += 1
                     continue
-                sol = round_to_mis(g, res.x[b])
+                sol = sols[b]
                 stats.fallback_events += int(res.fallbacks[b, : res.iters_run[b]].sum())
                 records.append(StartRecord(start_id, sol.weight, sol.independent, sol.maximal,
                                            int(res.iters_run[b]), elapsed))

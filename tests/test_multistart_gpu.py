@@ -126,3 +126,17 @@ def test_fast_mode_split_hubs_within_tolerance(dtype):
             assert np.allclose(res.step_inf[b], ref.step_inf, rtol=1e-6, atol=1e-12)
     again = P.run_multi(inst.graph, X, s, dtype=dtype)
     assert np.array_equal(again.x, res.x)  # deterministic piece order
+
+
+def test_round_many_equals_round_to_mis():
+    g = G.c3_ba(n=20_000).graph
+    rng = np.random.default_rng(5)
+    X = np.stack([rng.random(g.n) for _ in range(5)] + [np.full(g.n, 0.5), np.zeros(g.n)])
+    many = P.round_many(g, X)
+    for b in range(X.shape[0]):
+        one = P.round_to_mis(g, X[b])
+        sel, w, ind, mx = O.round_to_mis(g, X[b])
+        assert many[b] == one
+        assert list(many[b].members) == np.flatnonzero(sel).tolist() and many[b].weight == w
+        assert many[b].independent and many[b].maximal
+    assert P.round_many(g, np.zeros((0, g.n))) == []
