@@ -194,7 +194,7 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
     point-to-point through torch.distributed).  Strong scaling: the graph is
     the same at every N.  Timed with CUDA events on the stream the engine and
     NCCL share, max over ranks."""
-    from paper_2605_05330_b200.partition import DistExchange, EngineBackend, build_partitions
+    from paper_2605_05330_b200.partition import DistExchange, EngineBackend, build_partitions, partitioned_step
 
     dtype = args.dtype or inst.dtype
     sched = P.GammaSchedule.pursuit(iterations=args.iters)
@@ -217,9 +217,10 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for k in range(iters):
-            be.step(k)
             if ex is not None:
-                ex.halo(k)
+                partitioned_step(be, ex, k)
+            else:
+                be.step(k)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
@@ -243,9 +244,10 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
         t0 = time.perf_counter()
         be.begin(x0l, gam)
         for k in range(iters):
-            be.step(k)
             if ex is not None:
-                ex.halo(k)
+                partitioned_step(be, ex, k)
+            else:
+                be.step(k)
         be.end(iters)
         barrier()
         e2e.append(time.perf_counter() - t0)

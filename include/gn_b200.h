@@ -195,6 +195,13 @@ int gn_part_elem_bytes(const gn_part* p);
 int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
                   uint32_t flags);
 int gn_part_step(gn_part* p, int k, uintptr_t stream);
+/* Overlap of the halo with the step: gn_part_set_boundary names the owned
+ * rows peers hold as ghosts (call before gn_part_begin); then per iteration
+ * gn_part_step_range(which = 0: boundary rows), pack and post the exchange,
+ * gn_part_step_range(which = 1: interior rows) while it is in flight, wait,
+ * unpack.  gn_part_step runs both ranges. */
+int gn_part_set_boundary(gn_part* p, const int32_t* rows, int64_t count);
+int gn_part_step_range(gn_part* p, int k, int which, uintptr_t stream);
 int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count,
                  void* d_out, uintptr_t stream);
 int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first,

@@ -72,6 +72,8 @@ EXPORTED = (
     "gn_part_elem_bytes",
     "gn_part_begin",
     "gn_part_step",
+    "gn_part_set_boundary",
+    "gn_part_step_range",
     "gn_part_pack",
     "gn_part_unpack",
     "gn_part_end",
@@ -154,6 +156,8 @@ _SIGNATURES = {
     "gn_part_elem_bytes": (_I32, [_P]),
     "gn_part_begin": (_I32, [_P, _P, _P, _I32, _U32]),
     "gn_part_step": (_I32, [_P, _I32, ctypes.c_size_t]),
+    "gn_part_set_boundary": (_I32, [_P, _P, _I64]),
+    "gn_part_step_range": (_I32, [_P, _I32, _I32, ctypes.c_size_t]),
     "gn_part_pack": (_I32, [_P, _I32, _P, _I64, _P, ctypes.c_size_t]),
     "gn_part_unpack": (_I32, [_P, _I32, _P, _I64, _I64, ctypes.c_size_t]),
     "gn_part_end": (_I32, [_P, _I32, _P, _P, _P, _P, _PI]),

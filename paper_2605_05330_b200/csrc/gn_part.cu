@@ -20,6 +20,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,9 +33,16 @@ struct gn_part {
     int device = 0;
     int32_t* rowptr = nullptr;  // n_own+1
     int32_t* col = nullptr;     // local ids
-    int32_t* order = nullptr;   // owned rows, degree-descending (stable)
-    int64_t n_long = 0;         // order[0, n_long): rows split over a warp (fast mode)
-    int64_t n_long_fast = 0;    // rows above kPartLongDegree
+    // owned rows in processing order: the boundary rows (those peers hold as
+    // ghosts) first, then the interior; each range degree-descending (stable)
+    int32_t* order = nullptr;
+    std::vector<int32_t> h_order;   // host copy (re-split by gn_part_set_boundary)
+    std::vector<int32_t> h_rowptr;
+    int64_t n_bnd = 0;              // order[0, n_bnd): boundary rows
+    int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
+    // per range (0 boundary, 1 interior), set by gn_part_begin
+    int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0};
+    int r_nbl[2] = {0, 0}, r_nblocks[2] = {0, 0};
     double* w64 = nullptr;      // n_own + n_ghost
     // run state
     int iters = 0;
@@ -42,9 +51,7 @@ struct gn_part {
     void* yg[2] = {nullptr, nullptr};  // gathered precision, n_own + n_ghost
     void* v = nullptr;                 // state precision, n_own + n_ghost
     double* gam = nullptr;
-    double* part = nullptr;  // [iters][nblocks][4]: max|dx|, fallbacks, w.x', non-finite
-    int nblocks = 0;       // blocks per step (stats partials per iteration)
-    int nblocks_long = 0;  // of which the first handle the split rows
+    double* part[2] = {nullptr, nullptr};  // per range [iters][r_nblocks][4]: max|dx|, fallbacks, w.x', non-finite
     cudaStream_t own_stream = nullptr;
 };
 
@@ -230,12 +237,38 @@ __global__ void k_part_out(int64_t n, const TS* __restrict__ x, TOut* __restrict
 
 static int pblocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kPartThreads - 1) / kPartThreads, 1 << 16)); }
 
+// Processing order: rows listed in `bnd` (the boundary) first, then the
+// rest; each range degree-descending (stable), long rows leading.
+static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
+    const int64_t n_own = P->n_own;
+    const std::vector<int32_t>& rp = P->h_rowptr;
+    std::vector<uint8_t> is_b((size_t)std::max<int64_t>(n_own, 1), 0);
+    for (int64_t i = 0; i < nb; ++i) {
+        if (bnd[i] < 0 || bnd[i] >= n_own) return fail(GN_ERR_ARG, "boundary row out of range");
+        is_b[(size_t)bnd[i]] = 1;
+    }
+    auto deg = [&](int32_t r) { return rp[(size_t)r + 1] - rp[(size_t)r]; };
+    std::vector<int32_t> rb, ri;
+    for (int64_t i = 0; i < n_own; ++i) (is_b[(size_t)i] ? rb : ri).push_back((int32_t)i);
+    auto by_deg = [&](int32_t a, int32_t b) { return deg(a) > deg(b); };
+    std::stable_sort(rb.begin(), rb.end(), by_deg);
+    std::stable_sort(ri.begin(), ri.end(), by_deg);
+    P->n_bnd = (int64_t)rb.size();
+    P->long_fast[0] = P->long_fast[1] = 0;
+    while (P->long_fast[0] < (int64_t)rb.size() && deg(rb[(size_t)P->long_fast[0]]) > kPartLongDegree) ++P->long_fast[0];
+    while (P->long_fast[1] < (int64_t)ri.size() && deg(ri[(size_t)P->long_fast[1]]) > kPartLongDegree) ++P->long_fast[1];
+    P->h_order = rb;
+    P->h_order.insert(P->h_order.end(), ri.begin(), ri.end());
+    if (n_own) GN_CUDA(cudaMemcpy(P->order, P->h_order.data(), 4 * (size_t)n_own, cudaMemcpyHostToDevice));
+    return GN_OK;
+}
+
 static void part_free_run(gn_part* p) {
-    void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part};
+    void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part[0], p->part[1]};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
-    p->gam = p->part = nullptr;
+    p->gam = p->part[0] = p->part[1] = nullptr;
 }
 
 }  // namespace gn
@@ -279,21 +312,17 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
         return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
     }
     cudaMemcpy(P->rowptr, rp.data(), 4 * rp.size(), cudaMemcpyHostToDevice);
-    // owned rows by degree, descending (stable): balanced warps, long rows first
-    std::vector<int32_t> order((size_t)n_own);
-    for (int64_t i = 0; i < n_own; ++i) order[(size_t)i] = (int32_t)i;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int32_t a, int32_t b) { return rp[(size_t)a + 1] - rp[(size_t)a] > rp[(size_t)b + 1] - rp[(size_t)b]; });
-    while (P->n_long_fast < n_own &&
-           rp[(size_t)order[(size_t)P->n_long_fast] + 1] - rp[(size_t)order[(size_t)P->n_long_fast]] > kPartLongDegree)
-        ++P->n_long_fast;
+    if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
+    if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
+    P->h_rowptr = rp;
     if ((ce = cudaMalloc(&P->order, 4 * (size_t)std::max<int64_t>(n_own, 1))) != cudaSuccess) {
         delete P;
         return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
     }
-    if (n_own) cudaMemcpy(P->order, order.data(), 4 * (size_t)n_own, cudaMemcpyHostToDevice);
-    if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
-    if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
+    if ((rc = part_order(P, nullptr, 0))) {
+        delete P;
+        return rc;
+    }
     GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
     *out = P;
     return GN_OK;
@@ -324,18 +353,23 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     const size_t nb = (size_t)std::max<int64_t>(nall, 1);
     p->iters = iters;
     p->flags = flags;
-    // GN_EXACT: every row summed sequentially (bitwise the reference); else the
-    // longest rows are split over warps
-    p->n_long = (flags & GN_EXACT) ? 0 : p->n_long_fast;
-    p->nblocks_long = p->n_long ? (int)std::min<int64_t>((p->n_long + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
-    p->nblocks = p->nblocks_long + pblocks(p->n_own - p->n_long);
+    // per range (boundary, interior): GN_EXACT sums every row sequentially
+    // (bitwise the reference); otherwise the longest rows are split over warps
+    for (int r = 0; r < 2; ++r) {
+        p->r_start[r] = r ? p->n_bnd : 0;
+        p->r_count[r] = r ? p->n_own - p->n_bnd : p->n_bnd;
+        p->r_long[r] = (flags & GN_EXACT) ? 0 : p->long_fast[r];
+        p->r_nbl[r] = p->r_long[r] ? (int)std::min<int64_t>((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
+        p->r_nblocks[r] = p->r_count[r] ? p->r_nbl[r] + pblocks(p->r_count[r] - p->r_long[r]) : 0;
+    }
     GN_CUDA(cudaMalloc(&p->x[0], es * nb));
     GN_CUDA(cudaMalloc(&p->x[1], es * nb));
     GN_CUDA(cudaMalloc(&p->yg[0], gs * nb));
     GN_CUDA(cudaMalloc(&p->yg[1], gs * nb));
     GN_CUDA(cudaMalloc(&p->v, es * nb));
     GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
-    GN_CUDA(cudaMalloc((void**)&p->part, 32 * (size_t)iters * p->nblocks));
+    for (int r = 0; r < 2; ++r)
+        if (p->r_nblocks[r]) GN_CUDA(cudaMalloc((void**)&p->part[r], 32 * (size_t)iters * p->r_nblocks[r]));
     GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
     double* dx0 = nullptr;
     GN_CUDA(cudaMalloc((void**)&dx0, 8 * nb));
@@ -364,29 +398,51 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     return GN_OK;
 }
 
-int gn_part_step(gn_part* p, int k, uintptr_t stream) {
-    if (!p || k < 0 || k >= p->iters) return fail(GN_ERR_ARG, "iteration out of range");
-    cudaStream_t s = (cudaStream_t)stream;  // 0: the legacy default stream (orders with torch's)
+// one range of the owned rows (0: boundary, 1: interior) for iteration k
+static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
+    if (p->r_count[r] == 0) return GN_OK;
     const int cur = k & 1;
-    const int nb = p->nblocks;
+    const int nb = p->r_nblocks[r];
+    const int32_t* ord = p->order + p->r_start[r];
     switch (p->dtype) {
         case GN_F64:
             k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
-                (double*)p->x[cur ^ 1], (const double*)p->yg[cur], (double*)p->yg[cur ^ 1], p->gam, k, p->part);
+                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const double*)p->yg[cur],
+                (double*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         case GN_F32:
             k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const double*)p->v, (const double*)p->x[cur],
-                (double*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
+                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const float*)p->yg[cur],
+                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         default:
             k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                p->n_own, p->n_long, p->nblocks_long, p->order, p->rowptr, p->col, p->w64, (const float*)p->v, (const float*)p->x[cur],
-                (float*)p->x[cur ^ 1], (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, k, p->part);
+                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1], (const float*)p->yg[cur],
+                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
     }
     GN_LAUNCHED();
     return GN_OK;
+}
+
+int gn_part_step(gn_part* p, int k, uintptr_t stream) {
+    if (!p || k < 0 || k >= p->iters) return fail(GN_ERR_ARG, "iteration out of range");
+    cudaStream_t s = (cudaStream_t)stream;  // 0: the legacy default stream (orders with torch's)
+    int rc = part_step_range(p, k, 0, s);
+    return rc ? rc : part_step_range(p, k, 1, s);
+}
+
+int gn_part_step_range(gn_part* p, int k, int which, uintptr_t stream) {
+    if (!p || k < 0 || k >= p->iters || which < 0 || which > 1) return fail(GN_ERR_ARG, "bad gn_part_step_range");
+    return part_step_range(p, k, which, (cudaStream_t)stream);
+}
+
+int gn_part_set_boundary(gn_part* p, const int32_t* rows, int64_t count) {
+    if (!p || count < 0 || (count > 0 && !rows)) return fail(GN_ERR_ARG, "bad gn_part_set_boundary");
+    GN_CUDA(cudaSetDevice(p->device));
+    return part_order(p, rows, count);
 }
 
 int gn_part_elem_bytes(const gn_part* p) { return p ? (int)gather_bytes(p->dtype) : 0; }
@@ -426,12 +482,14 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
     GN_CUDA(cudaSetDevice(p->device));
     GN_CUDA(cudaDeviceSynchronize());
     double *dout = nullptr, *dx = nullptr;
-    GN_CUDA(cudaMalloc((void**)&dout, 32 * (size_t)std::max(done, 1)));
+    GN_CUDA(cudaMalloc((void**)&dout, 64 * (size_t)std::max(done, 1)));  // per range
     GN_CUDA(cudaMalloc((void**)&dx, 8 * (size_t)std::max<int64_t>(p->n_own, 1)));
-    if (done > 0) {
-        k_part_fold<<<(done + 7) / 8, 256>>>(p->part, p->nblocks, done, dout);
-        GN_LAUNCHED();
-    }
+    GN_CUDA(cudaMemset(dout, 0, 64 * (size_t)std::max(done, 1)));
+    for (int r = 0; r < 2 && done > 0; ++r)
+        if (p->r_nblocks[r]) {
+            k_part_fold<<<(done + 7) / 8, 256>>>(p->part[r], p->r_nblocks[r], done, dout + (size_t)r * 4 * done);
+            GN_LAUNCHED();
+        }
     if (p->n_own > 0) {
         if (state_bytes(p->dtype) == 8)
             k_part_out<double, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const double*)p->x[done & 1], dx);
@@ -439,8 +497,18 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
             k_part_out<float, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const float*)p->x[done & 1], dx);
         GN_LAUNCHED();
     }
+    std::vector<double> h2(8 * (size_t)std::max(done, 1));
+    GN_CUDA(cudaMemcpy(h2.data(), dout, 64 * (size_t)std::max(done, 1), cudaMemcpyDeviceToHost));
+    // boundary range, then interior range: max / sum / fp64 sum / max, fixed order
     std::vector<double> h(4 * (size_t)std::max(done, 1));
-    GN_CUDA(cudaMemcpy(h.data(), dout, 32 * (size_t)done, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < done; ++k) {
+        const double* a0 = &h2[(size_t)k * 4];
+        const double* a1 = &h2[(size_t)(done + k) * 4];
+        h[(size_t)k * 4] = a1[0] > a0[0] || a1[0] != a1[0] ? a1[0] : a0[0];
+        h[(size_t)k * 4 + 1] = a0[1] + a1[1];
+        h[(size_t)k * 4 + 2] = a0[2] + a1[2];
+        h[(size_t)k * 4 + 3] = std::max(a0[3], a1[3]);
+    }
     if (x_out && p->n_own) GN_CUDA(cudaMemcpy(x_out, dx, 8 * (size_t)p->n_own, cudaMemcpyDeviceToHost));
     cudaFree(dout);
     cudaFree(dx);

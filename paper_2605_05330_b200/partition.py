@@ -9,7 +9,9 @@ groups them by owning peer, since ranges are contiguous.  Every iteration:
     step     each part updates its owned rows (csrc/gn_part.cu), reading the
              published values of owned vertices and ghosts
     halo     each part packs the published values its peers hold as ghosts
-             and sends them; received buffers are unpacked into ghost slots
+             and sends them; received buffers are unpacked into ghost slots.
+             The boundary rows (those peers hold) are stepped first, so the
+             exchange runs while the interior rows are stepped
 
 Neighbour lists keep the global (reference) order, so a partitioned EXACT run
 is bitwise the single-GPU EXACT run (and the reference).  Exchanges: LocalExchange (all parts in one
@@ -123,6 +125,10 @@ class EngineBackend:
         self.elem = E.lib().gn_part_elem_bytes(h)
         self.tdtype = torch.float64 if self.elem == 8 else torch.float32
         self.send_idx = {q: torch.from_numpy(v).to(self.device) for q, v in spec.send_idx.items()}
+        # rows peers hold as ghosts go first, so their exchange overlaps the interior rows
+        bnd = (np.unique(np.concatenate(list(spec.send_idx.values()))).astype(np.int32) if spec.send_idx
+               else np.zeros(0, np.int32))
+        E.check(E.lib().gn_part_set_boundary(h, E.ptr(bnd), len(bnd)))
 
     def _stream(self) -> int:
         return self.torch.cuda.current_stream(self.device).cuda_stream
@@ -135,6 +141,12 @@ class EngineBackend:
 
     def step(self, k: int) -> None:
         self.E.check(self.E.lib().gn_part_step(self.h, k, self._stream()))
+
+    def step_boundary(self, k: int) -> None:
+        self.E.check(self.E.lib().gn_part_step_range(self.h, k, 0, self._stream()))
+
+    def step_interior(self, k: int) -> None:
+        self.E.check(self.E.lib().gn_part_step_range(self.h, k, 1, self._stream()))
 
     def empty(self, count: int):
         return self.torch.empty(count, dtype=self.tdtype, device=self.device)
@@ -181,13 +193,15 @@ class LocalExchange:
     def __init__(self, backends: Sequence):
         self.backends = list(backends)
 
-    def halo(self, k: int) -> None:
-        outgoing = {}
-        for p, b in enumerate(self.backends):
-            for q in b.spec.send_idx:
-                outgoing[(p, q)] = b.pack(k, q)
+    def start(self, k: int):
+        return {(p, q): b.pack(k, q) for p, b in enumerate(self.backends) for q in b.spec.send_idx}
+
+    def finish(self, k: int, outgoing) -> None:
         for (p, q), buf in outgoing.items():
             self.backends[q].unpack(k, p, buf)
+
+    def halo(self, k: int) -> None:
+        self.finish(k, self.start(k))
 
 
 class DistExchange:
@@ -201,7 +215,9 @@ class DistExchange:
         spec = backend.spec
         self.recv_from = [q for q in range(spec.parts) if q != spec.p and spec.ghost_ptr[q + 1] > spec.ghost_ptr[q]]
 
-    def halo(self, k: int) -> None:
+    def start(self, k: int):
+        """Pack the boundary values of step k and post the sends/receives (they
+        run on the communicator's stream, after the packs)."""
         dist, b = self.dist, self.b
         spec = b.spec
         ops, recvs = [], []
@@ -211,11 +227,18 @@ class DistExchange:
             ops.append(dist.P2POp(dist.irecv, buf, q, self.group))
         for q in spec.send_idx:
             ops.append(dist.P2POp(dist.isend, b.pack(k, q), q, self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return works, recvs
+
+    def finish(self, k: int, pending) -> None:
+        works, recvs = pending
+        for r in works:
+            r.wait()
         for q, buf in recvs:
-            b.unpack(k, q, buf)
+            self.b.unpack(k, q, buf)
+
+    def halo(self, k: int) -> None:
+        self.finish(k, self.start(k))
 
 
 @dataclass
@@ -227,13 +250,21 @@ class PartResult:
     bad: int
 
 
+def partitioned_step(backend, exchange, k: int) -> None:
+    """Step k of one partition with the halo overlapped: boundary rows, then
+    their exchange in flight while the interior rows run, then the ghosts."""
+    backend.step_boundary(k)
+    pending = exchange.start(k)
+    backend.step_interior(k)
+    exchange.finish(k, pending)
+
+
 def run_partition(backend, exchange, x0_local: np.ndarray, schedule: GammaSchedule) -> PartResult:
     """The pursuit on one partition (all ranks call this together)."""
     gam = schedule.table()
     backend.begin(x0_local, gam)
     for k in range(len(gam)):
-        backend.step(k)
-        exchange.halo(k)
+        partitioned_step(backend, exchange, k)
     x, si, fb, ms, bad = backend.end(len(gam))
     return PartResult(x, si, fb, ms, bad)
 
@@ -249,8 +280,11 @@ def run_local_partitions(g, x0: np.ndarray, schedule: GammaSchedule, parts: int,
         b.begin(s.local_x0(x0), gam)
     for k in range(len(gam)):
         for b in backends:
-            b.step(k)
-        ex.halo(k)
+            b.step_boundary(k)
+        pending = ex.start(k)
+        for b in backends:
+            b.step_interior(k)
+        ex.finish(k, pending)
     outs = [b.end(len(gam)) for b in backends]
     x = np.concatenate([o[0] for o in outs])
     return {"x": x, "step_inf": np.max([o[1] for o in outs], axis=0), "fallbacks": np.sum([o[2] for o in outs], axis=0),
