@@ -44,6 +44,9 @@
 #include "gn_internal.cuh"
 #include "gn_plan.h"
 
+#ifndef GN_HUB_ROUND
+#define GN_HUB_ROUND 8  // hub-piece gathers per lane per round (16 spills)
+#endif
 #ifndef GN_DBG_GATHER
 #define GN_DBG_GATHER 0  // timing experiments only (results are wrong when set)
 #endif
@@ -397,21 +400,36 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
             if (it.kind == kWhole || it.kind == kPiece) {
                 // not reached: slice items precede hub items in every warp list
             } else if (it.kind == kHubPiece) {
-                // lanes stride the piece's elements; fixed warp tree
+                // lanes stride the piece's elements, 16 per lane per round with
+                // the next round's indices loading under this round's gathers
+                // (a hub piece is a chain of rounds on its CTA's critical path);
+                // fixed warp tree
+                constexpr int R = GN_HUB_ROUND;
                 const int base = __ldg(a.hub_ptr + it.id);
                 TS s = TS(0);
                 int p = base + it.beg + lane;
                 const int e = base + it.end;
-                for (; p + 3 * 32 < e; p += 4 * 32) {
-                    const int j0 = __ldg(a.hub_col + p), j1 = __ldg(a.hub_col + p + 32);
-                    const int j2 = __ldg(a.hub_col + p + 64), j3 = __ldg(a.hub_col + p + 96);
-                    const TG y0 = yg[j0], y1 = yg[j1], y2 = yg[j2], y3 = yg[j3];
-                    s = A::add(s, (TS)y0);
-                    s = A::add(s, (TS)y1);
-                    s = A::add(s, (TS)y2);
-                    s = A::add(s, (TS)y3);
+                int jn[R];
+#pragma unroll
+                for (int u = 0; u < R; ++u) jn[u] = p + u * 32 < e ? __ldg(a.hub_col + p + u * 32) : 0;
+                for (; p + (R - 1) * 32 < e; p += R * 32) {
+                    int j[R];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) j[u] = jn[u];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        const int q = p + (R + u) * 32;
+                        jn[u] = q < e ? __ldg(a.hub_col + q) : 0;
+                    }
+                    TG y[R];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) y[u] = yg[j[u]];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) s = A::add(s, (TS)y[u]);
                 }
-                for (; p < e; p += 32) s = A::add(s, (TS)yg[__ldg(a.hub_col + p)]);
+#pragma unroll
+                for (int u = 0; u < R; ++u)  // the last partial round: its indices are in jn
+                    if (p + u * 32 < e) s = A::add(s, (TS)yg[jn[u]]);
                 s = warp_sum(s);
                 if (lane == 0) s_hslot[it.slot] = s;
             } else {  // kHubSeq (EXACT): one thread per hub row, sequential
@@ -778,6 +796,21 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const D
                     for (int i = i0; i < i1; ++i) per_kind[(size_t)hpn.items[(size_t)i].kind]++;
                 }
         }
+        if (getenv("GN_PLAN_DUMP")[0] == '2')
+            for (int b = 0; b < G; ++b) {
+                const int ph0 = hpn.phase_base[(size_t)b], ph1 = hpn.phase_base[(size_t)b + 1];
+                int cnt[4] = {0, 0, 0, 0}, res = 0;
+                long long elems = 0;
+                for (int ph = ph0; ph < ph1; ++ph)
+                    for (int i = hpn.phase_warp[(size_t)ph * (kWarps + 1)]; i < hpn.phase_warp[(size_t)ph * (kWarps + 1) + kWarps]; ++i) {
+                        const Item& it = hpn.items[(size_t)i];
+                        cnt[it.kind]++;
+                        if (it.smem >= 0) res++;
+                        elems += it.kind <= kPiece ? (long long)(it.end - it.beg) * 32 * in.B : (it.end - it.beg);
+                    }
+                fprintf(stderr, "[cta %d] whole=%d piece=%d hub=%d resident=%d elems=%lld combs=%d\n", b, cnt[0], cnt[1],
+                        cnt[2], res, elems, hpn.phase_comb[(size_t)ph1] - hpn.phase_comb[(size_t)ph0]);
+            }
         fprintf(stderr, "[plan] G=%d nhub=%d nslices=%d nsplit=%d items: whole=%d piece=%d hubpiece=%d hubseq=%d "
                         "per-warp mean=%.2f max=%d phases/CTA max=%d combines=%zu resident=%.1f MB\n",
                 G, g->nhub, g->nslices, g->nsplit, per_kind[0], per_kind[1], per_kind[2], per_kind[3],
