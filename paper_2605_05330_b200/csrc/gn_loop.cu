@@ -208,13 +208,16 @@ struct GatherDepth {  // gathers in flight per lane (register budget: 64K / (kTh
 template <typename TS, typename TI, typename TG>
 struct SlicePre {
     static constexpr int B = LaneVec<TI>::B;
-    // index vectors per batch, at most 4 (two batches of them are live at once)
-    static constexpr int NB = GatherDepth<TG>::value / B > 4 ? 4 : (GatherDepth<TG>::value / B > 0 ? GatherDepth<TG>::value / B : 1);
+    // int32-id layouts pad with the zero-valued vertex n (gn_graph.cu): no degree masks
+    static constexpr bool kSent = sizeof(TI) == 4;
+    // index vectors per batch, at most 4 (two batches of them are live at
+    // once); int32-id layouts walk an item pair interleaved (slice_consume2),
+    // half a batch per item
+    static constexpr int NBF = GatherDepth<TG>::value / B > 4 ? 4 : (GatherDepth<TG>::value / B > 0 ? GatherDepth<TG>::value / B : 1);
+    static constexpr int NB = kSent && NBF > 1 ? NBF / 2 : NBF;
     const uint4* base;  // block `beg` of the item, this lane
     int beg, nb, d, row;
     bool whole, valid;
-    // int32-id layouts pad with the zero-valued vertex n (gn_graph.cu): no degree masks
-    static constexpr bool kSent = sizeof(TI) == 4;
     RowIn<TS> in;
     uint4 v[NB];
 };
@@ -333,6 +336,47 @@ __device__ __forceinline__ TS slice_consume(SlicePre<TS, TI, TG>& p, const GSrc<
     return s;
 }
 
+// Both items of a pair at once (int32-id layouts, no degree masks): each
+// batch issues the gathers of the two items before adding either, so a pair
+// of short slices costs one memory round trip instead of two.  Each item's
+// sum stays sequential in position order.
+template <typename TS, typename TG, typename TI, bool HOT>
+__device__ __forceinline__ void slice_consume2(SlicePre<TS, TI, TG>& p0, SlicePre<TS, TI, TG>& p1,
+                                               const GSrc<TG, HOT>& yg, TS& s0, TS& s1) {
+    using A = Arith<TS>;
+    using V = LaneVec<TI>;
+    using SP = SlicePre<TS, TI, TG>;
+    constexpr int B = SP::B, NB = SP::NB;
+    s0 = TS(0);
+    s1 = TS(0);
+    const int be0 = p0.nb, be1 = p1.nb, be = max(be0, be1);
+    for (int b = 0; b < be; b += NB) {
+        uint4 vn0[NB], vn1[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            if (b + NB + u < be0) vn0[u] = p0.base[(size_t)(b + NB + u) * kSlice];
+            if (b + NB + u < be1) vn1[u] = p1.base[(size_t)(b + NB + u) * kSlice];
+        }
+        TG y0[NB * B], y1[NB * B];
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+#pragma unroll
+            for (int t = 0; t < B; ++t) {
+                y0[u * B + t] = b + u < be0 ? yg[V::get(p0.v[u], t)] : TG(0);
+                y1[u * B + t] = b + u < be1 ? yg[V::get(p1.v[u], t)] : TG(0);
+            }
+#pragma unroll
+        for (int q = 0; q < NB * B; ++q) s0 = A::add(s0, (TS)y0[q]);
+#pragma unroll
+        for (int q = 0; q < NB * B; ++q) s1 = A::add(s1, (TS)y1[q]);
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            p0.v[u] = vn0[u];
+            p1.v[u] = vn1[u];
+        }
+    }
+}
+
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -385,13 +429,22 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
                 if (two) slice_prefetch<TS, TG, TI>(a, it1, src, i + 1, s_res, lane, cur, p1);
             }
             ready = false;
-            const TS s0 = slice_consume<TS, TG, TI, HOT>(p0, yg);
-            if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
-            else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
-            if (two) {
-                const TS s1 = slice_consume<TS, TG, TI, HOT>(p1, yg);
+            if (SlicePre<TS, TI, TG>::kSent && two) {
+                TS s0, s1;
+                slice_consume2<TS, TG, TI, HOT>(p0, p1, yg, s0, s1);
+                if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
+                else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
                 if (!p1.whole) s_slot[it1.slot * kSlice + lane] = s1;
                 else if (p1.valid) update_row<TS, TG, TRACE>(a, p1.row, s1, p1.in, cur, g, k, tail, st);
+            } else {
+                const TS s0 = slice_consume<TS, TG, TI, HOT>(p0, yg);
+                if (!p0.whole) s_slot[it0.slot * kSlice + lane] = s0;
+                else if (p0.valid) update_row<TS, TG, TRACE>(a, p0.row, s0, p0.in, cur, g, k, tail, st);
+                if (two) {
+                    const TS s1 = slice_consume<TS, TG, TI, HOT>(p1, yg);
+                    if (!p1.whole) s_slot[it1.slot * kSlice + lane] = s1;
+                    else if (p1.valid) update_row<TS, TG, TRACE>(a, p1.row, s1, p1.in, cur, g, k, tail, st);
+                }
             }
             i += two ? 2 : 1;
         }
