@@ -941,8 +941,10 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     const size_t slot_bytes = (size_t)kMaxSlots * kSlice * sizeof(TS) + (size_t)kMaxHubSlots * sizeof(TS) + hot_bytes;
     const size_t static_bytes = 2048;  // publish scratch
     // index residency budget: what is left after the partial slots, capped so
-    // the L1 keeps room for the gathers (GN_SMEM_RES_KB overrides)
-    size_t res_cap = 96 * 1024;
+    // the L1 keeps room for the gathers -- the L1 is worth more than resident
+    // indices on the large (int32-id) graphs, whose gathers miss it most
+    // (C5: 3.0 -> 2.1 ms/iteration without residency); GN_SMEM_RES_KB overrides
+    size_t res_cap = sizeof(TI) == 2 ? 32 * 1024 : 0;
     if (const char* e = getenv("GN_SMEM_RES_KB")) res_cap = (size_t)atoi(e) * 1024;
     int smem_sm = 0;
     GN_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g->device));
@@ -958,16 +960,20 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     if (g->grid_override > 0) grid = std::min(maxb, g->grid_override);
     const DevicePlan* plan = nullptr;
     if ((rc = get_plan(g, grid, exact, res_cap, &plan))) return rc;
-    const int hub_slot_off = (int)((size_t)kMaxSlots * kSlice * sizeof(TS));
-    const int hot_off = (int)(((size_t)hub_slot_off + (size_t)kMaxHubSlots * sizeof(TS) + 15) / 16 * 16);
-    const int resident_off = (int)((slot_bytes + 15) / 16 * 16);
+    // shared memory sized to what the plan uses (whatever is left is L1)
+    const int hub_slot_off = (int)(((size_t)plan->max_slots * kSlice * sizeof(TS) + 15) / 16 * 16);
+    const int hot_off = (int)(((size_t)hub_slot_off + (size_t)plan->max_hub_slots * sizeof(TS) + 15) / 16 * 16);
+    const int resident_off = (int)(((size_t)hot_off + hot_bytes + 15) / 16 * 16);
     size_t dyn_smem = (size_t)resident_off + (size_t)plan->max_words * 16;
     // the CTA's item descriptors and slice-row degrees, when they fit
     int item_cache_off = 0;
     {
         const size_t off = (dyn_smem + 15) / 16 * 16;
         const size_t bytes = (size_t)plan->max_cta_items * (sizeof(Item) + kSlice * sizeof(int32_t));
-        if (!getenv("GN_NO_ITEM_CACHE") && plan->max_cta_items > 0 && off + bytes + static_bytes <= per_cta) {
+        // small enough not to cost the gathers their L1 (C5 scale 20: 67 KB of
+        // items made the iteration 30% slower)
+        if (!getenv("GN_NO_ITEM_CACHE") && plan->max_cta_items > 0 && bytes <= 32 * 1024 &&
+            off + bytes + static_bytes <= per_cta) {
             item_cache_off = (int)off;
             dyn_smem = off + bytes;
             GN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
