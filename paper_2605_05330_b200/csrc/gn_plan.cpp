@@ -117,6 +117,10 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
             int slots = 0, hslots = 0;
         };
         std::vector<Phase> phases(1);
+        int cta_pieces = 0;
+        for (const Unit& u : cu)
+            if (u.kind == 1) cta_pieces += (nblk(u.id) + kPieceBlocks - 1) / kPieceBlocks;
+        const int slot_cap = cta_pieces <= kMaxSlots ? kMaxSlots : kPhaseSlots;
         for (const Unit& u : cu) {
             if (u.kind == 0) {
                 whole.push_back(Item{kWhole, u.id, 0, nblk(u.id), -1, -1, 0, 0});
@@ -125,7 +129,7 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
             } else if (u.kind == 1) {
                 const int nb = nblk(u.id);
                 const int np = (nb + kPieceBlocks - 1) / kPieceBlocks;
-                if (phases.back().slots + np > kMaxSlots && phases.back().slots > 0) phases.emplace_back();
+                if (phases.back().slots + np > slot_cap && phases.back().slots > 0) phases.emplace_back();
                 Phase& ph = phases.back();
                 ph.combs.push_back(Combine{0, u.id, ph.slots, np});
                 for (int q = 0; q < np; ++q)
