@@ -317,7 +317,11 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
     // MinHash over the 128-byte lines (16 fp64 ids) a slice gathers: slices
     // with overlapping neighbourhoods get equal signatures w.p. = Jaccard, and
     // the plan places equal signatures on the same SM so its L1 serves them
-    L.sig.assign(getenv("GN_PLAN_COLOCATE") ? (size_t)L.nslices : 0, ~0ull);
+    // computed for the uint16-id graphs (small: cheap, and their dense rows
+    // reuse neighbourhoods -- C2 -2.5%); GN_PLAN_COLOCATE=1/0 forces it on/off
+    const char* colo = getenv("GN_PLAN_COLOCATE");
+    const bool want_sig = colo ? colo[0] == '1' : n <= 65536;
+    L.sig.assign(want_sig ? (size_t)L.nslices : 0, ~0ull);
     for (int32_t s = 0; s < (int32_t)L.sig.size(); ++s) {
         uint64_t m = ~0ull;
         for (int l = 0; l < kSlice; ++l) {

@@ -830,7 +830,7 @@ static int get_plan(gn_graph* g, int G, bool exact, size_t resident_cap, const D
     std::vector<int32_t> hp((size_t)g->nhub + 1);
     GN_CUDA(cudaMemcpy(hp.data(), g->hub_ptr, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
     PlanInput in{g->n, g->nhub, g->nslices, g->nsplit, g->idx16 ? 8 : 4, &sp, &hp, &g->slice_sig,
-                 getenv("GN_PLAN_COLOCATE") != nullptr};
+                 !g->slice_sig.empty()};
     HostPlan hpn;
     build_plan(in, G, exact, resident_cap, hpn);
     if (getenv("GN_PLAN_DUMP")) {  // diagnosis: items per warp by kind, phases, residency
@@ -940,11 +940,10 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     const size_t hot_bytes = hot ? (size_t)g->hot * sizeof(TG) : 0;
     const size_t slot_bytes = (size_t)kMaxSlots * kSlice * sizeof(TS) + (size_t)kMaxHubSlots * sizeof(TS) + hot_bytes;
     const size_t static_bytes = 2048;  // publish scratch
-    // index residency budget: what is left after the partial slots, capped so
-    // the L1 keeps room for the gathers -- the L1 is worth more than resident
-    // indices on the large (int32-id) graphs, whose gathers miss it most
-    // (C5: 3.0 -> 2.1 ms/iteration without residency); GN_SMEM_RES_KB overrides
-    size_t res_cap = sizeof(TI) == 2 ? 32 * 1024 : 0;
+    // index residency budget (GN_SMEM_RES_KB): off -- the L1 is worth more
+    // than resident indices (C5 scale 24: 3.0 -> 2.1 ms/iteration without;
+    // C2 with co-located slices: equal)
+    size_t res_cap = 0;
     if (const char* e = getenv("GN_SMEM_RES_KB")) res_cap = (size_t)atoi(e) * 1024;
     int smem_sm = 0;
     GN_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g->device));

@@ -58,9 +58,9 @@ void build_plan(const PlanInput& in, int G, bool exact, size_t cap, HostPlan& ou
     }
 
     // ---- level 1: units -> CTAs, longest-processing-time-first on total
-    // cost.  With `colocate` the slices are instead taken in signature order
-    // as contiguous runs filling each CTA to the mean (neighbourhood-sharing
-    // slices on one SM); measured slower on C2/C3, kept for experiments.
+    // cost.  With `colocate` (the uint16-id graphs) the slices are instead
+    // taken in signature order as contiguous runs filling each CTA to the mean
+    // (neighbourhood-sharing slices on one SM, whose L1 then serves them).
     std::vector<std::vector<Unit>> per_cta((size_t)G);
     std::vector<double> load((size_t)G, 0.0);
     double total = 0.0;
