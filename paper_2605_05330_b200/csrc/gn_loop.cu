@@ -502,17 +502,27 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
         }
         const int c0 = __ldg(a.phase_comb + ph), c1 = __ldg(a.phase_comb + ph + 1);
         if (c1 > c0) {
+            // the state of the warp's first combine row loads while the CTA
+            // waits for its slowest warp (it does not depend on the pieces)
+            Combine cb0{0, 0, 0, 0};
+            RowIn<TS> in0{TS(0), TS(0), 0.0};
+            if (c0 + warp < c1) {
+                cb0 = a.combs[c0 + warp];
+                const int r0 = cb0.kind == 0 ? a.nhub + cb0.id * kSlice + lane : cb0.id;
+                if (r0 < a.n && (cb0.kind == 0 || lane == 0)) in0 = row_in(a, r0, cur);
+            }
             __syncthreads();
             for (int c = c0 + warp; c < c1; c += kWarps) {
-                const Combine cb = a.combs[c];
+                const bool first = c == c0 + warp;
+                const Combine cb = first ? cb0 : a.combs[c];
                 if (cb.kind == 0) {
                     const int r = a.nhub + cb.id * kSlice + lane;
-                    const RowIn<TS> in = row_in(a, r, cur);
+                    const RowIn<TS> in = first ? in0 : row_in(a, r, cur);
                     TS tot = TS(0);
                     for (int q = 0; q < cb.nslot; ++q) tot = A::add(tot, s_slot[(cb.slot + q) * kSlice + lane]);
                     update_row<TS, TG, TRACE>(a, r, tot, in, cur, g, k, tail, st);
                 } else if (lane == 0) {
-                    const RowIn<TS> in = row_in(a, cb.id, cur);
+                    const RowIn<TS> in = first ? in0 : row_in(a, cb.id, cur);
                     TS tot = TS(0);
                     for (int q = 0; q < cb.nslot; ++q) tot = A::add(tot, s_hslot[cb.slot + q]);
                     update_row<TS, TG, TRACE>(a, cb.id, tot, in, cur, g, k, tail, st);
