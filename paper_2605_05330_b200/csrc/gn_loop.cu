@@ -14,8 +14,8 @@
 // fused with the per-iteration reductions: max|x'-x|, the fallback count,
 // the non-finite flag and fixed-order fp64 block partials of w.x' (the
 // objective) and, in trace mode, y.y, y.s, w.x (the energy terms of the
-// pre-step state).  Block stats go to a ring (plain stores, no atomics) that
-// all blocks fold cooperatively every kRing iterations.
+// pre-step state).  Warp stats go to a ring (plain stores, no atomics, no
+// CTA barrier) that all blocks fold cooperatively every kRing iterations.
 //
 // Work, decided once per (graph, grid, mode) on the host (build_plan):
 //   CTA items   long slices (the 32 warps split the slice's blocks) and hub
@@ -53,8 +53,8 @@
 
 namespace gn {
 
-constexpr int kRing = 1024;  // iterations of block stats kept before a fold
-constexpr int kRingW = 8;    // per block: 4 dot terms, max|dx|, fallbacks, non-finite, pad
+constexpr int kRing = 128;  // iterations of warp stats kept before a fold
+constexpr int kRingW = 8;   // per warp: 4 dot terms, max|dx|, fallbacks, non-finite, pad
 
 template <typename TS, typename TG>
 struct LoopArgs {
@@ -89,7 +89,7 @@ struct LoopArgs {
     int* bad;          // [iters]   1 if a non-finite state appeared
     int* status;       // [0] iterations run
     double* dots;      // [(iters+1)][4]: y.y, y.s, w.x (pre), w.x' (post)
-    double* ring;      // [kRing][grid][kRingW]
+    double* ring;      // [kRing][grid * kWarps][kRingW]
     unsigned int* barrier;
     double* x_hist;    // optional [iters][n], original order
     const int32_t* __restrict__ perm;
@@ -533,14 +533,10 @@ __device__ void pass(const LoopArgs<TS, TG>& a, int k, bool tail, Stats& st, TS*
     }
 }
 
-// Block-level fold of the per-thread stats; thread 0 stores them (plain
-// stores, no atomics) in this iteration's ring slot.
+// Warp-level fold of the per-thread stats; lane 0 stores the warp's partials
+// (plain stores, no atomics, no CTA barrier) in this iteration's ring slot.
 template <bool TRACE>
 __device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
-    __shared__ double s_acc[kWarps][4];
-    __shared__ double s_mx[kWarps];
-    __shared__ unsigned int s_fb[kWarps];
-    __shared__ int s_bad[kWarps];
     Stats st = st0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -553,30 +549,12 @@ __device__ void publish(const Stats& st0, double* __restrict__ ring_slot) {
 #pragma unroll
     for (int q = TRACE ? 0 : 3; q < 4; ++q) st.acc[q] = warp_sum_d(st.acc[q]);
     if (lane == 0) {
-        s_mx[warp] = st.mx;
-        s_fb[warp] = st.fbc;
-        s_bad[warp] = st.bad;
+        double* dst = ring_slot + ((size_t)blockIdx.x * kWarps + warp) * kRingW;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s_acc[warp][q] = st.acc[q];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mx = 0.0, acc[4] = {0.0, 0.0, 0.0, 0.0};
-        unsigned int f = 0;
-        int bad = 0;
-        for (int q = 0; q < kWarps; ++q) {
-            if (!(s_mx[q] <= mx)) mx = s_mx[q];
-            f += s_fb[q];
-            bad |= s_bad[q];
-#pragma unroll
-            for (int c = TRACE ? 0 : 3; c < 4; ++c) acc[c] = __dadd_rn(acc[c], s_acc[q][c]);
-        }
-        double* dst = ring_slot + (size_t)blockIdx.x * kRingW;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = acc[c];
-        dst[4] = mx;
-        dst[5] = (double)f;
-        dst[6] = bad ? 1.0 : 0.0;
+        for (int c = 0; c < 4; ++c) dst[c] = st.acc[c];
+        dst[4] = st.mx;
+        dst[5] = (double)st.fbc;
+        dst[6] = st.bad ? 1.0 : 0.0;
     }
 }
 
@@ -589,11 +567,11 @@ struct FoldOut {
 };
 
 // All blocks: fold ring slots [0, count) (iterations k0..k0+count-1), one
-// warp per (slot, quantity), block order fixed.
+// warp per (slot, quantity), partial order fixed.
 __device__ void fold_ring(const double* ring, int count, int k0, const FoldOut& o) {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
-    const int G = gridDim.x;
+    const int G = gridDim.x * kWarps;  // partials per iteration (one per warp)
     for (int t = gw; t < count * 7; t += nw) {
         const int slot = t / 7, c = t % 7;
         const double* src = ring + (size_t)slot * G * kRingW + c;
@@ -630,7 +608,7 @@ __device__ double ring_step_inf(const double* ring_slot) {
     __shared__ double s_m;
     if (threadIdx.x < 32) {
         double m = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+        for (int b = threadIdx.x; b < (int)gridDim.x * kWarps; b += 32) {
             const double v = __ldcg(ring_slot + (size_t)b * kRingW + 4);
             if (!(v <= m)) m = v;
         }
@@ -688,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_gn_loop(LoopArgs<TS, T
     const FoldOut fo{a.iters, a.step_inf, a.fb, a.bad, a.dots};
     unsigned int bar = 0;
     int ran = 0, k0 = 0;
-    const size_t ring_stride = (size_t)gridDim.x * kRingW;
+    const size_t ring_stride = (size_t)gridDim.x * kWarps * kRingW;
     // early first pairs pay on the uint16-index graphs (C2: -2%); with int32
     // indices the pair held across the barrier costs spills (C3: +4%)
     constexpr bool kEarly = sizeof(TI) == 2;
@@ -1008,7 +986,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     GN_CUDA(ws.alloc(&dfb, 8 * (size_t)iters));
     GN_CUDA(ws.alloc(&dbad, 4 * (size_t)iters));
     GN_CUDA(ws.alloc(&dots, 8 * 4 * (size_t)(iters + 1)));
-    GN_CUDA(ws.alloc(&ring, 8 * (size_t)kRingW * (size_t)std::min(kRing, iters + 1) * grid));
+    GN_CUDA(ws.alloc(&ring, 8 * (size_t)kRingW * (size_t)std::min(kRing, iters + 1) * grid * kWarps));
     GN_CUDA(ws.alloc(&status, 4 * sizeof(int)));
     GN_CUDA(ws.alloc(&barrier, sizeof(unsigned int)));
     GN_CUDA(ws.alloc(&chk, 2 * sizeof(int)));
