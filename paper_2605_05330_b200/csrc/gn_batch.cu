@@ -10,7 +10,8 @@
 //
 // Per CTA (graph b), once: local rows relabeled by degree (descending,
 // stable), cut into groups of 32 rows (one per lane of a warp); neighbour
-// lists (local uint16 ids, the reference's neighbour order) stored
+// lists (uint16 byte offsets of the neighbours' published values, the
+// reference's neighbour order) stored
 // position-major in pairs so a lane fetches positions p, p+1 with one 32-bit
 // shared load and a warp's fetch is 128 contiguous bytes.  Each thread owns
 // up to kRowsPerThread rows (dealt snake-wise over the degree order) whose
@@ -51,7 +52,7 @@ struct BatchLayout {
 };
 
 static int build_batch_layout(int64_t B, const int64_t* offsets, int64_t n, const int64_t* indptr,
-                              const int32_t* indices, BatchLayout& L) {
+                              const int32_t* indices, int gsz, BatchLayout& L) {
     L.B = B;
     L.n = n;
     L.voff.assign(offsets, offsets + B + 1);
@@ -61,7 +62,7 @@ static int build_batch_layout(int64_t B, const int64_t* offsets, int64_t n, cons
     L.lperm.assign((size_t)n, 0);
     for (int64_t b = 0; b < B; ++b) {
         const int64_t v0 = offsets[b], v1 = offsets[b + 1], nb = v1 - v0;
-        if (nb < 0 || nb > 65535) return fail(GN_ERR_ARG, "batch graph too large for the resident kernel");
+        if (nb < 0 || nb * gsz > 65535) return fail(GN_ERR_ARG, "batch graph too large for the resident kernel");
         std::vector<int32_t> order((size_t)nb);
         std::iota(order.begin(), order.end(), 0);
         auto dg = [&](int32_t l) { return indptr[v0 + l + 1] - indptr[v0 + l]; };
@@ -95,7 +96,8 @@ static int build_batch_layout(int64_t B, const int64_t* offsets, int64_t n, cons
                 const int64_t q = p - indptr[v0 + o];
                 const int64_t j = indices[p] - v0;
                 if (j < 0 || j >= nb) return fail(GN_ERR_ARG, "batch graphs must not share edges");
-                L.idx[base + (size_t)(go + (q / 2) * 64 + lane * 2 + (q % 2))] = (uint16_t)rank[(size_t)j];
+                // byte offset of the neighbour's published value (fits: nb * gsz < 2^16)
+                L.idx[base + (size_t)(go + (q / 2) * 64 + lane * 2 + (q % 2))] = (uint16_t)(rank[(size_t)j] * gsz);
             }
         }
     }
@@ -188,6 +190,9 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
     using A = Arith<TS>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TG* yc = s_y + cur * nb;
+    // neighbour ids are stored as byte offsets into the published values
+    const char* ycb = reinterpret_cast<const char*>(yc);
+    auto ldy = [ycb](uint32_t off) { return *reinterpret_cast<const TG*>(ycb + off); };
     TG* yn = s_y + (cur ^ 1) * nb;
     double mx = 0.0, acc[4] = {0.0, 0.0, 0.0, 0.0};
     unsigned int fbc = 0;
@@ -205,8 +210,8 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
         for (; p + 8 <= d; p += 8) {
             const uint32_t e0 = pi[(p / 2) * 32], e1 = pi[(p / 2 + 1) * 32];
             const uint32_t e2 = pi[(p / 2 + 2) * 32], e3 = pi[(p / 2 + 3) * 32];
-            const TG y0 = yc[e0 & 0xffff], y1 = yc[e0 >> 16], y2 = yc[e1 & 0xffff], y3 = yc[e1 >> 16];
-            const TG y4 = yc[e2 & 0xffff], y5 = yc[e2 >> 16], y6 = yc[e3 & 0xffff], y7 = yc[e3 >> 16];
+            const TG y0 = ldy(e0 & 0xffff), y1 = ldy(e0 >> 16), y2 = ldy(e1 & 0xffff), y3 = ldy(e1 >> 16);
+            const TG y4 = ldy(e2 & 0xffff), y5 = ldy(e2 >> 16), y6 = ldy(e3 & 0xffff), y7 = ldy(e3 >> 16);
             s = A::add(s, (TS)y0);
             s = A::add(s, (TS)y1);
             s = A::add(s, (TS)y2);
@@ -218,7 +223,7 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
         }
         for (; p < d; ++p) {
             const uint32_t e = pi[(p / 2) * 32];
-            s = A::add(s, (TS)yc[(p & 1) ? (e >> 16) : (e & 0xffff)]);
+            s = A::add(s, (TS)ldy((p & 1) ? (e >> 16) : (e & 0xffff)));
         }
         const TS yi = A::mul(R.v[q], R.x[q]);  // dynamics.py:104
         if (TRACE) {
@@ -406,7 +411,7 @@ int batch_create(int64_t B, const int64_t* offsets, int64_t n, const int64_t* in
     const int64_t nnz = n > 0 ? indptr[n] : 0;
     if (nnz >= (int64_t(1) << 31)) return fail(GN_ERR_ARG, "batch too large");
     BatchLayout L;
-    int rc = build_batch_layout(B, offsets, n, indptr, indices, L);
+    int rc = build_batch_layout(B, offsets, n, indptr, indices, (int)gather_bytes(dtype), L);
     if (rc) return rc;
     if (L.max_n > (int64_t)kBatchThreads * kRowsPerThread)
         return fail(GN_ERR_ARG, "batch graph has more vertices than the resident kernel holds");
