@@ -131,3 +131,28 @@ def test_c5_scale18_hot_cache_exact_bitwise():
     rf = P.run_engine(inst.graph, inst.x0, s, dtype="fp32", gammas=tab)
     np.testing.assert_allclose(rf.x, ref.x, rtol=0, atol=1e-5)
     assert np.array_equal(np.array(rf.trace.fallbacks), ref.fallbacks)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_results_independent_of_grid(dtype):
+    # pieces have fixed sizes, so the summation tree -- and every bit -- must
+    # not depend on how many CTAs run: with 1 or 3 CTAs a CTA holds far more
+    # pieces than one phase's slots (phases of 64), with 148 it holds few
+    inst = G.c3_ba()
+    g = inst.graph
+    s = P.GammaSchedule.pursuit(iterations=150)
+    h = g.device_graph(dtype)
+    outs = []
+    try:
+        for grid in (1, 3, 0):
+            h.set_grid(grid)
+            r = P.run_engine(g, inst.x0, s, dtype=dtype)
+            outs.append((r.x, np.asarray(r.trace.step_inf), np.asarray(r.trace.fallbacks)))
+    finally:
+        h.set_grid(0)
+    for x, si, fb in outs[1:]:
+        assert np.array_equal(x, outs[0][0])
+        assert np.array_equal(si, outs[0][1]) and np.array_equal(fb, outs[0][2])
+    ref = O.run(g, inst.x0, s.table(), s.final_gamma, threads=THREADS)
+    tol = 1e-9 if dtype == "fp64" else 1e-3
+    assert np.max(np.abs(outs[0][0] - ref.x)) <= tol
