@@ -217,6 +217,15 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf,
 int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c,
                 uint64_t seed, int device, int64_t* nnz, int64_t** indptr,
                 int32_t** indices);
+/* Canonical CSR (graph.py:78-124 build_graph, minus the weights) from an
+ * edge list u[m], v[m] (int64, any orientation, duplicates allowed) on the
+ * device: sort, deduplicate, symmetrise, sort.  Returns GN_ERR_ARG with
+ * *first_bad = the first edge (input order) that leaves [0, n) or is a
+ * self-loop.  *indptr_out (n+1 int64) / *indices_out (nnz int32) are
+ * released with gn_free_host. */
+int gn_csr_from_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                      int device, int64_t* first_bad, int64_t* nnz_out,
+                      int64_t** indptr_out, int32_t** indices_out);
 void gn_free_host(void* p);
 
 #ifdef __cplusplus

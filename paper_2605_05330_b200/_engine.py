@@ -78,6 +78,7 @@ EXPORTED = (
     "gn_part_unpack",
     "gn_part_end",
     "gn_gen_rmat",
+    "gn_csr_from_edges",
     "gn_free_host",
 )
 
@@ -163,6 +164,7 @@ _SIGNATURES = {
     "gn_part_end": (_I32, [_P, _I32, _P, _P, _P, _P, _PI]),
     "gn_gen_rmat": (_I32, [_I32, _I32, _D, _D, _D, ctypes.c_uint64, _I32, _PI64, ctypes.POINTER(_P),
                            ctypes.POINTER(_P)]),
+    "gn_csr_from_edges": (_I32, [_I64, _I64, _P, _P, _I32, _PI64, _PI64, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
     "gn_free_host": (None, [_P]),
 }
 

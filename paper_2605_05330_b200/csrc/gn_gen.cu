@@ -43,6 +43,22 @@ __global__ void k_rmat_keys(int64_t ne, int scale, double a, double ab, double a
     }
 }
 
+// Edge list -> undirected keys (min * n + max); the first edge (input order)
+// that leaves [0, n) or is a self-loop is recorded (graph.py:98-108).
+__global__ void k_edge_keys(int64_t m, uint64_t n, const int64_t* __restrict__ u, const int64_t* __restrict__ v,
+                            uint64_t* __restrict__ keys, unsigned long long* __restrict__ first_bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = u[e], b = v[e];
+        if (a < 0 || b < 0 || (uint64_t)a >= n || (uint64_t)b >= n || a == b) {
+            atomicMin(first_bad, (unsigned long long)e);
+            keys[e] = 0;
+            continue;
+        }
+        const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+        keys[e] = lo * n + hi;
+    }
+}
+
 // unique undirected key -> both directed keys (row * n + col)
 __global__ void k_symmetrize(int64_t m, uint64_t n, const uint64_t* __restrict__ ukeys, uint64_t* __restrict__ dkeys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
@@ -68,30 +84,19 @@ __global__ void k_csr(int64_t nnz, uint64_t n, const uint64_t* __restrict__ keys
     }
 }
 
-}  // namespace gn
-
-using namespace gn;
-
-extern "C" {
-
-int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed, int device,
-                int64_t* nnz_out, int64_t** indptr_out, int32_t** indices_out) {
-    *nnz_out = 0;
-    *indptr_out = nullptr;
-    *indices_out = nullptr;
-    if (scale < 1 || scale > 30 || edge_factor < 1) return fail(GN_ERR_ARG, "bad R-MAT parameters");
-    CallCtx ctx;
-    int rc = ctx.open(device);
-    if (rc) return rc;
-    cudaStream_t s = ctx.s;
-    const uint64_t n = 1ull << scale;
-    const int64_t ne = (int64_t)n * edge_factor;
-    uint64_t *k0 = nullptr, *k1 = nullptr, *d0 = nullptr, *d1 = nullptr;
+// Undirected edge keys (k0, ne of them, device; freed here) -> canonical
+// CSR on the host: sort, unique, drop the self-loop marker ~0, symmetrise,
+// sort again, row pointers.  *indptr_out / *indices_out are malloc'd.
+static int keys_to_csr(cudaStream_t s, uint64_t n, uint64_t* k0, int64_t ne, int64_t* nnz_out,
+                       int64_t** indptr_out, int32_t** indices_out) {
+    uint64_t *k1 = nullptr, *d0 = nullptr, *d1 = nullptr;
     int64_t* dcount = nullptr;
+    int64_t* dindptr = nullptr;
+    int32_t* dcol = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0, t2 = 0;
     auto cleanup = [&]() {
-        void* ptrs[] = {k0, k1, d0, d1, dcount, tmp};
+        void* ptrs[] = {k0, k1, d0, d1, dcount, tmp, dindptr, dcol};
         for (void* p : ptrs)
             if (p) cudaFree(p);
     };
@@ -103,30 +108,29 @@ int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64
             return cuda_fail(_e, #expr, __FILE__, __LINE__);                        \
         }                                                                           \
     } while (0)
-    GN_G(cudaMalloc(&k0, 8 * (size_t)ne));
-    GN_G(cudaMalloc(&k1, 8 * (size_t)ne));
-    GN_G(cudaMalloc(&dcount, 8));
     const int threads = 256, blocks = 148 * 16;
-    k_rmat_keys<<<blocks, threads, 0, s>>>(ne, scale, a, a + b, a + b + c, seed << 40, k0);
-    GN_G(cudaGetLastError());
-    note_launch();
-    const int bits = 2 * scale;
+    int bits = 1;
+    while (bits < 64 && (n * n) >> bits) ++bits;  // keys < n^2 (plus the marker ~0)
+    GN_G(cudaMalloc(&k1, 8 * (size_t)std::max<int64_t>(ne, 1)));
+    GN_G(cudaMalloc(&dcount, 8));
     GN_G(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k0, k1, ne, 0, 64, s));
     GN_G(cub::DeviceSelect::Unique(nullptr, t2, k1, k0, dcount, ne, s));
     tmp_bytes = std::max(tmp_bytes, t2);
-    GN_G(cudaMalloc(&tmp, tmp_bytes));
-    GN_G(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, k0, k1, ne, 0, 64, s));
-    note_launch();
-    GN_G(cub::DeviceSelect::Unique(tmp, tmp_bytes, k1, k0, dcount, ne, s));
-    note_launch();
+    GN_G(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
     int64_t nu = 0;
-    GN_G(cudaMemcpyAsync(&nu, dcount, 8, cudaMemcpyDeviceToHost, s));
-    GN_G(cudaStreamSynchronize(s));
-    // the self-loop marker ~0 sorts last: drop it
-    if (nu > 0) {
-        uint64_t last = 0;
-        GN_G(cudaMemcpy(&last, k0 + (nu - 1), 8, cudaMemcpyDeviceToHost));
-        if (last == ~0ull) --nu;
+    if (ne > 0) {
+        GN_G(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, k0, k1, ne, 0, 64, s));
+        note_launch();
+        GN_G(cub::DeviceSelect::Unique(tmp, tmp_bytes, k1, k0, dcount, ne, s));
+        note_launch();
+        GN_G(cudaMemcpyAsync(&nu, dcount, 8, cudaMemcpyDeviceToHost, s));
+        GN_G(cudaStreamSynchronize(s));
+        // the self-loop marker ~0 sorts last: drop it
+        if (nu > 0) {
+            uint64_t last = 0;
+            GN_G(cudaMemcpy(&last, k0 + (nu - 1), 8, cudaMemcpyDeviceToHost));
+            if (last == ~0ull) --nu;
+        }
     }
     cudaFree(k1);
     k1 = nullptr;
@@ -152,8 +156,6 @@ int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64
     k0 = nullptr;
     cudaFree(d0);
     d0 = nullptr;
-    int64_t* dindptr = nullptr;
-    int32_t* dcol = nullptr;
     GN_G(cudaMalloc(&dindptr, 8 * ((size_t)n + 1)));
     GN_G(cudaMalloc(&dcol, 4 * (size_t)std::max<int64_t>(nnz, 1)));
     if (nnz > 0) {
@@ -168,16 +170,12 @@ int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64
     if (!hptr || !hcol) {
         free(hptr);
         free(hcol);
-        cudaFree(dindptr);
-        cudaFree(dcol);
         cleanup();
-        return fail(GN_ERR_NOMEM, "host allocation for the generated graph failed");
+        return fail(GN_ERR_NOMEM, "host allocation for the CSR failed");
     }
     cudaError_t e1 = cudaMemcpyAsync(hptr, dindptr, 8 * ((size_t)n + 1), cudaMemcpyDeviceToHost, s);
     cudaError_t e2 = nnz ? cudaMemcpyAsync(hcol, dcol, 4 * (size_t)nnz, cudaMemcpyDeviceToHost, s) : cudaSuccess;
     cudaError_t e3 = cudaStreamSynchronize(s);
-    cudaFree(dindptr);
-    cudaFree(dcol);
     cleanup();
 #undef GN_G
     if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
@@ -189,6 +187,96 @@ int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64
     *indptr_out = hptr;
     *indices_out = hcol;
     return GN_OK;
+}
+
+}  // namespace gn
+
+using namespace gn;
+
+extern "C" {
+
+int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed, int device,
+                int64_t* nnz_out, int64_t** indptr_out, int32_t** indices_out) {
+    *nnz_out = 0;
+    *indptr_out = nullptr;
+    *indices_out = nullptr;
+    if (scale < 1 || scale > 30 || edge_factor < 1) return fail(GN_ERR_ARG, "bad R-MAT parameters");
+    CallCtx ctx;
+    int rc = ctx.open(device);
+    if (rc) return rc;
+    const uint64_t n = 1ull << scale;
+    const int64_t ne = (int64_t)n * edge_factor;
+    uint64_t* k0 = nullptr;
+    GN_CUDA(cudaMalloc(&k0, 8 * (size_t)ne));
+    k_rmat_keys<<<148 * 16, 256, 0, ctx.s>>>(ne, scale, a, a + b, a + b + c, seed << 40, k0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFree(k0);
+        return cuda_fail(e, "k_rmat_keys", __FILE__, __LINE__);
+    }
+    note_launch();
+    return keys_to_csr(ctx.s, n, k0, ne, nnz_out, indptr_out, indices_out);
+}
+
+int gn_csr_from_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v, int device, int64_t* first_bad,
+                      int64_t* nnz_out, int64_t** indptr_out, int32_t** indices_out) {
+    *nnz_out = 0;
+    *indptr_out = nullptr;
+    *indices_out = nullptr;
+    if (first_bad) *first_bad = -1;
+    if (n < 0 || m < 0 || (m > 0 && (!u || !v))) return fail(GN_ERR_ARG, "bad edge list");
+    if (n >= (int64_t(1) << 31)) return fail(GN_ERR_ARG, "vertex count must be below 2^31");
+    if (n == 0) {  // no vertex: any edge is out of range
+        if (m > 0) {
+            if (first_bad) *first_bad = 0;
+            return fail(GN_ERR_ARG, "edge endpoint out of range");
+        }
+        *indptr_out = (int64_t*)calloc(1, 8);
+        *indices_out = (int32_t*)calloc(1, 4);
+        return (*indptr_out && *indices_out) ? GN_OK : fail(GN_ERR_NOMEM, "host allocation failed");
+    }
+    CallCtx ctx;
+    int rc = ctx.open(device);
+    if (rc) return rc;
+    cudaStream_t s = ctx.s;
+    int64_t *du = nullptr, *dv = nullptr;
+    uint64_t* k0 = nullptr;
+    unsigned long long* dbad = nullptr;
+    auto release = [&]() {
+        void* ptrs[] = {du, dv, dbad};
+        for (void* p : ptrs)
+            if (p) cudaFree(p);
+    };
+    cudaError_t e;
+    const size_t mb = 8 * (size_t)std::max<int64_t>(m, 1);
+    if ((e = cudaMalloc(&du, mb)) != cudaSuccess || (e = cudaMalloc(&dv, mb)) != cudaSuccess ||
+        (e = cudaMalloc(&k0, mb)) != cudaSuccess || (e = cudaMalloc(&dbad, 8)) != cudaSuccess) {
+        release();
+        if (k0) cudaFree(k0);
+        return cuda_fail(e, "cudaMalloc", __FILE__, __LINE__);
+    }
+    unsigned long long none = ~0ull;
+    cudaMemcpyAsync(dbad, &none, 8, cudaMemcpyHostToDevice, s);
+    if (m > 0) {
+        cudaMemcpyAsync(du, u, 8 * (size_t)m, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dv, v, 8 * (size_t)m, cudaMemcpyHostToDevice, s);
+        k_edge_keys<<<148 * 16, 256, 0, s>>>(m, (uint64_t)std::max<int64_t>(n, 1), du, dv, k0, dbad);
+        note_launch();
+    }
+    unsigned long long hbad = none;
+    cudaMemcpyAsync(&hbad, dbad, 8, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    release();
+    if (e != cudaSuccess) {
+        cudaFree(k0);
+        return cuda_fail(e, "edge keys", __FILE__, __LINE__);
+    }
+    if (hbad != none) {  // graph.py:101-106: the caller reports the first offending edge
+        cudaFree(k0);
+        if (first_bad) *first_bad = (int64_t)hbad;
+        return fail(GN_ERR_ARG, "edge endpoint out of range or self-loop");
+    }
+    return keys_to_csr(s, (uint64_t)std::max<int64_t>(n, 1), k0, m, nnz_out, indptr_out, indices_out);
 }
 
 void gn_free_host(void* p) { free(p); }

@@ -11,6 +11,8 @@ vectorised numpy instead of the reference's per-edge Python loops
 
 from __future__ import annotations
 
+import ctypes
+
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass
@@ -182,6 +184,44 @@ class DeviceAdjacency:
         return self @ y
 
 
+# edge lists at least this long are turned into CSR on the GPU (gn_csr_from_edges)
+GPU_INGEST_MIN_EDGES = 1 << 20
+
+
+def _have_device() -> bool:
+    try:
+        return E.device_count() > 0
+    except E.EngineUnavailable:
+        return False
+
+
+def csr_from_edges_gpu(n: int, us, vs, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Canonical CSR built on the device (csrc/gn_gen.cu): sort, deduplicate,
+    symmetrise, sort -- identical to csr_from_edges.  Raises GraphError for
+    the first edge (input order) outside [0, n) or a self-loop."""
+    us = np.ascontiguousarray(us, dtype=np.int64)
+    vs = np.ascontiguousarray(vs, dtype=np.int64)
+    bad = ctypes.c_int64(-1)
+    nnz = ctypes.c_int64()
+    pp, pc = ctypes.c_void_p(), ctypes.c_void_p()
+    rc = E.lib().gn_csr_from_edges(n, len(us), E.ptr(us), E.ptr(vs), device, ctypes.byref(bad), ctypes.byref(nnz),
+                                   ctypes.byref(pp), ctypes.byref(pc))
+    if rc == E.GN_ERR_ARG and bad.value >= 0:
+        u, v = int(us[bad.value]), int(vs[bad.value])
+        if not (0 <= u < n and 0 <= v < n):
+            raise GraphError(f"edge ({u},{v}) has an endpoint outside [0,{n})")
+        raise GraphError(f"self-loop at vertex {u}")
+    E.check(rc)
+    try:
+        indptr = np.ctypeslib.as_array(ctypes.cast(pp, ctypes.POINTER(ctypes.c_int64)), shape=(n + 1,)).copy()
+        indices = (np.ctypeslib.as_array(ctypes.cast(pc, ctypes.POINTER(ctypes.c_int32)), shape=(nnz.value,))
+                   .astype(np.int64) if nnz.value else np.zeros(0, np.int64))
+    finally:
+        E.lib().gn_free_host(pp)
+        E.lib().gn_free_host(pc)
+    return indptr, indices
+
+
 def csr_from_edges(n: int, us: np.ndarray, vs: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     """Canonical symmetric CSR (sorted rows, no duplicates) from edge endpoints.
 
@@ -224,6 +264,10 @@ def build_graph(
         raise GraphError(f"weight of vertex {bad} must be positive and finite, got {w[bad]}")
     if isinstance(edges, np.ndarray):
         e = edges.astype(np.int64).reshape(-1, 2)
+        if len(e) >= GPU_INGEST_MIN_EDGES and _have_device():
+            # large edge lists: validation, dedup, symmetrisation and CSR on the device
+            indptr, indices = csr_from_edges_gpu(n, e[:, 0], e[:, 1])
+            return WeightedGraph(n, indptr, indices, w)
     else:
         lst = [(int(u), int(v)) for u, v in edges]
         e = np.array(lst, dtype=np.int64).reshape(-1, 2) if lst else np.zeros((0, 2), np.int64)
