@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gn_internal.cuh"
@@ -220,8 +221,9 @@ struct Layout {
     std::vector<int64_t> slice_ptr;
     std::vector<int32_t> row_deg;
     std::vector<int32_t> hub_ptr, hub_col;
-    std::vector<int32_t> sell32;
+    std::vector<int32_t> sell32, sell32s;   // sell32s / hub_cols: rows in ascending new id (fast mode)
     std::vector<uint16_t> sell16;
+    std::vector<int32_t> hub_cols;
     int idx16 = 0;
     int sentinel = 0;  // 1: padding positions hold id n (a vertex whose published value is always 0)
     int32_t maxdeg = 0;
@@ -233,6 +235,38 @@ static inline uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
+}
+
+// Fast-mode copies of the int32-id adjacency (sell32s, hub_cols): every row's
+// neighbours in ascending NEW id.  With the degree order of the relabeling the
+// lanes of a warp then gather their hottest neighbours at the same positions,
+// from the same few lines (C5 scale 24: 1.84 -> 1.75 ms/iteration).  The sum
+// order changes, so EXACT runs keep the reference-order arrays.
+static void build_sorted_copies(int64_t n, int B, Layout& L) {
+    L.sell32s = L.sell32;
+    L.hub_cols = L.hub_col;
+    const int64_t nreg = n - L.nhub;
+    const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    auto work = [&](int t) {
+        std::vector<int32_t> buf;
+        for (int32_t h = t; h < L.nhub; h += nt)
+            std::sort(L.hub_cols.begin() + L.hub_ptr[h], L.hub_cols.begin() + L.hub_ptr[h + 1]);
+        for (int32_t s = t; s < L.nslices; s += nt)
+            for (int l = 0; l < kSlice; ++l) {
+                const int64_t r = (int64_t)s * kSlice + l;
+                if (r >= nreg) continue;
+                const int d = L.row_deg[(size_t)r];
+                auto at = [&](int q) { return L.slice_ptr[s] + (q / B) * (kSlice * B) + (int64_t)l * B + q % B; };
+                buf.resize((size_t)d);
+                for (int q = 0; q < d; ++q) buf[(size_t)q] = L.sell32s[(size_t)at(q)];
+                std::sort(buf.begin(), buf.end());
+                for (int q = 0; q < d; ++q) L.sell32s[(size_t)at(q)] = buf[(size_t)q];
+            }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
 }
 
 static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indices, bool global_sort, Layout& L) {
@@ -249,7 +283,15 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
     // locality; a uniform-degree graph keeps its numbering) -- or globally,
     // when the hot-vertex cache is on, so the smallest new ids (the cached
     // ones) are the most gathered vertices
-    const size_t win = global_sort ? std::max<size_t>(regular.size(), 1) : (size_t)kSigma;
+    size_t win = global_sort ? std::max<size_t>(regular.size(), 1) : (size_t)kSigma;
+    // skewed degrees on an int32-id graph (power-law: BA, R-MAT): one global
+    // degree order, so the most gathered vertices share cache lines
+    if (n > 65536 && L.maxdeg > 8 * std::max<int64_t>(1, indptr[n] / std::max<int64_t>(n, 1)))
+        win = std::max<size_t>(regular.size(), 1);
+    if (const char* e = getenv("GN_SORT_WINDOW")) {
+        long long wv = atoll(e);
+        win = wv <= 0 ? std::max<size_t>(regular.size(), 1) : (size_t)wv;
+    }
     for (size_t w0 = 0; w0 < regular.size(); w0 += win) {
         size_t w1 = std::min(regular.size(), w0 + win);
         std::stable_sort(regular.begin() + w0, regular.begin() + w1,
@@ -355,6 +397,7 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
             }
         }
     }
+    if (!L.idx16 && !getenv("GN_NO_SORTED")) build_sorted_copies(n, B, L);
 }
 
 template <typename T>
@@ -377,7 +420,7 @@ static void free_graph(gn_graph* g) {
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
     void* ptrs[] = {g->rowptr, g->col, g->w64, g->perm, g->inv, g->v, g->w,
-                    g->hub_ptr, g->hub_col, g->slice_ptr, g->row_deg, g->sell};
+                    g->hub_ptr, g->hub_col, g->slice_ptr, g->row_deg, g->sell, g->sell_fast, g->hub_col_fast};
     for (void* p : ptrs) cudaFree(p);
     if (prev >= 0) cudaSetDevice(prev);
     delete g;
@@ -495,6 +538,11 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
         int32_t* p = nullptr;
         GN_UP(p, L.sell32.data(), (int64_t)L.sell32.size(), int32_t);
         g->sell = p;
+        if (!L.sell32s.empty()) {
+            GN_UP(p, L.sell32s.data(), (int64_t)L.sell32s.size(), int32_t);
+            g->sell_fast = p;
+            GN_UP(g->hub_col_fast, L.hub_cols.data(), (int64_t)L.hub_cols.size(), int32_t);
+        }
     }
     GN_TRY(cudaMalloc(&g->v, es * nb));
     GN_TRY(cudaMalloc(&g->w, es * nb));

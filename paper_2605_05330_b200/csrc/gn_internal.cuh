@@ -90,6 +90,8 @@ struct gn_graph {
     int64_t* slice_ptr = nullptr;  // nslices+1 element offsets (multiples of 32*B)
     int32_t* row_deg = nullptr;    // degree per slice row (n - nhub)
     void* sell = nullptr;          // int32 or uint16 new ids, position-major
+    void* sell_fast = nullptr;     // int32 ids only: rows in ascending new id (fast mode; null: use sell)
+    int32_t* hub_col_fast = nullptr;  // the same for hub_col
     int idx16 = 0;                 // 1: sell holds uint16 ids (n <= 65536); else int32 ids, padding = id n
     int64_t sell_elems = 0;
     std::vector<uint64_t> slice_sig;  // host: per-slice MinHash (gn_graph.cu, used by the plan)

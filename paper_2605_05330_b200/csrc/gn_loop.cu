@@ -1033,10 +1033,12 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     a.n = n;
     a.nhub = g->nhub;
     a.hub_ptr = g->hub_ptr;
-    a.hub_col = g->hub_col;
+    // fast mode reads the rows in ascending new id when the graph has that copy
+    const bool fast_layout = !exact && g->sell_fast;
+    a.hub_col = fast_layout ? g->hub_col_fast : g->hub_col;
     a.slice_ptr = g->slice_ptr;
     a.row_deg = g->row_deg;
-    a.sell = g->sell;
+    a.sell = fast_layout ? g->sell_fast : g->sell;
     a.v = (const TS*)g->v;
     a.w = (const TS*)g->w;
     a.x[0] = xa;
