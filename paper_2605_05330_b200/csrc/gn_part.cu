@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "gn_internal.cuh"
@@ -38,11 +39,19 @@ struct gn_part {
     int32_t* order = nullptr;
     std::vector<int32_t> h_order;   // host copy (re-split by gn_part_set_boundary)
     std::vector<int32_t> h_rowptr;
+    std::vector<int32_t> h_col;     // host copy of col (the SELL is rebuilt by gn_part_set_boundary)
     int64_t n_bnd = 0;              // order[0, n_bnd): boundary rows
+    // blocked SELL of the rows after each range's long prefix: slices of 32
+    // consecutive order positions, block b of a slice holds, lane after lane,
+    // positions 4b..4b+3 of each row (one 16-byte load per lane, 512
+    // contiguous bytes per warp); padding names the zero-valued slot n_all
+    int32_t* sell = nullptr;
+    int64_t* slice_ptr = nullptr;   // [nslices+1] element offsets
+    int64_t sl0[2] = {0, 0}, nsl[2] = {0, 0};  // per range: first slice, slice count
     int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
     // per range (0 boundary, 1 interior), set by gn_part_begin
-    int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0};
-    int r_nbl[2] = {0, 0}, r_nblocks[2] = {0, 0};
+    int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0}, r_csr[2] = {0, 0};
+    int r_nbl[2] = {0, 0}, r_ncb[2] = {0, 0}, r_nblocks[2] = {0, 0};
     double* w64 = nullptr;      // n_own + n_ghost
     // run state
     int iters = 0;
@@ -99,16 +108,20 @@ __device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double*
     ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
 }
 
-// One step of the owned rows.  Blocks [0, nbl) split the n_long longest rows
-// over warps (lanes stride the positions, fixed butterfly fold: fast mode
-// only); the other blocks give one thread to each remaining row, rows taken
-// in degree-descending order so a warp's rows have similar lengths, summed
-// sequentially in the reference's order (bitwise) with 8 gathers in flight.
+// One step of the owned rows of one range.  Blocks [0, nbl) split the n_long
+// longest rows over warps (lanes stride the positions, fixed butterfly fold:
+// fast mode only); blocks [nbl, nbl + ncb) give one thread to each of the
+// next n_csr rows (the long rows of an EXACT run) reading the CSR; the other
+// blocks give one warp to each slice of the blocked SELL, one thread per row.
+// Every thread-per-row sum is sequential in the reference's order (bitwise),
+// with 8 gathers in flight and the next index vectors loading under them.
 template <typename TS, typename TG>
-__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, int64_t n_long, int nbl,
-                                                            const int32_t* __restrict__ order,
+__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int nbl, int64_t n_csr, int ncb,
+                                                            int64_t count, const int32_t* __restrict__ order,
                                                             const int32_t* __restrict__ rowptr,
                                                             const int32_t* __restrict__ col,
+                                                            const int32_t* __restrict__ sell,
+                                                            const int64_t* __restrict__ slice_ptr, int64_t nsl,
                                                             const double* __restrict__ w64, const TS* __restrict__ v,
                                                             const TS* __restrict__ x, TS* __restrict__ xo,
                                                             const TG* __restrict__ yg, TG* __restrict__ ygo,
@@ -137,10 +150,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, int64
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
             if (lane == 0) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
         }
-    } else {
-        const int64_t nrest = n_own - n_long;
-        for (int64_t q = (int64_t)(blockIdx.x - nbl) * blockDim.x + threadIdx.x; q < nrest;
-             q += (int64_t)(gridDim.x - nbl) * blockDim.x) {
+    } else if ((int)blockIdx.x < nbl + ncb) {
+        for (int64_t q = (int64_t)(blockIdx.x - nbl) * blockDim.x + threadIdx.x; q < n_csr;
+             q += (int64_t)ncb * blockDim.x) {
             const int64_t i = order[n_long + q];
             const int32_t rb = rowptr[i], re = rowptr[i + 1];
             TS s = TS(0);
@@ -154,6 +166,42 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_own, int64
             }
             for (; p < re; ++p) s = A::add(s, (TS)yg[col[p]]);
             part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+        }
+    } else {
+        const int64_t pos0 = n_long + n_csr;  // first order position of slice 0
+        const int64_t nw = (int64_t)(gridDim.x - nbl - ncb) * kWarpsPerBlock;
+        for (int64_t sl = (int64_t)(blockIdx.x - nbl - ncb) * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
+            const int64_t pos = pos0 + sl * 32 + lane;
+            const bool valid = pos < count;
+            const int64_t i = valid ? order[pos] : 0;
+            const int64_t e0 = slice_ptr[sl];
+            const int nblk = (int)((slice_ptr[sl + 1] - e0) / 128);
+            const uint4* base = reinterpret_cast<const uint4*>(sell + e0) + lane;
+            constexpr int NV = kPartUnroll / 4;  // index vectors per batch
+            uint4 cv[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? __ldg(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+            TS s = TS(0);
+            for (int b = 0; b < nblk; b += NV) {
+                uint4 nv[NV];
+#pragma unroll
+                for (int u = 0; u < NV; ++u)
+                    nv[u] = b + NV + u < nblk ? __ldg(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+                TG y[4 * NV];
+#pragma unroll
+                for (int u = 0; u < NV; ++u) {
+                    const bool in = b + u < nblk;
+                    y[4 * u + 0] = in ? __ldg(yg + cv[u].x) : TG(0);
+                    y[4 * u + 1] = in ? __ldg(yg + cv[u].y) : TG(0);
+                    y[4 * u + 2] = in ? __ldg(yg + cv[u].z) : TG(0);
+                    y[4 * u + 3] = in ? __ldg(yg + cv[u].w) : TG(0);
+                }
+#pragma unroll
+                for (int q = 0; q < 4 * NV; ++q) s = A::add(s, (TS)y[q]);  // padding adds +0.0: bits unchanged
+#pragma unroll
+                for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+            }
+            if (valid) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -260,6 +308,50 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     P->h_order = rb;
     P->h_order.insert(P->h_order.end(), ri.begin(), ri.end());
     if (n_own) GN_CUDA(cudaMemcpy(P->order, P->h_order.data(), 4 * (size_t)n_own, cudaMemcpyHostToDevice));
+    // blocked SELL of each range's rows after its long prefix
+    const int32_t pad = (int32_t)(P->n_own + P->n_ghost);
+    std::vector<int64_t> sp(1, 0);
+    const int64_t rs[2] = {0, P->n_bnd}, rc[2] = {P->n_bnd, n_own - P->n_bnd};
+    std::vector<int64_t> first;  // per slice: first order position
+    for (int r = 0; r < 2; ++r) {
+        P->sl0[r] = (int64_t)sp.size() - 1;
+        const int64_t p0 = rs[r] + P->long_fast[r], p1 = rs[r] + rc[r];
+        P->nsl[r] = (p1 - p0 + 31) / 32;
+        for (int64_t q = p0; q < p1; q += 32) {
+            int32_t len = 0;
+            for (int64_t t = q; t < std::min(p1, q + 32); ++t) len = std::max(len, deg(P->h_order[(size_t)t]));
+            first.push_back(q);
+            sp.push_back(sp.back() + (int64_t)(len + 3) / 4 * 128);
+        }
+    }
+    std::vector<int32_t> sell((size_t)std::max<int64_t>(sp.back(), 1), pad);
+    const int64_t nslices = (int64_t)first.size();
+    const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    auto fill = [&](int t) {
+        for (int64_t sl = t; sl < nslices; sl += nt) {
+            const int64_t q = first[(size_t)sl];
+            const int64_t end = q < P->n_bnd ? P->n_bnd : n_own;
+            for (int l = 0; l < 32 && q + l < end; ++l) {
+                const int32_t row = P->h_order[(size_t)(q + l)];
+                for (int32_t e = rp[(size_t)row]; e < rp[(size_t)row + 1]; ++e) {
+                    const int32_t pos = e - rp[(size_t)row];
+                    sell[(size_t)(sp[(size_t)sl] + (pos / 4) * 128 + l * 4 + pos % 4)] = P->h_col[(size_t)e];
+                }
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(fill, t);
+    fill(0);
+    for (auto& x : th) x.join();
+    cudaFree(P->sell);
+    cudaFree(P->slice_ptr);
+    P->sell = nullptr;
+    P->slice_ptr = nullptr;
+    GN_CUDA(cudaMalloc(&P->sell, 4 * sell.size()));
+    GN_CUDA(cudaMalloc(&P->slice_ptr, 8 * sp.size()));
+    GN_CUDA(cudaMemcpy(P->sell, sell.data(), 4 * sell.size(), cudaMemcpyHostToDevice));
+    GN_CUDA(cudaMemcpy(P->slice_ptr, sp.data(), 8 * sp.size(), cudaMemcpyHostToDevice));
     return GN_OK;
 }
 
@@ -315,6 +407,7 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
     if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
     if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
     P->h_rowptr = rp;
+    P->h_col.assign(indices, indices + nnz);
     if ((ce = cudaMalloc(&P->order, 4 * (size_t)std::max<int64_t>(n_own, 1))) != cudaSuccess) {
         delete P;
         return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
@@ -337,6 +430,8 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
+    cudaFree(p->sell);
+    cudaFree(p->slice_ptr);
     cudaFree(p->w64);
     if (p->own_stream) cudaStreamDestroy(p->own_stream);
     if (prev >= 0) cudaSetDevice(prev);
@@ -360,12 +455,18 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_count[r] = r ? p->n_own - p->n_bnd : p->n_bnd;
         p->r_long[r] = (flags & GN_EXACT) ? 0 : p->long_fast[r];
         p->r_nbl[r] = p->r_long[r] ? (int)std::min<int64_t>((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
-        p->r_nblocks[r] = p->r_count[r] ? p->r_nbl[r] + pblocks(p->r_count[r] - p->r_long[r]) : 0;
+        p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
+        p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
+        const int sblocks = (int)std::min<int64_t>((p->nsl[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 16);
+        p->r_nblocks[r] = p->r_count[r] ? p->r_nbl[r] + p->r_ncb[r] + std::max(sblocks, 1) : 0;
     }
     GN_CUDA(cudaMalloc(&p->x[0], es * nb));
     GN_CUDA(cudaMalloc(&p->x[1], es * nb));
-    GN_CUDA(cudaMalloc(&p->yg[0], gs * nb));
-    GN_CUDA(cudaMalloc(&p->yg[1], gs * nb));
+    // published values + the zero-valued padding slot n_all
+    GN_CUDA(cudaMalloc(&p->yg[0], gs * (nb + 1)));
+    GN_CUDA(cudaMalloc(&p->yg[1], gs * (nb + 1)));
+    GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 1)));
+    GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 1)));
     GN_CUDA(cudaMalloc(&p->v, es * nb));
     GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
     for (int r = 0; r < 2; ++r)
@@ -407,19 +508,22 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
     switch (p->dtype) {
         case GN_F64:
             k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
+                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const double*)p->yg[cur],
                 (double*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         case GN_F32:
             k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
+                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const float*)p->yg[cur],
                 (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         default:
             k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_count[r], p->r_long[r], p->r_nbl[r], ord, p->rowptr, p->col, p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
+                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1], (const float*)p->yg[cur],
                 (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
     }
