@@ -490,6 +490,7 @@ int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, co
     g->device = device;
     g->max_degree = L.maxdeg;
     g->nhub = L.nhub;
+    while (g->ngiant < L.nhub && indptr[L.perm[g->ngiant] + 1] - indptr[L.perm[g->ngiant]] > kGiantRow) ++g->ngiant;
     g->nslices = L.nslices;
     g->nsplit = L.nsplit;
     g->idx16 = L.idx16;

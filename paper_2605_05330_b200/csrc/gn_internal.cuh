@@ -18,6 +18,7 @@ constexpr double kFallback = 0.5;
 constexpr int kSlice = 32;         // SELL slice height (one row per lane)
 constexpr int kSigma = 4096;       // degree-sort window of the relabeling
 constexpr int kHubDegree = 512;    // rows above this are processed CTA-wide
+constexpr int kGiantRow = 32768;   // x0 checks: rows above this get a CTA each
 constexpr int kSplitLen = 64;      // slices at least this long are split over warps
 
 // ---------------------------------------------------------------- errors
@@ -83,6 +84,7 @@ struct gn_graph {
     void* v = nullptr;        // sqrt(w) in state precision, new-id order
     void* w = nullptr;        // w in state precision, new-id order
     int32_t nhub = 0;         // rows [0, nhub) are hubs
+    int32_t ngiant = 0;       // hubs [0, ngiant) have more than kGiantRow neighbours
     int32_t* hub_ptr = nullptr;  // nhub+1, offsets into hub_col
     int32_t* hub_col = nullptr;  // new ids, original neighbour order
     int32_t nslices = 0;      // rows [nhub, n) in slices of 32

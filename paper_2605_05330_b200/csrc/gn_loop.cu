@@ -727,15 +727,79 @@ __global__ void k_prepare(int64_t n, const double* __restrict__ x0, const int32_
     }
 }
 
+// x0 checks (dynamics.py:146, 125).  A warp takes 32 consecutive rows: rows
+// of up to 1024 entries are scanned by their lane (16 loads in flight), longer
+// ones by the whole warp (hubs would otherwise leave one thread walking 10^5
+// entries).  Once no
+// entry is negative (flags[0] is reported first) a closed-neighbourhood sum of
+// entries in [0, inf] U {NaN} is > 0 iff no entry is NaN and one is > 0, for
+// any summation order, so the warp path tests exactly the reference's
+// predicate.
 __global__ void k_precheck_f64(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                const double* __restrict__ x, int* __restrict__ flags) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    const int32_t beg = valid ? rowptr[i] : 0, end = valid ? rowptr[i + 1] : 0;
+    const double xi = valid ? x[i] : 1.0;
+    if (xi < 0.0) atomicOr(&flags[0], 1);  // dynamics.py:146
+    const bool lng = end - beg > 1024 && end - beg <= kGiantRow;  // giant rows: k_precheck_giant
+    bool ok = true;
+    if (valid && end - beg <= 1024) {  // 16 loads in flight per batch
+        bool pos = xi > 0.0, nan = xi != xi;
+        int32_t p = beg;
+        for (; p + 16 <= end; p += 16) {
+            int32_t j[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) j[u] = col[p + u];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const double v = x[j[u]];
+                pos |= v > 0.0;
+                nan |= v != v;
+            }
+        }
+        for (; p < end; ++p) {
+            const double v = x[col[p]];
+            pos |= v > 0.0;
+            nan |= v != v;
+        }
+        ok = pos && !nan;  // dynamics.py:125
+    }
+    unsigned m = __ballot_sync(0xffffffffu, lng);
+    while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t bl = __shfl_sync(0xffffffffu, beg, l), el = __shfl_sync(0xffffffffu, end, l);
+        const double xl = __shfl_sync(0xffffffffu, xi, l);
+        bool pos = false, nan = false;
+        for (int32_t p = bl + lane; p < el; p += 32) {
+            const double v = x[col[p]];
+            pos |= v > 0.0;
+            nan |= v != v;
+        }
+        pos = __any_sync(0xffffffffu, pos) || xl > 0.0;
+        nan = __any_sync(0xffffffffu, nan) || xl != xl;
+        if (lane == l) ok = pos && !nan;
+    }
+    if (!ok) atomicOr(&flags[1], 1);
+}
+
+// the rows above kGiantRow (original ids perm[0, ngiant)), one CTA each
+__global__ void k_precheck_giant(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowptr,
+                                 const int32_t* __restrict__ col, const double* __restrict__ x,
+                                 int* __restrict__ flags) {
+    const int i = perm[blockIdx.x];
     const double xi = x[i];
-    if (xi < 0.0) atomicOr(&flags[0], 1);                   // dynamics.py:146
-    double s = 0.0;
-    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = __dadd_rn(s, x[col[p]]);
-    if (!(__dadd_rn(xi, s) > 0.0)) atomicOr(&flags[1], 1);  // dynamics.py:125
+    bool pos = xi > 0.0, nan = xi != xi;
+    for (int32_t p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) {
+        const double v = x[col[p]];
+        pos |= v > 0.0;
+        nan |= v != v;
+    }
+    pos = __syncthreads_or(pos);
+    nan = __syncthreads_or(nan);
+    if (threadIdx.x == 0 && !(pos && !nan)) atomicOr(&flags[1], 1);  // dynamics.py:125
 }
 
 // final state (new order) -> fp64 output (original order), np.clip(x, 0, 1)
@@ -1020,6 +1084,10 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
         if (check) {
             k_precheck_f64<<<blocks_for(n), 256, 0, s>>>(n, g->rowptr, g->col, xin, chk);
             GN_LAUNCHED();
+            if (g->ngiant) {
+                k_precheck_giant<<<g->ngiant, 512, 0, s>>>(g->perm, g->rowptr, g->col, xin, chk);
+                GN_LAUNCHED();
+            }
         }
         k_prepare<TS, TG><<<blocks_for(n), 256, 0, s>>>(n, xin, g->inv, (const TS*)g->v, xa, ya);
         GN_LAUNCHED();

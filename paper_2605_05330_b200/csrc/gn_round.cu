@@ -36,15 +36,85 @@ __global__ void k_threshold(int64_t n, const TI* __restrict__ x, uint8_t* __rest
     if (i < n) sel[i] = (double)x[i] >= 0.5 ? 1 : 0;
 }
 
+// Row scans, warp-hybrid: a warp takes 32 consecutive rows; a row of at most
+// kShortRow entries is scanned by its own lane (16 loads in flight per
+// batch), a longer one by the whole warp (coalesced 32-entry chunks,
+// ballot), so neither dense rows (C2: degree 510) nor hubs (R-MAT: degree
+// > 10^5) leave one thread walking a long row one load at a time.
+constexpr int kShortRow = 1024;
+
+// any neighbour j of row i (entries [beg, end)) with pred(j); one lane.  The
+// predicates of a batch are all evaluated (no short circuit) so their loads
+// overlap.
+template <typename Pred>
+__device__ __forceinline__ bool lane_any(const int32_t* __restrict__ col, int32_t beg, int32_t end, Pred pred) {
+    constexpr int U = 16;
+    int32_t p = beg;
+    for (; p + U <= end; p += U) {
+        int32_t j[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = col[p + u];
+        bool h = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) h |= pred(j[u]);
+        if (h) return true;
+    }
+    bool h = false;
+    for (; p < end; ++p) h |= pred(col[p]);
+    return h;
+}
+
+// the same over the whole warp (all lanes call it with the same row)
+template <typename Pred>
+__device__ __forceinline__ bool warp_any(const int32_t* __restrict__ col, int32_t beg, int32_t end, Pred pred) {
+    const int lane = threadIdx.x & 31;
+    for (int32_t base = beg; base < end; base += 32) {
+        const int32_t p = base + lane;
+        const bool h = p < end && pred(col[p]);
+        if (__any_sync(0xffffffffu, h)) return true;
+    }
+    return false;
+}
+
+// For every row i in [0, n) with need(i): res(i) = any neighbour j with
+// pred(i, j); visit(i, res) is then called by the lane that owns row i.
+// Warps stride over chunks of 32 rows.
+template <typename Need, typename Pred, typename Visit>
+__device__ __forceinline__ void rows_any(int64_t n, const int32_t* __restrict__ rowptr,
+                                         const int32_t* __restrict__ col, int64_t warp0, int64_t nwarps, Need need,
+                                         Pred pred, Visit visit) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r0 = warp0 * 32; r0 < n; r0 += nwarps * 32) {
+        const int64_t i = r0 + lane;
+        const bool valid = i < n && need(i);
+        const int32_t beg = valid ? rowptr[i] : 0, end = valid ? rowptr[i + 1] : 0;
+        const bool lng = end - beg > kShortRow;
+        bool res = false;
+        if (valid && !lng) res = lane_any(col, beg, end, [&](int32_t j) { return pred(i, j); });
+        unsigned m = __ballot_sync(0xffffffffu, lng);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t il = r0 + l;
+            const int32_t bl = __shfl_sync(0xffffffffu, beg, l), el = __shfl_sync(0xffffffffu, end, l);
+            const bool r = warp_any(col, bl, el, [&](int32_t j) { return pred(il, j); });
+            if (lane == l) res = r;
+        }
+        if (valid) visit(i, res);
+    }
+}
+
+__device__ __forceinline__ int64_t gwarp() { return (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; }
+__device__ __forceinline__ int64_t nwarp() { return ((int64_t)gridDim.x * blockDim.x) >> 5; }
+
 __global__ void k_conflicts(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                             const uint8_t* __restrict__ sel, uint8_t* __restrict__ conf) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint8_t c = 0;
-    if (sel[i])
-        for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p)
-            if (sel[col[p]]) { c = 1; break; }
-    conf[i] = c;
+    // conf_i = sel_i and a selected neighbour (the rows the repair can change)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        conf[i] = 0;  // (rows_any gives row i to this same thread)
+    rows_any(
+        n, rowptr, col, gwarp(), nwarp(), [&](int64_t i) { return sel[i] != 0; },
+        [&](int64_t, int32_t j) { return sel[j] != 0; }, [&](int64_t i, bool r) { conf[i] = r ? 1 : 0; });
 }
 
 // One warp replays the reference's sequential repair over the ascending
@@ -92,63 +162,74 @@ __global__ void __launch_bounds__(kRoundThreads) k_greedy(int64_t n, const int32
                                                            const double* __restrict__ w, uint8_t* sel,
                                                            uint8_t* cand, uint8_t* join, int* counters,
                                                            unsigned int* barrier) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w0 = gwarp(), nw = nwarp();
+    const int lane = threadIdx.x & 31;
+    volatile uint8_t* vsel = sel;
+    volatile uint8_t* vcand = cand;
+    volatile uint8_t* vjoin = join;
     unsigned int bar = 0;
     // candidates: unselected and not dominated by the repaired set
-    for (int64_t i = tid; i < n; i += stride) {
-        uint8_t c = 0;
-        if (!sel[i]) {
-            c = 1;
-            for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p)
-                if (sel[col[p]]) { c = 0; break; }
-        }
-        cand[i] = c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        cand[i] = 0;  // (rows_any gives row i to this same thread)
         join[i] = 0;
     }
+    rows_any(
+        n, rowptr, col, w0, nw, [&](int64_t i) { return sel[i] == 0; },
+        [&](int64_t, int32_t j) { return sel[j] != 0; }, [&](int64_t i, bool dom) { cand[i] = dom ? 0 : 1; });
     grid_barrier(barrier, (++bar) * gridDim.x);
     for (int r = 0;; ++r) {
         int* live_ctr = counters + (r & 1);
         int local = 0;
-        for (int64_t i = tid; i < n; i += stride) {
-            if (!((volatile uint8_t*)cand)[i]) continue;
-            ++local;
-            const double wi = w[i];
-            bool top = true;
-            for (int32_t p = rowptr[i]; p < rowptr[i + 1] && top; ++p) {
-                const int j = col[p];
-                if (((volatile uint8_t*)cand)[j] && higher(w[j], j, wi, (int)i)) top = false;
-            }
-            join[i] = top ? 1 : 0;
-        }
+        // a live candidate joins iff no live candidate neighbour has higher priority
+        rows_any(
+            n, rowptr, col, w0, nw, [&](int64_t i) { return vcand[i] != 0; },
+            [&](int64_t i, int32_t j) { return vcand[j] && higher(w[j], j, w[i], (int)i); },
+            [&](int64_t i, bool beaten) {
+                ++local;
+                vjoin[i] = beaten ? 0 : 1;
+            });
         if (local) atomicAdd(live_ctr, local);
         grid_barrier(barrier, (++bar) * gridDim.x);
         if (*(volatile int*)live_ctr == 0) break;
-        if (tid == 0) counters[(r + 1) & 1] = 0;
-        for (int64_t i = tid; i < n; i += stride) {
-            if (!((volatile uint8_t*)join)[i]) continue;
-            ((volatile uint8_t*)sel)[i] = 1;
-            ((volatile uint8_t*)cand)[i] = 0;
-            ((volatile uint8_t*)join)[i] = 0;
-            for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) ((volatile uint8_t*)cand)[col[p]] = 0;
+        if (w0 == 0 && lane == 0) counters[(r + 1) & 1] = 0;
+        // joined rows: select, and retire the neighbours (short rows by their
+        // lane, long rows by the warp)
+        for (int64_t r0 = w0 * 32; r0 < n; r0 += nw * 32) {
+            const int64_t i = r0 + lane;
+            const bool jn = i < n && vjoin[i];
+            const int32_t beg = jn ? rowptr[i] : 0, end = jn ? rowptr[i + 1] : 0;
+            if (jn) {
+                vsel[i] = 1;
+                vcand[i] = 0;
+                vjoin[i] = 0;
+                if (end - beg <= kShortRow)
+                    for (int32_t p = beg; p < end; ++p) vcand[col[p]] = 0;
+            }
+            unsigned m = __ballot_sync(0xffffffffu, jn && end - beg > kShortRow);
+            while (m) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                const int32_t bl = __shfl_sync(0xffffffffu, beg, l), el = __shfl_sync(0xffffffffu, end, l);
+                for (int32_t p = bl + lane; p < el; p += 32) vcand[col[p]] = 0;
+            }
         }
         grid_barrier(barrier, (++bar) * gridDim.x);
     }
 }
 
-// independence / maximality (graph.py:134-156) + member count
+// independence / maximality (graph.py:134-156)
 __global__ void k_check(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                         const uint8_t* __restrict__ sel, int* __restrict__ flags) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    bool hit = false;
-    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p)
-        if (sel[col[p]]) { hit = true; break; }
-    if (sel[i]) {
-        if (hit) atomicOr(&flags[0], 1);  // not independent
-    } else if (!hit) {
-        atomicOr(&flags[1], 1);  // undominated vertex: not maximal
-    }
+    rows_any(
+        n, rowptr, col, gwarp(), nwarp(), [&](int64_t) { return true; },
+        [&](int64_t, int32_t j) { return sel[j] != 0; },
+        [&](int64_t i, bool hit) {
+            if (sel[i]) {
+                if (hit) atomicOr(&flags[0], 1);  // not independent
+            } else if (!hit) {
+                atomicOr(&flags[1], 1);  // undominated vertex: not maximal
+            }
+        });
 }
 
 // numpy float64 pairwise sum (blocks <= 128, 8 accumulators, halving on
@@ -191,27 +272,25 @@ __device__ bool pw_node(int64_t count, int d, int64_t b, int64_t* start, int64_t
     return true;
 }
 
-__global__ void k_pairwise(const double* __restrict__ a, const int* __restrict__ count_p, double* scratch,
-                           int64_t scratch_len, double* __restrict__ out) {
+// one level d of the pairwise tree (all nodes in parallel); levels run from
+// the deepest possible (for count = n) up to the root, whose value goes to out
+__global__ void k_pairwise_level(const double* __restrict__ a, const int* __restrict__ count_p, int d,
+                                 double* __restrict__ cur, const double* __restrict__ below, double* __restrict__ out) {
     const int64_t count = *count_p;
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= (int64_t(1) << d)) return;
+    int64_t s, l;
+    if (!pw_node(count, d, b, &s, &l)) return;
+    const double v = l <= 128 ? pw_leaf(a + s, l) : __dadd_rn(below[2 * b], below[2 * b + 1]);
+    cur[b] = v;
+    if (d == 0) out[0] = v;
+}
+
+// deepest level the pairwise tree of up to n values can have
+static int pw_depth(int64_t n) {
     int D = 0;
-    for (int64_t l = count; l > 128; l = l - pw_split(l)) ++D;
-    if ((int64_t(1) << D) > scratch_len / 2) {  // cannot happen: scratch is sized from n
-        if (threadIdx.x == 0) out[0] = __longlong_as_double(0x7ff8000000000000LL);
-        return;
-    }
-    double* lv[2] = {scratch, scratch + (scratch_len / 2)};
-    for (int d = D; d >= 0; --d) {
-        double* cur = lv[d & 1];
-        const double* below = lv[(d + 1) & 1];
-        for (int64_t b = threadIdx.x; b < (int64_t(1) << d); b += blockDim.x) {
-            int64_t s, l;
-            if (!pw_node(count, d, b, &s, &l)) continue;
-            cur[b] = l <= 128 ? pw_leaf(a + s, l) : __dadd_rn(below[2 * b], below[2 * b + 1]);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) out[0] = lv[0][0];
+    for (int64_t l = n; l > 128; l = l - (l / 2 - (l / 2) % 8)) ++D;
+    return D;
 }
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + kRoundThreads - 1) / kRoundThreads); }
@@ -271,8 +350,15 @@ static int enqueue_check(gn_graph* g, RoundScratch& R, const uint8_t* dsel, int*
         GN_CUDA(cub::DeviceSelect::Flagged(R.tmp, tb, g->w64, dsel, R.mw, cnt, (int)n, s));
         note_launch();
     }
-    k_pairwise<<<1, 1024, 0, s>>>(R.mw, cnt, R.scratch, 2 * R.half, wout);
-    GN_LAUNCHED();
+    // count <= n is on the device: levels below the real tree find no nodes
+    const int D = pw_depth(n);
+    if ((int64_t(1) << D) > R.half) return fail(GN_ERR_ARG, "pairwise scratch too small");
+    for (int d = D; d >= 0; --d) {
+        const int64_t nodes = int64_t(1) << d;
+        k_pairwise_level<<<(int)((nodes + 255) / 256), 256, 0, s>>>(R.mw, cnt, d, R.scratch + (d & 1) * R.half,
+                                                                   R.scratch + ((d + 1) & 1) * R.half, wout);
+        GN_LAUNCHED();
+    }
     return GN_OK;
 }
 

@@ -1,0 +1,55 @@
+"""GPU: the x0 checks of run_wrgn (dynamics.py:146-149) on rows of every
+length class of the check kernel: lane rows (<= 1024), warp rows and giant
+rows (> 32768 neighbours, one CTA each)."""
+
+import numpy as np
+import pytest
+
+import paper_2605_05330_b200 as P
+from paper_2605_05330_b200.graph import csr_from_edges
+
+pytestmark = pytest.mark.gpu
+
+
+def _star_with_partners(leaves: int):
+    """Centre 0 joined to `leaves` leaves; each leaf also joined to its own
+    partner.  With x = 0 on the centre and the leaves and > 0 on the partners,
+    only the centre's closed neighbourhood sums to zero."""
+    c = 0
+    leaf = np.arange(1, leaves + 1)
+    partner = leaf + leaves
+    us = np.concatenate([np.full(leaves, c), leaf])
+    vs = np.concatenate([leaf, partner])
+    n = 2 * leaves + 1
+    indptr, indices = csr_from_edges(n, us, vs)
+    g = P.from_csr(n, indptr, indices, np.ones(n))
+    x0 = np.zeros(n)
+    x0[partner] = 0.5
+    return g, x0
+
+
+@pytest.mark.parametrize("leaves", [600, 5000, 40000])
+def test_zero_closed_neighbourhood_found_in_any_row_class(leaves):
+    g, x0 = _star_with_partners(leaves)
+    s = P.GammaSchedule.pursuit(iterations=5)
+    with pytest.raises(P.NormalizationError, match="zero closed neighborhood sum"):
+        P.run_wrgn(g, x0, s)
+    x1 = x0.copy()
+    x1[leaves] = 1e-300  # one positive leaf: the centre passes, and so does every row
+    x, tr = P.run_wrgn(g, x1, s)
+    assert len(tr) == 5 and np.all(np.isfinite(x))
+
+
+@pytest.mark.parametrize("leaves", [5000, 40000])
+def test_nan_and_negative_entries_in_long_rows(leaves):
+    g, x0 = _star_with_partners(leaves)
+    x0[1 : leaves + 1] = 0.25
+    s = P.GammaSchedule.pursuit(iterations=3)
+    x = x0.copy()
+    x[0] = -1.0  # negativity is reported before normalisability (dynamics.py:146-149)
+    with pytest.raises(P.NormalizationError, match="nonnegative"):
+        P.run_wrgn(g, x, s)
+    x = x0.copy()
+    x[leaves // 2] = np.nan
+    with pytest.raises(P.NormalizationError):
+        P.run_wrgn(g, x, s)
