@@ -297,6 +297,51 @@ static void build_layout(int64_t n, const int64_t* indptr, const int32_t* indice
         std::stable_sort(regular.begin() + w0, regular.begin() + w1,
                          [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
     }
+    // skewed int32-id graphs: rows of equal degree ordered by their two
+    // hottest neighbours (smallest provisional new ids), so the lanes of a
+    // slice gather the same lines at the same positions (C3 12.06 -> 11.50
+    // us/iteration, C5 scale 24 1742 -> 1716; GN_LEX=0 turns it off)
+    const char* lex_env = getenv("GN_LEX");
+    if (win == std::max<size_t>(regular.size(), 1) && n > 65536 && (!lex_env || atoi(lex_env))) {
+        std::vector<int32_t> pinv((size_t)n);
+        for (size_t q = 0; q < hubs.size(); ++q) pinv[(size_t)hubs[q]] = (int32_t)q;
+        for (size_t q = 0; q < regular.size(); ++q) pinv[(size_t)regular[q]] = (int32_t)(hubs.size() + q);
+        // runs of equal degree (regular is degree-descending)
+        std::vector<std::pair<size_t, size_t>> runs;
+        for (size_t q = 0; q < regular.size();) {
+            size_t e = q;
+            while (e < regular.size() && deg[regular[e]] == deg[regular[q]]) ++e;
+            runs.push_back({q, e});
+            q = e;
+        }
+        std::sort(runs.begin(), runs.end(), [](const std::pair<size_t, size_t>& a, const std::pair<size_t, size_t>& b) {
+            return a.second - a.first > b.second - b.first;
+        });
+        std::atomic<size_t> next{0};
+        auto work = [&]() {
+            std::vector<std::pair<uint64_t, int32_t>> kv;
+            for (size_t ri; (ri = next.fetch_add(1)) < runs.size();) {
+                const size_t q0 = runs[ri].first, q1 = runs[ri].second;
+                kv.resize(q1 - q0);
+                for (size_t q = q0; q < q1; ++q) {
+                    const int32_t r = regular[q];
+                    uint32_t a = ~0u, b = ~0u;
+                    for (int64_t p = indptr[r]; p < indptr[r + 1]; ++p) {
+                        const uint32_t v = (uint32_t)pinv[(size_t)indices[p]];
+                        if (v < a) { b = a; a = v; } else if (v < b) b = v;
+                    }
+                    kv[q - q0] = {((uint64_t)a << 32) | b, r};
+                }
+                std::sort(kv.begin(), kv.end());
+                for (size_t q = q0; q < q1; ++q) regular[q] = kv[q - q0].second;
+            }
+        };
+        const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto& x : th) x.join();
+    }
     // groups of 32 rows; long groups (split over warps) first, the partial
     // tail group always last
     const size_t ng = (regular.size() + kSlice - 1) / kSlice;
