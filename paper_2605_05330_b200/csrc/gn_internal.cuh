@@ -175,6 +175,8 @@ __device__ __forceinline__ void grid_wait(unsigned int* counter, unsigned int ta
 
 int coresident_blocks(const void* kernel, int threads, size_t smem, int device, int* out);
 void release_plans(const gn_graph* g);  // gn_loop.cu: cached launch plans of g
+// gn_loop.cu: the x0 checks of dynamics.py:146-149 on x (original order) into flags[0..1]
+int enqueue_precheck(const gn_graph* g, const double* x, int* flags, cudaStream_t s);
 void release_multi_plans(const gn_graph* g);  // gn_multi.cu: cached multi-start plans of g
 
 // gn_batch.cu: the resident (CTA-per-graph) kernel

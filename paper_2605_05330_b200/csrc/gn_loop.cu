@@ -818,6 +818,18 @@ __global__ void k_finalize(int64_t n, const TS* __restrict__ x0, const TS* __res
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, (n + 255) / 256); }
 
+int enqueue_precheck(const gn_graph* g, const double* x, int* flags, cudaStream_t s) {
+    if (g->n <= 0) return GN_OK;
+    k_precheck_f64<<<blocks_for(g->n), 256, 0, s>>>(g->n, g->rowptr, g->col, x, flags);
+    GN_LAUNCHED();
+    if (g->ngiant) {
+        k_precheck_giant<<<g->ngiant, 512, 0, s>>>(g->perm, g->rowptr, g->col, x, flags);
+        GN_LAUNCHED();
+    }
+    return GN_OK;
+}
+
+
 // ------------------------------------------------------------------ plan
 
 // Device copy of one HostPlan; built on first use and cached per (graph,
@@ -1082,12 +1094,7 @@ static int run_typed(gn_graph* g, const void* x0, const double* gammas, int iter
     const bool check = !(flags & GN_NO_CHECK);
     if (n > 0) {
         if (check) {
-            k_precheck_f64<<<blocks_for(n), 256, 0, s>>>(n, g->rowptr, g->col, xin, chk);
-            GN_LAUNCHED();
-            if (g->ngiant) {
-                k_precheck_giant<<<g->ngiant, 512, 0, s>>>(g->perm, g->rowptr, g->col, xin, chk);
-                GN_LAUNCHED();
-            }
+            if ((rc = enqueue_precheck(g, xin, chk, s))) return rc;
         }
         k_prepare<TS, TG><<<blocks_for(n), 256, 0, s>>>(n, xin, g->inv, (const TS*)g->v, xa, ya);
         GN_LAUNCHED();

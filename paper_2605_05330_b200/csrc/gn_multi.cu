@@ -443,17 +443,6 @@ __global__ void k_multi_finalize(int64_t n, int B, int Bp, const TS* __restrict_
     out[e] = xi;
 }
 
-__global__ void k_multi_precheck(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                 const double* __restrict__ x, int* __restrict__ flags) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double xi = x[i];
-    if (xi < 0.0) atomicOr(&flags[0], 1);  // dynamics.py:146
-    double s = 0.0;
-    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = __dadd_rn(s, x[col[p]]);
-    if (!(__dadd_rn(xi, s) > 0.0)) atomicOr(&flags[1], 1);  // dynamics.py:125
-}
-
 // ---- host plan (cached per graph, grid and mode) -------------------------
 // Fast mode splits rows longer than one warp's fair share over all teams of a
 // CTA (LPT over CTAs); the remaining rows, in the relabel order (degree-sorted:
@@ -673,8 +662,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     std::vector<int> hchk(2 * (size_t)B, 0), hskip((size_t)B, 0);
     if (!(flags & GN_NO_CHECK) && n > 0) {
         for (int b = 0; b < B; ++b) {
-            k_multi_precheck<<<blocks_of(n), 256, 0, s>>>(n, g->rowptr, g->col, xin + (size_t)b * n, chk + 2 * b);
-            GN_LAUNCHED();
+            if (int rc2 = enqueue_precheck(g, xin + (size_t)b * n, chk + 2 * b, s)) return rc2;
         }
         GN_CUDA(cudaMemcpyAsync(hchk.data(), chk, 8 * (size_t)B, cudaMemcpyDeviceToHost, s));
         GN_CUDA(cudaStreamSynchronize(s));

@@ -37,8 +37,15 @@ struct gn_part {
     // owned rows in processing order: the boundary rows (those peers hold as
     // ghosts) first, then the interior; each range degree-descending (stable)
     int32_t* order = nullptr;
-    std::vector<int32_t> h_order;   // host copy (re-split by gn_part_set_boundary)
-    std::vector<int32_t> h_rowptr;
+    std::vector<int32_t> h_rowptr;  // caller's local numbering
+    std::vector<double> h_w;        // n_own + n_ghost, caller's numbering
+    // owned rows are relabeled to their processing position (boundary range
+    // first, each range degree-descending): a row's state, weight and output
+    // are then read and written contiguously.  perm: new -> caller's id, inv:
+    // caller's -> new; ghosts keep their ids.  rowptr/col/w64 hold the
+    // relabeled graph (neighbour order unchanged: bitwise sums).
+    int32_t* perm = nullptr;
+    int32_t* inv = nullptr;
     std::vector<int32_t> h_col;     // host copy of col (the SELL is rebuilt by gn_part_set_boundary)
     int64_t n_bnd = 0;              // order[0, n_bnd): boundary rows
     // blocked SELL of the rows after each range's long prefix: slices of 32
@@ -70,12 +77,12 @@ constexpr int kPartThreads = 256;
 
 template <typename TS, typename TG>
 __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __restrict__ x0,
-                               const double* __restrict__ w64, TS* __restrict__ x, TS* __restrict__ v,
-                               TG* __restrict__ yg) {
+                               const int32_t* __restrict__ perm, const double* __restrict__ w64,
+                               TS* __restrict__ x, TS* __restrict__ v, TG* __restrict__ yg) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_all) return;
     const TS vi = (TS)sqrt(w64[i]);  // graph.py:42
-    const TS xi = (TS)x0[i];
+    const TS xi = (TS)x0[i < n_own ? (int64_t)perm[i] : i];  // x0 in the caller's numbering
     v[i] = vi;
     yg[i] = (TG)Arith<TS>::mul(vi, xi);
     if (i < n_own) x[i] = xi;
@@ -262,10 +269,10 @@ __global__ void k_part_fold(const double* __restrict__ part, int nblocks, int it
 }
 
 template <typename TG>
-__global__ void k_part_pack(const TG* __restrict__ yg, const int32_t* __restrict__ idx, int64_t count,
-                            TG* __restrict__ out) {
+__global__ void k_part_pack(const TG* __restrict__ yg, const int32_t* __restrict__ idx,
+                            const int32_t* __restrict__ inv, int64_t count, TG* __restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < count) out[i] = yg[idx[i]];
+    if (i < count) out[i] = yg[inv[idx[i]]];  // idx: the caller's owned ids
 }
 
 template <typename TG>
@@ -275,20 +282,41 @@ __global__ void k_part_unpack(TG* __restrict__ yg, int64_t first, const TG* __re
 }
 
 template <typename TS, typename TOut>
-__global__ void k_part_out(int64_t n, const TS* __restrict__ x, TOut* __restrict__ out) {
+__global__ void k_part_out(int64_t n, const TS* __restrict__ x, const int32_t* __restrict__ perm,
+                           TOut* __restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
         double xi = (double)x[i];
-        out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);  // dynamics.py:179
+        out[perm[i]] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);  // dynamics.py:179, caller's numbering
     }
 }
 
 static int pblocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kPartThreads - 1) / kPartThreads, 1 << 16)); }
 
+template <typename F>
+static void parallel_for(int64_t n, F f) {
+    const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back([&, t]() { for (int64_t i = t; i < n; i += nt) f(i); });
+    for (int64_t i = 0; i < n; i += nt) f(i);
+    for (auto& x : th) x.join();
+}
+
+template <typename T>
+static int upload_into(T** dst, const std::vector<T>& h) {
+    cudaFree(*dst);
+    *dst = nullptr;
+    GN_CUDA(cudaMalloc((void**)dst, sizeof(T) * std::max<size_t>(h.size(), 1)));
+    if (!h.empty()) GN_CUDA(cudaMemcpy(*dst, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return GN_OK;
+}
+
 // Processing order: rows listed in `bnd` (the boundary) first, then the
-// rest; each range degree-descending (stable), long rows leading.
+// rest; each range degree-descending (stable), long rows leading.  Owned rows
+// are relabeled to their position in this order and the device graph (CSR,
+// weights, blocked SELL) is rebuilt in the new numbering.
 static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
-    const int64_t n_own = P->n_own;
+    const int64_t n_own = P->n_own, nall = P->n_own + P->n_ghost;
     const std::vector<int32_t>& rp = P->h_rowptr;
     std::vector<uint8_t> is_b((size_t)std::max<int64_t>(n_own, 1), 0);
     for (int64_t i = 0; i < nb; ++i) {
@@ -305,53 +333,61 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     P->long_fast[0] = P->long_fast[1] = 0;
     while (P->long_fast[0] < (int64_t)rb.size() && deg(rb[(size_t)P->long_fast[0]]) > kPartLongDegree) ++P->long_fast[0];
     while (P->long_fast[1] < (int64_t)ri.size() && deg(ri[(size_t)P->long_fast[1]]) > kPartLongDegree) ++P->long_fast[1];
-    P->h_order = rb;
-    P->h_order.insert(P->h_order.end(), ri.begin(), ri.end());
-    if (n_own) GN_CUDA(cudaMemcpy(P->order, P->h_order.data(), 4 * (size_t)n_own, cudaMemcpyHostToDevice));
+    std::vector<int32_t> perm = rb;
+    perm.insert(perm.end(), ri.begin(), ri.end());
+    std::vector<int32_t> inv((size_t)n_own), order((size_t)n_own);
+    for (int64_t r = 0; r < n_own; ++r) {
+        inv[(size_t)perm[(size_t)r]] = (int32_t)r;
+        order[(size_t)r] = (int32_t)r;  // rows are numbered in processing order
+    }
+    // the relabeled CSR (neighbour order kept) and weights
+    std::vector<int32_t> nrp((size_t)n_own + 1, 0);
+    for (int64_t r = 0; r < n_own; ++r) nrp[(size_t)r + 1] = nrp[(size_t)r] + deg(perm[(size_t)r]);
+    std::vector<int32_t> ncol((size_t)P->nnz);
+    parallel_for(n_own, [&](int64_t r) {
+        const int32_t o = perm[(size_t)r];
+        int32_t* dst = ncol.data() + nrp[(size_t)r];
+        for (int32_t e = rp[(size_t)o]; e < rp[(size_t)o + 1]; ++e) {
+            const int32_t c = P->h_col[(size_t)e];
+            *dst++ = c < n_own ? inv[(size_t)c] : c;
+        }
+    });
+    std::vector<double> nw((size_t)nall);
+    for (int64_t i = 0; i < nall; ++i) nw[(size_t)i] = P->h_w[(size_t)(i < n_own ? perm[(size_t)i] : i)];
     // blocked SELL of each range's rows after its long prefix
-    const int32_t pad = (int32_t)(P->n_own + P->n_ghost);
+    const int32_t pad = (int32_t)nall;
     std::vector<int64_t> sp(1, 0);
     const int64_t rs[2] = {0, P->n_bnd}, rc[2] = {P->n_bnd, n_own - P->n_bnd};
-    std::vector<int64_t> first;  // per slice: first order position
+    std::vector<int64_t> first;  // per slice: first row
     for (int r = 0; r < 2; ++r) {
         P->sl0[r] = (int64_t)sp.size() - 1;
         const int64_t p0 = rs[r] + P->long_fast[r], p1 = rs[r] + rc[r];
         P->nsl[r] = (p1 - p0 + 31) / 32;
         for (int64_t q = p0; q < p1; q += 32) {
             int32_t len = 0;
-            for (int64_t t = q; t < std::min(p1, q + 32); ++t) len = std::max(len, deg(P->h_order[(size_t)t]));
+            for (int64_t t = q; t < std::min(p1, q + 32); ++t) len = std::max(len, nrp[(size_t)t + 1] - nrp[(size_t)t]);
             first.push_back(q);
             sp.push_back(sp.back() + (int64_t)(len + 3) / 4 * 128);
         }
     }
     std::vector<int32_t> sell((size_t)std::max<int64_t>(sp.back(), 1), pad);
-    const int64_t nslices = (int64_t)first.size();
-    const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
-    auto fill = [&](int t) {
-        for (int64_t sl = t; sl < nslices; sl += nt) {
-            const int64_t q = first[(size_t)sl];
-            const int64_t end = q < P->n_bnd ? P->n_bnd : n_own;
-            for (int l = 0; l < 32 && q + l < end; ++l) {
-                const int32_t row = P->h_order[(size_t)(q + l)];
-                for (int32_t e = rp[(size_t)row]; e < rp[(size_t)row + 1]; ++e) {
-                    const int32_t pos = e - rp[(size_t)row];
-                    sell[(size_t)(sp[(size_t)sl] + (pos / 4) * 128 + l * 4 + pos % 4)] = P->h_col[(size_t)e];
-                }
+    parallel_for((int64_t)first.size(), [&](int64_t sl) {
+        const int64_t q = first[(size_t)sl];
+        const int64_t end = q < P->n_bnd ? P->n_bnd : n_own;
+        for (int l = 0; l < 32 && q + l < end; ++l) {
+            const int64_t row = q + l;
+            for (int32_t e = nrp[(size_t)row]; e < nrp[(size_t)row + 1]; ++e) {
+                const int32_t pos = e - nrp[(size_t)row];
+                sell[(size_t)(sp[(size_t)sl] + (pos / 4) * 128 + l * 4 + pos % 4)] = ncol[(size_t)e];
             }
         }
-    };
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) th.emplace_back(fill, t);
-    fill(0);
-    for (auto& x : th) x.join();
-    cudaFree(P->sell);
-    cudaFree(P->slice_ptr);
-    P->sell = nullptr;
-    P->slice_ptr = nullptr;
-    GN_CUDA(cudaMalloc(&P->sell, 4 * sell.size()));
-    GN_CUDA(cudaMalloc(&P->slice_ptr, 8 * sp.size()));
-    GN_CUDA(cudaMemcpy(P->sell, sell.data(), 4 * sell.size(), cudaMemcpyHostToDevice));
-    GN_CUDA(cudaMemcpy(P->slice_ptr, sp.data(), 8 * sp.size(), cudaMemcpyHostToDevice));
+    });
+    int rcode;
+    if ((rcode = upload_into(&P->rowptr, nrp)) || (rcode = upload_into(&P->col, ncol)) ||
+        (rcode = upload_into(&P->w64, nw)) || (rcode = upload_into(&P->perm, perm)) ||
+        (rcode = upload_into(&P->inv, inv)) || (rcode = upload_into(&P->order, order)) ||
+        (rcode = upload_into(&P->sell, sell)) || (rcode = upload_into(&P->slice_ptr, sp)))
+        return rcode;
     return GN_OK;
 }
 
@@ -396,22 +432,9 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
     std::vector<int32_t> rp((size_t)n_own + 1);
     for (int64_t i = 0; i <= n_own; ++i) rp[(size_t)i] = (int32_t)(n_own > 0 ? indptr[i] : 0);
     const int64_t nall = n_own + n_ghost;
-    cudaError_t ce;
-    if ((ce = cudaMalloc(&P->rowptr, 4 * ((size_t)n_own + 1))) != cudaSuccess ||
-        (ce = cudaMalloc(&P->col, 4 * (size_t)std::max<int64_t>(nnz, 1))) != cudaSuccess ||
-        (ce = cudaMalloc(&P->w64, 8 * (size_t)std::max<int64_t>(nall, 1))) != cudaSuccess) {
-        delete P;
-        return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
-    }
-    cudaMemcpy(P->rowptr, rp.data(), 4 * rp.size(), cudaMemcpyHostToDevice);
-    if (nnz) cudaMemcpy(P->col, indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice);
-    if (nall) cudaMemcpy(P->w64, w, 8 * (size_t)nall, cudaMemcpyHostToDevice);
     P->h_rowptr = rp;
     P->h_col.assign(indices, indices + nnz);
-    if ((ce = cudaMalloc(&P->order, 4 * (size_t)std::max<int64_t>(n_own, 1))) != cudaSuccess) {
-        delete P;
-        return cuda_fail(ce, "cudaMalloc", __FILE__, __LINE__);
-    }
+    P->h_w.assign(w, w + nall);
     if ((rc = part_order(P, nullptr, 0))) {
         delete P;
         return rc;
@@ -430,6 +453,8 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
+    cudaFree(p->perm);
+    cudaFree(p->inv);
     cudaFree(p->sell);
     cudaFree(p->slice_ptr);
     cudaFree(p->w64);
@@ -479,15 +504,15 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         const int blocks = pblocks(nall);
         switch (p->dtype) {
             case GN_F64:
-                k_part_prepare<double, double><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (double*)p->x[0],
+                k_part_prepare<double, double><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->perm, p->w64, (double*)p->x[0],
                                                                           (double*)p->v, (double*)p->yg[0]);
                 break;
             case GN_F32:
-                k_part_prepare<double, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (double*)p->x[0],
+                k_part_prepare<double, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->perm, p->w64, (double*)p->x[0],
                                                                          (double*)p->v, (float*)p->yg[0]);
                 break;
             default:
-                k_part_prepare<float, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->w64, (float*)p->x[0],
+                k_part_prepare<float, float><<<blocks, kPartThreads>>>(p->n_own, nall, dx0, p->perm, p->w64, (float*)p->x[0],
                                                                         (float*)p->v, (float*)p->yg[0]);
         }
         GN_LAUNCHED();
@@ -559,9 +584,9 @@ int gn_part_pack(gn_part* p, int k, const int32_t* d_idx, int64_t count, void* d
     const void* src = p->yg[(k & 1) ^ 1];
     const int blocks = (int)((count + 255) / 256);
     if (gather_bytes(p->dtype) == 8)
-        k_part_pack<double><<<blocks, 256, 0, s>>>((const double*)src, d_idx, count, (double*)d_out);
+        k_part_pack<double><<<blocks, 256, 0, s>>>((const double*)src, d_idx, p->inv, count, (double*)d_out);
     else
-        k_part_pack<float><<<blocks, 256, 0, s>>>((const float*)src, d_idx, count, (float*)d_out);
+        k_part_pack<float><<<blocks, 256, 0, s>>>((const float*)src, d_idx, p->inv, count, (float*)d_out);
     GN_LAUNCHED();
     return GN_OK;
 }
@@ -596,9 +621,9 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
         }
     if (p->n_own > 0) {
         if (state_bytes(p->dtype) == 8)
-            k_part_out<double, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const double*)p->x[done & 1], dx);
+            k_part_out<double, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const double*)p->x[done & 1], p->perm, dx);
         else
-            k_part_out<float, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const float*)p->x[done & 1], dx);
+            k_part_out<float, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const float*)p->x[done & 1], p->perm, dx);
         GN_LAUNCHED();
     }
     std::vector<double> h2(8 * (size_t)std::max(done, 1));
