@@ -53,6 +53,8 @@ struct gn_part {
     // positions 4b..4b+3 of each row (one 16-byte load per lane, 512
     // contiguous bytes per warp); padding names the zero-valued slot n_all
     int32_t* sell = nullptr;
+    int32_t* sell_fast = nullptr;   // fast mode: every row in ascending new id (hot neighbours first)
+    int32_t* col_fast = nullptr;
     int64_t* slice_ptr = nullptr;   // [nslices+1] element offsets
     int64_t sl0[2] = {0, 0}, nsl[2] = {0, 0};  // per range: first slice, slice count
     int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
@@ -370,23 +372,31 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             sp.push_back(sp.back() + (int64_t)(len + 3) / 4 * 128);
         }
     }
-    std::vector<int32_t> sell((size_t)std::max<int64_t>(sp.back(), 1), pad);
-    parallel_for((int64_t)first.size(), [&](int64_t sl) {
-        const int64_t q = first[(size_t)sl];
-        const int64_t end = q < P->n_bnd ? P->n_bnd : n_own;
-        for (int l = 0; l < 32 && q + l < end; ++l) {
-            const int64_t row = q + l;
-            for (int32_t e = nrp[(size_t)row]; e < nrp[(size_t)row + 1]; ++e) {
-                const int32_t pos = e - nrp[(size_t)row];
-                sell[(size_t)(sp[(size_t)sl] + (pos / 4) * 128 + l * 4 + pos % 4)] = ncol[(size_t)e];
+    auto fill_sell = [&](const std::vector<int32_t>& cc) {
+        std::vector<int32_t> sell((size_t)std::max<int64_t>(sp.back(), 1), pad);
+        parallel_for((int64_t)first.size(), [&](int64_t sl) {
+            const int64_t q = first[(size_t)sl];
+            const int64_t end = q < P->n_bnd ? P->n_bnd : n_own;
+            for (int l = 0; l < 32 && q + l < end; ++l) {
+                const int64_t row = q + l;
+                for (int32_t e = nrp[(size_t)row]; e < nrp[(size_t)row + 1]; ++e) {
+                    const int32_t pos = e - nrp[(size_t)row];
+                    sell[(size_t)(sp[(size_t)sl] + (pos / 4) * 128 + l * 4 + pos % 4)] = cc[(size_t)e];
+                }
             }
-        }
-    });
+        });
+        return sell;
+    };
     int rcode;
     if ((rcode = upload_into(&P->rowptr, nrp)) || (rcode = upload_into(&P->col, ncol)) ||
         (rcode = upload_into(&P->w64, nw)) || (rcode = upload_into(&P->perm, perm)) ||
         (rcode = upload_into(&P->inv, inv)) || (rcode = upload_into(&P->order, order)) ||
-        (rcode = upload_into(&P->sell, sell)) || (rcode = upload_into(&P->slice_ptr, sp)))
+        (rcode = upload_into(&P->sell, fill_sell(ncol))) || (rcode = upload_into(&P->slice_ptr, sp)))
+        return rcode;
+    // fast-mode copies: rows in ascending new id (the sum order changes;
+    // EXACT runs read the reference-order arrays above)
+    parallel_for(n_own, [&](int64_t r) { std::sort(ncol.begin() + nrp[(size_t)r], ncol.begin() + nrp[(size_t)r + 1]); });
+    if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
     return GN_OK;
 }
@@ -456,6 +466,8 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->perm);
     cudaFree(p->inv);
     cudaFree(p->sell);
+    cudaFree(p->sell_fast);
+    cudaFree(p->col_fast);
     cudaFree(p->slice_ptr);
     cudaFree(p->w64);
     if (p->own_stream) cudaStreamDestroy(p->own_stream);
@@ -530,25 +542,28 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
     const int cur = k & 1;
     const int nb = p->r_nblocks[r];
     const int32_t* ord = p->order + p->r_start[r];
+    const bool fast = !(p->flags & GN_EXACT);
+    const int32_t* col = fast ? p->col_fast : p->col;
+    const int32_t* sell = fast ? p->sell_fast : p->sell;
     switch (p->dtype) {
         case GN_F64:
             k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
-                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
+                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const double*)p->yg[cur],
                 (double*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         case GN_F32:
             k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
-                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
+                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const float*)p->yg[cur],
                 (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
             break;
         default:
             k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, p->col,
-                p->sell + 0, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
+                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
+                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1], (const float*)p->yg[cur],
                 (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
     }
