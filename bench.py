@@ -150,13 +150,17 @@ def cpu_reference(inst, seconds: float = 12.0, threads: int | None = None) -> di
             "iters": k, "seconds": dt}
 
 
-def ncu_traffic(config: str):
-    """DRAM bytes per loop-kernel launch from the committed ncu summary."""
+def ncu_traffic(config: str, iters: int):
+    """DRAM bytes (read + write) per launch of `iters` iterations, from the
+    committed ncu --set full summary of the same kernel (scaled by iterations
+    when the capture ran fewer, e.g. 5 iterations of C5)."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if f.exists():
         try:
-            d = json.loads(f.read_text())
-            return d.get(config, {}).get("dram_bytes_per_launch")
+            d = json.loads(f.read_text()).get(config, {})
+            if d.get("dram_bytes_per_launch") is None:
+                return None
+            return d["dram_bytes_per_launch"] / (d.get("iters_per_launch") or iters) * iters
         except Exception:
             return None
     return None
@@ -479,7 +483,16 @@ def main():
     b_iter = algorithmic_bytes(g.n, 2 * inst.m, s_bytes) + 3 * s_bytes * g.n * (starts - 1)
     loop_avg = statistics.mean(loop_ms)
     achieved = b_iter * iters / (loop_avg * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config) if starts == 1 else None
+    traffic = ncu_traffic(args.config, iters) if starts == 1 else None
+    if traffic is None:
+        traffic_note = None
+    elif traffic < 0.5 * b_iter * iters:
+        traffic_note = (f"DRAM traffic is {traffic / (b_iter * iters):.3f}x the algorithmic bytes: the graph stays in "
+                        "L2/shared memory across the iterations of a launch, so achieved/frac are the algorithmic "
+                        "rate of SURVEY 8(d), not DRAM bandwidth")
+    else:
+        traffic_note = (f"DRAM traffic is {traffic / (b_iter * iters):.2f}x the algorithmic bytes (index stream plus "
+                        "L2 misses of the gathered values)")
     info = {"n": g.n}
 
     cpu = None
@@ -519,7 +532,7 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_name,
                      "bytes_per_launch": b_iter * iters, "b_iter": b_iter, "peak_source": peak_src,
-                     "loop_ms": loop_avg},
+                     "loop_ms": loop_avg, "traffic_note": traffic_note},
         "cpu_baseline": cpu,
         "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         "gpu_launches": int(launches),

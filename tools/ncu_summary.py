@@ -71,7 +71,7 @@ def summarize_rep(rep, label, config, iters):
     if config:
         sf = ROOT / "profiles" / "ncu_summary.json"
         s = json.loads(sf.read_text()) if sf.exists() else {}
-        loop = [m for n, m in out.items() if "k_gn_loop" in n]
+        loop = [m for n, m in out.items() if "k_gn_loop" in n or "k_gn_batch" in n or "k_gn_multi" in n]
         if loop:
             s[config] = {"label": label, "dram_bytes_per_launch": loop[0]["dram_bytes_per_launch"],
                          "iters_per_launch": iters}
