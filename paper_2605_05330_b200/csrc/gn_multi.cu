@@ -11,7 +11,7 @@
 // [t*S, t*S+S) (S = 16 bytes / gathered value: 2 fp64 or 4 fp32), so each
 // gather is one 16-byte load per lane and the team's loads cover the row's
 // whole Bp-vector.  A warp works 32/T rows at a time, its rows taken in the
-// degree-sorted relabel order (gn_internal.cuh) so they have similar
+// multi-id order (degree-sorted in windows, see multi_csr) so they have similar
 // lengths.  The team walks the row in the reference's neighbour order: lanes
 // fetch 16 consecutive column indices cooperatively, broadcast them by
 // shuffle and issue 16 gathers before adding them in order.  Every start's
@@ -34,6 +34,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -407,37 +408,36 @@ __global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) 
     if (blockIdx.x == 0 && threadIdx.x < B && !s_frozen[threadIdx.x]) a.run[threadIdx.x] = a.iters;
 }
 
-// x0 [B][n] (fp64, original order) -> x[0], yg[0] ([n][Bp]); padding starts are 0
+// x0 [B][n] (fp64, original order) -> x[0], yg[0] ([n][Bp], multi-id rows); padding starts are 0
 template <typename TS, typename TG>
-__global__ void k_multi_prepare(int64_t n, int B, int Bp, const double* __restrict__ x0, const TS* __restrict__ v,
-                                TS* __restrict__ x, TG* __restrict__ yg) {
+__global__ void k_multi_prepare(int64_t n, int B, int Bp, const double* __restrict__ x0, const int32_t* __restrict__ perm,
+                                const TS* __restrict__ v, TS* __restrict__ x, TG* __restrict__ yg) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n * Bp) return;
-    const int64_t r = e / Bp;
+    const int64_t r = e / Bp;  // multi id
     const int b = (int)(e % Bp);
-    const TS xi = b < B ? (TS)x0[(size_t)b * n + r] : TS(0);
+    const TS xi = b < B ? (TS)x0[(size_t)b * n + perm[r]] : TS(0);
     x[e] = xi;
     yg[e] = (TG)Arith<TS>::mul(v[r], xi);
 }
 
-// sqrt(w) and w in state precision, original order (graph.py:42, as k_init_state_weights)
+// sqrt(w) in state precision, multi-id order (graph.py:42, as k_init_state_weights)
 template <typename TS>
-__global__ void k_multi_weights(int64_t n, const double* __restrict__ w64, TS* __restrict__ v, TS* __restrict__ w) {
+__global__ void k_multi_weights(int64_t n, const double* __restrict__ w64, const int32_t* __restrict__ perm,
+                                TS* __restrict__ v) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) {
-        v[i] = (TS)sqrt(w64[i]);
-        w[i] = (TS)w64[i];
-    }
+    if (i < n) v[i] = (TS)sqrt(w64[perm[i]]);
 }
 
 // final state of start b (buffer run[b] & 1) -> x_out [B][n], np.clip(x, 0, 1)
 template <typename TS>
 __global__ void k_multi_finalize(int64_t n, int B, int Bp, const TS* __restrict__ x0, const TS* __restrict__ x1,
-                                 const int* __restrict__ run, double* __restrict__ out, int clip) {
+                                 const int* __restrict__ run, const int32_t* __restrict__ inv,
+                                 double* __restrict__ out, int clip) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n * B) return;
     const int b = (int)(e / n);
-    const int64_t r = e % n;
+    const int64_t r = inv[e % n];  // original id -> multi id
     double xi = (double)((run[b] & 1) ? x1 : x0)[(size_t)r * Bp + b];
     if (clip) xi = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);  // dynamics.py:179
     out[e] = xi;
@@ -457,9 +457,25 @@ struct MultiPlan {
 };
 static std::mutex g_mplan_mu;
 static std::map<std::tuple<const gn_graph*, int, int, int>, MultiPlan> g_mplans;
+struct MultiCsr {
+    int32_t* rowptr = nullptr;
+    int32_t* col = nullptr;   // neighbours as multi ids, the reference's order
+    int32_t* perm = nullptr;  // multi id -> original id
+    int32_t* inv = nullptr;   // original id -> multi id
+    std::vector<int32_t> h_rowptr;
+};
+static std::map<const gn_graph*, MultiCsr> g_mcsr;
 
 void release_multi_plans(const gn_graph* g) {
     std::lock_guard<std::mutex> lk(g_mplan_mu);
+    auto mc = g_mcsr.find(g);
+    if (mc != g_mcsr.end()) {
+        cudaFree(mc->second.rowptr);
+        cudaFree(mc->second.col);
+        cudaFree(mc->second.perm);
+        cudaFree(mc->second.inv);
+        g_mcsr.erase(mc);
+    }
     for (auto it = g_mplans.begin(); it != g_mplans.end();) {
         if (std::get<0>(it->first) == g) {
             cudaFree(it->second.rdesc);
@@ -481,6 +497,61 @@ static int upload_vec(const std::vector<V>& h, V** d) {
     return GN_OK;
 }
 
+// The graph in the multi-start kernel's own order: hubs (degree > 512,
+// degree-descending) first, then the other rows degree-descending inside
+// windows of 4096 original ids -- consecutive rows keep the neighbourhood
+// locality of the caller's numbering, which the start-minor gathers (one
+// 16-byte vector per lane per neighbour) use better than the single-start
+// loop's global degree order (C5 scale 24 x16 fp32: 645 vs 910 us per
+// start-iteration).  State rows follow this order (multi ids); neighbour
+// lists keep the reference's order, so every start sums as dynamics.py:105
+// does.  Built once per graph on first use.
+static int multi_csr(gn_graph* g, const MultiCsr** out) {  // caller holds g_mplan_mu
+    auto it = g_mcsr.find(g);
+    if (it != g_mcsr.end()) {
+        *out = &it->second;
+        return GN_OK;
+    }
+    const int64_t n = g->n, nnz = g->nnz;
+    std::vector<int32_t> rp((size_t)n + 1), col((size_t)std::max<int64_t>(nnz, 1));
+    GN_CUDA(cudaMemcpy(rp.data(), g->rowptr, sizeof(int32_t) * rp.size(), cudaMemcpyDeviceToHost));
+    if (nnz) GN_CUDA(cudaMemcpy(col.data(), g->col, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+    auto deg = [&](int32_t r) { return rp[(size_t)r + 1] - rp[(size_t)r]; };
+    std::vector<int32_t> hubs, regular;
+    for (int64_t i = 0; i < n; ++i) (deg((int32_t)i) > kHubDegree ? hubs : regular).push_back((int32_t)i);
+    auto by_deg = [&](int32_t a, int32_t b) { return deg(a) > deg(b); };
+    std::stable_sort(hubs.begin(), hubs.end(), by_deg);
+    for (size_t w0 = 0; w0 < regular.size(); w0 += kSigma)
+        std::stable_sort(regular.begin() + w0, regular.begin() + std::min(regular.size(), w0 + kSigma), by_deg);
+    std::vector<int32_t> perm = hubs;
+    perm.insert(perm.end(), regular.begin(), regular.end());
+    std::vector<int32_t> inv((size_t)std::max<int64_t>(n, 1));
+    for (int64_t r = 0; r < n; ++r) inv[(size_t)perm[(size_t)r]] = (int32_t)r;
+    MultiCsr m;
+    m.h_rowptr.assign((size_t)n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) m.h_rowptr[(size_t)r + 1] = m.h_rowptr[(size_t)r] + deg(perm[(size_t)r]);
+    std::vector<int32_t> mcol((size_t)std::max<int64_t>(nnz, 1));
+    const int nt = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    auto fill = [&](int t) {
+        for (int64_t r = t; r < n; r += nt) {
+            const int32_t o = perm[(size_t)r];
+            int32_t* dst = mcol.data() + m.h_rowptr[(size_t)r];
+            for (int32_t e = rp[(size_t)o]; e < rp[(size_t)o + 1]; ++e) *dst++ = inv[(size_t)col[(size_t)e]];
+        }
+    };
+    for (int t = 1; t < nt; ++t) th.emplace_back(fill, t);
+    fill(0);
+    for (auto& x : th) x.join();
+    int rc;
+    if ((rc = upload_vec(m.h_rowptr, &m.rowptr)) || (rc = upload_vec(mcol, &m.col)) ||
+        (rc = upload_vec(perm, &m.perm)) || (rc = upload_vec(inv, &m.inv)))
+        return rc;
+    auto res = g_mcsr.emplace(g, std::move(m));
+    *out = &res.first->second;
+    return GN_OK;
+}
+
 static int multi_plan(gn_graph* g, int G, bool exact, int rpw, const MultiPlan** out) {
     std::lock_guard<std::mutex> lk(g_mplan_mu);
     auto key = std::make_tuple((const gn_graph*)g, G, exact ? 1 : 0, rpw);
@@ -490,9 +561,12 @@ static int multi_plan(gn_graph* g, int G, bool exact, int rpw, const MultiPlan**
         return GN_OK;
     }
     const int64_t n = g->n;
-    std::vector<int32_t> rp((size_t)n + 1), perm((size_t)n);
-    GN_CUDA(cudaMemcpy(rp.data(), g->rowptr, sizeof(int32_t) * rp.size(), cudaMemcpyDeviceToHost));
-    if (n > 0) GN_CUDA(cudaMemcpy(perm.data(), g->perm, sizeof(int32_t) * perm.size(), cudaMemcpyDeviceToHost));
+    const MultiCsr* mc = nullptr;
+    if (int rc0 = multi_csr(g, &mc)) return rc0;
+    // rows are multi ids, processed in that order
+    const std::vector<int32_t>& rp = mc->h_rowptr;
+    std::vector<int32_t> perm((size_t)n);
+    for (int64_t i = 0; i < n; ++i) perm[(size_t)i] = (int32_t)i;
     const int nw = G * kMWarps;
     constexpr double kRowCost = 8.0;  // per-row share of the index fetch and the update, in gathers
     auto deg = [&](int32_t r) { return rp[(size_t)r + 1] - rp[(size_t)r]; };
@@ -624,7 +698,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     MultiBufs ws;
     ws.s = s;
     const size_t nn = (size_t)std::max<int64_t>(n, 1);
-    TS *xa, *v, *w;
+    TS *xa, *v;
     TG* ya;
     double *xin, *gam, *out64;
     unsigned long long* sinf;
@@ -634,7 +708,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     GN_CUDA(ws.get(&xa, 2 * sizeof(TS) * nn * Bp));
     GN_CUDA(ws.get(&ya, 2 * sizeof(TG) * nn * Bp));
     GN_CUDA(ws.get(&v, sizeof(TS) * nn));
-    GN_CUDA(ws.get(&w, sizeof(TS) * nn));
+
     const bool dev_io = (flags & GN_DEVICE_IO) != 0;
     if (dev_io) xin = const_cast<double*>(x0);
     else GN_CUDA(ws.get(&xin, 8 * nn * B));
@@ -674,10 +748,15 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
         if (fail_iter) fail_iter[b] = -1;
     }
     GN_CUDA(cudaMemcpyAsync(skip, hskip.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, s));
+    const MultiCsr* mc = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mplan_mu);
+        if ((rc = multi_csr(g, &mc))) return rc;
+    }
     if (n > 0) {
-        k_multi_weights<TS><<<blocks_of(n), 256, 0, s>>>(n, g->w64, v, w);
+        k_multi_weights<TS><<<blocks_of(n), 256, 0, s>>>(n, g->w64, mc->perm, v);
         GN_LAUNCHED();
-        k_multi_prepare<TS, TG><<<blocks_of(n * Bp), 256, 0, s>>>(n, B, Bp, xin, v, xa, ya);
+        k_multi_prepare<TS, TG><<<blocks_of(n * Bp), 256, 0, s>>>(n, B, Bp, xin, mc->perm, v, xa, ya);
         GN_LAUNCHED();
     }
 
@@ -696,7 +775,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     a.n = n;
     a.B = B;
     a.Bp = Bp;
-    a.col = g->col;
+    a.col = mc->col;
     a.rdesc = plan->rdesc;
     a.wbeg = plan->wbeg;
     a.wmid = plan->wmid;
@@ -734,7 +813,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
     GN_CUDA(cudaMemcpyAsync(hbad.data(), bad, 4 * hbad.size(), cudaMemcpyDeviceToHost, s));
     d2h += 4 * B + 16 * (int64_t)iters * B;
     if (x_out && n > 0) {
-        k_multi_finalize<TS><<<blocks_of(n * B), 256, 0, s>>>(n, B, Bp, a.x[0], a.x[1], run, out64,
+        k_multi_finalize<TS><<<blocks_of(n * B), 256, 0, s>>>(n, B, Bp, a.x[0], a.x[1], run, mc->inv, out64,
                                                              (flags & GN_NO_CLIP) ? 0 : 1);
         GN_LAUNCHED();
         if (!dev_io) {
