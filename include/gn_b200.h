@@ -52,6 +52,8 @@ extern "C" {
 #define GN_ERR_NODEV 7
 #define GN_ERR_ZERO_DENOM 8 /* fitness(): d <= 0 (dynamics.py:246-247) */
 #define GN_ERR_ZERO_MASS 9  /* simplex_state(): mass <= 0 (dynamics.py:231-232) */
+#define GN_ERR_FORMAT 10    /* gn_mwis_parse: io.py FormatError (message in err) */
+#define GN_PARSE_FALLBACK 11 /* gn_mwis_parse: text outside the native grammar (see gn_io.cpp) */
 
 /* run flags */
 #define GN_TRACE 0x1u      /* energy / pre_energy per iteration (record_trace) */
@@ -227,6 +229,21 @@ int gn_csr_from_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
                       int device, int64_t* first_bad, int64_t* nnz_out,
                       int64_t** indptr_out, int32_t** indices_out);
 void gn_free_host(void* p);
+
+/* ---- instance text ------------------------------------
+ * gn_mwis_parse replaces io.py:43-102 parse_instance up to its build_graph
+ * call: the DIMACS-flavoured MWIS text (len bytes) is checked line by line
+ * with the reference's rules and messages.  GN_OK: *out holds n, the
+ * weights (1-based id i at w[i-1]) and the 0-based edges in file order
+ * (gn_mwis_info / gn_mwis_copy, released by gn_mwis_free); the caller builds
+ * the graph (build_graph, graph.py:78-124).  GN_ERR_FORMAT: err holds the
+ * FormatError text.  GN_PARSE_FALLBACK: the text uses what only Python's
+ * int()/float()/str methods read (non-ASCII, '_', huge integers, ...). */
+typedef struct gn_mwis gn_mwis;
+int gn_mwis_parse(const char* text, int64_t len, gn_mwis** out, char* err, int64_t err_len);
+int gn_mwis_info(const gn_mwis* r, int64_t* n, int64_t* m);
+int gn_mwis_copy(const gn_mwis* r, double* w, int64_t* edges /* [m][2] */);
+void gn_mwis_free(gn_mwis* r);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,8 @@ GN_ERR_NOMEM = 6
 GN_ERR_NODEV = 7
 GN_ERR_ZERO_DENOM = 8
 GN_ERR_ZERO_MASS = 9
+GN_ERR_FORMAT = 10
+GN_PARSE_FALLBACK = 11
 
 GN_TRACE = 0x1
 GN_EARLY_EXIT = 0x2
@@ -80,6 +82,10 @@ EXPORTED = (
     "gn_gen_rmat",
     "gn_csr_from_edges",
     "gn_free_host",
+    "gn_mwis_parse",
+    "gn_mwis_info",
+    "gn_mwis_copy",
+    "gn_mwis_free",
 )
 
 
@@ -165,6 +171,10 @@ _SIGNATURES = {
     "gn_gen_rmat": (_I32, [_I32, _I32, _D, _D, _D, ctypes.c_uint64, _I32, _PI64, ctypes.POINTER(_P),
                            ctypes.POINTER(_P)]),
     "gn_csr_from_edges": (_I32, [_I64, _I64, _P, _P, _I32, _PI64, _PI64, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "gn_mwis_parse": (_I32, [ctypes.c_char_p, _I64, ctypes.POINTER(_P), ctypes.c_char_p, _I64]),
+    "gn_mwis_info": (_I32, [_P, _PI64, _PI64]),
+    "gn_mwis_copy": (_I32, [_P, _P, _P]),
+    "gn_mwis_free": (None, [_P]),
     "gn_free_host": (None, [_P]),
 }
 
