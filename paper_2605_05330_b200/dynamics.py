@@ -216,13 +216,13 @@ def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early
     E.check(rc)
     k = ran.value
     trace = SolveTrace()
-    trace.gamma = [float(v) for v in gam[:k]]
-    trace.step_inf = [float(v) for v in step_inf[:k]]
-    trace.fallbacks = [int(v) for v in fallbacks[:k]]
-    trace.objective = [float(v) for v in mass[:k]]
+    trace.gamma = gam[:k].tolist()  # Python floats / ints, as the reference's lists hold
+    trace.step_inf = step_inf[:k].tolist()
+    trace.fallbacks = fallbacks[:k].tolist()
+    trace.objective = mass[:k].tolist()
     if record_trace:
-        trace.energy = [float(v) for v in energy[:k]]
-        trace.pre_energy = [float(v) for v in pre_energy[:k]]
+        trace.energy = energy[:k].tolist()
+        trace.pre_energy = pre_energy[:k].tolist()
         trace.mass = list(trace.objective)
     stats = {f: getattr(st, f) for f, _ in E.RunStats._fields_}
     return RunResult(x_out, trace, stats, hist[:k] if history else None)

@@ -51,9 +51,9 @@ class MultiResult:
     def trace(self, b: int) -> SolveTrace:
         k = int(self.iters_run[b])
         t = SolveTrace()
-        t.gamma = [float(v) for v in self.gammas[:k]]
-        t.step_inf = [float(v) for v in self.step_inf[b, :k]]
-        t.fallbacks = [int(v) for v in self.fallbacks[b, :k]]
+        t.gamma = self.gammas[:k].tolist()
+        t.step_inf = self.step_inf[b, :k].tolist()
+        t.fallbacks = self.fallbacks[b, :k].tolist()
         return t
 
 

@@ -6,9 +6,9 @@ run() { local name=$1; shift; timeout 1200 "$@" > $M/$name.json 2> $M/$name.err;
 nproc > $M/host_nproc.txt; uptime > $M/host_uptime.txt
 run bench_c2 python bench.py
 run bench_c2_reference python bench.py --impl reference
-run bench_c3 python bench.py --config C3 --no-cpu-baseline
-run bench_c4 python bench.py --config C4 --no-cpu-baseline
-run bench_c5 python bench.py --config C5 --no-cpu-baseline --steps 3 --warmup 3
+run bench_c3 python bench.py --config C3
+run bench_c4 python bench.py --config C4
+run bench_c5 python bench.py --config C5 --steps 3 --warmup 3
 run bench_c5_part python bench.py --config C5 --partition --no-cpu-baseline --steps 3 --warmup 3
 run bench_c2_x16 python bench.py --starts 16 --no-cpu-baseline
 run bench_c3_x16 python bench.py --config C3 --starts 16 --no-cpu-baseline
