@@ -210,6 +210,28 @@ int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first,
                    int64_t count, uintptr_t stream);
 int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf,
                 int64_t* fallbacks, double* mass, int* bad);
+/* Direct halo over peer memory (the fused alternative to pack + NCCL +
+ * unpack): the boundary step stores every published value straight into the
+ * ghost slots of the peers that hold it (P2P stores over NVLink, issued as
+ * the rows finish), then a flag per peer.  Sequence per run, after
+ * gn_part_begin: gn_part_peer_init (this part's rank, the peers that push to
+ * it), gn_part_peer_buffers (yg[2] and the flag array to hand to the peers:
+ * pointers in one process, gn_ipc_get_handle across processes),
+ * gn_part_peer_add per peer (its buffers, the caller's owned ids it holds as
+ * ghosts, in its ghost order, and the slot of the first of them in its yg),
+ * gn_part_peer_commit.  Per iteration k: gn_part_peer_wait, gn_part_step
+ * (the boundary range pushes), gn_part_peer_signal. */
+int gn_part_peer_init(gn_part* p, int parts, int me, const int32_t* expect, int nexpect);
+int gn_part_peer_buffers(const gn_part* p, void** yg0, void** yg1, void** inflags);
+int gn_part_peer_add(gn_part* p, int rank, void* yg0, void* yg1, void* inflags,
+                     const int32_t* owned, int64_t count, int64_t slot0);
+int gn_part_peer_commit(gn_part* p);
+int gn_part_peer_wait(gn_part* p, int k, uintptr_t stream);
+int gn_part_peer_signal(gn_part* p, int k, uintptr_t stream);
+/* CUDA IPC of one device allocation between the processes of a node. */
+int gn_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */);
+int gn_ipc_open_handle(const void* handle, int device, void** dptr);
+int gn_ipc_close(void* dptr);
 
 /* ---- graph generation on the device (BASELINE config C5) ----
  * R-MAT with 2^scale vertices and edge_factor * 2^scale samples, quadrant

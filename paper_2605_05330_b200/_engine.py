@@ -82,6 +82,15 @@ EXPORTED = (
     "gn_gen_rmat",
     "gn_csr_from_edges",
     "gn_free_host",
+    "gn_part_peer_init",
+    "gn_part_peer_buffers",
+    "gn_part_peer_add",
+    "gn_part_peer_commit",
+    "gn_part_peer_wait",
+    "gn_part_peer_signal",
+    "gn_ipc_get_handle",
+    "gn_ipc_open_handle",
+    "gn_ipc_close",
     "gn_mwis_parse",
     "gn_mwis_info",
     "gn_mwis_copy",
@@ -171,6 +180,15 @@ _SIGNATURES = {
     "gn_gen_rmat": (_I32, [_I32, _I32, _D, _D, _D, ctypes.c_uint64, _I32, _PI64, ctypes.POINTER(_P),
                            ctypes.POINTER(_P)]),
     "gn_csr_from_edges": (_I32, [_I64, _I64, _P, _P, _I32, _PI64, _PI64, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "gn_part_peer_init": (_I32, [_P, _I32, _I32, _P, _I32]),
+    "gn_part_peer_buffers": (_I32, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "gn_part_peer_add": (_I32, [_P, _I32, _P, _P, _P, _P, _I64, _I64]),
+    "gn_part_peer_commit": (_I32, [_P]),
+    "gn_part_peer_wait": (_I32, [_P, _I32, ctypes.c_uint64]),
+    "gn_part_peer_signal": (_I32, [_P, _I32, ctypes.c_uint64]),
+    "gn_ipc_get_handle": (_I32, [_P, _P]),
+    "gn_ipc_open_handle": (_I32, [_P, _I32, ctypes.POINTER(_P)]),
+    "gn_ipc_close": (_I32, [_P]),
     "gn_mwis_parse": (_I32, [ctypes.c_char_p, _I64, ctypes.POINTER(_P), ctypes.c_char_p, _I64]),
     "gn_mwis_info": (_I32, [_P, _PI64, _PI64]),
     "gn_mwis_copy": (_I32, [_P, _P, _P]),

@@ -46,6 +46,7 @@ struct gn_part {
     // relabeled graph (neighbour order unchanged: bitwise sums).
     int32_t* perm = nullptr;
     int32_t* inv = nullptr;
+    std::vector<int32_t> h_inv;     // host copy of inv
     std::vector<int32_t> h_col;     // host copy of col (the SELL is rebuilt by gn_part_set_boundary)
     int64_t n_bnd = 0;              // order[0, n_bnd): boundary rows
     // blocked SELL of the rows after each range's long prefix: slices of 32
@@ -71,6 +72,24 @@ struct gn_part {
     double* gam = nullptr;
     double* part[2] = {nullptr, nullptr};  // per range [iters][r_nblocks][4]: max|dx|, fallbacks, w.x', non-finite
     cudaStream_t own_stream = nullptr;
+    // direct halo over peer memory (gn_part_peer_*): the boundary step stores
+    // each published value straight into the ghost slots of the peers that
+    // hold it (NVLink P2P stores, issued as the rows finish), then flags them
+    int me = 0, parts = 0;
+    int64_t* inflags = nullptr;              // [parts] incoming: inflags[q] = iterations peer q has pushed
+    int32_t* expect = nullptr;               // peers that push to this part
+    int nexpect = 0;
+    struct Peer { int rank; void* yg[2]; int64_t* flags; };
+    std::vector<Peer> peers;
+    std::vector<int32_t> h_push_row, h_push_peer;
+    std::vector<int64_t> h_push_slot;
+    int32_t* push_ptr = nullptr;             // [n_bnd+1] over the boundary rows (new ids)
+    int32_t* push_peer = nullptr;
+    int64_t* push_slot = nullptr;
+    void** push_dst[2] = {nullptr, nullptr}; // per parity: the peers' yg buffers
+    int64_t** peer_flags = nullptr;          // the peers' flag arrays
+    int* halo_bad = nullptr;                 // set when a peer's flag did not arrive in time
+    int npush_peers = 0;
 };
 
 namespace gn {
@@ -117,6 +136,23 @@ __device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double*
     ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
 }
 
+// Direct halo: the rows of [0, rows) (the boundary) store their published
+// value into every peer ghost slot that holds them.
+struct PartPush {
+    const int32_t* __restrict__ ptr;   // [rows+1], or null: no pushes
+    const int32_t* __restrict__ peer;
+    const int64_t* __restrict__ slot;
+    void* const* __restrict__ dst;     // [peers] the buffers this step writes (next parity)
+    int64_t rows;
+};
+
+template <typename TG>
+__device__ __forceinline__ void push_row(const PartPush& P, int64_t i, const TG* __restrict__ ygo) {
+    if (P.ptr == nullptr || i >= P.rows) return;
+    const TG val = ygo[i];  // written by this thread just before
+    for (int32_t e = P.ptr[i]; e < P.ptr[i + 1]; ++e) static_cast<TG*>(P.dst[P.peer[e]])[P.slot[e]] = val;
+}
+
 // One step of the owned rows of one range.  Blocks [0, nbl) split the n_long
 // longest rows over warps (lanes stride the positions, fixed butterfly fold:
 // fast mode only); blocks [nbl, nbl + ncb) give one thread to each of the
@@ -135,7 +171,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
                                                             const TS* __restrict__ x, TS* __restrict__ xo,
                                                             const TG* __restrict__ yg, TG* __restrict__ ygo,
                                                             const double* __restrict__ gam, int k,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part, PartPush push) {
     using A = Arith<TS>;
     const TS g = (TS)gam[k];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,7 +193,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
             for (; p < re; p += 32) s = A::add(s, (TS)yg[col[p]]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-            if (lane == 0) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            if (lane == 0) {
+                part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+                push_row<TG>(push, i, ygo);
+            }
         }
     } else if ((int)blockIdx.x < nbl + ncb) {
         for (int64_t q = (int64_t)(blockIdx.x - nbl) * blockDim.x + threadIdx.x; q < n_csr;
@@ -175,6 +214,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
             }
             for (; p < re; ++p) s = A::add(s, (TS)yg[col[p]]);
             part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            push_row<TG>(push, i, ygo);
         }
     } else {
         const int64_t pos0 = n_long + n_csr;  // first order position of slice 0
@@ -210,7 +250,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
 #pragma unroll
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
-            if (valid) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            if (valid) {
+                part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+                push_row<TG>(push, i, ygo);
+            }
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -242,6 +285,40 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
         dst[1] = t[1];
         dst[2] = t[2];
         dst[3] = t[3];
+    }
+}
+
+// Direct halo protocol, per iteration k: wait until every peer that pushes
+// here has finished step k-1 (its values of step k-1 are in our ghost slots,
+// and it has read the buffer our pushes of step k will overwrite), step the
+// boundary rows with their pushes, step the interior, then flag every peer.
+// The spin is bounded (~10 s): a missing peer sets bad[0] instead of hanging.
+__global__ void k_part_wait(const int64_t* flags, const int32_t* __restrict__ expect, int nexpect, int64_t k,
+                            int* bad) {
+    for (int i = threadIdx.x; i < nexpect; i += blockDim.x) {
+        const int64_t* f = flags + expect[i];
+        long long t0 = 0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            long long v;
+            asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v >= k) break;
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000LL) {
+                atomicExch(bad, 1);
+                break;
+            }
+            __nanosleep(200);
+        }
+    }
+}
+
+__global__ void k_part_signal(int64_t* const* __restrict__ peer_flags, int npeers, int me, int64_t value) {
+    __threadfence_system();  // this part's pushes (earlier kernels on the stream) before the flags
+    for (int i = threadIdx.x; i < npeers; i += blockDim.x) {
+        int64_t* f = peer_flags[i] + me;
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(f), "l"((long long)value) : "memory");
     }
 }
 
@@ -403,6 +480,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         });
         return sell;
     };
+    P->h_inv = inv;
     int rcode;
     if ((rcode = upload_into(&P->rowptr, nrp)) || (rcode = upload_into(&P->col, ncol)) ||
         (rcode = upload_into(&P->w64, nw)) || (rcode = upload_into(&P->perm, perm)) ||
@@ -415,6 +493,15 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
     return GN_OK;
+}
+
+static void part_free_push(gn_part* p) {
+    void* q[] = {p->push_ptr, p->push_peer, p->push_slot, p->push_dst[0], p->push_dst[1], p->peer_flags};
+    for (void* x : q) cudaFree(x);
+    p->push_ptr = p->push_peer = nullptr;
+    p->push_slot = nullptr;
+    p->push_dst[0] = p->push_dst[1] = nullptr;
+    p->peer_flags = nullptr;
 }
 
 static void part_free_run(gn_part* p) {
@@ -481,6 +568,10 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->order);
     cudaFree(p->perm);
     cudaFree(p->inv);
+    part_free_push(p);
+    cudaFree(p->inflags);
+    cudaFree(p->expect);
+    cudaFree(p->halo_bad);
     cudaFree(p->sell);
     cudaFree(p->sell_fast);
     cudaFree(p->col_fast);
@@ -547,6 +638,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         // the ghost slots of the other buffer are filled by unpack before they are read
         GN_CUDA(cudaMemcpy(p->yg[1], p->yg[0], gs * (size_t)nall, cudaMemcpyDeviceToDevice));
     }
+    if (p->inflags) GN_CUDA(cudaMemset(p->inflags, 0, 8 * (size_t)p->parts));  // a new run: no step pushed yet
+    if (p->halo_bad) GN_CUDA(cudaMemset(p->halo_bad, 0, sizeof(int)));
     GN_CUDA(cudaDeviceSynchronize());
     cudaFree(dx0);
     return GN_OK;
@@ -558,6 +651,9 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
     const int cur = k & 1;
     const int nb = p->r_nblocks[r];
     const int32_t* ord = p->order + p->r_start[r];
+    PartPush push{nullptr, nullptr, nullptr, nullptr, 0};
+    if (r == 0 && p->push_ptr)
+        push = PartPush{p->push_ptr, p->push_peer, p->push_slot, p->push_dst[(k + 1) & 1], p->n_bnd};
     const bool fast = !(p->flags & GN_EXACT);
     const int32_t* col = fast ? p->col_fast : p->col;
     const int32_t* sell = fast ? p->sell_fast : p->sell;
@@ -567,21 +663,21 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
                 p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
                 sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const double*)p->yg[cur],
-                (double*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
+                (double*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
             break;
         case GN_F32:
             k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
                 p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
                 sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const float*)p->yg[cur],
-                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
+                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
             break;
         default:
             k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
                 p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
                 sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
                 (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1], (const float*)p->yg[cur],
-                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r]);
+                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
     }
     GN_LAUNCHED();
     return GN_OK;
@@ -672,6 +768,11 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
     if (x_out && p->n_own) GN_CUDA(cudaMemcpy(x_out, dx, 8 * (size_t)p->n_own, cudaMemcpyDeviceToHost));
     cudaFree(dout);
     cudaFree(dx);
+    if (p->halo_bad) {
+        int hb = 0;
+        GN_CUDA(cudaMemcpy(&hb, p->halo_bad, sizeof(int), cudaMemcpyDeviceToHost));
+        if (hb) return fail(GN_ERR_CUDA, "direct halo: a peer's step flag did not arrive within 10 s");
+    }
     if (bad) *bad = -1;
     for (int k = 0; k < done; ++k) {
         if (step_inf) step_inf[k] = h[(size_t)k * 4];
@@ -679,6 +780,136 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
         if (mass) mass[k] = h[(size_t)k * 4 + 2];
         if (bad && *bad < 0 && h[(size_t)k * 4 + 3] != 0.0) *bad = k;
     }
+    return GN_OK;
+}
+
+// ---- direct halo over peer memory
+int gn_part_peer_init(gn_part* p, int parts, int me, const int32_t* expect, int nexpect) {
+    if (!p || parts < 1 || me < 0 || me >= parts || nexpect < 0 || (nexpect > 0 && !expect))
+        return fail(GN_ERR_ARG, "bad gn_part_peer_init arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    for (int i = 0; i < nexpect; ++i)
+        if (expect[i] < 0 || expect[i] >= parts || expect[i] == me) return fail(GN_ERR_ARG, "bad expected peer");
+    part_free_push(p);
+    p->peers.clear();
+    p->h_push_row.clear();
+    p->h_push_peer.clear();
+    p->h_push_slot.clear();
+    if (p->parts != parts) {
+        cudaFree(p->inflags);
+        p->inflags = nullptr;
+        GN_CUDA(cudaMalloc((void**)&p->inflags, 8 * (size_t)parts));  // its own allocation: IPC-exportable
+    }
+    if (!p->halo_bad) GN_CUDA(cudaMalloc((void**)&p->halo_bad, sizeof(int)));
+    p->parts = parts;
+    p->me = me;
+    GN_CUDA(cudaMemset(p->inflags, 0, 8 * (size_t)parts));
+    GN_CUDA(cudaMemset(p->halo_bad, 0, sizeof(int)));
+    std::vector<int32_t> ex(expect, expect + nexpect);
+    if (int rc = upload_into(&p->expect, ex)) return rc;
+    p->nexpect = nexpect;
+    return GN_OK;
+}
+
+int gn_part_peer_buffers(const gn_part* p, void** yg0, void** yg1, void** inflags) {
+    if (!p || !p->yg[0]) return fail(GN_ERR_ARG, "gn_part_peer_buffers: call after gn_part_begin");
+    if (yg0) *yg0 = p->yg[0];
+    if (yg1) *yg1 = p->yg[1];
+    if (inflags) *inflags = p->inflags;
+    return GN_OK;
+}
+
+int gn_part_peer_add(gn_part* p, int rank, void* yg0, void* yg1, void* inflags, const int32_t* owned,
+                     int64_t count, int64_t slot0) {
+    if (!p || !yg0 || !yg1 || !inflags || count < 0 || (count > 0 && !owned) || slot0 < 0)
+        return fail(GN_ERR_ARG, "bad gn_part_peer_add arguments");
+    int idx = -1;
+    for (size_t j = 0; j < p->peers.size(); ++j)
+        if (p->peers[j].rank == rank) idx = (int)j;
+    if (idx < 0) {
+        idx = (int)p->peers.size();
+        p->peers.push_back(gn_part::Peer{rank, {yg0, yg1}, (int64_t*)inflags});
+    }
+    for (int64_t i = 0; i < count; ++i) {
+        if (owned[i] < 0 || owned[i] >= p->n_own) return fail(GN_ERR_ARG, "pushed row out of range");
+        const int32_t row = p->h_inv[(size_t)owned[i]];
+        if (row >= p->n_bnd) return fail(GN_ERR_ARG, "pushed row is not a boundary row (gn_part_set_boundary)");
+        p->h_push_row.push_back(row);
+        p->h_push_peer.push_back(idx);
+        p->h_push_slot.push_back(slot0 + i);
+    }
+    return GN_OK;
+}
+
+int gn_part_peer_commit(gn_part* p) {
+    if (!p) return fail(GN_ERR_ARG, "null partition");
+    GN_CUDA(cudaSetDevice(p->device));
+    part_free_push(p);
+    const size_t np = p->h_push_row.size();
+    std::vector<int32_t> ptr((size_t)p->n_bnd + 1, 0), peer(std::max<size_t>(np, 1)), order(np);
+    std::vector<int64_t> slot(std::max<size_t>(np, 1));
+    for (size_t e = 0; e < np; ++e) ptr[(size_t)p->h_push_row[e] + 1]++;
+    for (int64_t r = 0; r < p->n_bnd; ++r) ptr[(size_t)r + 1] += ptr[(size_t)r];
+    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t e = 0; e < np; ++e) {
+        const int32_t at = fill[(size_t)p->h_push_row[e]]++;
+        peer[(size_t)at] = p->h_push_peer[e];
+        slot[(size_t)at] = p->h_push_slot[e];
+    }
+    std::vector<void*> d0, d1;
+    std::vector<int64_t*> fl;
+    for (const auto& q : p->peers) {
+        d0.push_back(q.yg[0]);
+        d1.push_back(q.yg[1]);
+        fl.push_back(q.flags);
+    }
+    int rc;
+    if ((rc = upload_into(&p->push_ptr, ptr)) || (rc = upload_into(&p->push_peer, peer)) ||
+        (rc = upload_into(&p->push_slot, slot)) || (rc = upload_into(&p->push_dst[0], d0)) ||
+        (rc = upload_into(&p->push_dst[1], d1)) || (rc = upload_into(&p->peer_flags, fl)))
+        return rc;
+    p->npush_peers = (int)p->peers.size();
+    return GN_OK;
+}
+
+int gn_part_peer_wait(gn_part* p, int k, uintptr_t stream) {
+    if (!p || !p->inflags) return fail(GN_ERR_ARG, "gn_part_peer_wait before gn_part_peer_init");
+    if (k == 0 || p->nexpect == 0) return GN_OK;  // step 0 reads the ghosts of x0
+    k_part_wait<<<1, 32, 0, (cudaStream_t)stream>>>(p->inflags, p->expect, p->nexpect, k, p->halo_bad);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+int gn_part_peer_signal(gn_part* p, int k, uintptr_t stream) {
+    if (!p || !p->peer_flags) return fail(GN_ERR_ARG, "gn_part_peer_signal before gn_part_peer_commit");
+    if (p->npush_peers == 0) return GN_OK;
+    k_part_signal<<<1, 32, 0, (cudaStream_t)stream>>>(p->peer_flags, p->npush_peers, p->me, (int64_t)k + 1);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+// CUDA IPC of one allocation (the peer buffers of another process on the node)
+int gn_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */) {
+    if (!dptr || !handle) return fail(GN_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    GN_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, sizeof(h));
+    return GN_OK;
+}
+
+int gn_ipc_open_handle(const void* handle, int device, void** dptr) {
+    if (!handle || !dptr) return fail(GN_ERR_ARG, "null argument");
+    GN_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    GN_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return GN_OK;
+}
+
+int gn_ipc_close(void* dptr) {
+    if (!dptr) return GN_OK;
+    GN_CUDA(cudaIpcCloseMemHandle(dptr));
     return GN_OK;
 }
 

@@ -14,9 +14,13 @@ groups them by owning peer, since ranges are contiguous.  Every iteration:
              exchange runs while the interior rows are stepped
 
 Neighbour lists keep the global (reference) order, so a partitioned EXACT run
-is bitwise the single-GPU EXACT run (and the reference).  Exchanges: LocalExchange (all parts in one
-process, e.g. one GPU, for tests) and DistExchange (one part per rank,
-torch.distributed send/recv: NCCL over NVLink on GPUs, gloo on CPU tests).
+is bitwise the single-GPU EXACT run (and the reference).  Exchanges:
+LocalExchange (all parts in one process, e.g. one GPU, for tests) and
+DistExchange (one part per rank, torch.distributed send/recv: NCCL over
+NVLink on GPUs, gloo on CPU tests) pack, send and unpack; LocalPeerExchange
+and DistPeerExchange (CUDA IPC between the ranks of a node) fuse the halo
+into the boundary kernel: each boundary value is stored straight into the
+ghost slots of the peers that hold it, then a flag per peer (gn_part_peer_*).
 The compute backend is pluggable; EngineBackend is the CUDA engine.
 """
 
@@ -163,6 +167,30 @@ class EngineBackend:
         self.E.check(self.E.lib().gn_part_unpack(self.h, k, ctypes.c_void_p(buf.data_ptr()), first, buf.numel(),
                                                  self._stream()))
 
+    # ---- direct halo over peer memory (gn_part_peer_*)
+    def peer_init(self, parts: int, me: int, expect) -> None:
+        ex = np.ascontiguousarray(expect, dtype=np.int32)
+        self.E.check(self.E.lib().gn_part_peer_init(self.h, parts, me, self.E.ptr(ex), len(ex)))
+
+    def peer_buffers(self) -> tuple[int, int, int]:
+        a, b, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self.E.check(self.E.lib().gn_part_peer_buffers(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(f)))
+        return a.value, b.value, f.value
+
+    def peer_add(self, rank: int, bufs, owned, slot0: int) -> None:
+        own = np.ascontiguousarray(owned, dtype=np.int32)
+        self.E.check(self.E.lib().gn_part_peer_add(self.h, rank, bufs[0], bufs[1], bufs[2], self.E.ptr(own),
+                                                   len(own), int(slot0)))
+
+    def peer_commit(self) -> None:
+        self.E.check(self.E.lib().gn_part_peer_commit(self.h))
+
+    def peer_wait(self, k: int) -> None:
+        self.E.check(self.E.lib().gn_part_peer_wait(self.h, k, self._stream()))
+
+    def peer_signal(self, k: int) -> None:
+        self.E.check(self.E.lib().gn_part_peer_signal(self.h, k, self._stream()))
+
     def end(self, done: int):
         E = self.E
         x = np.empty(self.spec.n_own)
@@ -187,7 +215,25 @@ class EngineBackend:
 
 # ---------------------------------------------------------------- exchanges
 
-class LocalExchange:
+class _PackedHalo:
+    """Halo protocol of the pack / send / unpack exchanges: the boundary
+    values are packed and posted after the boundary rows, received and
+    unpacked after the interior rows."""
+
+    def setup(self) -> None:
+        pass
+
+    def before(self, k: int) -> None:
+        pass
+
+    def after_boundary(self, k: int):
+        return self.start(k)
+
+    def after_interior(self, k: int, pending) -> None:
+        self.finish(k, pending)
+
+
+class LocalExchange(_PackedHalo):
     """All partitions in this process: the halo is a buffer hand-over."""
 
     def __init__(self, backends: Sequence):
@@ -204,7 +250,7 @@ class LocalExchange:
         self.finish(k, self.start(k))
 
 
-class DistExchange:
+class DistExchange(_PackedHalo):
     """One partition per rank; grouped point-to-point sends/receives
     (torch.distributed: NCCL on GPUs, gloo on CPU)."""
 
@@ -241,6 +287,92 @@ class DistExchange:
         self.finish(k, self.start(k))
 
 
+def _expected_peers(spec: PartSpec) -> list[int]:
+    """Peers whose vertices this part holds as ghosts: they push to it (and,
+    the graph being symmetric, it pushes to them)."""
+    return [q for q in range(spec.parts) if q != spec.p and spec.ghost_ptr[q + 1] > spec.ghost_ptr[q]]
+
+
+class _PeerHalo:
+    """Halo protocol of the direct (peer-memory) exchanges: no host work per
+    iteration -- the boundary kernel pushes, then per-peer flags."""
+
+    def before(self, k: int) -> None:
+        for b in self._mine():
+            b.peer_wait(k)
+
+    def after_boundary(self, k: int):
+        return None
+
+    def after_interior(self, k: int, pending) -> None:
+        for b in self._mine():
+            b.peer_signal(k)
+
+
+class LocalPeerExchange(_PeerHalo):
+    """All partitions in this process (e.g. on one GPU): the boundary step of
+    each part stores its values straight into the other parts' ghost slots."""
+
+    def __init__(self, backends: Sequence):
+        self.backends = list(backends)
+
+    def _mine(self):
+        return self.backends
+
+    def setup(self) -> None:
+        for b in self.backends:
+            b.peer_init(b.spec.parts, b.spec.p, _expected_peers(b.spec))
+        bufs = [b.peer_buffers() for b in self.backends]
+        for p, b in enumerate(self.backends):
+            for q, owned in b.spec.send_idx.items():
+                peer = self.backends[q].spec
+                b.peer_add(q, bufs[q], owned, peer.n_own + int(peer.ghost_ptr[p]))
+            b.peer_commit()
+
+
+class DistPeerExchange(_PeerHalo):
+    """One partition per rank: the peers' buffers are mapped with CUDA IPC
+    (handles exchanged once per run over torch.distributed), and the boundary
+    kernel's stores travel over NVLink as the rows finish."""
+
+    def __init__(self, backend, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.b, self.group = dist, backend, group
+        self._opened: list[int] = []
+
+    def _mine(self):
+        return [self.b]
+
+    def setup(self) -> None:
+        E, b = self.b.E, self.b
+        spec = b.spec
+        for ptr in self._opened:
+            E.lib().gn_ipc_close(ptr)
+        self._opened = []
+        b.peer_init(spec.parts, spec.p, _expected_peers(spec))
+        handles = []
+        for ptr in b.peer_buffers():
+            h = ctypes.create_string_buffer(64)
+            E.check(E.lib().gn_ipc_get_handle(ptr, h))
+            handles.append(h.raw)
+        allh = [None] * spec.parts
+        self.dist.all_gather_object(allh, (spec.n_own, [int(x) for x in spec.ghost_ptr], handles), group=self.group)
+        dev = b.device.index or 0
+        for q, owned in spec.send_idx.items():
+            n_own_q, ghost_ptr_q, hq = allh[q]
+            ptrs = []
+            for raw in hq:
+                out = ctypes.c_void_p()
+                E.check(E.lib().gn_ipc_open_handle(ctypes.create_string_buffer(raw, 64), dev, ctypes.byref(out)))
+                ptrs.append(out.value)
+                self._opened.append(out.value)
+            b.peer_add(q, ptrs, owned, n_own_q + ghost_ptr_q[spec.p])
+        b.peer_commit()
+        # every rank has reset its flags (gn_part_begin) and mapped its peers
+        self.dist.barrier(group=self.group)
+
+
 @dataclass
 class PartResult:
     x: np.ndarray            # owned entries (clipped)
@@ -252,33 +384,47 @@ class PartResult:
 
 def partitioned_step(backend, exchange, k: int) -> None:
     """Step k of one partition with the halo overlapped: boundary rows, then
-    their exchange in flight while the interior rows run, then the ghosts."""
+    their exchange in flight while the interior rows run, then the ghosts
+    (pack/send/unpack exchanges), or the boundary rows' direct pushes and the
+    peer flags (peer exchanges)."""
+    exchange.before(k)
     backend.step_boundary(k)
-    pending = exchange.start(k)
+    pending = exchange.after_boundary(k)
     backend.step_interior(k)
-    exchange.finish(k, pending)
+    exchange.after_interior(k, pending)
 
 
 def run_partition(backend, exchange, x0_local: np.ndarray, schedule: GammaSchedule) -> PartResult:
     """The pursuit on one partition (all ranks call this together)."""
     gam = schedule.table()
     backend.begin(x0_local, gam)
+    exchange.setup()
     for k in range(len(gam)):
         partitioned_step(backend, exchange, k)
     x, si, fb, ms, bad = backend.end(len(gam))
     return PartResult(x, si, fb, ms, bad)
 
 
-def run_local_partitions(g, x0: np.ndarray, schedule: GammaSchedule, parts: int, make_backend) -> dict:
+def run_local_partitions(g, x0: np.ndarray, schedule: GammaSchedule, parts: int, make_backend,
+                         halo: str = "copy") -> dict:
     """All parts of g in this process (e.g. on one GPU): returns the global x
-    and the combined per-iteration trace (max / sum / sum over parts)."""
+    and the combined per-iteration trace (max / sum / sum over parts).
+    halo: "copy" (pack / hand-over / unpack) or "peer" (direct pushes)."""
     specs = build_partitions(g, parts)
     backends = [make_backend(s) for s in specs]
-    ex = LocalExchange(backends)
+    ex = LocalPeerExchange(backends) if halo == "peer" else LocalExchange(backends)
     gam = schedule.table()
     for b, s in zip(backends, specs):
         b.begin(s.local_x0(x0), gam)
+    ex.setup()
     for k in range(len(gam)):
+        if halo == "peer":
+            for b in backends:  # each part: wait, boundary (pushes), interior, flags
+                b.peer_wait(k)
+                b.step_boundary(k)
+                b.step_interior(k)
+                b.peer_signal(k)
+            continue
         for b in backends:
             b.step_boundary(k)
         pending = ex.start(k)

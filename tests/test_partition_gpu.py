@@ -37,3 +37,25 @@ def test_partitioned_fast_mode_within_tolerance(parts):
     np.testing.assert_allclose(out["step_inf"], ref.step_inf, rtol=1e-6, atol=1e-12)
     again = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"))
     np.testing.assert_array_equal(again["x"], out["x"])
+
+
+@pytest.mark.parametrize("dtype,parts", [("fp64", 3), ("fp32", 4)])
+def test_peer_halo_bitwise(dtype, parts):
+    # the boundary kernel stores straight into the peers' ghost slots (gn_part_peer_*)
+    inst = G.c5_rmat(13)
+    s = P.GammaSchedule.pursuit(iterations=200)
+    out = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype=dtype, exact=True),
+                               halo="peer")
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, dtype=dtype)
+    np.testing.assert_array_equal(out["x"], ref.x)
+    np.testing.assert_array_equal(out["step_inf"], ref.step_inf)
+    np.testing.assert_array_equal(out["fallbacks"], ref.fallbacks)
+
+
+def test_peer_halo_fast_mode_equals_copy_halo():
+    inst = G.c5_rmat(14)
+    s = P.GammaSchedule.pursuit(iterations=150)
+    a = run_local_partitions(inst.graph, inst.x0, s, 3, lambda sp: EngineBackend(sp, dtype="fp32"), halo="peer")
+    b = run_local_partitions(inst.graph, inst.x0, s, 3, lambda sp: EngineBackend(sp, dtype="fp32"), halo="copy")
+    np.testing.assert_array_equal(a["x"], b["x"])
+    np.testing.assert_array_equal(a["step_inf"], b["step_inf"])
