@@ -194,11 +194,14 @@ def run_reference(args, ws, rank):
 def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
     """C5 as BASELINE names it: the graph vertex-range partitioned over the N
     ranks (partition.py), each rank stepping its owned rows (gn_part_step) and
-    exchanging boundary values with its peers every iteration (NCCL
-    point-to-point through torch.distributed).  Strong scaling: the graph is
+    exchanging boundary values with its peers every iteration: the boundary
+    kernel's direct stores into the peers' ghost slots over NVLink (--halo
+    peer, the default) or NCCL point-to-point through torch.distributed
+    (--halo nccl).  Strong scaling: the graph is
     the same at every N.  Timed with CUDA events on the stream the engine and
     NCCL share, max over ranks."""
-    from paper_2605_05330_b200.partition import DistExchange, EngineBackend, build_partitions, partitioned_step
+    from paper_2605_05330_b200.partition import (DistExchange, DistPeerExchange, EngineBackend, build_partitions,
+                                                 partitioned_step)
 
     dtype = args.dtype or inst.dtype
     sched = P.GammaSchedule.pursuit(iterations=args.iters)
@@ -206,7 +209,9 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
     iters = len(gam)
     spec = build_partitions(inst.graph, ws)[rank]
     be = EngineBackend(spec, dtype=dtype, device=local)
-    ex = DistExchange(be) if ws > 1 else None
+    # the halo: direct stores into the peers' ghost slots over NVLink (CUDA IPC
+    # mappings, the default) or pack + NCCL send/recv + unpack (--halo nccl)
+    ex = (DistPeerExchange(be) if args.halo == "peer" else DistExchange(be)) if ws > 1 else None
     x0l = spec.local_x0(inst.x0)
     dev = torch.device("cuda", local)
 
@@ -217,6 +222,8 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
 
     def step():
         be.begin(x0l, gam)
+        if ex is not None:
+            ex.setup()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -247,6 +254,8 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
         barrier()
         t0 = time.perf_counter()
         be.begin(x0l, gam)
+        if ex is not None:
+            ex.setup()
         for k in range(iters):
             if ex is not None:
                 partitioned_step(be, ex, k)
@@ -285,7 +294,9 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
                     "api": "partition.EngineBackend begin/step/halo/end (host x0 in, owned x out), rank 0 shown"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None,
-                         "kernel": "gn::k_part_step (one launch per iteration and part) + NCCL halo",
+                         "kernel": "gn::k_part_step (one launch per iteration and part)" + (
+                             "" if ws == 1 else (" + direct peer halo (stores into peer ghost slots, CUDA IPC)"
+                                                 if args.halo == "peer" else " + NCCL halo")),
                          "b_iter": b_iter, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs) x n_gpus"},
             "cpu_baseline": None,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
@@ -310,6 +321,8 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="C5 under torchrun: direct stores into the peers' ghost slots (default) or NCCL send/recv")
     ap.add_argument("--partition", action="store_true",
                     help="C5: vertex-range partitioned engine (the default for C5 under torchrun, N>1)")
     ap.add_argument("--starts", type=int, default=1,

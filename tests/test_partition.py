@@ -159,3 +159,169 @@ def test_two_rank_gloo_halo_exchange_is_bitwise_unpartitioned():
     np.testing.assert_array_equal(x, ref.x)
     np.testing.assert_array_equal(np.max([o[2] for o in out], axis=0), ref.step_inf)
     np.testing.assert_array_equal(np.sum([o[3] for o in out], axis=0), ref.fallbacks)
+
+
+# ---- the direct (peer-memory) halo protocol, two processes on CPU --------
+# DistPeerExchange runs unchanged; the "device buffers" are POSIX shared
+# memory blocks and the "CUDA IPC handles" their names, so the handle
+# exchange, the slot arithmetic and the wait / push / signal ordering are
+# exercised with two ranks that really run concurrently.
+
+class _FakeLib:
+    def __init__(self, be):
+        self.be = be
+
+    def gn_ipc_get_handle(self, ptr, h):
+        import ctypes
+
+        name = self.be.names[ptr].encode().ljust(64, b"\0")
+        ctypes.memmove(h, name, 64)
+        return 0
+
+    def gn_ipc_open_handle(self, h, dev, pout):
+        from multiprocessing import shared_memory
+
+        name = bytes(h.raw).rstrip(b"\0").decode()
+        shm = shared_memory.SharedMemory(name=name)
+        pid = 10_000 + len(self.be.opened)
+        self.be.opened[pid] = shm
+        pout._obj.value = pid
+        return 0
+
+    def gn_ipc_close(self, ptr):
+        shm = self.be.opened.pop(ptr, None)
+        if shm is not None:
+            shm.close()
+        return 0
+
+
+class _FakeE:
+    def __init__(self, be):
+        self._lib = _FakeLib(be)
+
+    def lib(self):
+        return self._lib
+
+    @staticmethod
+    def check(rc):
+        assert rc == 0
+
+
+class NumpyPeerBackend(NumpyBackend):
+    """NumpyBackend whose halo is the peer protocol over shared memory."""
+
+    def __init__(self, spec):
+        super().__init__(spec)
+        from types import SimpleNamespace
+
+        self.E = _FakeE(self)
+        self.device = SimpleNamespace(index=0)
+        self.names, self.opened, self.own = {}, {}, []
+
+    def _block(self, key, shape, dtype):
+        from multiprocessing import shared_memory
+
+        shm = shared_memory.SharedMemory(create=True, size=max(int(np.prod(shape)) * np.dtype(dtype).itemsize, 8))
+        self.own.append(shm)
+        self.names[key] = shm.name
+        a = np.ndarray(shape, dtype=dtype, buffer=shm.buf)
+        a[...] = 0
+        return a
+
+    def _view(self, pid, dtype):
+        shm = self.opened[pid]
+        return np.ndarray((shm.size // np.dtype(dtype).itemsize,), dtype=dtype, buffer=shm.buf)
+
+    def begin(self, x0_local, gammas):
+        super().begin(x0_local, gammas)
+        nall = self.spec.n_own + self.spec.n_ghost
+        self.y = [self._block(1, (nall,), np.float64), self._block(2, (nall,), np.float64)]
+        self.y[0][:] = self.v * x0_local
+        self.y[1][:] = self.v * x0_local
+
+    def peer_init(self, parts, me, expect):
+        self.me, self.expect, self.pushes = me, list(expect), []
+        self.flags = self._block(3, (parts,), np.int64)
+
+    def peer_buffers(self):
+        return 1, 2, 3
+
+    def peer_add(self, rank, bufs, owned, slot0):
+        self.pushes.append((rank, bufs, np.asarray(owned), int(slot0)))
+
+    def peer_commit(self):
+        pass
+
+    def peer_wait(self, k):
+        import time
+
+        t0 = time.time()
+        while k > 0 and any(self.flags[q] < k for q in self.expect):
+            assert time.time() - t0 < 60, "peer flag did not arrive"
+            time.sleep(0.0005)
+
+    def step_boundary(self, k):
+        self.step(k)
+        nxt = self.y[(k & 1) ^ 1]
+        for rank, bufs, owned, slot0 in self.pushes:  # straight into the peer's ghost slots
+            self._view(bufs[(k + 1) & 1], np.float64)[slot0:slot0 + len(owned)] = nxt[owned]
+
+    def peer_signal(self, k):
+        for rank, bufs, owned, slot0 in self.pushes:
+            self._view(bufs[2], np.int64)[self.me] = k + 1
+
+    def close(self):
+        for shm in list(self.opened.values()) + self.own:
+            shm.close()
+        for shm in self.own:
+            shm.unlink()
+
+
+def _peer_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2605_05330_b200.partition import DistPeerExchange
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    be = None
+    try:
+        inst = _graph()
+        s = P.GammaSchedule.pursuit(iterations=120)
+        spec = build_partitions(inst.graph, world)[rank]
+        be = NumpyPeerBackend(spec)
+        res = run_partition(be, DistPeerExchange(be), spec.local_x0(inst.x0), s)
+        out = [None] * world
+        dist.all_gather_object(out, (spec.lo, res.x, res.step_inf, res.fallbacks))
+        if rank == 0:
+            q.put(out)
+        dist.barrier()
+    finally:
+        if be is not None:
+            be.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_halo_protocol_multiprocess_is_bitwise_unpartitioned(world):
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    x = np.concatenate([o[1] for o in out])
+    inst = _graph()
+    s = P.GammaSchedule.pursuit(iterations=120)
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma)
+    np.testing.assert_array_equal(x, ref.x)
+    np.testing.assert_array_equal(np.max([o[2] for o in out], axis=0), ref.step_inf)
