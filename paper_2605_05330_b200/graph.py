@@ -15,6 +15,7 @@ import ctypes
 
 import threading
 from collections import OrderedDict
+import dataclasses
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -336,18 +337,67 @@ def set_weight(g, members: Iterable[int]) -> float:
     return _member_report(g, _check_members(g, members))[0]
 
 
-@dataclass(frozen=True)
 class MisSolution:
     """A vertex subset claimed independent, with validity flags (graph.py:165-186).
 
     members is sorted ascending; weight is the recomputable sum of
     vertex weights over members.
+
+    Same fields, construction, equality, hashing, repr and immutability as
+    the reference's frozen dataclass.  A solution made by the engine keeps
+    its members as an index array and builds the ``members`` tuple of
+    Python ints on first access (a 14M-member R-MAT MIS costs ~0.4 s of
+    tuple building otherwise, paid only by callers that read it).
     """
 
-    members: tuple[int, ...]
-    weight: float
-    independent: bool
-    maximal: bool
+    __slots__ = ("_members", "_idx", "weight", "independent", "maximal")
+
+    def __init__(self, members: Iterable[int] = (), weight: float = 0.0, independent: bool = False,
+                 maximal: bool = False):
+        object.__setattr__(self, "_members", tuple(members))
+        object.__setattr__(self, "_idx", None)
+        object.__setattr__(self, "weight", weight)
+        object.__setattr__(self, "independent", independent)
+        object.__setattr__(self, "maximal", maximal)
+
+    @classmethod
+    def _lazy(cls, idx: np.ndarray, weight: float, independent: bool, maximal: bool) -> "MisSolution":
+        """From a sorted index array (engine results): members built on first access."""
+        sol = cls.__new__(cls)
+        object.__setattr__(sol, "_members", None)
+        object.__setattr__(sol, "_idx", np.asarray(idx, dtype=np.int64))
+        object.__setattr__(sol, "weight", weight)
+        object.__setattr__(sol, "independent", independent)
+        object.__setattr__(sol, "maximal", maximal)
+        return sol
+
+    @property
+    def members(self) -> tuple[int, ...]:
+        if self._members is None:
+            object.__setattr__(self, "_members", tuple(self._idx.tolist()))
+            object.__setattr__(self, "_idx", None)
+        return self._members
+
+    def __setattr__(self, name, value):
+        raise dataclasses.FrozenInstanceError(f"cannot assign to field {name!r}")
+
+    def __delattr__(self, name):
+        raise dataclasses.FrozenInstanceError(f"cannot delete field {name!r}")
+
+    def _key(self):
+        return (self.members, self.weight, self.independent, self.maximal)
+
+    def __eq__(self, other):
+        if other.__class__ is not self.__class__:
+            return NotImplemented
+        return self._key() == other._key()
+
+    def __hash__(self):
+        return hash(self._key())
+
+    def __repr__(self):
+        return (f"MisSolution(members={self.members!r}, weight={self.weight!r}, "
+                f"independent={self.independent!r}, maximal={self.maximal!r})")
 
     @classmethod
     def from_members(cls, g, members: Iterable[int]) -> "MisSolution":
