@@ -450,7 +450,7 @@ def main():
     gc.collect()
     gc.freeze()
     x0_host = torch.from_numpy(np.ascontiguousarray(inst.x0)).pin_memory().numpy()
-    e2e_t = []
+    e2e_t, round_t = [], []
     h2d = d2h = 0
     for i in range(args.warmup + args.steps):
         barrier()
@@ -469,6 +469,7 @@ def main():
                   f"call {r.stats['total_ms']:.2f} ms loop {r.stats['loop_ms']:.2f} ms", file=sys.stderr, flush=True)
         if i >= args.warmup:
             e2e_t.append(time.perf_counter() - t0)
+            round_t.append(time.perf_counter() - t1)
             h2d = r.stats["h2d_bytes"] + 8 * g.n * starts          # + the rounding's state upload
             d2h = r.stats["d2h_bytes"] + (g.n + 64) * starts       # + membership mask and flags
     del sol
@@ -540,7 +541,8 @@ def main():
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": ("paper_2605_05330_b200.run_multi + round_many" if starts > 1 else
-                        "paper_2605_05330_b200.run_engine + round_to_mis") + " (host numpy in, MIS out)"},
+                        "paper_2605_05330_b200.run_engine + round_to_mis") + " (host numpy in, MIS out)",
+                "round_ms_per_step": 1e3 * statistics.mean(round_t) if round_t else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_name,
