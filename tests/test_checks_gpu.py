@@ -5,6 +5,8 @@ rows (> 32768 neighbours, one CTA each)."""
 import numpy as np
 import pytest
 
+import gn_oracle as O
+
 import paper_2605_05330_b200 as P
 from paper_2605_05330_b200.graph import csr_from_edges
 
@@ -38,6 +40,10 @@ def test_zero_closed_neighbourhood_found_in_any_row_class(leaves):
     x1[leaves] = 1e-300  # one positive leaf: the centre passes, and so does every row
     x, tr = P.run_wrgn(g, x1, s)
     assert len(tr) == 5 and np.all(np.isfinite(x))
+    ref = O.run(g, x1, s.table(), s.final_gamma)  # hub rows of every class, int32 layouts from 40000 leaves
+    np.testing.assert_allclose(x, ref.x, rtol=1e-9, atol=0)
+    xe, _ = P.run_wrgn(g, x1, s, exact=True)
+    np.testing.assert_array_equal(xe, ref.x)
 
 
 @pytest.mark.parametrize("leaves", [5000, 40000])
