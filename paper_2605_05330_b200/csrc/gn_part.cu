@@ -146,10 +146,31 @@ struct PartPush {
     int64_t rows;
 };
 
+// Delta halo: the buffer a step writes was written two steps earlier, here
+// and in every peer ghost slot alike (both start as v * x0), so a value
+// bitwise equal to that one is already in place at the peers and is not
+// sent again -- exact, and converged vertices stop costing NVLink traffic.
 template <typename TG>
-__device__ __forceinline__ void push_row(const PartPush& P, int64_t i, const TG* __restrict__ ygo) {
+__device__ __forceinline__ TG push_old(const PartPush& P, int64_t i, const TG* __restrict__ ygo) {
+    return (P.ptr != nullptr && i < P.rows) ? ygo[i] : TG(0);
+}
+
+template <typename TG>
+__device__ __forceinline__ bool same_bits(TG a, TG b);
+template <>
+__device__ __forceinline__ bool same_bits<double>(double a, double b) {
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
+template <>
+__device__ __forceinline__ bool same_bits<float>(float a, float b) {
+    return __float_as_int(a) == __float_as_int(b);
+}
+
+template <typename TG>
+__device__ __forceinline__ void push_row(const PartPush& P, int64_t i, const TG* __restrict__ ygo, TG old) {
     if (P.ptr == nullptr || i >= P.rows) return;
     const TG val = ygo[i];  // written by this thread just before
+    if (same_bits(val, old)) return;
     for (int32_t e = P.ptr[i]; e < P.ptr[i + 1]; ++e) static_cast<TG*>(P.dst[P.peer[e]])[P.slot[e]] = val;
 }
 
@@ -194,8 +215,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
             if (lane == 0) {
+                const TG old = push_old<TG>(push, i, ygo);
                 part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-                push_row<TG>(push, i, ygo);
+                push_row<TG>(push, i, ygo, old);
             }
         }
     } else if ((int)blockIdx.x < nbl + ncb) {
@@ -213,8 +235,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
                 for (int u = 0; u < kPartUnroll; ++u) s = A::add(s, (TS)y[u]);
             }
             for (; p < re; ++p) s = A::add(s, (TS)yg[col[p]]);
+            const TG old = push_old<TG>(push, i, ygo);
             part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-            push_row<TG>(push, i, ygo);
+            push_row<TG>(push, i, ygo, old);
         }
     } else {
         const int64_t pos0 = n_long + n_csr;  // first order position of slice 0
@@ -251,8 +274,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int 
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
             if (valid) {
+                const TG old = push_old<TG>(push, i, ygo);
                 part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-                push_row<TG>(push, i, ygo);
+                push_row<TG>(push, i, ygo, old);
             }
         }
     }
