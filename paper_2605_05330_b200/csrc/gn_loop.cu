@@ -200,9 +200,12 @@ struct GSrc {
 // degree, row state and first index vectors are already loading, and item
 // i+2's descriptor too.  Each item costs about one memory round trip instead
 // of four dependent ones.
+#ifndef GN_GD_F32
+#define GN_GD_F32 16  // fp32 gathers: 32 in flight spilled (C2 fp32: 23.1 -> 19.4 us/iteration at 16; C5 unchanged)
+#endif
 template <typename TG>
 struct GatherDepth {  // gathers in flight per lane (register budget: 64K / (kThreads * kCtasPerSm))
-    static constexpr int value = (sizeof(TG) == 4 ? 32 : 16) / kCtasPerSm;
+    static constexpr int value = (sizeof(TG) == 4 ? GN_GD_F32 : 16) / kCtasPerSm;
 };
 
 template <typename TS, typename TI, typename TG>
