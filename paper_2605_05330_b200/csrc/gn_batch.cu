@@ -177,7 +177,7 @@ template <typename TS>
 struct OwnRows {
     TS x[kRowsPerThread], v[kRowsPerThread];
     double w[kRowsPerThread];
-    int deg[kRowsPerThread], go[kRowsPerThread], orig[kRowsPerThread];
+    int deg[kRowsPerThread], go[kRowsPerThread];  // original ids are re-read from lperm when needed
 };
 
 // One pass over the CTA's graph (tail: only the trace dots of the current
@@ -243,7 +243,7 @@ __device__ __forceinline__ void batch_pass(const BatchArgs<TS, TG>& a, OwnRows<T
         acc[3] = __dadd_rn(acc[3], __dmul_rn(R.w[q], (double)o));
         R.x[q] = o;
         yn[r] = (TG)A::mul(R.v[q], o);
-        if (a.x_hist) a.x_hist[(size_t)k * (size_t)a.n_total + (size_t)(v0 + R.orig[q])] = (double)o;
+        if (a.x_hist) a.x_hist[(size_t)k * (size_t)a.n_total + (size_t)(v0 + a.lperm[v0 + r])] = (double)o;
     }
     // one block reduction; its barrier also publishes yn
 #pragma unroll
@@ -315,10 +315,8 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_gn_batch(BatchArgs<TS, TG>
         R.v[q] = TS(0);
         R.w[q] = 0.0;
         R.go[q] = 0;
-        R.orig[q] = 0;
         if (r < nb) {
             const int o = a.lperm[v0 + r];
-            R.orig[q] = o;
             R.deg[q] = a.deg[v0 + r];
             R.go[q] = a.goff[g0 + r / 32] + (r % 32) * 2;
             const double w = a.w64[v0 + o];
@@ -367,7 +365,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_gn_batch(BatchArgs<TS, TG>
         if (r < nb) {
             double xo = (double)R.x[q];
             if (a.clip) xo = xo < 0.0 ? 0.0 : (xo > 1.0 ? 1.0 : xo);
-            a.x_out[v0 + R.orig[q]] = xo;
+            a.x_out[v0 + a.lperm[v0 + r]] = xo;
         }
     }
     if (threadIdx.x == 0) {
