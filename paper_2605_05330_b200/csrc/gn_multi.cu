@@ -44,7 +44,11 @@ namespace gn {
 
 constexpr int kMThreads = 512;
 constexpr int kMWarps = kMThreads / 32;
-constexpr int kMU = 16;       // gathers in flight per lane
+// gathers in flight per lane: 16 on graphs with long rows (C2: 13.6 us per
+// start-iteration against 15.8 with 8), 8 on short-row graphs, where the
+// deeper batch mostly masks and spills (C3 5.3 -> 4.8, R-MAT 24 636 -> 578)
+constexpr int kMUDeep = 16, kMUShort = 8;
+static inline int multi_mu(const gn_graph* g) { return g->n > 0 && g->nnz >= 64 * g->n ? kMUDeep : kMUShort; }
 constexpr int kMaxStarts = 64;
 
 template <typename TG>
@@ -94,7 +98,7 @@ struct MultiArgs {
     unsigned int* barrier;
 };
 
-template <int T>
+template <int T, int kMU>
 struct TeamIdx {
     static constexpr int NI = (kMU + T - 1) / T;  // index registers per lane
     // positions q + i*T + t (i*T + t < kMU) of a segment of length len
@@ -111,19 +115,19 @@ struct TeamIdx {
 // Sequential sum, for the lane's S starts, of positions [0, len) of one row
 // segment (colp = its first column index); idx holds the first index chunk.
 // lmax / lmin: the warp's longest / shortest segment (all teams step together).
-template <typename TS, typename TG, int T>
+template <typename TS, typename TG, int T, int kMU>
 __device__ __forceinline__ void team_sum(const int32_t* __restrict__ colp, int len, int lmax, int lmin,
-                                         int (&idx)[TeamIdx<T>::NI], const TG* __restrict__ ybase, int Bp,
+                                         int (&idx)[TeamIdx<T, kMU>::NI], const TG* __restrict__ ybase, int Bp,
                                          int tbase, int t, TS (&acc)[Pack<TG>::S]) {
     using A = Arith<TS>;
     using P = Pack<TG>;
     using PT = typename P::T;
-    constexpr int S = P::S, NI = TeamIdx<T>::NI;
+    constexpr int S = P::S, NI = TeamIdx<T, kMU>::NI;
 #pragma unroll
     for (int s = 0; s < S; ++s) acc[s] = TS(0);
     for (int q = 0; q < lmax; q += kMU) {
         int nidx[NI];
-        TeamIdx<T>::load(colp, q + kMU, len, t, nidx);
+        TeamIdx<T, kMU>::load(colp, q + kMU, len, t, nidx);
         PT val[kMU];
         if (q + kMU <= lmin) {
 #pragma unroll
@@ -228,10 +232,10 @@ __device__ __forceinline__ void step_segment(StepPos q, const RowDesc& d, int te
     len = (int)((int64_t)d.deg * (part + 1) / parts) - beg;
 }
 
-template <typename TS, typename TG, int T>
+template <typename TS, typename TG, int T, int kMU>
 __global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) {
     using A = Arith<TS>;
-    using TI = TeamIdx<T>;
+    using TI = TeamIdx<T, kMU>;
     constexpr int S = Pack<TG>::S, NI = TI::NI;
     constexpr int RPW = 32 / T;              // rows a warp works at once
     constexpr int NT = kMWarps * RPW;        // teams per CTA
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_gn_multi(MultiArgs<TS, TG> a) 
             const int lmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)l0);
             const int lmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)l0);
             TS acc[S];
-            team_sum<TS, TG, T>(a.col + d0.rb + b0, l0, lmax, lmin, idx, ybase, Bp, tbase, t, acc);
+            team_sum<TS, TG, T, kMU>(a.col + d0.rb + b0, l0, lmax, lmin, idx, ybase, Bp, tbase, t, acc);
             if (q0.ph == kStepTeam) {
                 if (d0.r >= 0) {
 #pragma unroll
@@ -575,7 +579,7 @@ static int multi_plan(gn_graph* g, int G, bool exact, int rpw, const MultiPlan**
     const double share = total / nw;  // one warp's fair share
     // fast mode: rows longer than a warp's share (and 2048) are split over a
     // CTA; rows whose walk would outlast a team's share are split over a warp
-    const double cta_min = std::max(2048.0, share), warp_min = std::max(2.0 * kMU, share / rpw);
+    const double cta_min = std::max(2048.0, share), warp_min = std::max(2.0 * kMUDeep, share / rpw);
     std::vector<int32_t> split, wrows, trows;
     trows.reserve((size_t)n);
     for (int64_t i = 0; i < n; ++i) {
@@ -640,20 +644,20 @@ static int multi_plan(gn_graph* g, int G, bool exact, int rpw, const MultiPlan**
     return GN_OK;
 }
 
-template <typename TS, typename TG, int T>
-static void* multi_kernel() {
-    return (void*)k_gn_multi<TS, TG, T>;
+template <typename TS, typename TG, int MU>
+static void* pick_kernel_mu(int T) {
+    switch (T) {
+        case 2: return (void*)k_gn_multi<TS, TG, 2, MU>;
+        case 4: return (void*)k_gn_multi<TS, TG, 4, MU>;
+        case 8: return (void*)k_gn_multi<TS, TG, 8, MU>;
+        case 16: return (void*)k_gn_multi<TS, TG, 16, MU>;
+        default: return (void*)k_gn_multi<TS, TG, 32, MU>;
+    }
 }
 
 template <typename TS, typename TG>
-static void* pick_kernel(int T) {
-    switch (T) {
-        case 2: return multi_kernel<TS, TG, 2>();
-        case 4: return multi_kernel<TS, TG, 4>();
-        case 8: return multi_kernel<TS, TG, 8>();
-        case 16: return multi_kernel<TS, TG, 16>();
-        default: return multi_kernel<TS, TG, 32>();
-    }
+static void* pick_kernel(int T, int mu) {
+    return mu == kMUDeep ? pick_kernel_mu<TS, TG, kMUDeep>(T) : pick_kernel_mu<TS, TG, kMUShort>(T);
 }
 
 // stream-ordered scratch owned by one call
@@ -760,7 +764,7 @@ static int multi_typed(gn_graph* g, int B, const double* x0, const double* gamma
         GN_LAUNCHED();
     }
 
-    void* kern = pick_kernel<TS, TG>(T);
+    void* kern = pick_kernel<TS, TG>(T, multi_mu(g));
     int maxb = 1;
     if ((rc = coresident_blocks(kern, kMThreads, 0, g->device, &maxb))) return rc;
     if (maxb < 1) return fail(GN_ERR_CUDA, "multi-start kernel cannot be resident");
