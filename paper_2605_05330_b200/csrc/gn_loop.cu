@@ -203,9 +203,12 @@ struct GSrc {
 #ifndef GN_GD_F32
 #define GN_GD_F32 16  // fp32 gathers: 32 in flight spilled (C2 fp32: 23.1 -> 19.4 us/iteration at 16; C5 unchanged)
 #endif
+#ifndef GN_GD_F64
+#define GN_GD_F64 16
+#endif
 template <typename TG>
 struct GatherDepth {  // gathers in flight per lane (register budget: 64K / (kThreads * kCtasPerSm))
-    static constexpr int value = (sizeof(TG) == 4 ? GN_GD_F32 : 16) / kCtasPerSm;
+    static constexpr int value = (sizeof(TG) == 4 ? GN_GD_F32 : GN_GD_F64) / kCtasPerSm;
 };
 
 template <typename TS, typename TI, typename TG>
