@@ -181,8 +181,11 @@ __device__ __forceinline__ void push_row(const PartPush& P, int64_t i, const TG*
 // blocks give one warp to each slice of the blocked SELL, one thread per row.
 // Every thread-per-row sum is sequential in the reference's order (bitwise),
 // with 8 gathers in flight and the next index vectors loading under them.
+#ifndef GN_PART_MINB
+#define GN_PART_MINB 1
+#endif
 template <typename TS, typename TG>
-__global__ void __launch_bounds__(kPartThreads) k_part_step(int64_t n_long, int nbl, int64_t n_csr, int ncb,
+__global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_t n_long, int nbl, int64_t n_csr, int ncb,
                                                             int64_t count, const int32_t* __restrict__ order,
                                                             const int32_t* __restrict__ rowptr,
                                                             const int32_t* __restrict__ col,
