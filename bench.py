@@ -303,6 +303,9 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
             "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
+    if ex is not None and hasattr(ex, "close"):
+        barrier()  # no peer still writes into our buffers
+        ex.close()
     be.close()
     if ws > 1:
         torch.distributed.destroy_process_group()

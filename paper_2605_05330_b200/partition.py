@@ -372,6 +372,12 @@ class DistPeerExchange(_PeerHalo):
         # every rank has reset its flags (gn_part_begin) and mapped its peers
         self.dist.barrier(group=self.group)
 
+    def close(self) -> None:
+        """Unmap the peers' buffers (after the last run)."""
+        for ptr in self._opened:
+            self.b.E.lib().gn_ipc_close(ptr)
+        self._opened = []
+
 
 @dataclass
 class PartResult:
