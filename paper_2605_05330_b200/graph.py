@@ -395,6 +395,9 @@ class MisSolution:
     def __hash__(self):
         return hash(self._key())
 
+    def __reduce__(self):  # pickle / copy: the reference dataclass's fields
+        return (MisSolution, (self.members, self.weight, self.independent, self.maximal))
+
     def __repr__(self):
         return (f"MisSolution(members={self.members!r}, weight={self.weight!r}, "
                 f"independent={self.independent!r}, maximal={self.maximal!r})")

@@ -46,3 +46,18 @@ def test_no_cpu_fallback_without_device():
         P.round_to_mis(g, np.array([1.0, 0.0, 1.0]))
     with pytest.raises(P.EngineUnavailable):
         P.gn_step(g, [1, 1, 1], 1.0)
+
+
+def test_mis_solution_value_semantics():
+    import copy
+    import pickle
+
+    from paper_2605_05330_b200.graph import MisSolution
+
+    a = MisSolution(members=(1, 5, 7), weight=2.5, independent=True, maximal=False)
+    b = MisSolution._lazy(np.array([1, 5, 7]), 2.5, True, False)  # as engine results are built
+    assert a == b and hash(a) == hash(b) and repr(a) == repr(b)
+    assert pickle.loads(pickle.dumps(b)) == a and copy.deepcopy(b) == a
+    assert b.members == (1, 5, 7) and all(type(m) is int for m in b.members)
+    with pytest.raises(Exception):
+        b.weight = 3.0
