@@ -163,7 +163,8 @@ int gn_multi_run(gn_graph* g, int num_starts, const double* x0,
  * gn_run gives graph by graph -- on one CTA with the graph resident in shared
  * memory.  Graphs must have <= 4096 vertices and fit in shared memory.
  * Outputs are per graph: step_inf / fallbacks / mass are [B][iters],
- * iters_run / status (GN_OK or the gn_run error code) / fail_iter are [B]. */
+ * iters_run / status (GN_OK or the gn_run error code) / fail_iter are [B];
+ * trace entries past a graph's iters_run are written as 0. */
 typedef struct gn_batch gn_batch;
 int gn_batch_create(int64_t num_graphs, const int64_t* offsets, int64_t n,
                     const int64_t* indptr, const int32_t* indices,
