@@ -474,7 +474,8 @@ def main():
             e2e_t.append(time.perf_counter() - t0)
             round_t.append(time.perf_counter() - t1)
             h2d = r.stats["h2d_bytes"] + 8 * g.n * starts          # + the rounding's state upload
-            d2h = r.stats["d2h_bytes"] + (g.n + 64) * starts       # + membership mask and flags
+            # + the rounding's output: member ids (round_to_mis) or membership masks (round_many), and flags
+            d2h = r.stats["d2h_bytes"] + (8 * len(sol._idx) + 64 if starts == 1 else (g.n + 64) * starts)
     del sol
     e2e_total = sum(e2e_t)
     if ws > 1:

@@ -126,6 +126,12 @@ int gn_fitness(gn_graph* g, const double* p, double gamma, double* f_out,
  * sum over members in ascending order (bitwise equal to w[idx].sum()). */
 int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected,
              double* weight, int* independent, int* maximal, int64_t* count);
+/* gn_round returning the members themselves: members (capacity n) receives
+ * the *count selected vertex ids in ascending order, compacted on the device
+ * (what MisSolution.members holds; replaces the host scan of the mask). */
+int gn_round_members(gn_graph* g, const void* x, uint32_t flags,
+                     int64_t* members, double* weight, int* independent,
+                     int* maximal, int64_t* count);
 /* round_to_mis of num_states states (x: [num_states][n] fp64, host or, with
  * GN_DEVICE_IO, device) with one synchronisation: selected [num_states][n]
  * (may be NULL), weight / independent / maximal / count [num_states]. */

@@ -61,6 +61,7 @@ EXPORTED = (
     "gn_simplex_state",
     "gn_fitness",
     "gn_round",
+    "gn_round_members",
     "gn_round_many",
     "gn_check_members",
     "gn_multi_run",
@@ -153,6 +154,7 @@ _SIGNATURES = {
     "gn_simplex_state": (_I32, [_P, _P, _P]),
     "gn_fitness": (_I32, [_P, _P, _D, _P, _PD]),
     "gn_round": (_I32, [_P, _P, _U32, _P, _PD, _PI, _PI, _PI64]),
+    "gn_round_members": (_I32, [_P, _P, _U32, _P, _PD, _PI, _PI, _PI64]),
     "gn_round_many": (_I32, [_P, _I32, _P, _U32, _P, _P, _P, _P, _P]),
     "gn_check_members": (_I32, [_P, _P, _PD, _PI, _PI, _PI64]),
     "gn_multi_run": (

@@ -396,7 +396,7 @@ static int enqueue_round(gn_graph* g, RoundScratch& R, const TI* dx, uint8_t* se
 
 // B roundings (states x[b], host or device fp64) with one synchronisation.
 static int round_batch(gn_graph* g, int B, const double* x, bool dev_x, uint8_t* selected, double* weight,
-                       int* independent, int* maximal, int64_t* count) {
+                       int* independent, int* maximal, int64_t* count, int64_t* members = nullptr) {
     CallCtx ctx;
     int rc = ctx.open(g->device);
     if (rc) return rc;
@@ -420,6 +420,19 @@ static int round_batch(gn_graph* g, int B, const double* x, bool dev_x, uint8_t*
         rc = enqueue_round<double>(g, R, xs + (size_t)b * n, sel + nb * b);
         if (rc == GN_OK) rc = enqueue_check(g, R, sel + nb * b, dflags + 3 * b, dflags + 3 * b + 2, dw + b);
     }
+    // the member list of a single rounding, compacted on the device (B == 1)
+    int64_t *dmem = nullptr, *dmcnt = nullptr;
+    void* mtmp = nullptr;
+    if (members && rc == GN_OK && n > 0) {
+        size_t tb = 0;
+        thrust::counting_iterator<int64_t> ids(0);
+        GN_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, sel, dmem, dmcnt, (int)n, s));
+        GN_CUDA(cudaMallocAsync(&mtmp, std::max<size_t>(tb, 16), s));
+        GN_CUDA(cudaMallocAsync((void**)&dmem, 8 * nb, s));
+        GN_CUDA(cudaMallocAsync((void**)&dmcnt, 8, s));
+        GN_CUDA(cub::DeviceSelect::Flagged(mtmp, tb, ids, sel, dmem, dmcnt, (int)n, s));
+        note_launch();
+    }
     std::vector<int> hf(3 * (size_t)B);
     if (rc == GN_OK) {
         cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, s);
@@ -428,10 +441,20 @@ static int round_batch(gn_graph* g, int B, const double* x, bool dev_x, uint8_t*
             for (int b = 0; b < B; ++b)
                 cudaMemcpyAsync(selected + (size_t)n * b, sel + nb * b, (size_t)n, cudaMemcpyDeviceToHost, s);
     }
-    void* ptrs[] = {sel, dx, dw, dflags};
+    cudaError_t e = cudaSuccess;
+    if (dmem) {
+        // the count decides how many ids come back: one extra synchronisation
+        int64_t hcnt = 0;
+        cudaMemcpyAsync(&hcnt, dmcnt, 8, cudaMemcpyDeviceToHost, s);
+        e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess && hcnt > 0)
+            cudaMemcpyAsync(members, dmem, 8 * (size_t)hcnt, cudaMemcpyDeviceToHost, s);
+    }
+    void* ptrs[] = {sel, dx, dw, dflags, dmem, dmcnt, mtmp};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, s);
-    cudaError_t e = cudaStreamSynchronize(s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
     if (rc != GN_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "round sync", __FILE__, __LINE__);
     for (int b = 0; b < B; ++b) {
@@ -454,6 +477,14 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected, doub
     if (g->n > 0 && !x) return fail(GN_ERR_ARG, "null state");
     return round_batch(g, 1, (const double*)x, (flags & GN_DEVICE_IO) != 0, selected, weight, independent, maximal,
                        count);
+}
+
+int gn_round_members(gn_graph* g, const void* x, uint32_t flags, int64_t* members, double* weight, int* independent,
+                     int* maximal, int64_t* count) {
+    if (!g) return fail(GN_ERR_ARG, "null graph");
+    if (g->n > 0 && (!x || !members)) return fail(GN_ERR_ARG, "null state or member buffer");
+    return round_batch(g, 1, (const double*)x, (flags & GN_DEVICE_IO) != 0, nullptr, weight, independent, maximal,
+                       count, members);
 }
 
 int gn_round_many(gn_graph* g, int num_states, const void* x, uint32_t flags, uint8_t* selected, double* weight,

@@ -59,3 +59,22 @@ def test_nan_and_negative_entries_in_long_rows(leaves):
     x[leaves // 2] = np.nan
     with pytest.raises(P.NormalizationError):
         P.run_wrgn(g, x, s)
+
+
+@pytest.mark.parametrize("n,p", [(0, 0.0), (1, 0.0), (300, 0.05), (20000, 0.0005)])
+def test_round_members_match_the_mask(n, p):
+    """round_to_mis's device-compacted member ids (gn_round_members) equal the
+    mask of gn_round, and the flags and weight agree."""
+    from paper_2605_05330_b200.dynamics import round_result
+
+    rng = np.random.default_rng([7, n])
+    iu, ju = np.triu_indices(n, 1) if n < 1000 else (rng.integers(0, n, 10 * n), rng.integers(0, n, 10 * n))
+    keep = (rng.random(len(iu)) < p) & (iu != ju) if n < 1000 else iu != ju
+    indptr, indices = csr_from_edges(n, iu[keep], ju[keep])
+    g = P.from_csr(n, indptr, indices, 1.0 - rng.random(n))
+    x = rng.random(n)
+    sol = P.round_to_mis(g, x)
+    sel, weight, ind, mx = round_result(g, x)
+    assert sol.members == tuple(int(i) for i in np.flatnonzero(sel))
+    assert (sol.weight, sol.independent, sol.maximal) == (weight, ind, mx)
+    assert sol.independent and sol.maximal
