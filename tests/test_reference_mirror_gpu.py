@@ -287,3 +287,31 @@ def test_concurrent_callers_are_deterministic():
     with ThreadPoolExecutor(6) as pool:
         parallel = list(pool.map(one, x0s))
     assert serial == parallel
+
+
+@pytest.mark.parametrize("n", [6000, 120000])
+def test_concurrent_callers_on_the_loop_kernel_are_deterministic(n):
+    """Threads sharing one graph large enough for the cooperative loop kernel
+    (and the cooperative greedy of the rounding) -- a few CTAs, and a grid
+    that fills the GPU: each call owns its stream and workspace, so results
+    equal the serial ones bit for bit."""
+    from paper_2605_05330_b200.graph import csr_from_edges
+
+    rng = np.random.default_rng(11)
+    us, vs = rng.integers(0, n, 8 * n), rng.integers(0, n, 8 * n)
+    keep = us != vs
+    indptr, indices = csr_from_edges(n, us[keep], vs[keep])
+    g = P.from_csr(n, indptr, indices, 1.0 - rng.random(n))
+    s = P.GammaSchedule.pursuit(iterations=200)
+    x0s = [P.init_random(n, [1, i]) for i in range(8)]
+    assert P.run_engine(g, x0s[0], s).stats["grid_blocks"] > (1 if n < 10000 else 100)
+
+    def one(x0):
+        x, tr = P.run_wrgn(g, x0, s)
+        sol = P.round_to_mis(g, x)
+        return x.tobytes(), tuple(tr.step_inf), sol.members, sol.weight
+
+    serial = [one(x0) for x0 in x0s]
+    with ThreadPoolExecutor(8) as pool:
+        parallel = list(pool.map(one, x0s))
+    assert serial == parallel
