@@ -743,69 +743,62 @@ __global__ void k_prepare(int64_t n, const double* __restrict__ x0, const int32_
 // predicate.
 __global__ void k_precheck_f64(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                const double* __restrict__ x, int* __restrict__ flags) {
+    // With no negative entry (flags[0] takes precedence) x_i + sum_j x_j is a
+    // sum of nonnegatives: it is > 0 iff some term is > 0, and NaN iff some
+    // term is NaN -- and a NaN vertex fails its own row.  So each vertex tests
+    // itself for NaN, and only rows whose own entry is not positive look at
+    // their neighbours, stopping at the first positive one.
     const int lane = threadIdx.x & 31;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid = i < n;
-    const int32_t beg = valid ? rowptr[i] : 0, end = valid ? rowptr[i + 1] : 0;
     const double xi = valid ? x[i] : 1.0;
     if (xi < 0.0) atomicOr(&flags[0], 1);  // dynamics.py:146
+    const bool need = valid && !(xi > 0.0) && xi == xi;
+    const int32_t beg = need ? rowptr[i] : 0, end = need ? rowptr[i + 1] : 0;
     const bool lng = end - beg > 1024 && end - beg <= kGiantRow;  // giant rows: k_precheck_giant
-    bool ok = true;
-    if (valid && end - beg <= 1024) {  // 16 loads in flight per batch
-        bool pos = xi > 0.0, nan = xi != xi;
+    bool ok = xi == xi;  // dynamics.py:125 (NaN row)
+    if (need && end - beg <= 1024) {  // 16 loads in flight per batch
+        bool pos = false;
         int32_t p = beg;
-        for (; p + 16 <= end; p += 16) {
+        for (; p + 16 <= end && !pos; p += 16) {
             int32_t j[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) j[u] = col[p + u];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const double v = x[j[u]];
-                pos |= v > 0.0;
-                nan |= v != v;
-            }
+            for (int u = 0; u < 16; ++u) pos |= x[j[u]] > 0.0;
         }
-        for (; p < end; ++p) {
-            const double v = x[col[p]];
-            pos |= v > 0.0;
-            nan |= v != v;
-        }
-        ok = pos && !nan;  // dynamics.py:125
+        for (; p < end && !pos; ++p) pos |= x[col[p]] > 0.0;
+        ok = pos;
     }
     unsigned m = __ballot_sync(0xffffffffu, lng);
     while (m) {
         const int l = __ffs(m) - 1;
         m &= m - 1;
         const int32_t bl = __shfl_sync(0xffffffffu, beg, l), el = __shfl_sync(0xffffffffu, end, l);
-        const double xl = __shfl_sync(0xffffffffu, xi, l);
-        bool pos = false, nan = false;
-        for (int32_t p = bl + lane; p < el; p += 32) {
-            const double v = x[col[p]];
-            pos |= v > 0.0;
-            nan |= v != v;
+        bool pos = false;
+        for (int32_t b0 = bl; b0 < el; b0 += 32) {  // uniform trip: the vote is warp-wide
+            if (b0 + lane < el) pos |= x[col[b0 + lane]] > 0.0;
+            if (__any_sync(0xffffffffu, pos)) break;
         }
-        pos = __any_sync(0xffffffffu, pos) || xl > 0.0;
-        nan = __any_sync(0xffffffffu, nan) || xl != xl;
-        if (lane == l) ok = pos && !nan;
+        pos = __any_sync(0xffffffffu, pos);
+        if (lane == l) ok = pos;
     }
     if (!ok) atomicOr(&flags[1], 1);
 }
 
-// the rows above kGiantRow (original ids perm[0, ngiant)), one CTA each
+// the rows above kGiantRow (original ids perm[0, ngiant)), one CTA each; as
+// above, a row whose own entry is positive (or NaN: its own thread flagged it)
+// needs no scan
 __global__ void k_precheck_giant(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowptr,
                                  const int32_t* __restrict__ col, const double* __restrict__ x,
                                  int* __restrict__ flags) {
     const int i = perm[blockIdx.x];
     const double xi = x[i];
-    bool pos = xi > 0.0, nan = xi != xi;
-    for (int32_t p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) {
-        const double v = x[col[p]];
-        pos |= v > 0.0;
-        nan |= v != v;
-    }
+    if (xi > 0.0 || xi != xi) return;
+    bool pos = false;
+    for (int32_t p = rowptr[i] + threadIdx.x; p < rowptr[i + 1]; p += blockDim.x) pos |= x[col[p]] > 0.0;
     pos = __syncthreads_or(pos);
-    nan = __syncthreads_or(nan);
-    if (threadIdx.x == 0 && !(pos && !nan)) atomicOr(&flags[1], 1);  // dynamics.py:125
+    if (threadIdx.x == 0 && !pos) atomicOr(&flags[1], 1);  // dynamics.py:125
 }
 
 // final state (new order) -> fp64 output (original order), np.clip(x, 0, 1)

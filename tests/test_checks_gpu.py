@@ -78,3 +78,41 @@ def test_round_members_match_the_mask(n, p):
     assert sol.members == tuple(int(i) for i in np.flatnonzero(sel))
     assert (sol.weight, sol.independent, sol.maximal) == (weight, ind, mx)
     assert sol.independent and sol.maximal
+
+
+@pytest.mark.parametrize("leaves", [600, 5000, 40000])
+@pytest.mark.parametrize("pattern", ["sparse_pos", "centre_only", "one_leaf", "nan_leaf", "nan_partner", "all_zero_leaves"])
+def test_x0_check_early_exit_matches_the_reference_predicate(leaves, pattern):
+    """The run's x0 check stops a row at its first positive entry and tests
+    NaN per vertex; on rows of every length class it must agree with the
+    reference predicate all(x + A @ x > 0) (dynamics.py:122-126,148-149)."""
+    import scipy.sparse as sp
+
+    g, _ = _star_with_partners(leaves)
+    n = g.n
+    rng = np.random.default_rng([leaves, len(pattern)])
+    x = np.zeros(n)
+    if pattern == "sparse_pos":
+        x[rng.choice(n, n // 3, replace=False)] = rng.random(n // 3) + 0.1
+    elif pattern == "centre_only":
+        x[0] = 1.0
+    elif pattern == "one_leaf":
+        x[leaves] = 1e-300
+        x[leaves + 1 :] = 0.5
+    elif pattern == "nan_leaf":
+        x[:] = 0.5
+        x[leaves // 2 + 1] = np.nan
+    elif pattern == "nan_partner":
+        x[:] = 0.5
+        x[-1] = np.nan
+    else:
+        x[leaves + 1 :] = 0.5
+    A = sp.csr_matrix((np.ones(len(g.indices)), g.indices, g.indptr), shape=(n, n))
+    with np.errstate(invalid="ignore"):
+        expect = bool(np.all(x + A @ x > 0))
+    s = P.GammaSchedule.pursuit(iterations=2)
+    if expect:
+        P.run_wrgn(g, x, s)
+    else:
+        with pytest.raises(P.NormalizationError, match="zero closed neighborhood sum"):
+            P.run_wrgn(g, x, s)
