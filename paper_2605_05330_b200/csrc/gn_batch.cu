@@ -382,9 +382,17 @@ __global__ void k_precheck_batch(int64_t n, const int32_t* __restrict__ rowptr, 
     const double xi = x[i];
     const int b = gid[i];
     if (xi < 0.0) atomicOr(&flags[2 * b], 1);
-    double s = 0.0;
-    for (int32_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = __dadd_rn(s, x[col[p]]);
-    if (!(__dadd_rn(xi, s) > 0.0)) atomicOr(&flags[2 * b + 1], 1);
+    // with no negative entry in the graph (reported first) the closed sum is
+    // > 0 iff some entry is > 0 and NaN iff some entry is NaN (whose own row
+    // fails): only rows with x_i == 0 scan, up to their first positive neighbour
+    if (xi != xi) {
+        atomicOr(&flags[2 * b + 1], 1);
+        return;
+    }
+    if (xi > 0.0) return;
+    bool pos = false;
+    for (int32_t p = rowptr[i]; p < rowptr[i + 1] && !pos; ++p) pos = x[col[p]] > 0.0;
+    if (!pos) atomicOr(&flags[2 * b + 1], 1);
 }
 
 // Per-graph outputs in the caller's [B][iters] layout, made on the device so

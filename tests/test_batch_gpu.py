@@ -72,3 +72,32 @@ def test_c4_shard_batch_vs_packed_streaming():
     np.testing.assert_array_equal(res.x, packed.x)
     np.testing.assert_array_equal(res.step_inf.max(axis=0), np.array(packed.trace.step_inf))
     np.testing.assert_array_equal(res.fallbacks.sum(axis=0), np.array(packed.trace.fallbacks))
+
+
+def test_batch_x0_checks_match_the_reference_predicate():
+    """Per-graph x0 checks (early exit at the first positive entry, NaN per
+    vertex) against all(x + A @ x > 0) on sparse-zero, NaN and all-zero starts."""
+    import scipy.sparse as sp
+
+    graphs = _corpus(40, seed=31)
+    rng = np.random.default_rng(5)
+    x0s = []
+    for k, g in enumerate(graphs):
+        x = np.zeros(g.n)
+        kind = k % 4
+        if kind == 0:
+            x = P.init_random(g.n, [3, k])
+        elif kind == 1:  # mostly zero: some rows have no positive closed entry
+            pick = rng.random(g.n) < 0.15
+            x[pick] = rng.random(int(pick.sum())) + 0.01
+        elif kind == 2:
+            x = P.init_random(g.n, [3, k])
+            x[int(rng.integers(g.n))] = np.nan
+        x0s.append(x)
+    bt = GraphBatch.from_graphs(graphs)
+    res = bt.run(np.concatenate(x0s), P.GammaSchedule.pursuit(iterations=5))
+    for b, (g, x) in enumerate(zip(graphs, x0s)):
+        A = sp.csr_matrix((np.ones(len(g.indices)), g.indices, g.indptr), shape=(g.n, g.n))
+        with np.errstate(invalid="ignore"):
+            ok = bool(np.all(x + A @ x > 0))
+        assert res.status[b] == (0 if ok else 4), (b, k % 4)
