@@ -1,6 +1,7 @@
 """The C-ABI library loads and exports every symbol include/gn_b200.h
 declares; without a device every entry point fails loudly (no CPU path)."""
 
+import ctypes
 import re
 from pathlib import Path
 
@@ -61,3 +62,34 @@ def test_mis_solution_value_semantics():
     assert b.members == (1, 5, 7) and all(type(m) is int for m in b.members)
     with pytest.raises(Exception):
         b.weight = 3.0
+
+
+def test_null_handles_are_argument_errors_with_messages():
+    """The C ABI validates its handles before touching a device: a NULL
+    graph / batch / partition is GN_ERR_ARG with a message (runs on CPU)."""
+    from paper_2605_05330_b200 import _engine as E
+
+    L = E.load_library()
+    z = None
+    cases = {
+        "gn_run": (L.gn_run, (z,) * 16, "null graph"),
+        "gn_round": (L.gn_round, (z, z, 0, z, z, z, z, z), "null graph"),
+        "gn_round_members": (L.gn_round_members, (z, z, 0, z, z, z, z, z), "null graph"),
+        "gn_round_many": (L.gn_round_many, (z, 1, z, 0, z, z, z, z, z), "null graph"),
+        "gn_check_members": (L.gn_check_members, (z, z, z, z, z, z), "null graph"),
+        "gn_spmv": (L.gn_spmv, (z, z, z), "null graph"),
+        "gn_is_normalizable": (L.gn_is_normalizable, (z, z, z), "null graph"),
+        "gn_weighted_mass": (L.gn_weighted_mass, (z, z, z), "null graph"),
+        "gn_simplex_state": (L.gn_simplex_state, (z, z, z), "null graph"),
+        "gn_graph_info": (L.gn_graph_info, (z,) * 7, "null graph"),
+        "gn_batch_info": (L.gn_batch_info, (z,) * 5, "null batch"),
+        "gn_part_info": (L.gn_part_info, (z,) * 4, "null partition"),
+    }
+    for name, (fn, args, msg) in cases.items():
+        nargs = len(fn.argtypes)
+        call_args = list(args[:nargs]) + [None] * (nargs - len(args))
+        for k, t in enumerate(fn.argtypes):  # scalars: zero of their type
+            if t in (ctypes.c_int, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64, ctypes.c_double) and call_args[k] is None:
+                call_args[k] = 0
+        assert fn(*call_args) == E.GN_ERR_ARG, name
+        assert msg in E.last_error(), name
