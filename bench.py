@@ -1,16 +1,24 @@
 #!/usr/bin/env python3
 """GN engine benchmark: GN edge-updates/s (undirected edges x iterations / s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
 A step is one run_wrgn over one instance: the reference's default pursuit
-schedule (linear gamma 0.9 -> 1.5, 1000 iterations, dynamics.py:58-63) on the
-workload BASELINE.json's metric is quoted on at one GPU -- configs[1], the
-256x256 assignment conflict graph (C2), fp32 gathered values.  N > 1: one
-process per GPU (torchrun), each rank runs its own replica (C2 does not
-shard: "replicas only"), `value` counts all ranks' edge updates
-over the max-over-ranks device time.  --config C4 shards the C4 batch instead
-(1024 graphs per rank, no collectives).
+schedule (linear gamma 0.9 -> 1.5, 1000 iterations, dynamics.py:58-63).
+
+Default workload: BASELINE config C5 (R-MAT scale 24, 16.8 M vertices,
+260 M edges, fp32 gathered values) through the vertex-range partitioned
+engine: one part per GPU, every iteration from a device-side schedule (one
+CUDA-graph launch per run), the halo between parts pushed over NVLink into
+the peers' ghost slots (--halo peer) or exchanged by NCCL (--halo nccl).
+N = 1 is one part (no halo); N > 1 is strong scaling of the same graph.
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one process per GPU).
+
+Other configs: --config C2 (the 256x256 assignment conflict graph, the
+persistent loop kernel; replicas at N > 1), C4 (1024 graphs per rank, batch
+kernel, no collectives), C1/C3 (replicas), --config C5 --engine loop (the
+single-GPU persistent loop kernel).
 
 Printed JSON keys follow the driver contract; see DESIGN.md "Measurement".
 """
@@ -21,6 +29,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -43,7 +52,8 @@ CONFIG_TEXT = {
           "w ~ U(0,1] fp32, pursuit 0.9->1.5 x1000",
     "C3": "Barabasi-Albert n=200,000 m=5 (999,975 edges), integer weights U{1..200} fp64, pursuit x1000",
     "C4": "1024 independent ER graphs n=2000 avg degree 16 per GPU, packed block-diagonal, fp32, pursuit x1000",
-    "C5": "R-MAT edge factor 16 (a=.57,b=c=.19), symmetrised, dedup, fp32, pursuit x1000 (scale in config.scale)",
+    "C5": "R-MAT scale 24 (16.8M vertices), edge factor 16 (a=.57,b=c=.19), symmetrised, dedup, w ~ U(0,1] fp32, "
+          "pursuit 0.9->1.5 x1000, vertex-range partitioned over the GPUs with a per-iteration halo",
 }
 
 
@@ -54,19 +64,41 @@ def dist_env():
     return ws, rank, local
 
 
-def make_instance(config: str, rank: int, scale: int):
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-run this command as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def make_instance(config: str, rank: int, ws: int, scale: int):
     from paper_2605_05330_b200 import generators as G
 
     if config == "C1":
-        return G.c1_er()
+        return G.c1_er(), None
     if config == "C2":
-        return G.c2_assignment()
+        return G.c2_assignment(), None
     if config == "C3":
-        return G.c3_ba()
+        return G.c3_ba(), None
     if config == "C4":
-        return G.c4_batch(graphs=1024, first=rank * 1024).instance
+        from paper_2605_05330_b200.parallel import shard_range
+
+        lo, hi = shard_range(1024 * ws, ws, rank)
+        batch = G.c4_batch(graphs=hi - lo, first=lo)
+        return batch.instance, batch
     if config == "C5":
-        return G.c5_rmat_gpu(scale) if scale >= 18 else G.c5_rmat(scale)
+        return (G.c5_rmat_gpu(scale) if scale >= 18 else G.c5_rmat(scale)), None
     raise SystemExit(f"unknown config {config}")
 
 
@@ -74,6 +106,37 @@ def algorithmic_bytes(n: int, nnz: int, s: int) -> int:
     """B_iter = 4 nnz + P (n+1) + 3 s n (P = 4 below 2^31 entries)."""
     p = 4 if nnz < 2**31 else 8
     return 4 * nnz + p * (n + 1) + 3 * s * n
+
+
+def engine_dtype(args, inst) -> str:
+    # C1-C3 run in the reference's own arithmetic (C2's graph stays in L2, so
+    # binary64 gathers cost no bandwidth); C4/C5 gather binary32 values
+    return args.dtype or ("fp64" if args.config in ("C1", "C2", "C3") else inst.dtype)
+
+
+def config_dict(args, inst, ws: int, dtype: str, extra: dict | None = None) -> dict:
+    """The workload description both arms print (same keys, same values)."""
+    part = args.config == "C5" and args.engine == "part"
+    d = {
+        "workload": args.config + ": " + CONFIG_TEXT[args.config] + (
+            f"; {args.starts} starts per call" if args.starts > 1 else ""),
+        "n": int(inst.n), "m": int(inst.m), "iters": int(args.iters), "schedule": "pursuit 0.9->1.5",
+        "scale": args.scale if args.config == "C5" else None,
+        "parallelism": (f"partition x{ws}" if part else
+                        f"batch shard x{ws} (1024 graphs/rank)" if args.config == "C4" else f"replicas x{ws}"),
+        "engine": (("partitioned (gn_part_run: device-side schedule" +
+                    (f", {args.halo} halo)" if ws > 1 else ", one part)")) if part else
+                   "batch (gn_batch_run)" if args.config == "C4" else
+                   "multi-start (gn_multi_run)" if args.starts > 1 else "loop (gn_run)"),
+        "engine_dtype": dtype,
+        "starts": args.starts,
+        "l2": "flushed between steps (256 MB write); the iterations inside a step re-read the graph",
+        "index_format": "uint16" if inst.n <= 65536 and not part else "int32",
+        "inputs": "w and x0 binary32-representable (BASELINE: fp32 weights)",
+    }
+    if extra:
+        d.update(extra)
+    return d
 
 
 class ClockSampler:
@@ -129,35 +192,133 @@ def flush_l2(torch, dev):
     buf.fill_(1)
 
 
-def cpu_reference(inst, seconds: float = 12.0, threads: int | None = None) -> dict:
-    """The CPU path (oracle port of the reference, fp64, all host threads) on
-    a bounded sample of the same workload: the first S pursuit iterations."""
+# ---------------------------------------------------------------- CPU arms
+
+def cpu_port(inst, seconds: float, threads: int) -> dict:
+    """The oracle port (oracle/gn_oracle.c: the reference's fp64 arithmetic,
+    bitwise; rows in fixed 4096-row chunks over `threads` OpenMP threads) on
+    a bounded sample: the first k pursuit iterations of the same instance."""
     import gn_oracle as O
     from paper_2605_05330_b200 import GammaSchedule
 
-    threads = threads or O.default_threads()
     tab = GammaSchedule.pursuit().table()
     t0 = time.perf_counter()
-    O.run(inst.graph, inst.x0, tab[:2], 1.5, threads=threads)
-    per = max((time.perf_counter() - t0) / 2, 1e-6)
-    k = int(min(1000, max(2, seconds / per)))
+    O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)
+    per = max(time.perf_counter() - t0, 1e-6)
+    k = int(min(1000, max(1, seconds / per)))
     t0 = time.perf_counter()
     O.run(inst.graph, inst.x0, tab[:k], 1.5, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": inst.m * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {k} of the 1000 pursuit iterations of {inst.name} in fp64 "
-                      f"(oracle/gn_oracle.c, OpenMP row-parallel, bitwise the reference), {dt:.2f} s",
+            "sample": f"first {k} of the 1000 pursuit iterations of {inst.name} in fp64 on {threads} host "
+                      f"thread(s) (oracle/gn_oracle.c, OpenMP over fixed row chunks, bitwise the reference's "
+                      f"arithmetic), {dt:.2f} s incl. the x0 check",
             "iters": k, "seconds": dt}
 
 
-def ncu_traffic(config: str, iters: int):
+def reference_module():
+    """The unmodified reference package: baseline/_ref (installed with pip
+    --target, travels to the GPU box) or, in the build container, its source
+    tree.  None when neither is importable."""
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "graphnorm" / "dynamics.py").exists():
+            if str(p) not in sys.path:
+                sys.path.insert(0, str(p))
+            try:
+                import graphnorm.dynamics as D
+                import graphnorm.graph as RG
+
+                return D, RG, str(p)
+            except Exception:
+                return None
+    return None
+
+
+def cpu_reference_scipy(inst, seconds: float) -> dict | None:
+    """The reference's own run_wrgn (numpy + scipy csr_matvec, one thread per
+    trajectory, as solver.py runs each start) on a bounded sample: a k-step
+    pursuit (GammaSchedule(0.9, 1.5, k): same per-iteration work; the x0
+    check's SpMV is inside the timed call).  The WeightedGraph is built
+    straight from the instance's CSR (the reference constructor, graph.py:35-46)."""
+    mod = reference_module()
+    if mod is None:
+        return None
+    D, RG, where = mod
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    g = RG.WeightedGraph(inst.graph.n, np.array(inst.graph.indptr), np.array(inst.graph.indices),
+                         np.array(inst.graph.w, dtype=np.float64))
+    t0 = time.perf_counter()
+    D.run_wrgn(g, inst.x0, D.GammaSchedule(0.9, 1.5, 2))
+    per = max((time.perf_counter() - t0) / 3, 1e-6)  # 2 steps + the check's SpMV
+    k = int(min(1000, max(2, seconds / per)))
+    t0 = time.perf_counter()
+    D.run_wrgn(g, inst.x0, D.GammaSchedule(0.9, 1.5, k))
+    dt = time.perf_counter() - t0
+    del g
+    return {"value": inst.m * k / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"graphnorm.dynamics.run_wrgn (unmodified reference from {where}, scipy csr_matvec), "
+                      f"a {k}-iteration pursuit on {inst.name}, {dt:.2f} s",
+            "iters": k, "seconds": dt}
+
+
+def cpu_baselines(inst, seconds: float) -> dict:
+    """cpu_baseline for the JSON line: the port on every host thread (the
+    reported value), plus the port on one thread and the reference's own
+    scipy run_wrgn (one thread per trajectory: what the reference does)."""
+    threads = host_threads()
+    par = cpu_port(inst, seconds, threads)
+    one = cpu_port(inst, seconds / 2, 1)
+    ref = None
+    try:
+        ref = cpu_reference_scipy(inst, seconds / 2)
+    except MemoryError:
+        ref = None
+    out = {k: par[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    out["port_1thread"] = {k: one[k] for k in ("value", "cores", "sample")}
+    out["reference_scipy"] = ({k: ref[k] for k in ("value", "cores", "kind", "sample")} if ref else
+                              {"unavailable": "graphnorm not importable (baseline/_ref missing)"})
+    return out
+
+
+def run_reference(args, ws, rank) -> int:
+    """--impl reference: the reference's CPU path on the host cores (rank 0
+    only).  Each step times the oracle port of the reference's arithmetic on
+    every host thread over a bounded sample of the workload; the reference's
+    own scipy run_wrgn and the 1-thread port are reported beside it."""
+    if rank != 0:
+        return 0
+    inst, _ = make_instance(args.config, 0, 1, args.scale)
+    threads = host_threads()
+    vals, base = [], None
+    for i in range(args.warmup + args.steps):
+        r = cpu_port(inst, args.ref_seconds, threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    v = statistics.median(vals)
+    extra = cpu_baselines(inst, 2 * args.ref_seconds)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "strong" if args.config == "C5" and args.engine == "part" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
+        "config": config_dict(args, inst, ws if ws > 1 else args.gpus, engine_dtype(args, inst)),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": base["kind"], "sample": base["sample"],
+                         "port_1thread": extra["port_1thread"], "reference_scipy": extra["reference_scipy"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ncu_traffic(key: str, iters: int):
     """DRAM bytes (read + write) per launch of `iters` iterations, from the
     committed ncu --set full summary of the same kernel (scaled by iterations
-    when the capture ran fewer, e.g. 5 iterations of C5)."""
+    when the capture ran fewer)."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if f.exists():
         try:
-            d = json.loads(f.read_text()).get(config, {})
+            d = json.loads(f.read_text()).get(key, {})
             if d.get("dram_bytes_per_launch") is None:
                 return None
             return d["dram_bytes_per_launch"] / (d.get("iters_per_launch") or iters) * iters
@@ -166,145 +327,143 @@ def ncu_traffic(config: str, iters: int):
     return None
 
 
-def run_reference(args, ws, rank):
-    if rank != 0:
-        return 0
-    inst = make_instance(args.config, 0, args.scale)
-    vals = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference(inst, seconds=args.ref_seconds)
-        if i >= args.warmup:
-            vals.append(r["value"])
-            base = r
-    v = statistics.median(vals)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config + ": " + CONFIG_TEXT[args.config], "n": inst.n, "m": inst.m},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
-                         "sample": base["sample"]},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
+def peak_hbm() -> tuple[float, str]:
+    pf = ROOT / "MEASURED_PEAKS.json"
+    if pf.exists():
+        peaks = json.loads(pf.read_text())
+        if "hbm_gbs" in peaks:
+            return float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
+def traffic_note(traffic, algo):
+    if traffic is None:
+        return None
+    if traffic < 0.5 * algo:
+        return (f"DRAM traffic is {traffic / algo:.3f}x the algorithmic bytes: the graph stays in L2/shared memory "
+                "across the iterations of a launch, so achieved/frac are the algorithmic rate of SURVEY 8(d), not "
+                "DRAM bandwidth")
+    return f"DRAM traffic is {traffic / algo:.2f}x the algorithmic bytes (index stream plus L2 misses of the gathers)"
+
+
+# ---------------------------------------------------------------- GPU arms
+
+def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
     """C5 as BASELINE names it: the graph vertex-range partitioned over the N
-    ranks (partition.py), each rank stepping its owned rows (gn_part_step) and
-    exchanging boundary values with its peers every iteration: the boundary
-    kernel's direct stores into the peers' ghost slots over NVLink (--halo
-    peer, the default) or NCCL point-to-point through torch.distributed
-    (--halo nccl).  Strong scaling: the graph is
-    the same at every N.  Timed with CUDA events on the stream the engine and
-    NCCL share, max over ranks."""
-    from paper_2605_05330_b200.partition import (DistExchange, DistPeerExchange, EngineBackend, build_partitions,
-                                                 partitioned_step)
+    ranks (partition.py), each rank building only its own part from its own
+    rows.  Every run: fence the ranks, gn_part_begin, the halo handshake
+    (once), then all iterations from one CUDA-graph launch (gn_part_run: with
+    N > 1 the graph holds the flag waits, boundary and interior steps, the
+    coalesced pushes into the peers' ghost slots and the flags).  --halo nccl
+    runs the host-driven pack / NCCL send-recv / unpack loop instead.
+    Strong scaling: the graph is the same at every N.  Timed with CUDA events
+    on the stream the engine launches on, max over ranks."""
+    from paper_2605_05330_b200.partition import (DistExchange, DistPeerExchange, EngineBackend, NoExchange,
+                                                 build_partition, run_partition)
 
-    dtype = args.dtype or inst.dtype
+    dtype = engine_dtype(args, inst)
     sched = P.GammaSchedule.pursuit(iterations=args.iters)
     gam = sched.table()
     iters = len(gam)
-    spec = build_partitions(inst.graph, ws)[rank]
+    t_spec = time.perf_counter()
+    spec = build_partition(inst.graph, ws, rank)
     be = EngineBackend(spec, dtype=dtype, device=local)
-    # the halo: direct stores into the peers' ghost slots over NVLink (CUDA IPC
-    # mappings, the default) or pack + NCCL send/recv + unpack (--halo nccl)
-    ex = (DistPeerExchange(be) if args.halo == "peer" else DistExchange(be)) if ws > 1 else None
+    setup_s = time.perf_counter() - setup_t0
+    spec_s = time.perf_counter() - t_spec
+    if ws == 1:
+        ex = NoExchange(be)
+    else:
+        ex = DistPeerExchange(be) if args.halo == "peer" else DistExchange(be)
     x0l = spec.local_x0(inst.x0)
+    x0_pin = torch.from_numpy(x0l).pin_memory()
+    x0p = x0_pin.numpy()
     dev = torch.device("cuda", local)
+    devsched = ex.device_schedule
 
-    def barrier():
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-
-    def step():
-        be.begin(x0l, gam)
-        if ex is not None:
-            ex.setup()
-        barrier()
+    def timed_run():
+        ex.fence()
+        be.begin(x0p, gam)
+        ex.setup()
+        torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for k in range(iters):
-            if ex is not None:
+        if devsched:
+            be.run(0, iters)
+        else:
+            from paper_2605_05330_b200.partition import partitioned_step
+
+            for k in range(iters):
                 partitioned_step(be, ex, k)
-            else:
-                be.step(k)
         e1.record()
-        torch.cuda.synchronize()
+        torch.cuda.synchronize(dev)
         return e0.elapsed_time(e1)
 
     for _ in range(args.warmup):
         flush_l2(torch, dev)
-        step()
+        timed_run()
     launches0 = E.launch_count()
     times = []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(torch, dev)
-            barrier()
-            times.append(step())
+            times.append(timed_run())
     launches = E.launch_count() - launches0
     total_ms = float(sum(times))
-    # e2e: host x0 in, the owned x out, every step (begin .. end)
+    # e2e through the public API: host x0 in (pinned), every iteration, the owned x out
     e2e = []
-    for _ in range(args.steps):
-        barrier()
+    res = None
+    for i in range(args.warmup + args.steps):
+        ex.fence()
         t0 = time.perf_counter()
-        be.begin(x0l, gam)
-        if ex is not None:
-            ex.setup()
-        for k in range(iters):
-            if ex is not None:
-                partitioned_step(be, ex, k)
-            else:
-                be.step(k)
-        be.end(iters)
-        barrier()
-        e2e.append(time.perf_counter() - t0)
+        res = run_partition(be, ex, x0p, sched)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
     e2e_total = sum(e2e)
+    t = torch.tensor([total_ms, e2e_total, setup_s], device=dev, dtype=torch.float64)
     if ws > 1:
-        t = torch.tensor([total_ms, e2e_total], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, e2e_total = float(t[0].item()), float(t[1].item())
+    total_ms, e2e_total, setup_max = (float(v) for v in t.tolist())
     if rank == 0:
         m, n = inst.m, inst.graph.n
         value = m * iters * args.steps / (total_ms * 1e-3)
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-        peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak, peak_src = peak_hbm()
         s_bytes = 8 if dtype == "fp64" else 4
         b_iter = algorithmic_bytes(n, 2 * m, s_bytes)
         achieved = b_iter * iters * args.steps / (total_ms * 1e-3) / 1e9
+        traffic = ncu_traffic("C5part", iters) if ws == 1 else None
         clk = clocks.summary()
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baselines(inst, args.ref_seconds)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": {"fp64": "f64", "fp32": "f32-gather/f64-state", "fp32_pure": "f32"}[dtype],
             "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
-            "config": {"workload": "C5: " + CONFIG_TEXT["C5"] + f"; vertex-range partitioned over {ws} GPU(s)",
-                       "n": n, "m": m, "iters": iters, "scale": args.scale, "parallelism": f"partition x{ws}",
-                       "ghosts_rank0": spec.n_ghost, "owned_rank0": spec.n_own,
-                       "l2": "flushed between steps (256 MB write)", "engine_dtype": dtype},
+            "config": config_dict(args, inst, ws, dtype, {
+                "ghosts_rank0": spec.n_ghost, "owned_rank0": spec.n_own,
+                "host_setup_s_rank0": round(setup_s, 2), "host_setup_s_max": round(setup_max, 2),
+                "part_build_s_rank0": round(spec_s, 2)}),
             "e2e": {"value": m * iters * args.steps / e2e_total, "unit": UNIT,
                     "h2d_bytes_per_step": 8 * (spec.n_own + spec.n_ghost) + 8 * iters,
                     "d2h_bytes_per_step": 8 * spec.n_own + 32 * iters,
-                    "api": "partition.EngineBackend begin/step/halo/end (host x0 in, owned x out), rank 0 shown"},
+                    "api": "partition.run_partition (host x0 in, owned x and per-iteration stats out), rank 0 shown"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
-                         "frac": achieved / (peak * ws), "traffic": None,
-                         "kernel": "gn::k_part_step (one launch per iteration and part)" + (
-                             "" if ws == 1 else (" + direct peer halo (stores into peer ghost slots, CUDA IPC)"
+                         "frac": achieved / (peak * ws), "traffic": traffic,
+                         "traffic_note": traffic_note(traffic, b_iter * iters),
+                         "kernel": "gn::k_part_step (1 launch per iteration per part, replayed from a CUDA graph)" + (
+                             "" if ws == 1 else (" + coalesced pushes into the peers' ghost slots (CUDA IPC)"
                                                  if args.halo == "peer" else " + NCCL halo")),
-                         "b_iter": b_iter, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs) x n_gpus"},
-            "cpu_baseline": None,
+                         "b_iter": b_iter, "peak_source": peak_src + (f" x {ws} GPUs" if ws > 1 else "")},
+            "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
-    if ex is not None and hasattr(ex, "close"):
-        barrier()  # no peer still writes into our buffers
+    if hasattr(ex, "close"):
+        ex.fence()  # no peer still writes into our buffers
         ex.close()
     be.close()
     if ws > 1:
@@ -312,62 +471,14 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E) -> int:
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
-    ap.add_argument("--scale", type=int, default=24, help="R-MAT scale for C5 (BASELINE: 24)")
-    ap.add_argument("--dtype", default=None, help="engine dtype (default: fp64 for C1-C3, fp32 for C4/C5)")
-    ap.add_argument("--iters", type=int, default=1000)
-    ap.add_argument("--ref-seconds", type=float, default=4.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
-                    help="C5 under torchrun: direct stores into the peers' ghost slots (default) or NCCL send/recv")
-    ap.add_argument("--partition", action="store_true",
-                    help="C5: vertex-range partitioned engine (the default for C5 under torchrun, N>1)")
-    ap.add_argument("--starts", type=int, default=1,
-                    help="starts per instance (SURVEY 8f f1): >1 runs them together through gn_multi_run")
-    args = ap.parse_args()
-    ws, rank, local = dist_env()
-    if args.impl == "reference":
-        return run_reference(args, ws, rank)
+def run_single(args, ws, rank, local, inst, batch, torch, P, E) -> int:
+    """C1-C4 (and C5 --engine loop): one engine call per step on each rank
+    (replicas, or the rank's own batch shard for C4)."""
+    from paper_2605_05330_b200.batch import GraphBatch
 
-    import torch
-
-    import paper_2605_05330_b200 as P
-    from paper_2605_05330_b200 import _engine as E
-
-    E.load_library()
-    if E.device_count() < 1:
-        raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-
-    if args.config == "C4":
-        from paper_2605_05330_b200 import generators as G
-        from paper_2605_05330_b200.batch import GraphBatch
-        from paper_2605_05330_b200.parallel import shard_range
-
-        lo, hi = shard_range(1024 * ws, ws, rank)
-        batch = G.c4_batch(graphs=hi - lo, first=lo)
-        inst = batch.instance
-    else:
-        inst = make_instance(args.config, rank, args.scale)
-        batch = None
     g = inst.graph
-    if args.config == "C5" and (ws > 1 or args.partition):
-        return run_partitioned(args, ws, rank, local, inst, torch, P, E)
-    # C2's graph stays in L2, so binary64 gathers cost no bandwidth and avoid
-    # the fp32->fp64 conversions of the mixed dtype: run it in the reference's
-    # own arithmetic
-    dtype = args.dtype or ("fp64" if args.config in ("C1", "C2", "C3") else inst.dtype)
+    dtype = engine_dtype(args, inst)
     sched = P.GammaSchedule.pursuit(iterations=args.iters)
     gam = np.ascontiguousarray(sched.table())
     iters = len(gam)
@@ -386,7 +497,8 @@ def main():
         kernel_name = "gn::k_gn_batch (one CTA per graph, graph resident in shared memory)"
 
         def device_step():
-            r = gb.run(None, sched, device_x0=x0_dev.data_ptr(), device_x_out=x_out.data_ptr(), traces=False)
+            # per-graph traces (step_inf, fallbacks, objective) are part of every run (dynamics.py:165-168)
+            r = gb.run(None, sched, device_x0=x0_dev.data_ptr(), device_x_out=x_out.data_ptr(), traces=True)
             st = E.RunStats()
             for f, _ in E.RunStats._fields_:
                 setattr(st, f, r.stats[f])
@@ -428,7 +540,6 @@ def main():
     barrier()
     launches0 = E.launch_count()
     step_ms, loop_ms = [], []
-    wall0 = time.perf_counter()
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(torch, dev)
@@ -437,7 +548,6 @@ def main():
             step_ms.append(st.total_ms)
             loop_ms.append(st.loop_ms)
     barrier()
-    wall = time.perf_counter() - wall0
     launches = E.launch_count() - launches0
     total_ms = float(sum(step_ms))
     if ws > 1:
@@ -447,12 +557,14 @@ def main():
     edges_all = inst.m * ws * starts
     value = edges_all * iters * args.steps / (total_ms * 1e-3)
 
-    # ---- e2e through the public API: host x0 in, MIS out, every step.
+    # ---- e2e through the public API: host x0 in, MIS out, every step; the
+    # state stays in HBM between the run and the rounding (device_state).
     # The harness has torch loaded (millions of tracked objects): move them
     # out of the collector's way so a full collection cannot land in a step.
     gc.collect()
     gc.freeze()
     x0_host = torch.from_numpy(np.ascontiguousarray(inst.x0)).pin_memory().numpy()
+    x0s_host = torch.from_numpy(np.ascontiguousarray(x0s)).pin_memory().numpy()
     e2e_t, round_t = [], []
     h2d = d2h = 0
     for i in range(args.warmup + args.steps):
@@ -460,12 +572,19 @@ def main():
         t0 = time.perf_counter()
         if batch is not None:
             r = gb.run(x0_host, sched)
+            t1 = time.perf_counter()
+            sol = P.round_to_mis(g, r.x)  # the packed graph: per-graph roundings, block by block
+            xbytes = 8 * g.n
         elif starts > 1:
-            r = P.run_multi(g, x0s, sched, dtype=dtype, device=local)
+            r = P.run_multi(g, x0s_host, sched, dtype=dtype, device=local)
+            t1 = time.perf_counter()
+            sol = P.round_many(g, r.x)
+            xbytes = 8 * g.n * starts
         else:
-            r = P.run_engine(g, x0_host, sched, dtype=dtype, device=local)
-        t1 = time.perf_counter()
-        sol = P.round_many(g, r.x) if starts > 1 else P.round_to_mis(g, r.x)
+            r = P.run_engine(g, x0_host, sched, dtype=dtype, device=local, device_state=True)
+            t1 = time.perf_counter()
+            sol = P.round_to_mis(g, r.x)
+            xbytes = 8 * g.n  # x0 uploaded by run_engine; x is handed to the rounding in HBM
         barrier()
         if os.environ.get("GN_BENCH_VERBOSE"):
             print(f"e2e step {i}: run {1e3 * (t1 - t0):.2f} ms, round {1e3 * (time.perf_counter() - t1):.2f} ms, "
@@ -473,7 +592,7 @@ def main():
         if i >= args.warmup:
             e2e_t.append(time.perf_counter() - t0)
             round_t.append(time.perf_counter() - t1)
-            h2d = r.stats["h2d_bytes"] + 8 * g.n * starts          # + the rounding's state upload
+            h2d = r.stats["h2d_bytes"] + xbytes  # + the rounding's state upload, or run_engine's x0 upload
             # + the rounding's output: member ids (round_to_mis) or membership masks (round_many), and flags
             d2h = r.stats["d2h_bytes"] + (8 * len(sol._idx) + 64 if starts == 1 else (g.n + 64) * starts)
     del sol
@@ -489,12 +608,7 @@ def main():
             torch.distributed.destroy_process_group()
         return 0
 
-    peaks = {}
-    pf = ROOT / "MEASURED_PEAKS.json"
-    if pf.exists():
-        peaks = json.loads(pf.read_text())
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    peak, peak_src = peak_hbm()
     s_bytes = 8 if dtype == "fp64" else 4  # s = element size of the state vectors
     # SURVEY 8(d) per iteration; with several starts the index stream is read
     # once for all of them and the state streams once per start
@@ -502,65 +616,88 @@ def main():
     loop_avg = statistics.mean(loop_ms)
     achieved = b_iter * iters / (loop_avg * 1e-3) / 1e9
     traffic = ncu_traffic(args.config, iters) if starts == 1 else None
-    if traffic is None:
-        traffic_note = None
-    elif traffic < 0.5 * b_iter * iters:
-        traffic_note = (f"DRAM traffic is {traffic / (b_iter * iters):.3f}x the algorithmic bytes: the graph stays in "
-                        "L2/shared memory across the iterations of a launch, so achieved/frac are the algorithmic "
-                        "rate of SURVEY 8(d), not DRAM bandwidth")
-    else:
-        traffic_note = (f"DRAM traffic is {traffic / (b_iter * iters):.2f}x the algorithmic bytes (index stream plus "
-                        "L2 misses of the gathered values)")
-    info = {"n": g.n}
-
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference(inst, seconds=args.ref_seconds)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-
+        cpu = cpu_baselines(inst, args.ref_seconds)
     clk = clocks.summary()
     line = {
-        "metric": METRIC,
-        "value": value,
-        "unit": UNIT,
-        "n_gpus": ws,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {"fp64": "f64", "fp32": "f32-gather/f64-state", "fp32_pure": "f32"}[dtype],
         "data": "synthetic (seeded generators, paper_2605_05330_b200/generators.py)",
-        "config": {
-            "workload": args.config + ": " + CONFIG_TEXT[args.config] + (f"; {starts} starts per call" if starts > 1 else ""),
-            "n": g.n, "m": inst.m, "iters": iters, "schedule": "pursuit 0.9->1.5",
-            "scale": args.scale if args.config == "C5" else None,
-            "parallelism": f"replicas x{ws}" if args.config != "C4" else f"batch shard x{ws} (1024 graphs/rank)",
-            "l2": "flushed between steps (256 MB write); the 1000 iterations inside a step re-read the graph",
-            "index_format": "uint16" if info["n"] <= 65536 else "int32",
-            "inputs": "w and x0 binary32-representable (BASELINE configs[1]: fp32 weights)",
-            "engine_dtype": dtype,
-            "starts": starts,
-        },
+        "config": config_dict(args, inst, ws, dtype),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": ("paper_2605_05330_b200.run_multi + round_many" if starts > 1 else
-                        "paper_2605_05330_b200.run_engine + round_to_mis") + " (host numpy in, MIS out)",
+                        "GraphBatch.run + round_to_mis" if batch is not None else
+                        "paper_2605_05330_b200.run_engine(device_state=True) + round_to_mis") +
+                       " (host numpy in, MIS out)",
                 "round_ms_per_step": 1e3 * statistics.mean(round_t) if round_t else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": kernel_name,
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                      "bytes_per_launch": b_iter * iters, "b_iter": b_iter, "peak_source": peak_src,
-                     "loop_ms": loop_avg, "traffic_note": traffic_note},
+                     "loop_ms": loop_avg, "traffic_note": traffic_note(traffic, b_iter * iters)},
         "cpu_baseline": cpu,
         "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         "gpu_launches": int(launches),
-        "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--engine", default="part", choices=["part", "loop"],
+                    help="C5: the partitioned engine (default; one part per GPU) or the single-GPU loop kernel")
+    ap.add_argument("--scale", type=int, default=24, help="R-MAT scale for C5 (BASELINE: 24)")
+    ap.add_argument("--dtype", default=None, help="engine dtype (default: fp64 for C1-C3, fp32 for C4/C5)")
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--ref-seconds", type=float, default=6.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="C5 with N > 1: coalesced pushes into the peers' ghost slots (default) or NCCL send/recv")
+    ap.add_argument("--partition", action="store_true", help="(kept for old command lines: same as --engine part)")
+    ap.add_argument("--starts", type=int, default=1,
+                    help="starts per instance (SURVEY 8f f1): >1 runs them together through gn_multi_run")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # rank env check (tests)
+    args = ap.parse_args()
+    if args.partition:
+        args.engine = "part"
+    ws, rank, local = dist_env()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if args.dry_run:
+        print(json.dumps({"rank": rank, "world_size": ws, "local_rank": local, "gpus": args.gpus,
+                          "master": os.environ.get("MASTER_ADDR"), "config": args.config}), flush=True)
+        return 0
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+
+    import paper_2605_05330_b200 as P
+    from paper_2605_05330_b200 import _engine as E
+
+    E.load_library()
+    if E.device_count() < 1:
+        raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    setup_t0 = time.perf_counter()
+    inst, batch = make_instance(args.config, rank, ws, args.scale)
+    if args.config == "C5" and args.engine == "part":
+        return run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0)
+    return run_single(args, ws, rank, local, inst, batch, torch, P, E)
 
 
 if __name__ == "__main__":

@@ -218,16 +218,23 @@ int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first,
 int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf,
                 int64_t* fallbacks, double* mass, int* bad);
 /* Direct halo over peer memory (the fused alternative to pack + NCCL +
- * unpack): the boundary step stores every published value straight into the
- * ghost slots of the peers that hold it (P2P stores over NVLink, issued as
- * the rows finish), then a flag per peer.  Sequence per run, after
- * gn_part_begin: gn_part_peer_init (this part's rank, the peers that push to
- * it), gn_part_peer_buffers (yg[2] and the flag array to hand to the peers:
- * pointers in one process, gn_ipc_get_handle across processes),
- * gn_part_peer_add per peer (its buffers, the caller's owned ids it holds as
- * ghosts, in its ghost order, and the slot of the first of them in its yg),
- * gn_part_peer_commit.  Per iteration k: gn_part_peer_wait, gn_part_step
- * (the boundary range pushes), gn_part_peer_signal. */
+ * unpack): the interior step's first blocks copy the boundary rows' new
+ * values straight into the ghost slots of the peers that hold them (P2P
+ * stores over NVLink, sorted by (peer, slot) so a warp writes 32 consecutive
+ * slots, overlapped with the interior rows), then a flag per peer.  Sequence,
+ * after the first gn_part_begin: gn_part_peer_init (this part's rank, the
+ * peers that push to it), gn_part_peer_buffers (yg[2] and the flag array to
+ * hand to the peers: pointers in one process, gn_ipc_get_handle across
+ * processes), gn_part_peer_add per peer (its buffers, the caller's owned ids
+ * it holds as ghosts, in its ghost order, and the slot of the first of them
+ * in its yg), gn_part_peer_commit.  The buffers stay put across later runs
+ * of the same length, so the setup is done once.  Per iteration k:
+ * gn_part_peer_wait, gn_part_step (the interior launch pushes),
+ * gn_part_peer_signal -- or all iterations at once with gn_part_run.
+ * Flags carry the run epoch (one per gn_part_begin; all parts of a run call
+ * it equally often): a late flag of an earlier run cannot satisfy a wait.
+ * Between runs the caller fences every rank (device sync + barrier) before
+ * gn_part_begin and again after it, before the first step. */
 int gn_part_peer_init(gn_part* p, int parts, int me, const int32_t* expect, int nexpect);
 int gn_part_peer_buffers(const gn_part* p, void** yg0, void** yg1, void** inflags);
 int gn_part_peer_add(gn_part* p, int rank, void* yg0, void* yg1, void* inflags,
@@ -235,6 +242,18 @@ int gn_part_peer_add(gn_part* p, int rank, void* yg0, void* yg1, void* inflags,
 int gn_part_peer_commit(gn_part* p);
 int gn_part_peer_wait(gn_part* p, int k, uintptr_t stream);
 int gn_part_peer_signal(gn_part* p, int k, uintptr_t stream);
+/* Iterations [k0, k1) of the current run from a device-side schedule: the
+ * per-iteration launches (with the direct halo: wait, boundary rows,
+ * interior rows + pushes, signal) captured once into a CUDA graph and
+ * replayed with one launch on `stream`; no host work per iteration.  Replaces
+ * the Python loop over dynamics.py:155-178. */
+int gn_part_run(gn_part* p, int k0, int k1, uintptr_t stream);
+/* Every part of one graph held by this process (one device): iterations
+ * [k0, k1) of all parts interleaved in one captured schedule (per k, per
+ * part: wait, boundary, interior + pushes, signal), launched once on
+ * `stream` and synchronised -- the multi-GPU schedule with the parts run one
+ * after another, so no wait depends on a kernel that is not already done. */
+int gn_part_run_group(gn_part* const* parts, int nparts, int k0, int k1, uintptr_t stream);
 /* CUDA IPC of one device allocation between the processes of a node. */
 int gn_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */);
 int gn_ipc_open_handle(const void* handle, int device, void** dptr);

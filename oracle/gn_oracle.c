@@ -25,7 +25,8 @@
  *
  * Rows are independent within one step, so the row loop may run on several
  * OpenMP threads without changing any bit of x; max/count reductions are
- * order-free.  Dot products (trace mode, objective) stay sequential.
+ * order-free.  Dot products (trace mode, objective) are folded from fixed
+ * row chunks in chunk order (see GNO_CHUNK), independent of the thread count.
  */
 #include <math.h>
 #include <stdint.h>
@@ -75,57 +76,82 @@ void gno_spmv(int64_t n, const int64_t* indptr, const int32_t* indices,
 }
 
 /* ---------------------------------------------------------------------------
+ * Threading.  One step's rows are cut into fixed chunks of GNO_CHUNK rows
+ * (independent of the thread count); OpenMP threads take chunks dynamically
+ * (R-MAT puts its hubs at low ids) and each chunk keeps its own fallback
+ * count, max|dx|, finiteness and the three dot products of energy() /
+ * weighted_mass() (dynamics.py:210-224).  The chunk partials are then folded
+ * in chunk order, so every output -- x bitwise, and the dots too -- is the
+ * same for any number of threads.  (The reference's w @ x is a BLAS ddot,
+ * itself not a sequential sum; the dots are compared at 1e-12.)
+ * ------------------------------------------------------------------------- */
+#define GNO_CHUNK 4096
+
+typedef struct {
+    int64_t fb;
+    double mx;
+    int fin;
+    double d1, d2, d3;
+} chunk_part;
+
+static chunk_part* parts_alloc(int64_t n, int64_t* nch) {
+    *nch = (n + GNO_CHUNK - 1) / GNO_CHUNK;
+    return (chunk_part*)calloc((size_t)(*nch ? *nch : 1), sizeof(chunk_part));
+}
+
+static void parts_fold(const chunk_part* P, int64_t nch, int64_t* nfb, double* step_inf,
+                       int* finite, double* dots) {
+    int64_t fb = 0;
+    double mx = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    int fin = 1;
+    for (int64_t c = 0; c < nch; ++c) {
+        fb += P[c].fb;
+        if (P[c].mx > mx) mx = P[c].mx;
+        fin = fin && P[c].fin;
+        d1 += P[c].d1; d2 += P[c].d2; d3 += P[c].d3;
+    }
+    *nfb = fb;
+    *step_inf = mx;
+    *finite = fin;
+    if (dots) { dots[0] = d1; dots[1] = d2; dots[2] = d3; }
+}
+
+/* ---------------------------------------------------------------------------
  * One step, fp64: dynamics.py:_step 102-108.  Also returns max|x'-x|
  * (run_wrgn's step_inf, dynamics.py:165) and the isfinite verdict
- * (dynamics.py:175).  When dots != NULL it accumulates, sequentially over
- * rows, y.y, y.(Ay) and w.x of the PRE-step state (the three terms of
- * energy(), dynamics.py:210-219).
+ * (dynamics.py:175).  When dots != NULL it also returns y.y, y.(Ay) and w.x
+ * of the PRE-step state (the three terms of energy(), dynamics.py:210-219).
  * ------------------------------------------------------------------------- */
 static void step_f64(int64_t n, const int64_t* indptr, const int32_t* indices,
                      const double* v, const double* w, const double* x,
                      const double* y, double gamma, double* xo, double* yo,
                      int64_t* nfb, double* step_inf, int* finite, double* dots) {
-    int64_t fb = 0;
-    double mx = 0.0;
-    int fin = 1;
-    if (dots) {
-        double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        for (int64_t i = lo; i < hi; ++i) {
             double s = 0.0;
             for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
             double yi = y[i];
             double d = yi + gamma * s;
             double o;
-            if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++fb; }
+            if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++q.fb; }
             xo[i] = o;
             yo[i] = v[i] * o;
             double diff = fabs(o - x[i]);
-            if (diff > mx) mx = diff;
-            if (!isfinite(o)) fin = 0;
-            d1 += yi * yi;
-            d2 += yi * s;
-            d3 += w[i] * x[i];
+            if (diff > q.mx) q.mx = diff;
+            if (!isfinite(o)) q.fin = 0;
+            q.d1 += yi * yi;
+            q.d2 += yi * s;
+            q.d3 += w[i] * x[i];
         }
-        dots[0] = d1; dots[1] = d2; dots[2] = d3;
-    } else {
-#pragma omp parallel for schedule(static) reduction(+ : fb) reduction(max : mx) reduction(&& : fin)
-        for (int64_t i = 0; i < n; ++i) {
-            double s = 0.0;
-            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
-            double yi = y[i];
-            double d = yi + gamma * s;
-            double o;
-            if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++fb; }
-            xo[i] = o;
-            yo[i] = v[i] * o;
-            double diff = fabs(o - x[i]);
-            if (diff > mx) mx = diff;
-            fin = fin && isfinite(o);
-        }
+        P[c] = q;
     }
-    *nfb = fb;
-    *step_inf = mx;
-    *finite = fin;
+    parts_fold(P, nch, nfb, step_inf, finite, dots);
+    free(P);
 }
 
 /* Same step carried out in binary32 (the engine's fp32 arithmetic). */
@@ -133,33 +159,34 @@ static void step_f32(int64_t n, const int64_t* indptr, const int32_t* indices,
                      const float* v, const float* w, const float* x,
                      const float* y, float gamma, float* xo, float* yo,
                      int64_t* nfb, double* step_inf, int* finite, double* dots) {
-    int64_t fb = 0;
-    float mx = 0.0f;
-    int fin = 1;
-    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : fb) reduction(max : mx) reduction(&& : fin) if (!dots)
-    for (int64_t i = 0; i < n; ++i) {
-        float s = 0.0f;
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
-        float yi = y[i];
-        float d = yi + gamma * s;
-        float o;
-        if ((double)d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = (float)FALLBACK_VALUE; ++fb; }
-        xo[i] = o;
-        yo[i] = v[i] * o;
-        float diff = fabsf(o - x[i]);
-        if (diff > mx) mx = diff;
-        fin = fin && isfinite(o);
-        if (dots) {
-            d1 += (double)yi * (double)yi;
-            d2 += (double)yi * (double)s;
-            d3 += (double)w[i] * (double)x[i];
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        float mx = 0.0f;
+        for (int64_t i = lo; i < hi; ++i) {
+            float s = 0.0f;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
+            float yi = y[i];
+            float d = yi + gamma * s;
+            float o;
+            if ((double)d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = (float)FALLBACK_VALUE; ++q.fb; }
+            xo[i] = o;
+            yo[i] = v[i] * o;
+            float diff = fabsf(o - x[i]);
+            if (diff > mx) mx = diff;
+            if (!isfinite(o)) q.fin = 0;
+            q.d1 += (double)yi * (double)yi;
+            q.d2 += (double)yi * (double)s;
+            q.d3 += (double)w[i] * (double)x[i];
         }
+        q.mx = (double)mx;
+        P[c] = q;
     }
-    if (dots) { dots[0] = d1; dots[1] = d2; dots[2] = d3; }
-    *nfb = fb;
-    *step_inf = (double)mx;
-    *finite = fin;
+    parts_fold(P, nch, nfb, step_inf, finite, dots);
+    free(P);
 }
 
 
@@ -171,79 +198,120 @@ static void step_mixed(int64_t n, const int64_t* indptr, const int32_t* indices,
                        const double* v, const double* w, const double* x,
                        const float* yg, double gamma, double* xo, float* ygo,
                        int64_t* nfb, double* step_inf, int* finite, double* dots) {
-    int64_t fb = 0;
-    double mx = 0.0;
-    int fin = 1;
-    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : fb) reduction(max : mx) reduction(&& : fin) if (!dots)
-    for (int64_t i = 0; i < n; ++i) {
-        double s = 0.0;
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
-        double yi = v[i] * x[i];
-        double d = yi + gamma * s;
-        double o;
-        if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++fb; }
-        xo[i] = o;
-        ygo[i] = (float)(v[i] * o);
-        double diff = fabs(o - x[i]);
-        if (diff > mx) mx = diff;
-        fin = fin && isfinite(o);
-        if (dots) {
-            d1 += yi * yi;
-            d2 += yi * s;
-            d3 += w[i] * x[i];
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        for (int64_t i = lo; i < hi; ++i) {
+            double s = 0.0;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
+            double yi = v[i] * x[i];
+            double d = yi + gamma * s;
+            double o;
+            if (d > SAFE_DIV_THRESHOLD) o = yi / d; else { o = FALLBACK_VALUE; ++q.fb; }
+            xo[i] = o;
+            ygo[i] = (float)(v[i] * o);
+            double diff = fabs(o - x[i]);
+            if (diff > q.mx) q.mx = diff;
+            if (!isfinite(o)) q.fin = 0;
+            q.d1 += yi * yi;
+            q.d2 += yi * s;
+            q.d3 += w[i] * x[i];
         }
+        P[c] = q;
     }
-    if (dots) { dots[0] = d1; dots[1] = d2; dots[2] = d3; }
-    *nfb = fb;
-    *step_inf = mx;
-    *finite = fin;
+    parts_fold(P, nch, nfb, step_inf, finite, dots);
+    free(P);
+}
+
+/* The dots of a state without stepping (the trace tail after the last step):
+ * the same chunked fold as the steps' pre-state dots. */
+static void dots_f64(int64_t n, const int64_t* indptr, const int32_t* indices,
+                     const double* w, const double* x, const double* y, double* dots) {
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        for (int64_t i = lo; i < hi; ++i) {
+            double s = 0.0;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
+            q.d1 += y[i] * y[i];
+            q.d2 += y[i] * s;
+            q.d3 += w[i] * x[i];
+        }
+        P[c] = q;
+    }
+    int64_t fb; double mx; int fin;
+    parts_fold(P, nch, &fb, &mx, &fin, dots);
+    free(P);
 }
 
 static void dots_mixed(int64_t n, const int64_t* indptr, const int32_t* indices,
                        const double* v, const double* w, const double* x, const float* yg, double* dots) {
-    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        double s = 0.0;
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
-        double yi = v[i] * x[i];
-        d1 += yi * yi;
-        d2 += yi * s;
-        d3 += w[i] * x[i];
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        for (int64_t i = lo; i < hi; ++i) {
+            double s = 0.0;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += (double)yg[indices[p]];
+            double yi = v[i] * x[i];
+            q.d1 += yi * yi;
+            q.d2 += yi * s;
+            q.d3 += w[i] * x[i];
+        }
+        P[c] = q;
     }
-    dots[0] = d1; dots[1] = d2; dots[2] = d3;
-}
-
-/* Sequential dots of a state without stepping (trace tail). */
-static void dots_f64(int64_t n, const int64_t* indptr, const int32_t* indices,
-                     const double* w, const double* x, const double* y, double* dots) {
-    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        double s = 0.0;
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
-        d1 += y[i] * y[i];
-        d2 += y[i] * s;
-        d3 += w[i] * x[i];
-    }
-    dots[0] = d1; dots[1] = d2; dots[2] = d3;
+    int64_t fb; double mx; int fin;
+    parts_fold(P, nch, &fb, &mx, &fin, dots);
+    free(P);
 }
 
 static void dots_f32(int64_t n, const int64_t* indptr, const int32_t* indices,
                      const float* w, const float* x, const float* y, double* dots) {
-    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        float s = 0.0f;
-        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
-        d1 += (double)y[i] * (double)y[i];
-        d2 += (double)y[i] * (double)s;
-        d3 += (double)w[i] * (double)x[i];
+    int64_t nch;
+    chunk_part* P = parts_alloc(n, &nch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo = c * GNO_CHUNK, hi = lo + GNO_CHUNK < n ? lo + GNO_CHUNK : n;
+        chunk_part q = {0, 0.0, 1, 0.0, 0.0, 0.0};
+        for (int64_t i = lo; i < hi; ++i) {
+            float s = 0.0f;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += y[indices[p]];
+            q.d1 += (double)y[i] * (double)y[i];
+            q.d2 += (double)y[i] * (double)s;
+            q.d3 += (double)w[i] * (double)x[i];
+        }
+        P[c] = q;
     }
-    dots[0] = d1; dots[1] = d2; dots[2] = d3;
+    int64_t fb; double mx; int fin;
+    parts_fold(P, nch, &fb, &mx, &fin, dots);
+    free(P);
 }
 
 /* energy from the three dots: dynamics.py:219 */
 static double energy_of(const double* dots, double gamma) {
     return 0.5 * (dots[0] + gamma * dots[1]) - dots[2];
+}
+
+/* The dots of step k's PRE-step state x_k are the post-step terms of
+ * iteration k-1 (energy(x_k, gamma_{k-1}) and w.x_k, dynamics.py:170-173) and
+ * the pre-energy of iteration k (dynamics.py:163): one SpMV per iteration
+ * serves both, and only the state after the last step needs its own pass
+ * (k == iters_run, called after the loop). */
+static void post_dots(int k, int tail, const double* gammas, const double* dots, int trace,
+                      double* energy, double* pre_energy, double* mass) {
+    if (trace && !tail) pre_energy[k] = energy_of(dots, gammas[k]);
+    if (k > 0) {
+        if (trace) energy[k - 1] = energy_of(dots, gammas[k - 1]);
+        if (mass) mass[k - 1] = dots[2];
+    }
 }
 
 /* Public single step (gn_step, dynamics.py:111-119), fp64. */
@@ -296,7 +364,8 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
         if (!ok) return GNO_ERR_NOT_NORMALIZABLE;
     }
     size_t nb = (size_t)(n ? n : 1);
-    double dots[3], dots_next[3];
+    double dots[3];
+    const int want_dots = trace || mass;
     int rc = GNO_OK;
     int k, ran = 0;
     if (dtype == 0) {
@@ -314,20 +383,12 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             double g = gammas[k], si;
             int fin;
             int64_t fb;
-            int want_dots = trace || mass;
             step_f64(n, indptr, indices, v, w, xa, ya, g, xb, yb, &fb, &si, &fin,
                      want_dots ? dots : NULL);
             if (n == 0) si = 0.0;
             step_inf[k] = si;
             fallbacks[k] = fb;
-            if (want_dots) {
-                dots_f64(n, indptr, indices, w, xb, yb, dots_next);
-                if (trace) {
-                    pre_energy[k] = energy_of(dots, g);
-                    energy[k] = energy_of(dots_next, g);
-                }
-                if (mass) mass[k] = dots_next[2];
-            }
+            if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist) memcpy(x_hist + (size_t)k * (size_t)n, xb, sizeof(double) * (size_t)n);
             double* t;
             t = xa; xa = xb; xb = t;
@@ -337,6 +398,10 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             if (early && g == final_gamma && si < 1e-12) break;   /* dynamics.py:177 */
         }
         *iters_run = ran;
+        if (want_dots && ran > 0) {
+            dots_f64(n, indptr, indices, w, xa, ya, dots);
+            post_dots(ran, 1, gammas, dots, trace, energy, pre_energy, mass);
+        }
         for (int64_t i = 0; i < n; ++i) {  /* np.clip, dynamics.py:179 */
             double xi = xa[i];
             x_out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);
@@ -357,20 +422,12 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             double g = gammas[k], si;
             int fin;
             int64_t fb;
-            int want_dots = trace || mass;
             step_mixed(n, indptr, indices, v, w, xa, ya, g, xb, yb, &fb, &si, &fin,
                        want_dots ? dots : NULL);
             if (n == 0) si = 0.0;
             step_inf[k] = si;
             fallbacks[k] = fb;
-            if (want_dots) {
-                dots_mixed(n, indptr, indices, v, w, xb, yb, dots_next);
-                if (trace) {
-                    pre_energy[k] = energy_of(dots, g);
-                    energy[k] = energy_of(dots_next, g);
-                }
-                if (mass) mass[k] = dots_next[2];
-            }
+            if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist) memcpy(x_hist + (size_t)k * (size_t)n, xb, sizeof(double) * (size_t)n);
             double* t = xa; xa = xb; xb = t;
             float* tf = ya; ya = yb; yb = tf;
@@ -379,6 +436,10 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             if (early && g == final_gamma && si < 1e-12) break;
         }
         *iters_run = ran;
+        if (want_dots && ran > 0) {
+            dots_mixed(n, indptr, indices, v, w, xa, ya, dots);
+            post_dots(ran, 1, gammas, dots, trace, energy, pre_energy, mass);
+        }
         for (int64_t i = 0; i < n; ++i) {
             double xi = xa[i];
             x_out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);
@@ -401,20 +462,12 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             double g = gammas[k], si;
             int fin;
             int64_t fb;
-            int want_dots = trace || mass;
             step_f32(n, indptr, indices, v, wf, xa, ya, (float)g, xb, yb, &fb, &si, &fin,
                      want_dots ? dots : NULL);
             if (n == 0) si = 0.0;
             step_inf[k] = si;
             fallbacks[k] = fb;
-            if (want_dots) {
-                dots_f32(n, indptr, indices, wf, xb, yb, dots_next);
-                if (trace) {
-                    pre_energy[k] = energy_of(dots, g);
-                    energy[k] = energy_of(dots_next, g);
-                }
-                if (mass) mass[k] = dots_next[2];
-            }
+            if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist)
                 for (int64_t i = 0; i < n; ++i) x_hist[(size_t)k * (size_t)n + (size_t)i] = (double)xb[i];
             float* t;
@@ -425,6 +478,10 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             if (early && g == final_gamma && si < 1e-12) break;   /* dynamics.py:177 */
         }
         *iters_run = ran;
+        if (want_dots && ran > 0) {
+            dots_f32(n, indptr, indices, wf, xa, ya, dots);
+            post_dots(ran, 1, gammas, dots, trace, energy, pre_energy, mass);
+        }
         for (int64_t i = 0; i < n; ++i) {
             double xi = (double)xa[i];
             x_out[i] = xi < 0.0 ? 0.0 : (xi > 1.0 ? 1.0 : xi);

@@ -76,20 +76,40 @@ struct gn_part {
     // each published value straight into the ghost slots of the peers that
     // hold it (NVLink P2P stores, issued as the rows finish), then flags them
     int me = 0, parts = 0;
-    int64_t* inflags = nullptr;              // [parts] incoming: inflags[q] = iterations peer q has pushed
+    int64_t* inflags = nullptr;              // [parts] incoming: inflags[q] = (epoch << 32) + steps peer q has pushed
     int32_t* expect = nullptr;               // peers that push to this part
     int nexpect = 0;
     struct Peer { int rank; void* yg[2]; int64_t* flags; };
     std::vector<Peer> peers;
     std::vector<int32_t> h_push_row, h_push_peer;
     std::vector<int64_t> h_push_slot;
-    int32_t* push_ptr = nullptr;             // [n_bnd+1] over the boundary rows (new ids)
+    // the push list, sorted by (peer, ghost slot): entry e copies the owned
+    // value push_src[e] into slot push_slot[e] of peer push_peer[e], so the
+    // threads of a warp write 32 consecutive slots of one peer (coalesced
+    // 128-byte NVLink writes)
+    int32_t* push_src = nullptr;
     int32_t* push_peer = nullptr;
     int64_t* push_slot = nullptr;
+    int64_t n_push = 0;
     void** push_dst[2] = {nullptr, nullptr}; // per parity: the peers' yg buffers
     int64_t** peer_flags = nullptr;          // the peers' flag arrays
     int* halo_bad = nullptr;                 // set when a peer's flag did not arrive in time
     int npush_peers = 0;
+    // run epoch: incremented by every gn_part_begin (all parts of a run call it
+    // the same number of times); flag values carry it in their high 32 bits,
+    // so a late flag of an earlier run can never satisfy a wait of this one
+    int64_t epoch = 0;
+    int64_t* d_epoch = nullptr;
+    // run buffers are kept across runs while their sizes do not change (their
+    // addresses are exported to the peers over CUDA IPC)
+    int64_t alloc_nall = -1;
+    int alloc_dtype = -1, alloc_iters = 0, alloc_nblocks[2] = {0, 0};
+    // device-side schedule (gn_part_run): the iterations' launches captured
+    // once into a CUDA graph, rebuilt when `gen` (buffers, push list) moves
+    uint64_t gen = 1, g_gen = 0;
+    int g_k0 = -1, g_k1 = -1;
+    int64_t g_nodes = 0;
+    cudaGraphExec_t gexec = nullptr;
 };
 
 namespace gn {
@@ -136,43 +156,19 @@ __device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double*
     ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
 }
 
-// Direct halo: the rows of [0, rows) (the boundary) store their published
-// value into every peer ghost slot that holds them.
+// Direct halo: the interior step's first `nblocks` blocks copy the boundary
+// rows' new values (written by the boundary step, the previous launch on the
+// stream) into the peers' ghost slots while the other blocks step the
+// interior rows -- the NVLink transfer overlaps the interior.  Entries are
+// sorted by (peer, slot): consecutive threads store consecutive slots.
 struct PartPush {
-    const int32_t* __restrict__ ptr;   // [rows+1], or null: no pushes
+    const int32_t* __restrict__ src;   // new local ids of the pushed rows
     const int32_t* __restrict__ peer;
     const int64_t* __restrict__ slot;
     void* const* __restrict__ dst;     // [peers] the buffers this step writes (next parity)
-    int64_t rows;
+    int64_t n;
+    int nblocks;                       // 0: no pushes in this launch
 };
-
-// Delta halo: the buffer a step writes was written two steps earlier, here
-// and in every peer ghost slot alike (both start as v * x0), so a value
-// bitwise equal to that one is already in place at the peers and is not
-// sent again -- exact, and converged vertices stop costing NVLink traffic.
-template <typename TG>
-__device__ __forceinline__ TG push_old(const PartPush& P, int64_t i, const TG* __restrict__ ygo) {
-    return (P.ptr != nullptr && i < P.rows) ? ygo[i] : TG(0);
-}
-
-template <typename TG>
-__device__ __forceinline__ bool same_bits(TG a, TG b);
-template <>
-__device__ __forceinline__ bool same_bits<double>(double a, double b) {
-    return __double_as_longlong(a) == __double_as_longlong(b);
-}
-template <>
-__device__ __forceinline__ bool same_bits<float>(float a, float b) {
-    return __float_as_int(a) == __float_as_int(b);
-}
-
-template <typename TG>
-__device__ __forceinline__ void push_row(const PartPush& P, int64_t i, const TG* __restrict__ ygo, TG old) {
-    if (P.ptr == nullptr || i >= P.rows) return;
-    const TG val = ygo[i];  // written by this thread just before
-    if (same_bits(val, old)) return;
-    for (int32_t e = P.ptr[i]; e < P.ptr[i + 1]; ++e) static_cast<TG*>(P.dst[P.peer[e]])[P.slot[e]] = val;
-}
 
 // One step of the owned rows of one range.  Blocks [0, nbl) split the n_long
 // longest rows over warps (lanes stride the positions, fixed butterfly fold:
@@ -197,12 +193,19 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
                                                             const double* __restrict__ gam, int k,
                                                             double* __restrict__ part, PartPush push) {
     using A = Arith<TS>;
+    if ((int)blockIdx.x < push.nblocks) {  // the halo blocks
+        const int64_t stride = (int64_t)push.nblocks * blockDim.x;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < push.n; e += stride)
+            static_cast<TG*>(push.dst[__ldg(push.peer + e)])[__ldg(push.slot + e)] = ygo[__ldg(push.src + e)];
+        return;
+    }
+    const int bid = (int)blockIdx.x - push.nblocks, nbid = (int)gridDim.x - push.nblocks;
     const TS g = (TS)gam[k];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
-    if ((int)blockIdx.x < nbl) {
-        for (int64_t q = (int64_t)blockIdx.x * kWarpsPerBlock + warp; q < n_long; q += (int64_t)nbl * kWarpsPerBlock) {
+    if (bid < nbl) {
+        for (int64_t q = (int64_t)bid * kWarpsPerBlock + warp; q < n_long; q += (int64_t)nbl * kWarpsPerBlock) {
             const int64_t i = order[q];
             const int32_t rb = rowptr[i], re = rowptr[i + 1];
             TS s = TS(0);
@@ -217,14 +220,10 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
             for (; p < re; p += 32) s = A::add(s, (TS)yg[col[p]]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-            if (lane == 0) {
-                const TG old = push_old<TG>(push, i, ygo);
-                part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-                push_row<TG>(push, i, ygo, old);
-            }
+            if (lane == 0) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
         }
-    } else if ((int)blockIdx.x < nbl + ncb) {
-        for (int64_t q = (int64_t)(blockIdx.x - nbl) * blockDim.x + threadIdx.x; q < n_csr;
+    } else if (bid < nbl + ncb) {
+        for (int64_t q = (int64_t)(bid - nbl) * blockDim.x + threadIdx.x; q < n_csr;
              q += (int64_t)ncb * blockDim.x) {
             const int64_t i = order[n_long + q];
             const int32_t rb = rowptr[i], re = rowptr[i + 1];
@@ -238,14 +237,12 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
                 for (int u = 0; u < kPartUnroll; ++u) s = A::add(s, (TS)y[u]);
             }
             for (; p < re; ++p) s = A::add(s, (TS)yg[col[p]]);
-            const TG old = push_old<TG>(push, i, ygo);
             part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-            push_row<TG>(push, i, ygo, old);
         }
     } else {
         const int64_t pos0 = n_long + n_csr;  // first order position of slice 0
-        const int64_t nw = (int64_t)(gridDim.x - nbl - ncb) * kWarpsPerBlock;
-        for (int64_t sl = (int64_t)(blockIdx.x - nbl - ncb) * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
+        const int64_t nw = (int64_t)(nbid - nbl - ncb) * kWarpsPerBlock;
+        for (int64_t sl = (int64_t)(bid - nbl - ncb) * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
             const int64_t pos = pos0 + sl * 32 + lane;
             const bool valid = pos < count;
             const int64_t i = valid ? order[pos] : 0;
@@ -276,11 +273,7 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
 #pragma unroll
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
-            if (valid) {
-                const TG old = push_old<TG>(push, i, ygo);
-                part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-                push_row<TG>(push, i, ygo, old);
-            }
+            if (valid) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -307,7 +300,7 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
             t[2] = __dadd_rn(t[2], red[q][2]);
             t[3] = fmax(t[3], red[q][3]);
         }
-        double* dst = part + ((size_t)k * gridDim.x + blockIdx.x) * 4;
+        double* dst = part + ((size_t)k * nbid + bid) * 4;
         dst[0] = t[0];
         dst[1] = t[1];
         dst[2] = t[2];
@@ -320,8 +313,9 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
 // and it has read the buffer our pushes of step k will overwrite), step the
 // boundary rows with their pushes, step the interior, then flag every peer.
 // The spin is bounded (~10 s): a missing peer sets bad[0] instead of hanging.
-__global__ void k_part_wait(const int64_t* flags, const int32_t* __restrict__ expect, int nexpect, int64_t k,
-                            int* bad) {
+__global__ void k_part_wait(const int64_t* flags, const int32_t* __restrict__ expect, int nexpect,
+                            const int64_t* __restrict__ epoch, int64_t k, int* bad) {
+    const int64_t target = (*epoch << 32) + k;
     for (int i = threadIdx.x; i < nexpect; i += blockDim.x) {
         const int64_t* f = flags + expect[i];
         long long t0 = 0;
@@ -329,7 +323,7 @@ __global__ void k_part_wait(const int64_t* flags, const int32_t* __restrict__ ex
         for (;;) {
             long long v;
             asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-            if (v >= k) break;
+            if (v >= target) break;
             long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             if (t - t0 > 10000000000LL) {
@@ -341,8 +335,10 @@ __global__ void k_part_wait(const int64_t* flags, const int32_t* __restrict__ ex
     }
 }
 
-__global__ void k_part_signal(int64_t* const* __restrict__ peer_flags, int npeers, int me, int64_t value) {
+__global__ void k_part_signal(int64_t* const* __restrict__ peer_flags, int npeers, int me,
+                              const int64_t* __restrict__ epoch, int64_t step) {
     __threadfence_system();  // this part's pushes (earlier kernels on the stream) before the flags
+    const int64_t value = (*epoch << 32) + step;
     for (int i = threadIdx.x; i < npeers; i += blockDim.x) {
         int64_t* f = peer_flags[i] + me;
         asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(f), "l"((long long)value) : "memory");
@@ -523,10 +519,12 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
 }
 
 static void part_free_push(gn_part* p) {
-    void* q[] = {p->push_ptr, p->push_peer, p->push_slot, p->push_dst[0], p->push_dst[1], p->peer_flags};
+    void* q[] = {p->push_src, p->push_peer, p->push_slot, p->push_dst[0], p->push_dst[1], p->peer_flags};
     for (void* x : q) cudaFree(x);
-    p->push_ptr = p->push_peer = nullptr;
+    p->push_src = p->push_peer = nullptr;
     p->push_slot = nullptr;
+    p->n_push = 0;
+    p->gen++;
     p->push_dst[0] = p->push_dst[1] = nullptr;
     p->peer_flags = nullptr;
 }
@@ -537,6 +535,17 @@ static void part_free_run(gn_part* p) {
         if (q) cudaFree(q);
     p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
     p->gam = p->part[0] = p->part[1] = nullptr;
+    p->alloc_nall = -1;
+    p->alloc_dtype = -1;
+    p->alloc_iters = 0;
+    p->alloc_nblocks[0] = p->alloc_nblocks[1] = 0;
+    p->gen++;
+}
+
+static void part_free_graph(gn_part* p) {
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+    p->g_gen = 0;
 }
 
 }  // namespace gn
@@ -589,7 +598,9 @@ int gn_part_destroy(gn_part* p) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
+    part_free_graph(p);
     part_free_run(p);
+    cudaFree(p->d_epoch);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -613,10 +624,10 @@ int gn_part_destroy(gn_part* p) {
 int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters, uint32_t flags) {
     if (!p || iters < 1 || !gammas) return fail(GN_ERR_ARG, "bad gn_part_begin arguments");
     GN_CUDA(cudaSetDevice(p->device));
-    part_free_run(p);
     const int64_t nall = p->n_own + p->n_ghost;
     const size_t es = state_bytes(p->dtype), gs = gather_bytes(p->dtype);
     const size_t nb = (size_t)std::max<int64_t>(nall, 1);
+    if (p->flags != flags) p->gen++;  // the captured schedule depends on the mode
     p->iters = iters;
     p->flags = flags;
     // per range (boundary, interior): GN_EXACT sums every row sequentially
@@ -631,18 +642,34 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         const int sblocks = (int)std::min<int64_t>((p->nsl[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 16);
         p->r_nblocks[r] = p->r_count[r] ? p->r_nbl[r] + p->r_ncb[r] + std::max(sblocks, 1) : 0;
     }
-    GN_CUDA(cudaMalloc(&p->x[0], es * nb));
-    GN_CUDA(cudaMalloc(&p->x[1], es * nb));
-    // published values + the zero-valued padding slot n_all
-    GN_CUDA(cudaMalloc(&p->yg[0], gs * (nb + 1)));
-    GN_CUDA(cudaMalloc(&p->yg[1], gs * (nb + 1)));
+    // the run buffers stay where they are while their sizes hold: the yg
+    // buffers are mapped by the peers (CUDA IPC) and named by the captured
+    // schedule
+    if (p->alloc_nall != nall || p->alloc_dtype != p->dtype || p->alloc_iters != iters ||
+        p->alloc_nblocks[0] != p->r_nblocks[0] || p->alloc_nblocks[1] != p->r_nblocks[1]) {
+        part_free_run(p);
+        GN_CUDA(cudaMalloc(&p->x[0], es * nb));
+        GN_CUDA(cudaMalloc(&p->x[1], es * nb));
+        // published values + the zero-valued padding slot n_all
+        GN_CUDA(cudaMalloc(&p->yg[0], gs * (nb + 1)));
+        GN_CUDA(cudaMalloc(&p->yg[1], gs * (nb + 1)));
+        GN_CUDA(cudaMalloc(&p->v, es * nb));
+        GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
+        for (int r = 0; r < 2; ++r)
+            if (p->r_nblocks[r]) GN_CUDA(cudaMalloc((void**)&p->part[r], 32 * (size_t)iters * p->r_nblocks[r]));
+        p->alloc_nall = nall;
+        p->alloc_dtype = p->dtype;
+        p->alloc_iters = iters;
+        p->alloc_nblocks[0] = p->r_nblocks[0];
+        p->alloc_nblocks[1] = p->r_nblocks[1];
+    }
     GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 1)));
     GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 1)));
-    GN_CUDA(cudaMalloc(&p->v, es * nb));
-    GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
-    for (int r = 0; r < 2; ++r)
-        if (p->r_nblocks[r]) GN_CUDA(cudaMalloc((void**)&p->part[r], 32 * (size_t)iters * p->r_nblocks[r]));
     GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
+    // a new run epoch (see gn_part::epoch)
+    if (!p->d_epoch) GN_CUDA(cudaMalloc((void**)&p->d_epoch, sizeof(int64_t)));
+    p->epoch++;
+    GN_CUDA(cudaMemcpy(p->d_epoch, &p->epoch, sizeof(int64_t), cudaMemcpyHostToDevice));
     double* dx0 = nullptr;
     GN_CUDA(cudaMalloc((void**)&dx0, 8 * nb));
     if (nall) GN_CUDA(cudaMemcpy(dx0, x0, 8 * (size_t)nall, cudaMemcpyHostToDevice));
@@ -665,7 +692,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         // the ghost slots of the other buffer are filled by unpack before they are read
         GN_CUDA(cudaMemcpy(p->yg[1], p->yg[0], gs * (size_t)nall, cudaMemcpyDeviceToDevice));
     }
-    if (p->inflags) GN_CUDA(cudaMemset(p->inflags, 0, 8 * (size_t)p->parts));  // a new run: no step pushed yet
+    // (inflags are not reset: flags of an earlier epoch are below every target
+    // of this one, and a peer may already have signalled this epoch)
     if (p->halo_bad) GN_CUDA(cudaMemset(p->halo_bad, 0, sizeof(int)));
     GN_CUDA(cudaDeviceSynchronize());
     cudaFree(dx0);
@@ -674,13 +702,15 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
 
 // one range of the owned rows (0: boundary, 1: interior) for iteration k
 static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
-    if (p->r_count[r] == 0) return GN_OK;
+    if (p->r_count[r] == 0 && !(r == 1 && p->n_push > 0)) return GN_OK;
     const int cur = k & 1;
-    const int nb = p->r_nblocks[r];
     const int32_t* ord = p->order + p->r_start[r];
-    PartPush push{nullptr, nullptr, nullptr, nullptr, 0};
-    if (r == 0 && p->push_ptr)
-        push = PartPush{p->push_ptr, p->push_peer, p->push_slot, p->push_dst[(k + 1) & 1], p->n_bnd};
+    PartPush push{nullptr, nullptr, nullptr, nullptr, 0, 0};
+    // the boundary rows' pushes ride on the interior launch
+    if (r == 1 && p->n_push > 0)
+        push = PartPush{p->push_src, p->push_peer, p->push_slot, p->push_dst[(k + 1) & 1], p->n_push,
+                        (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
+    const int nb = (p->r_count[r] ? p->r_nblocks[r] : 0) + push.nblocks;
     const bool fast = !(p->flags & GN_EXACT);
     const int32_t* col = fast ? p->col_fast : p->col;
     const int32_t* sell = fast ? p->sell_fast : p->sell;
@@ -873,15 +903,19 @@ int gn_part_peer_commit(gn_part* p) {
     GN_CUDA(cudaSetDevice(p->device));
     part_free_push(p);
     const size_t np = p->h_push_row.size();
-    std::vector<int32_t> ptr((size_t)p->n_bnd + 1, 0), peer(std::max<size_t>(np, 1)), order(np);
+    // (peer, slot) order: each peer's ghost slots are one contiguous range
+    std::vector<size_t> ord(np);
+    for (size_t e = 0; e < np; ++e) ord[e] = e;
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+        return p->h_push_peer[a] != p->h_push_peer[b] ? p->h_push_peer[a] < p->h_push_peer[b]
+                                                       : p->h_push_slot[a] < p->h_push_slot[b];
+    });
+    std::vector<int32_t> src(std::max<size_t>(np, 1)), peer(std::max<size_t>(np, 1));
     std::vector<int64_t> slot(std::max<size_t>(np, 1));
-    for (size_t e = 0; e < np; ++e) ptr[(size_t)p->h_push_row[e] + 1]++;
-    for (int64_t r = 0; r < p->n_bnd; ++r) ptr[(size_t)r + 1] += ptr[(size_t)r];
-    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
-    for (size_t e = 0; e < np; ++e) {
-        const int32_t at = fill[(size_t)p->h_push_row[e]]++;
-        peer[(size_t)at] = p->h_push_peer[e];
-        slot[(size_t)at] = p->h_push_slot[e];
+    for (size_t j = 0; j < np; ++j) {
+        src[j] = p->h_push_row[ord[j]];
+        peer[j] = p->h_push_peer[ord[j]];
+        slot[j] = p->h_push_slot[ord[j]];
     }
     std::vector<void*> d0, d1;
     std::vector<int64_t*> fl;
@@ -891,27 +925,135 @@ int gn_part_peer_commit(gn_part* p) {
         fl.push_back(q.flags);
     }
     int rc;
-    if ((rc = upload_into(&p->push_ptr, ptr)) || (rc = upload_into(&p->push_peer, peer)) ||
+    if ((rc = upload_into(&p->push_src, src)) || (rc = upload_into(&p->push_peer, peer)) ||
         (rc = upload_into(&p->push_slot, slot)) || (rc = upload_into(&p->push_dst[0], d0)) ||
         (rc = upload_into(&p->push_dst[1], d1)) || (rc = upload_into(&p->peer_flags, fl)))
         return rc;
+    p->n_push = (int64_t)np;
     p->npush_peers = (int)p->peers.size();
+    p->gen++;
+    return GN_OK;
+}
+
+static int part_wait(gn_part* p, int k, cudaStream_t s) {
+    if (k == 0 || p->nexpect == 0) return GN_OK;  // step 0 reads the ghosts of x0
+    k_part_wait<<<1, 32, 0, s>>>(p->inflags, p->expect, p->nexpect, p->d_epoch, k, p->halo_bad);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
+static int part_signal(gn_part* p, int k, cudaStream_t s) {
+    if (p->npush_peers == 0) return GN_OK;
+    k_part_signal<<<1, 32, 0, s>>>(p->peer_flags, p->npush_peers, p->me, p->d_epoch, (int64_t)k + 1);
+    GN_LAUNCHED();
     return GN_OK;
 }
 
 int gn_part_peer_wait(gn_part* p, int k, uintptr_t stream) {
     if (!p || !p->inflags) return fail(GN_ERR_ARG, "gn_part_peer_wait before gn_part_peer_init");
-    if (k == 0 || p->nexpect == 0) return GN_OK;  // step 0 reads the ghosts of x0
-    k_part_wait<<<1, 32, 0, (cudaStream_t)stream>>>(p->inflags, p->expect, p->nexpect, k, p->halo_bad);
-    GN_LAUNCHED();
-    return GN_OK;
+    if (!p->d_epoch) return fail(GN_ERR_ARG, "gn_part_peer_wait before gn_part_begin");
+    return part_wait(p, k, (cudaStream_t)stream);
 }
 
 int gn_part_peer_signal(gn_part* p, int k, uintptr_t stream) {
     if (!p || !p->peer_flags) return fail(GN_ERR_ARG, "gn_part_peer_signal before gn_part_peer_commit");
-    if (p->npush_peers == 0) return GN_OK;
-    k_part_signal<<<1, 32, 0, (cudaStream_t)stream>>>(p->peer_flags, p->npush_peers, p->me, (int64_t)k + 1);
-    GN_LAUNCHED();
+    if (!p->d_epoch) return fail(GN_ERR_ARG, "gn_part_peer_signal before gn_part_begin");
+    return part_signal(p, k, (cudaStream_t)stream);
+}
+
+// Iterations [k0, k1) from a device-side schedule: the launches of every
+// iteration -- with the direct halo: wait for the peers' flags, boundary
+// rows, interior rows + pushes, flag the peers -- captured once into a CUDA
+// graph and replayed with one cudaGraphLaunch (no host work per iteration).
+// The graph names only buffers that stay put across runs (gn_part_begin) and
+// reads the run epoch from device memory, so one capture serves every run of
+// the same length and mode; it is rebuilt when the buffers or the push list
+// change.
+int gn_part_run(gn_part* p, int k0, int k1, uintptr_t stream) {
+    if (!p || k0 < 0 || k1 > p->iters || k0 >= k1 || !p->gam) return fail(GN_ERR_ARG, "bad gn_part_run arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    const bool peer = p->peer_flags != nullptr || p->nexpect > 0;
+    if (!p->gexec || p->g_gen != p->gen || p->g_k0 != k0 || p->g_k1 != k1) {
+        part_free_graph(p);
+        cudaStream_t cs = p->own_stream;
+        GN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        int rc = GN_OK;
+        const int64_t before = gn_launch_count();
+        for (int k = k0; k < k1 && rc == GN_OK; ++k) {
+            if (peer && p->inflags) rc = part_wait(p, k, cs);
+            if (!rc) rc = part_step_range(p, k, 0, cs);
+            if (!rc) rc = part_step_range(p, k, 1, cs);
+            if (!rc && peer && p->peer_flags) rc = part_signal(p, k, cs);
+        }
+        const int64_t nodes = gn_launch_count() - before;
+        note_launch(-nodes);  // counted when the graph runs
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+        e = cudaGraphInstantiate(&p->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            p->gexec = nullptr;
+            return cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+        }
+        p->g_gen = p->gen;
+        p->g_k0 = k0;
+        p->g_k1 = k1;
+        p->g_nodes = nodes;
+    }
+    GN_CUDA(cudaGraphLaunch(p->gexec, (cudaStream_t)stream));
+    note_launch(p->g_nodes);
+    return GN_OK;
+}
+
+// All parts of one graph held by this process (e.g. one GPU): iterations
+// [k0, k1) of every part interleaved in one captured schedule -- for each k,
+// for each part: wait, boundary rows, interior rows + pushes, signal -- so a
+// part's wait only ever finds flags that earlier nodes of the same stream
+// have set (no kernel waits on one that may not be running).  The schedule
+// of the multi-GPU run with the parts serialised; built, launched once and
+// released (tests and single-GPU measurements).
+int gn_part_run_group(gn_part* const* parts, int nparts, int k0, int k1, uintptr_t stream) {
+    if (!parts || nparts < 1) return fail(GN_ERR_ARG, "bad gn_part_run_group arguments");
+    for (int i = 0; i < nparts; ++i)
+        if (!parts[i] || k0 < 0 || k1 > parts[i]->iters || k0 >= k1 || !parts[i]->gam ||
+            parts[i]->device != parts[0]->device)
+            return fail(GN_ERR_ARG, "bad gn_part_run_group arguments");
+    GN_CUDA(cudaSetDevice(parts[0]->device));
+    cudaStream_t cs = parts[0]->own_stream;
+    GN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = GN_OK;
+    const int64_t before = gn_launch_count();
+    for (int k = k0; k < k1 && rc == GN_OK; ++k)
+        for (int i = 0; i < nparts && rc == GN_OK; ++i) {
+            gn_part* p = parts[i];
+            if (p->inflags) rc = part_wait(p, k, cs);
+            if (!rc) rc = part_step_range(p, k, 0, cs);
+            if (!rc) rc = part_step_range(p, k, 1, cs);
+            if (!rc && p->peer_flags) rc = part_signal(p, k, cs);
+        }
+    const int64_t nodes = gn_launch_count() - before;
+    note_launch(-nodes);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+    e = cudaGraphLaunch(exec, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaGraphExecDestroy(exec);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch", __FILE__, __LINE__);
+    note_launch(nodes);
     return GN_OK;
 }
 

@@ -128,6 +128,18 @@ class SolveTrace:
         return len(self.gamma)
 
 
+def _device_state(g, x):
+    """A CUDA fp64 tensor of n entries (a state kept in HBM, e.g.
+    run_engine(..., device_state=True).x), or None for host arrays."""
+    if type(x).__module__.split(".")[0] != "torch" or not getattr(x, "is_cuda", False):
+        return None
+    import torch
+
+    if x.dtype != torch.float64 or tuple(x.shape) != (g.n,) or not x.is_contiguous():
+        raise ValueError(f"device state must be a contiguous float64 CUDA tensor of shape ({g.n},)")
+    return x
+
+
 def _as_state(g, x) -> np.ndarray:
     x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     if x.shape != (g.n,):
@@ -178,14 +190,26 @@ class RunResult:
 
 def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early_exit: bool = False, *,
                dtype=None, exact=None, device=None, history: bool = False,
-               gammas: Optional[np.ndarray] = None) -> RunResult:
+               gammas: Optional[np.ndarray] = None, device_state: bool = False) -> RunResult:
     """run_wrgn with the engine's extras (stats, optional per-iteration x).
 
     ``gammas`` replaces the schedule's table (e.g. a prefix of a pursuit
     schedule); the early-exit test still compares with schedule.final_gamma.
+    ``device_state``: x0 may be a CUDA fp64 tensor and the result's x stays
+    in HBM as one (GN_DEVICE_IO), ready for round_to_mis / round_many without
+    a host round trip (the solver's run -> round hand-over, solver.py:75,88).
     """
-    x = _as_state(g, x0)
-    h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
+    dev = _opt("device", device)
+    h = device_graph(g, _opt("dtype", dtype), dev)
+    x_dev = _device_state(g, x0)
+    if device_state or x_dev is not None:
+        import torch
+
+        if x_dev is None:
+            x_dev = torch.from_numpy(_as_state(g, x0)).to(torch.device("cuda", dev))
+        x = None
+    else:
+        x = _as_state(g, x0)
     gam = np.ascontiguousarray(schedule.table() if gammas is None else np.asarray(gammas, dtype=np.float64))
     iters = len(gam)
     step_inf = np.zeros(iters, dtype=np.float64)
@@ -194,19 +218,28 @@ def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early
     energy = np.zeros(iters, dtype=np.float64) if record_trace else None
     pre_energy = np.zeros(iters, dtype=np.float64) if record_trace else None
     hist = np.zeros((iters, g.n), dtype=np.float64) if history else None
-    x_out = np.empty(g.n, dtype=np.float64)
     ran = ctypes.c_int(0)
     fail = ctypes.c_int(-1)
     st = E.RunStats()
     flags = 0
+    if x is None:
+        import torch
+
+        x_out = torch.empty(g.n, dtype=torch.float64, device=x_dev.device)
+        torch.cuda.current_stream(x_dev.device).synchronize()  # x0 is in place before the engine's stream reads it
+        flags |= E.GN_DEVICE_IO
+        xin, xo = ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(x_out.data_ptr())
+    else:
+        x_out = np.empty(g.n, dtype=np.float64)
+        xin, xo = E.ptr(x), E.ptr(x_out)
     if record_trace:
         flags |= E.GN_TRACE
     if early_exit:
         flags |= E.GN_EARLY_EXIT
     if _opt("exact", exact):
         flags |= E.GN_EXACT
-    rc = E.lib().gn_run(h.handle, E.ptr(x), E.ptr(gam), iters, float(schedule.final_gamma), flags,
-                        E.ptr(x_out), E.ptr(step_inf), E.ptr(fallbacks), E.ptr(mass), E.ptr(energy),
+    rc = E.lib().gn_run(h.handle, xin, E.ptr(gam), iters, float(schedule.final_gamma), flags,
+                        xo, E.ptr(step_inf), E.ptr(fallbacks), E.ptr(mass), E.ptr(energy),
                         E.ptr(pre_energy), E.ptr(hist), ctypes.byref(ran), ctypes.byref(fail),
                         ctypes.byref(st))
     if rc in _RUN_ERRORS:
@@ -325,9 +358,19 @@ def round_result(g, x, *, dtype=None, device=None) -> tuple[np.ndarray, float, b
 def round_many(g, xs, *, device=None) -> list[MisSolution]:
     """round_to_mis of every row of xs ([B, n]) in one engine call (the
     rounding kernels of all states are queued back to back, one sync)."""
-    X = np.ascontiguousarray(np.asarray(xs, dtype=np.float64))
+    flags = 0
+    if type(xs).__module__.split(".")[0] == "torch" and getattr(xs, "is_cuda", False):
+        import torch
+
+        if xs.dtype != torch.float64 or xs.dim() != 2 or xs.shape[1] != g.n or not xs.is_contiguous():
+            raise ValueError(f"device states must be a contiguous float64 CUDA tensor of shape (B, {g.n})")
+        X, xp, flags = xs, ctypes.c_void_p(xs.data_ptr()), E.GN_DEVICE_IO
+        torch.cuda.current_stream(xs.device).synchronize()
+    else:
+        X = np.ascontiguousarray(np.asarray(xs, dtype=np.float64))
+        xp = E.ptr(X)
     if X.ndim != 2 or X.shape[1] != g.n:
-        raise ValueError(f"states have shape {X.shape}, expected (B, {g.n})")
+        raise ValueError(f"states have shape {tuple(X.shape)}, expected (B, {g.n})")
     B = X.shape[0]
     if B == 0:
         return []
@@ -337,7 +380,7 @@ def round_many(g, xs, *, device=None) -> list[MisSolution]:
     ind = np.zeros(B, dtype=np.int32)
     mx = np.zeros(B, dtype=np.int32)
     cnt = np.zeros(B, dtype=np.int64)
-    E.check(E.lib().gn_round_many(h.handle, B, E.ptr(X), 0, E.ptr(sel), E.ptr(weight), E.ptr(ind), E.ptr(mx),
+    E.check(E.lib().gn_round_many(h.handle, B, xp, flags, E.ptr(sel), E.ptr(weight), E.ptr(ind), E.ptr(mx),
                                   E.ptr(cnt)))
     return [MisSolution._lazy(np.flatnonzero(sel[b, : g.n].view(np.bool_)), weight=float(weight[b]),
                         independent=bool(ind[b]), maximal=bool(mx[b])) for b in range(B)]
@@ -350,14 +393,23 @@ def round_to_mis(g, x) -> MisSolution:
     (ties keep the larger index), then completes greedily by descending
     weight (ties prefer the smaller index).
     """
-    x = _as_state(g, x)
-    h = any_device_graph(g, _opt("device", None))
+    x_dev = _device_state(g, x)
+    if x_dev is not None:  # the state stays in HBM (run_engine(..., device_state=True))
+        import torch
+
+        torch.cuda.current_stream(x_dev.device).synchronize()
+        xp, flags = ctypes.c_void_p(x_dev.data_ptr()), E.GN_DEVICE_IO
+        h = any_device_graph(g, x_dev.device.index or 0)
+    else:
+        x = _as_state(g, x)
+        xp, flags = E.ptr(x), 0
+        h = any_device_graph(g, _opt("device", None))
     members = np.empty(max(g.n, 1), dtype=np.int64)  # ids compacted on the device (no host scan of a mask)
     weight = ctypes.c_double()
     ind = ctypes.c_int()
     mx = ctypes.c_int()
     cnt = ctypes.c_int64()
-    E.check(E.lib().gn_round_members(h.handle, E.ptr(x), 0, E.ptr(members), ctypes.byref(weight), ctypes.byref(ind),
+    E.check(E.lib().gn_round_members(h.handle, xp, flags, E.ptr(members), ctypes.byref(weight), ctypes.byref(ind),
                                      ctypes.byref(mx), ctypes.byref(cnt)))
     return MisSolution._lazy(members[: cnt.value], weight=weight.value, independent=bool(ind.value),
                              maximal=bool(mx.value))

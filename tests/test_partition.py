@@ -98,6 +98,33 @@ def test_local_views_reproduce_global_rows_and_halo_lists():
             np.testing.assert_array_equal(owned_by_q, sent)
 
 
+def _send_lists_from_all_parts(g, parts):
+    """The send lists as the peers see them: p sends to q the ids of q's
+    ghosts that p owns (every part's rows are needed for this)."""
+    specs = build_partitions(g, parts)
+    out = {}
+    for p, sp in enumerate(specs):
+        for q, sq in enumerate(specs):
+            need = sq.ghosts[sq.ghost_ptr[p]:sq.ghost_ptr[p + 1]]
+            if q != p and len(need):
+                out[(p, q)] = (need - sp.lo).astype(np.int32)
+    return out
+
+
+@pytest.mark.parametrize("parts", [2, 3, 5, 8])
+def test_own_rows_send_lists_match_peer_ghost_lists(parts):
+    """build_partition derives a part's send lists from its own rows only
+    (the graph is symmetric); they equal the ghost lists of the peers."""
+    from paper_2605_05330_b200 import generators as G
+
+    for inst in (_graph(), G.c5_rmat(12), G.c3_ba(n=3000, m=4)):
+        ref = _send_lists_from_all_parts(inst.graph, parts)
+        got = {(p, q): v for p, sp in enumerate(build_partitions(inst.graph, parts)) for q, v in sp.send_idx.items()}
+        assert ref.keys() == got.keys()
+        for key in ref:
+            np.testing.assert_array_equal(ref[key], got[key])
+
+
 def test_local_exchange_protocol_is_bitwise_unpartitioned():
     inst = _graph()
     s = P.GammaSchedule.pursuit(iterations=200)
@@ -217,6 +244,8 @@ class NumpyPeerBackend(NumpyBackend):
         self.E = _FakeE(self)
         self.device = SimpleNamespace(index=0)
         self.names, self.opened, self.own = {}, {}, []
+        self._yblk = None
+        self.epoch = 0
 
     def _block(self, key, shape, dtype):
         from multiprocessing import shared_memory
@@ -233,15 +262,24 @@ class NumpyPeerBackend(NumpyBackend):
         return np.ndarray((shm.size // np.dtype(dtype).itemsize,), dtype=dtype, buffer=shm.buf)
 
     def begin(self, x0_local, gammas):
+        # as gn_part_begin: the buffers stay put across runs (the peers keep
+        # their mappings), a new epoch, the flags are not reset
         super().begin(x0_local, gammas)
         nall = self.spec.n_own + self.spec.n_ghost
-        self.y = [self._block(1, (nall,), np.float64), self._block(2, (nall,), np.float64)]
+        if self._yblk is None:
+            self._yblk = [self._block(1, (nall,), np.float64), self._block(2, (nall,), np.float64)]
+        self.y = self._yblk
         self.y[0][:] = self.v * x0_local
         self.y[1][:] = self.v * x0_local
+        self.epoch += 1
+
+    def sync(self):
+        pass
 
     def peer_init(self, parts, me, expect):
         self.me, self.expect, self.pushes = me, list(expect), []
         self.flags = self._block(3, (parts,), np.int64)
+        self.inits = getattr(self, "inits", 0) + 1
 
     def peer_buffers(self):
         return 1, 2, 3
@@ -256,7 +294,8 @@ class NumpyPeerBackend(NumpyBackend):
         import time
 
         t0 = time.time()
-        while k > 0 and any(self.flags[q] < k for q in self.expect):
+        target = (self.epoch << 32) + k
+        while k > 0 and any(self.flags[q] < target for q in self.expect):
             assert time.time() - t0 < 60, "peer flag did not arrive"
             time.sleep(0.0005)
 
@@ -268,7 +307,7 @@ class NumpyPeerBackend(NumpyBackend):
 
     def peer_signal(self, k):
         for rank, bufs, owned, slot0 in self.pushes:
-            self._view(bufs[2], np.int64)[self.me] = k + 1
+            self._view(bufs[2], np.int64)[self.me] = (self.epoch << 32) + k + 1
 
     def close(self):
         for shm in list(self.opened.values()) + self.own:
@@ -290,7 +329,13 @@ def _peer_worker(rank, world, port, q):
         s = P.GammaSchedule.pursuit(iterations=120)
         spec = build_partitions(inst.graph, world)[rank]
         be = NumpyPeerBackend(spec)
-        res = run_partition(be, DistPeerExchange(be), spec.local_x0(inst.x0), s)
+        ex = DistPeerExchange(be)
+        # two runs back to back on the same exchange: the second reuses the
+        # first handshake, and the fence + epochs keep them apart
+        res0 = run_partition(be, ex, spec.local_x0(inst.x0), s)
+        res = run_partition(be, ex, spec.local_x0(inst.x0), s)
+        assert be.inits == 1 and be.epoch == 2
+        assert np.array_equal(res0.x, res.x)
         out = [None] * world
         dist.all_gather_object(out, (spec.lo, res.x, res.step_inf, res.fallbacks))
         if rank == 0:
