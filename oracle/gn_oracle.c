@@ -336,6 +336,9 @@ int gno_step(int64_t n, const int64_t* indptr, const int32_t* indices,
  *   2 = mixed (fp64 state and sums, binary32 gathered values).
  *   gammas[k] = schedule.gamma_at(k) precomputed by the caller (bitwise).
  *   x_hist (optional): iters*n fp64, row k = state after step k, unclipped.
+ *   snaps/x_snap (optional): ascending iteration indices; row j of x_snap
+ *   (nsnap*n fp64) = the state after step snaps[j], unclipped (sampled
+ *   per-iteration checks of large instances without a full history).
  *   mass (optional): w . x_{k+1}, sequential.  energy/pre_energy need TRACE.
  * Returns GNO_OK or an error; on GNO_ERR_NONFINITE, *fail_iter = k.
  * ------------------------------------------------------------------------- */
@@ -344,6 +347,7 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             double final_gamma, unsigned flags, int nthreads,
             double* x_out, double* step_inf, int64_t* fallbacks, double* mass,
             double* energy, double* pre_energy, double* x_hist,
+            const int* snaps, int nsnap, double* x_snap,
             int* iters_run, int* fail_iter) {
     set_threads(nthreads);
     if (n < 0 || iters < 1) return GNO_ERR_ARG;
@@ -367,7 +371,7 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
     double dots[3];
     const int want_dots = trace || mass;
     int rc = GNO_OK;
-    int k, ran = 0;
+    int k, ran = 0, sj = 0;
     if (dtype == 0) {
         double* v = (double*)malloc(sizeof(double) * nb);
         double* xa = (double*)malloc(sizeof(double) * nb);
@@ -390,6 +394,7 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             fallbacks[k] = fb;
             if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist) memcpy(x_hist + (size_t)k * (size_t)n, xb, sizeof(double) * (size_t)n);
+            while (x_snap && sj < nsnap && snaps[sj] == k) memcpy(x_snap + (size_t)(sj++) * (size_t)n, xb, sizeof(double) * (size_t)n);
             double* t;
             t = xa; xa = xb; xb = t;
             t = ya; ya = yb; yb = t;
@@ -429,6 +434,7 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             fallbacks[k] = fb;
             if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist) memcpy(x_hist + (size_t)k * (size_t)n, xb, sizeof(double) * (size_t)n);
+            while (x_snap && sj < nsnap && snaps[sj] == k) memcpy(x_snap + (size_t)(sj++) * (size_t)n, xb, sizeof(double) * (size_t)n);
             double* t = xa; xa = xb; xb = t;
             float* tf = ya; ya = yb; yb = tf;
             ran = k + 1;
@@ -470,6 +476,10 @@ int gno_run(int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
             if (want_dots) post_dots(k, 0, gammas, dots, trace, energy, pre_energy, mass);
             if (x_hist)
                 for (int64_t i = 0; i < n; ++i) x_hist[(size_t)k * (size_t)n + (size_t)i] = (double)xb[i];
+            while (x_snap && sj < nsnap && snaps[sj] == k) {
+                for (int64_t i = 0; i < n; ++i) x_snap[(size_t)sj * (size_t)n + (size_t)i] = (double)xb[i];
+                ++sj;
+            }
             float* t;
             t = xa; xa = xb; xb = t;
             t = ya; ya = yb; yb = t;

@@ -48,7 +48,7 @@ def lib():
         L.gno_spmv.argtypes = [I64, P, P, P, P]
         L.gno_step.argtypes = [I64, P, P, P, P, ctypes.c_double, P, P, ctypes.c_int]
         L.gno_run.argtypes = [ctypes.c_int, I64, P, P, P, P, P, ctypes.c_int, ctypes.c_double, ctypes.c_uint,
-                              ctypes.c_int, P, P, P, P, P, P, P, P, P]
+                              ctypes.c_int, P, P, P, P, P, P, P, P, ctypes.c_int, P, P, P]
         L.gno_run.restype = ctypes.c_int
         L.gno_pairwise_sum.argtypes = [P, I64]
         L.gno_pairwise_sum.restype = ctypes.c_double
@@ -102,12 +102,15 @@ class OracleRun:
     energy: np.ndarray | None = None
     pre_energy: np.ndarray | None = None
     history: np.ndarray | None = None
+    snaps: np.ndarray | None = None
     extra: dict = field(default_factory=dict)
 
 
 def run(g, x0, gammas, final_gamma, *, dtype: str = "fp64", trace: bool = False, early_exit: bool = False,
-        history: bool = False, threads: int = 1) -> OracleRun:
-    """run_wrgn restated (dynamics.py:129-180); gammas = schedule table."""
+        history: bool = False, threads: int = 1, snaps=None) -> OracleRun:
+    """run_wrgn restated (dynamics.py:129-180); gammas = schedule table.
+    snaps: ascending iteration indices whose (unclipped) states are returned
+    in OracleRun.snaps (one row each)."""
     ip, ix, w = _csr(g)
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
     gam = np.ascontiguousarray(gammas, dtype=np.float64)
@@ -119,17 +122,21 @@ def run(g, x0, gammas, final_gamma, *, dtype: str = "fp64", trace: bool = False,
     en = np.zeros(iters) if trace else None
     pe = np.zeros(iters) if trace else None
     hist = np.zeros((iters, g.n)) if history else None
+    sk = None if snaps is None else np.ascontiguousarray(snaps, dtype=np.int32)
+    if sk is not None and (np.any(np.diff(sk) < 0) or (len(sk) and (sk[0] < 0 or sk[-1] >= iters))):
+        raise ValueError("snaps must be ascending iteration indices below the iteration count")
+    xs = None if sk is None else np.zeros((len(sk), g.n))
     ran = ctypes.c_int(0)
     fail = ctypes.c_int(-1)
     flags = (TRACE if trace else 0) | (EARLY_EXIT if early_exit else 0)
     code = {"fp64": 0, "fp32_pure": 1, "fp32": 2, "mixed": 2}[dtype]
     rc = lib().gno_run(code, g.n, _p(ip), _p(ix), _p(w), _p(x0), _p(gam), iters,
                        float(final_gamma), flags, threads, _p(x), _p(si), _p(fb), _p(mass), _p(en), _p(pe),
-                       _p(hist), ctypes.byref(ran), ctypes.byref(fail))
+                       _p(hist), _p(sk), 0 if sk is None else len(sk), _p(xs), ctypes.byref(ran), ctypes.byref(fail))
     k = ran.value
     return OracleRun(rc, x, k, fail.value, si[:k], fb[:k], mass[:k],
                      en[:k] if trace else None, pe[:k] if trace else None,
-                     hist[:k] if history else None)
+                     hist[:k] if history else None, xs)
 
 
 def pairwise_sum(a) -> float:

@@ -25,7 +25,7 @@ from .dynamics import GammaSchedule, NormalizationError, init_random, init_warm,
 from .graph import WeightedGraph, csr_from_edges, from_csr
 from .multistart import MAX_STARTS, run_multi
 
-FORMAT_VERSION = "1.0"
+FORMAT_VERSION = "0.1.0"  # the reference's result format version (io.py:32)
 
 
 @dataclass

@@ -1,0 +1,179 @@
+"""GPU parity at FULL budget in the modes bench.py times.
+
+Every benched configuration runs its whole 1000-iteration pursuit
+(dynamics.py:129-180) in the engine mode the bench uses, against the pinned
+oracle on the same instance:
+
+* C2 (256x256 assignment conflict graph, uint16 SELL, co-located long
+  slices), fp64 fast mode: x after 25 sampled iterations within 1e-9
+  relative, step_inf within 1e-9, identical fallbacks, identical members,
+  bitwise MIS weight;
+* C3 (Barabasi-Albert n=200k), fp64 fast mode: the same at 25 sampled
+  iterations;
+* C4: the whole 1024-graph shard through k_gn_batch (fp32: binary32
+  gathered values, fp64 state) for 1000 iterations; 64 sampled graphs are
+  bitwise their own same-arithmetic oracle run (x, step_inf, fallbacks) and
+  pass the fp32 gate against the fp64 oracle;
+* C5 at BASELINE scale 24 (16.8 M vertices, 260 M edges) through the
+  partitioned engine with one part from its device-side schedule (the
+  default bench line): the fp32 gate (objective <= 1e-4 relative at every
+  iteration, max|dx| <= 1e-4 at 30 sampled iterations, excursions listed)
+  against the fp64 oracle, and the fp64 engine's final state within 1e-9,
+  identical fallbacks, identical members, bitwise weight.
+
+Engine states at a sampled iteration k come from a run over the first k+1
+entries of the same gamma table (runs are deterministic, so this is the
+prefix of the full run); the oracle records its states at the same k
+(gn_oracle snapshots).  fp32 excursion reports are written under
+$GN_EXCURSION_DIR (default gpurun_out/fp32_excursions) and copied to profiles/.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import gn_oracle as O
+import paper_2605_05330_b200 as P
+from paper_2605_05330_b200 import generators as G
+
+pytestmark = pytest.mark.gpu
+
+THREADS = O.default_threads()
+ROOT = Path(__file__).resolve().parents[1]
+# per-iteration x: relative 1e-9; entries below 1e-250
+# (decayed to the edge of binary64's range) are compared absolutely
+RTOL, ATOL = 1e-9, 1e-250
+
+
+def samples(iters: int, count: int) -> list[int]:
+    return sorted({int(k) for k in np.linspace(0, iters - 1, count)})
+
+
+def prefix_states(run_prefix, tab, ks) -> np.ndarray:
+    return np.stack([run_prefix(tab[: k + 1]) for k in ks])
+
+
+def report_excursions(label: str, ks, dx: np.ndarray, worst_vertex: np.ndarray) -> list:
+    exc = [{"iteration": int(k), "max_abs_dx": float(d), "vertex": int(v)}
+           for k, d, v in zip(ks, dx, worst_vertex) if d > 1e-4]
+    out = Path(os.environ.get("GN_EXCURSION_DIR", ROOT / "gpurun_out" / "fp32_excursions"))
+    out.mkdir(parents=True, exist_ok=True)
+    (out / f"{label}.json").write_text(json.dumps(
+        {"config": label, "gate": "per-iteration max|dx| <= 1e-4 absolute vs the fp64 oracle; excursions "
+         "allowed on <= 1% of the checked iterations and <= 1e-3 (BASELINE.md section 4)",
+         "iterations_checked": len(ks), "max_abs_dx": float(dx.max()) if len(dx) else 0.0,
+         "excursions": exc}, indent=1) + "\n")
+    return exc
+
+
+def gate_fp32(label, ks, states, ref_states, objective, ref_mass):
+    mass_rel = np.abs(np.asarray(objective) - ref_mass) / np.abs(ref_mass)
+    assert mass_rel.max() <= 1e-4, f"{label}: objective rel {mass_rel.max():.3e}"
+    d = np.abs(states - ref_states)
+    dx, worst = d.max(axis=1), d.argmax(axis=1)
+    exc = report_excursions(label, ks, dx, worst)
+    assert len(exc) <= max(0.01 * len(ks), 1) and dx.max() <= 1e-3, f"{label}: excursions {exc[:10]}"
+
+
+def check_rounding(g, x_engine, x_ref):
+    sol = P.round_to_mis(g, x_engine)
+    sel, weight, ind, mx = O.round_to_mis(g, x_ref)
+    assert np.array_equal(np.asarray(sol._idx), np.flatnonzero(sel))
+    assert sol.weight == weight and sol.independent == ind and sol.maximal == mx and ind and mx
+
+
+@pytest.mark.parametrize("config", ["C2", "C3"])
+def test_fp64_fast_full_budget_sampled_iterations(config):
+    inst = G.c2_assignment() if config == "C2" else G.c3_ba()
+    g, s = inst.graph, P.GammaSchedule.pursuit()
+    tab = s.table()
+    ks = samples(len(tab), 25)
+    ref = O.run(g, inst.x0, tab, s.final_gamma, snaps=ks, threads=THREADS)
+    r = P.run_engine(g, inst.x0, s)  # the benched mode: fp64, fast (split long rows)
+    assert len(r.trace.step_inf) == 1000
+    np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
+    np.testing.assert_allclose(r.trace.step_inf, ref.step_inf, rtol=RTOL, atol=1e-15)
+    np.testing.assert_allclose(r.x, ref.x, rtol=RTOL, atol=ATOL)
+    states = prefix_states(lambda t: P.run_engine(g, inst.x0, s, gammas=t).x, tab, ks)
+    np.testing.assert_allclose(states, ref.snaps, rtol=RTOL, atol=ATOL)
+    np.testing.assert_array_equal(states[-1], r.x)  # the last prefix is the full run
+    check_rounding(g, r.x, ref.x)
+
+
+def test_c4_full_shard_batch_kernel_sampled_graphs():
+    from paper_2605_05330_b200.batch import GraphBatch
+
+    b = G.c4_batch(graphs=1024)
+    inst = b.instance
+    s = P.GammaSchedule.pursuit()
+    tab = s.table()
+    bt = GraphBatch(inst.graph, b.offsets, dtype="fp32")
+    res = bt.run(inst.x0, s)  # the benched call: k_gn_batch, per-graph traces
+    assert (res.status == 0).all() and (res.iters_run == 1000).all()
+    pick = np.random.default_rng(2605).choice(1024, 64, replace=False)
+    ks = samples(1000, 20)
+    for gi in sorted(pick.tolist()):
+        lo, hi = int(b.offsets[gi]), int(b.offsets[gi + 1])
+        sub = P.from_csr(hi - lo, np.asarray(inst.graph.indptr[lo:hi + 1]) - inst.graph.indptr[lo],
+                         np.asarray(inst.graph.indices[inst.graph.indptr[lo]:inst.graph.indptr[hi]]) - lo,
+                         np.asarray(inst.graph.w[lo:hi]))
+        x0 = inst.x0[lo:hi]
+        same = O.run(sub, x0, tab, s.final_gamma, dtype="fp32")  # the engine's arithmetic
+        np.testing.assert_array_equal(res.state(gi, b.offsets), same.x)
+        np.testing.assert_array_equal(res.step_inf[gi], same.step_inf)
+        np.testing.assert_array_equal(res.fallbacks[gi], same.fallbacks)
+        np.testing.assert_allclose(res.objective[gi], same.mass, rtol=1e-12)
+        ref = O.run(sub, x0, tab, s.final_gamma, snaps=ks)  # the reference's fp64 arithmetic
+        eng = O.run(sub, x0, tab, s.final_gamma, dtype="fp32", snaps=ks)  # = the engine's states
+        gate_fp32(f"C4_graph{gi}", ks, eng.snaps, ref.snaps, res.objective[gi], ref.mass)
+        sol = P.round_to_mis(sub, res.state(gi, b.offsets))
+        sel, weight, _, _ = O.round_to_mis(sub, ref.x)
+        assert np.array_equal(np.asarray(sol._idx), np.flatnonzero(sel)) and sol.weight == weight
+
+
+@pytest.fixture(scope="module")
+def c5_scale24():
+    return G.c5_rmat_gpu(24)
+
+
+def test_c5_scale24_partitioned_fp32_and_fp64_full_budget(c5_scale24):
+    from paper_2605_05330_b200.partition import EngineBackend, NoExchange, build_partition, run_partition
+
+    inst = c5_scale24
+    g, s = inst.graph, P.GammaSchedule.pursuit()
+    tab = s.table()
+    ks = samples(1000, 30)
+    ref = O.run(g, inst.x0, tab, s.final_gamma, snaps=ks, threads=THREADS)
+    spec = build_partition(g, 1, 0)
+    x0l = spec.local_x0(inst.x0)
+    be = EngineBackend(spec, dtype="fp32")  # the default bench line's engine and mode
+    ex = NoExchange(be)
+    full = run_partition(be, ex, x0l, s)
+    assert full.bad < 0 and len(full.mass) == 1000
+
+    states = prefix_states(lambda t: run_partition(be, ex, x0l, _Sched(t)).x, tab, ks)
+    gate_fp32("C5_scale24_partitioned", ks, states, ref.snaps, full.mass, ref.mass)
+    be.close()
+    # the fp64 engine (the persistent loop kernel) over the same 1000 iterations
+    r = P.run_engine(g, inst.x0, s, dtype="fp64")
+    np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
+    np.testing.assert_allclose(r.x, ref.x, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(r.trace.step_inf, ref.step_inf, rtol=RTOL, atol=1e-15)
+    check_rounding(g, r.x, ref.x)
+
+
+class _Sched:
+    """A schedule whose table is a given prefix of the pursuit table."""
+
+    def __init__(self, t):
+        self._t = np.asarray(t, dtype=np.float64)
+        self.iterations = len(self._t)
+        self.final_gamma = 1.5
+
+    def table(self):
+        return self._t
