@@ -254,6 +254,12 @@ int gn_part_run(gn_part* p, int k0, int k1, uintptr_t stream);
  * `stream` and synchronised -- the multi-GPU schedule with the parts run one
  * after another, so no wait depends on a kernel that is not already done. */
 int gn_part_run_group(gn_part* const* parts, int nparts, int k0, int k1, uintptr_t stream);
+/* Measurement aid (not on the solve path): ms per launch of one piece of
+ * iteration 0 of the current run on the interior range -- mode 0 the step
+ * kernel, 1 its warp-split long rows only, 2 its SELL slices only, 3..6 the
+ * slices' gather walk alone with real gathers / no gathers (index stream
+ * only) / L1-resident gathers / random gathers.  Call after gn_part_begin. */
+int gn_part_probe(gn_part* p, int mode, int reps, double* ms);
 /* CUDA IPC of one device allocation between the processes of a node. */
 int gn_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */);
 int gn_ipc_open_handle(const void* handle, int device, void** dptr);

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _engine as E
-from .dynamics import GammaSchedule, NormalizationError, _opt
+from .dynamics import GammaSchedule, NormalizationError, _opt, gamma_table
 from .graph import WeightedGraph, csr_from_edges, dtype_code, from_csr
 
 
@@ -81,7 +81,7 @@ class GraphBatch:
         """run_wrgn on every graph.  x0 is the packed start (host numpy), or
         device_x0/device_x_out are fp64 CUDA pointers (inputs already in HBM)."""
         iters = schedule.iterations
-        gam = np.ascontiguousarray(schedule.table())
+        gam = gamma_table(schedule)
         B = self.B
         si = np.zeros((B, iters))
         fb = np.zeros((B, iters), dtype=np.int64)

@@ -393,6 +393,58 @@ __global__ void k_part_out(int64_t n, const TS* __restrict__ x, const int32_t* _
     }
 }
 
+// ---- gather probes (gn_part_probe; measurement aids, not on the solve path)
+// The SELL walk of k_part_step's thread-per-row branch with the update
+// replaced by a plain store of the sum, in five variants that bound what the
+// step can reach on this graph: MODE 1 the real gathers; 2 the index stream
+// alone (no gathers); 3 every gather redirected into a 4096-entry table (L1
+// hits: the walk's instruction and latency floor); 4 random gathers over the
+// same table size (hash of the position; no locality at all).
+template <typename TG, int MODE>
+__global__ void __launch_bounds__(kPartThreads) k_part_probe(const int32_t* __restrict__ sell,
+                                                             const int64_t* __restrict__ slice_ptr, int64_t nsl,
+                                                             int64_t count, int64_t pos0, const TG* __restrict__ yg,
+                                                             uint32_t nall, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kWarpsPerBlock = kPartThreads / 32;
+    const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
+    for (int64_t sl = (int64_t)blockIdx.x * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
+        const int64_t pos = pos0 + sl * 32 + lane;
+        const int64_t e0 = slice_ptr[sl];
+        const int nblk = (int)((slice_ptr[sl + 1] - e0) / 128);
+        const uint4* base = reinterpret_cast<const uint4*>(sell + e0) + lane;
+        constexpr int NV = kPartUnroll / 4;
+        uint4 cv[NV];
+#pragma unroll
+        for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? __ldg(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+        double s = 0.0;
+        for (int b = 0; b < nblk; b += NV) {
+            uint4 nv[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u)
+                nv[u] = b + NV + u < nblk ? __ldg(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+            TG y[4 * NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const bool in = b + u < nblk;
+                const uint32_t id[4] = {(uint32_t)cv[u].x, (uint32_t)cv[u].y, (uint32_t)cv[u].z, (uint32_t)cv[u].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t j = id[c];
+                    if (MODE == 3) j &= 4095u;
+                    if (MODE == 4) j = (uint32_t)(((uint64_t)(pos * 2654435761u + (b + u) * 40503u + c) * 0x9E3779B1u) % nall);
+                    y[4 * u + c] = !in ? TG(0) : (MODE == 2 ? (TG)(j & 1u) : __ldg(yg + j));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4 * NV; ++q) s += (double)y[q];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+        }
+        if (pos < count) out[pos] = s;
+    }
+}
+
 static int pblocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kPartThreads - 1) / kPartThreads, 1 << 16)); }
 
 template <typename F>
@@ -1079,6 +1131,93 @@ int gn_ipc_open_handle(const void* handle, int device, void** dptr) {
 int gn_ipc_close(void* dptr) {
     if (!dptr) return GN_OK;
     GN_CUDA(cudaIpcCloseMemHandle(dptr));
+    return GN_OK;
+}
+
+// Measurement aid: time (ms per launch, CUDA events, `reps` launches after
+// one warm-up) of one piece of iteration 0 of the current run, on the
+// interior range (all rows when there is one part):
+//   mode 0  k_part_step, the whole range
+//   mode 1  k_part_step, only the warp-split long rows
+//   mode 2  k_part_step, only the SELL slices (thread per row)
+//   mode 3..6  the probe walk of the slices (k_part_probe MODE 1..4)
+int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
+    if (!p || !p->gam || mode < 0 || mode > 6 || reps < 1 || !ms) return fail(GN_ERR_ARG, "bad gn_part_probe arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    const int r = p->r_count[1] ? 1 : 0;
+    if (!p->r_count[r]) { *ms = 0.0; return GN_OK; }
+    cudaStream_t s = p->own_stream;
+    const bool fast = !(p->flags & GN_EXACT);
+    const int32_t* col = fast ? p->col_fast : p->col;
+    const int32_t* sell = fast ? p->sell_fast : p->sell;
+    const int32_t* ord = p->order + p->r_start[r];
+    const int64_t pos0 = p->r_long[r] + p->r_csr[r];
+    const int nsb = p->r_nblocks[r] - p->r_nbl[r] - p->r_ncb[r];
+    double* out = nullptr;
+    GN_CUDA(cudaMalloc((void**)&out, 8 * (size_t)std::max<int64_t>(p->r_count[r], 1)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    PartPush none{nullptr, nullptr, nullptr, nullptr, 0, 0};
+    auto launch = [&]() {
+        const int cur = 0;
+        if (mode <= 2) {
+            const int64_t nl = p->r_long[r];
+            const int nbl = mode == 2 ? 0 : p->r_nbl[r];
+            const int64_t ncsr = mode == 0 ? p->r_csr[r] : 0;
+            const int ncb = mode == 0 ? p->r_ncb[r] : 0;
+            const int64_t nsl = mode == 1 ? 0 : p->nsl[r];
+            const int nb = mode == 1 ? std::max(nbl, 1) : mode == 2 ? std::max(nsb, 1) : p->r_nblocks[r];
+            // mode 2 keeps the slices' order positions (pos0 = n_long + n_csr)
+            const int64_t nlong_arg = mode == 2 ? pos0 : nl;
+            if (p->dtype == GN_F32)
+                k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
+                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
+                    p->w64, (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1],
+                    (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
+            else if (p->dtype == GN_F64)
+                k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
+                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
+                    p->w64, (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1],
+                    (const double*)p->yg[cur], (double*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
+            else
+                k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
+                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
+                    p->w64, (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1],
+                    (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
+        } else {
+            const int nb = std::max(nsb, 1);
+            const uint32_t nall = (uint32_t)(p->n_own + p->n_ghost);
+            const int64_t cnt = p->r_count[r];
+            const int64_t* sp = p->slice_ptr + p->sl0[r];
+            if (gather_bytes(p->dtype) == 4) {
+                const float* y = (const float*)p->yg[0];
+                if (mode == 3) k_part_probe<float, 1><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 4) k_part_probe<float, 2><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 5) k_part_probe<float, 3><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 6) k_part_probe<float, 4><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+            } else {
+                const double* y = (const double*)p->yg[0];
+                if (mode == 3) k_part_probe<double, 1><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 4) k_part_probe<double, 2><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 5) k_part_probe<double, 3><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+                if (mode == 6) k_part_probe<double, 4><<<nb, kPartThreads, 0, s>>>(sell, sp, p->nsl[r], cnt, pos0, y, nall, out);
+            }
+        }
+    };
+    launch();
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < reps; ++i) launch();
+    cudaEventRecord(e1, s);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (e != cudaSuccess) return cuda_fail(e, "gn_part_probe", __FILE__, __LINE__);
+    GN_LAUNCHED();
+    *ms = (double)t / reps;
     return GN_OK;
 }
 

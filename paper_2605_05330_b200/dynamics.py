@@ -128,6 +128,18 @@ class SolveTrace:
         return len(self.gamma)
 
 
+def gamma_table(schedule) -> np.ndarray:
+    """gamma_at(k) for every k of the run (dynamics.py:65-69), as a float64
+    array: GammaSchedule.table() for the engine's own schedules, else the
+    schedule's own gamma_at -- so the reference's graphnorm.GammaSchedule
+    (or any object with iterations / gamma_at / final_gamma) drives the
+    engine with bitwise its own values."""
+    t = getattr(schedule, "table", None)
+    if callable(t):
+        return np.ascontiguousarray(t(), dtype=np.float64)
+    return np.array([schedule.gamma_at(k) for k in range(int(schedule.iterations))], dtype=np.float64)
+
+
 def _device_state(g, x):
     """A CUDA fp64 tensor of n entries (a state kept in HBM, e.g.
     run_engine(..., device_state=True).x), or None for host arrays."""
@@ -210,7 +222,7 @@ def run_engine(g, x0, schedule: GammaSchedule, record_trace: bool = False, early
         x = None
     else:
         x = _as_state(g, x0)
-    gam = np.ascontiguousarray(schedule.table() if gammas is None else np.asarray(gammas, dtype=np.float64))
+    gam = np.ascontiguousarray(gamma_table(schedule) if gammas is None else np.asarray(gammas, dtype=np.float64))
     iters = len(gam)
     step_inf = np.zeros(iters, dtype=np.float64)
     fallbacks = np.zeros(iters, dtype=np.int64)
@@ -425,6 +437,7 @@ __all__ = [
     "SolveTrace",
     "energy",
     "fitness",
+    "gamma_table",
     "gn_step",
     "init_random",
     "init_warm",

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _engine as E
-from .dynamics import GammaSchedule, SolveTrace, _opt
+from .dynamics import GammaSchedule, SolveTrace, _opt, gamma_table
 from .graph import device_graph
 
 MAX_STARTS = 64
@@ -75,7 +75,7 @@ def run_multi(g, x0s, schedule: GammaSchedule, early_exit: bool = False, *, dtyp
     if not 1 <= B <= MAX_STARTS:
         raise ValueError(f"between 1 and {MAX_STARTS} starts per call")
     h = device_graph(g, _opt("dtype", dtype), _opt("device", device))
-    gam = np.ascontiguousarray(schedule.table())
+    gam = gamma_table(schedule)
     iters = len(gam)
     x = np.empty((B, g.n))
     si = np.zeros((B, iters))

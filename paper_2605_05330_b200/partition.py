@@ -32,7 +32,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .dynamics import GammaSchedule
+from .dynamics import GammaSchedule, gamma_table
 
 
 @dataclass
@@ -500,7 +500,7 @@ def run_partition(backend, exchange, x0_local: np.ndarray, schedule: GammaSchedu
     the ranks, reset the run, then every iteration -- from the device-side
     schedule (one CUDA-graph launch) when the exchange allows it, else one
     host-driven step per iteration (dynamics.py:155-178)."""
-    gam = schedule.table()
+    gam = gamma_table(schedule)
     exchange.fence()
     backend.begin(x0_local, gam)
     exchange.setup()
@@ -534,7 +534,7 @@ def run_local_partitions(g, x0: np.ndarray, schedule: GammaSchedule, parts: int,
     specs = build_partitions(g, parts)
     backends = [make_backend(s) for s in specs]
     ex = LocalPeerExchange(backends) if halo == "peer" else LocalExchange(backends)
-    gam = schedule.table()
+    gam = gamma_table(schedule)
     for _ in range(runs):
         outs = _local_run(backends, specs, ex, x0, gam, halo, device_schedule)
     x = np.concatenate([o[0] for o in outs])
