@@ -417,6 +417,9 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
         t0 = time.perf_counter()
         res = run_partition(be, ex, x0p, sched)
         torch.cuda.synchronize(dev)
+        if os.environ.get("GN_BENCH_VERBOSE"):
+            print(f"e2e step {i}: {1e3 * (time.perf_counter() - t0):.1f} ms; " +
+                  ", ".join(f"{k} {1e3 * v:.1f} ms" for k, v in be.last_times.items()), file=sys.stderr, flush=True)
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
     e2e_total = sum(e2e)

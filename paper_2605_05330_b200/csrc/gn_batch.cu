@@ -746,6 +746,7 @@ extern "C" {
 
 int gn_batch_create(int64_t num_graphs, const int64_t* offsets, int64_t n, const int64_t* indptr,
                     const int32_t* indices, const double* w, int dtype, int device, gn_batch** out) {
+    GN_NVTX("gn_batch_create");
     if (!valid_dtype(dtype)) return fail(GN_ERR_ARG, "dtype must be GN_F64, GN_F32 or GN_F32_PURE");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -775,6 +776,7 @@ int gn_batch_destroy(gn_batch* b) {
 int gn_batch_run(gn_batch* b, const void* x0, const double* gammas, int iters, double final_gamma, uint32_t flags,
                  void* x_out, double* step_inf, int64_t* fallbacks, double* mass, int* iters_run, int* status,
                  int* fail_iter, gn_run_stats* stats) {
+    GN_NVTX("gn_batch_run");
     if (!b) return fail(GN_ERR_ARG, "null batch");
     if (iters < 1) return fail(GN_ERR_ARG, "iterations must be positive");
     if (!gammas || (b->n > 0 && !x0)) return fail(GN_ERR_ARG, "null input array");

@@ -197,6 +197,7 @@ extern "C" {
 
 int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed, int device,
                 int64_t* nnz_out, int64_t** indptr_out, int32_t** indices_out) {
+    GN_NVTX("gn_gen_rmat");
     *nnz_out = 0;
     *indptr_out = nullptr;
     *indices_out = nullptr;
@@ -220,6 +221,7 @@ int gn_gen_rmat(int scale, int edge_factor, double a, double b, double c, uint64
 
 int gn_csr_from_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v, int device, int64_t* first_bad,
                       int64_t* nnz_out, int64_t** indptr_out, int32_t** indices_out) {
+    GN_NVTX("gn_csr_from_edges");
     *nnz_out = 0;
     *indptr_out = nullptr;
     *indices_out = nullptr;

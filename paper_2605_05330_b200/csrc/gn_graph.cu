@@ -496,6 +496,7 @@ int gn_device_count(int* count) {
 
 int gn_graph_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* w, int dtype,
                     int device, gn_graph** out) {
+    GN_NVTX("gn_graph_create");
     *out = nullptr;
     if (n < 0) return fail(GN_ERR_ARG, "vertex count must be nonnegative");
     if (!valid_dtype(dtype)) return fail(GN_ERR_ARG, "dtype must be GN_F64, GN_F32 or GN_F32_PURE");
@@ -673,6 +674,7 @@ int gn_spmv(gn_graph* g, const double* in, double* out) {
 }
 
 int gn_is_normalizable(gn_graph* g, const double* x, int* ok) {
+    GN_NVTX("gn_is_normalizable");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     CallCtx ctx;
     int rc = ctx.open(g->device);
@@ -696,6 +698,7 @@ int gn_is_normalizable(gn_graph* g, const double* x, int* ok) {
 }
 
 int gn_energy(gn_graph* g, const double* x, double gamma, double* energy) {
+    GN_NVTX("gn_energy");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     CallCtx ctx;
     int rc = ctx.open(g->device);

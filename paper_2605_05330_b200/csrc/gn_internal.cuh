@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 #include <vector>
 
@@ -26,6 +28,16 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 void note_launch(int64_t k = 1);
+
+// NVTX range over one ABI call (header-only NVTX3: a no-op unless a tool
+// such as nsys / ncu --nvtx is attached), named after the ABI entry point.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define GN_NVTX(name) ::gn::NvtxRange gn_nvtx_range_(name)
 
 #define GN_CUDA(expr)                                                      \
     do {                                                                   \

@@ -1268,6 +1268,7 @@ extern "C" {
 int gn_run(gn_graph* g, const void* x0, const double* gammas, int iters, double final_gamma, uint32_t flags,
            void* x_out, double* step_inf, int64_t* fallbacks, double* mass, double* energy, double* pre_energy,
            double* x_hist, int* iters_run, int* fail_iter, gn_run_stats* stats) {
+    GN_NVTX("gn_run");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (iters < 1) return fail(GN_ERR_ARG, "iterations must be positive");
     if (!gammas || (g->n > 0 && !x0)) return fail(GN_ERR_ARG, "null input array");
@@ -1293,6 +1294,7 @@ int gn_run(gn_graph* g, const void* x0, const double* gammas, int iters, double 
 }
 
 int gn_step(gn_graph* g, const double* x, double gamma, uint32_t flags, double* out, int64_t* nfb) {
+    GN_NVTX("gn_step");
     double si = 0.0;
     int64_t fb = 0;
     int ran = 0, fi = -1;

@@ -872,6 +872,7 @@ using namespace gn;
 extern "C" int gn_multi_run(gn_graph* g, int num_starts, const double* x0, const double* gammas, int iters,
                             double final_gamma, uint32_t flags, double* x_out, double* step_inf, int64_t* fallbacks,
                             int* iters_run, int* status, int* fail_iter, gn_run_stats* stats) {
+    GN_NVTX("gn_multi_run");
     if (!g || !x0 || !status || (iters > 0 && !gammas)) return fail(GN_ERR_ARG, "null argument");
     if (num_starts < 1 || num_starts > kMaxStarts) return fail(GN_ERR_ARG, "num_starts must be in [1, 64]");
     if (iters < 0) return fail(GN_ERR_ARG, "iters must be >= 0");

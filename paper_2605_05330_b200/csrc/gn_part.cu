@@ -59,6 +59,19 @@ struct gn_part {
     int64_t* slice_ptr = nullptr;   // [nslices+1] element offsets
     int64_t sl0[2] = {0, 0}, nsl[2] = {0, 0};  // per range: first slice, slice count
     int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
+    // fast mode: the long rows of each range cut into pieces of kPiece
+    // adjacency entries (fixed sizes: the sum tree, and every bit, is the
+    // same on any grid).  Piece j covers col[pc_beg[j], pc_end[j]); long row
+    // q of range r owns pieces [lp[lp0[r] + q], lp[lp0[r] + q + 1]).  Warps
+    // sum pieces into pc_sum; k_part_long_combine adds a row's pieces in
+    // piece order and updates the row.
+    int32_t* pc_beg = nullptr;
+    int32_t* pc_end = nullptr;
+    int32_t* lp = nullptr;
+    double* pc_sum = nullptr;
+    int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
+    int r_ncomb[2] = {0, 0};                 // per range: combine blocks
+    double* part_long[2] = {nullptr, nullptr};  // per range [iters][r_ncomb][4]
     // per range (0 boundary, 1 interior), set by gn_part_begin
     int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0}, r_csr[2] = {0, 0};
     int r_nbl[2] = {0, 0}, r_ncb[2] = {0, 0}, r_nblocks[2] = {0, 0};
@@ -103,13 +116,19 @@ struct gn_part {
     // run buffers are kept across runs while their sizes do not change (their
     // addresses are exported to the peers over CUDA IPC)
     int64_t alloc_nall = -1;
-    int alloc_dtype = -1, alloc_iters = 0, alloc_nblocks[2] = {0, 0};
+    int alloc_dtype = -1, alloc_iters = 0, alloc_nblocks[2] = {0, 0}, alloc_ncomb[2] = {0, 0};
     // device-side schedule (gn_part_run): the iterations' launches captured
     // once into a CUDA graph, rebuilt when `gen` (buffers, push list) moves
     uint64_t gen = 1, g_gen = 0;
     int g_k0 = -1, g_k1 = -1;
     int64_t g_nodes = 0;
     cudaGraphExec_t gexec = nullptr;
+    // host <-> device staging kept across runs: x0 in (caller's numbering)
+    // and x out; the per-range stats of gn_part_end
+    double* io = nullptr;
+    int64_t io_n = 0;
+    double* dout = nullptr;
+    int64_t dout_n = 0;
 };
 
 namespace gn {
@@ -130,6 +149,15 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
 }
 
 constexpr int kPartLongDegree = 512;
+constexpr int kPiece = 2048;  // adjacency entries per long-row piece (fast mode)
+
+// The long rows' pieces (fast mode; see gn_part::pc_beg)
+struct PartLong {
+    const int32_t* __restrict__ beg;
+    const int32_t* __restrict__ end;
+    double* __restrict__ sum;
+    int64_t n;
+};
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
 #endif
@@ -177,8 +205,10 @@ struct PartPush {
 // blocks give one warp to each slice of the blocked SELL, one thread per row.
 // Every thread-per-row sum is sequential in the reference's order (bitwise),
 // with 8 gathers in flight and the next index vectors loading under them.
+// 4 blocks of 256 threads per SM (64 registers, no spills): 32 warps to hide
+// the gathers' latency (C5 scale 24: 1.71 -> 1.59 ms per iteration vs 3)
 #ifndef GN_PART_MINB
-#define GN_PART_MINB 1
+#define GN_PART_MINB 4
 #endif
 template <typename TS, typename TG>
 __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_t n_long, int nbl, int64_t n_csr, int ncb,
@@ -191,7 +221,8 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
                                                             const TS* __restrict__ x, TS* __restrict__ xo,
                                                             const TG* __restrict__ yg, TG* __restrict__ ygo,
                                                             const double* __restrict__ gam, int k,
-                                                            double* __restrict__ part, PartPush push) {
+                                                            double* __restrict__ part, PartPush push,
+                                                            PartLong lng) {
     using A = Arith<TS>;
     if ((int)blockIdx.x < push.nblocks) {  // the halo blocks
         const int64_t stride = (int64_t)push.nblocks * blockDim.x;
@@ -205,22 +236,38 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
     constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
     if (bid < nbl) {
-        for (int64_t q = (int64_t)bid * kWarpsPerBlock + warp; q < n_long; q += (int64_t)nbl * kWarpsPerBlock) {
-            const int64_t i = order[q];
-            const int32_t rb = rowptr[i], re = rowptr[i + 1];
+        // long rows, fast mode: one warp per piece of kPiece entries; lanes
+        // stride the positions, 8 gathers in flight per lane with the next 8
+        // indices loading under them; fixed butterfly fold.  The rows are
+        // updated by k_part_long_combine (pieces added in piece order).
+        for (int64_t q = (int64_t)bid * kWarpsPerBlock + warp; q < lng.n; q += (int64_t)nbl * kWarpsPerBlock) {
+            const int32_t pb = __ldg(lng.beg + q), pe = __ldg(lng.end + q);
             TS s = TS(0);
-            int32_t p = rb + lane;
-            for (; p + 3 * 32 < re; p += 4 * 32) {
-                const TG y0 = yg[col[p]], y1 = yg[col[p + 32]], y2 = yg[col[p + 64]], y3 = yg[col[p + 96]];
-                s = A::add(s, (TS)y0);
-                s = A::add(s, (TS)y1);
-                s = A::add(s, (TS)y2);
-                s = A::add(s, (TS)y3);
+            constexpr int U = 8;
+            int32_t idx[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t pp = pb + lane + 32 * u;
+                idx[u] = pp < pe ? __ldg(col + pp) : -1;
             }
-            for (; p < re; p += 32) s = A::add(s, (TS)yg[col[p]]);
+            for (int32_t p = pb + lane; p < pe; p += 32 * U) {
+                int32_t nidx[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int32_t pp = p + 32 * (U + u);
+                    nidx[u] = pp < pe ? __ldg(col + pp) : -1;
+                }
+                TG y[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) y[u] = idx[u] >= 0 ? __ldg(yg + idx[u]) : TG(0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) s = A::add(s, (TS)y[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) idx[u] = nidx[u];
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-            if (lane == 0) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            if (lane == 0) lng.sum[q] = (double)s;
         }
     } else if (bid < nbl + ncb) {
         for (int64_t q = (int64_t)(bid - nbl) * blockDim.x + threadIdx.x; q < n_csr;
@@ -301,6 +348,54 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
             t[3] = fmax(t[3], red[q][3]);
         }
         double* dst = part + ((size_t)k * nbid + bid) * 4;
+        dst[0] = t[0];
+        dst[1] = t[1];
+        dst[2] = t[2];
+        dst[3] = t[3];
+    }
+}
+
+// Long rows, fast mode: row q of the range adds its pieces' sums in piece
+// order and is updated (dynamics.py:104-107); per-block stats as k_part_step.
+template <typename TS, typename TG>
+__global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
+    int64_t n_long, int64_t first, const int32_t* __restrict__ lp, const double* __restrict__ pc_sum,
+    const double* __restrict__ w64, const TS* __restrict__ v, const TS* __restrict__ x, TS* __restrict__ xo,
+    TG* __restrict__ ygo, const double* __restrict__ gam, int k, double* __restrict__ part) {
+    using A = Arith<TS>;
+    const TS g = (TS)gam[k];
+    double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n_long) {
+        TS s = TS(0);
+        for (int32_t j = lp[q]; j < lp[q + 1]; ++j) s = A::add(s, (TS)pc_sum[j]);
+        part_update<TS, TG>(first + q, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+    }
+    __shared__ double red[kPartThreads / 32][4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double m = __shfl_xor_sync(0xffffffffu, mx, o);
+        if (!(m <= mx)) mx = m;
+        fb += __shfl_xor_sync(0xffffffffu, fb, o);
+        ob = __dadd_rn(ob, __shfl_xor_sync(0xffffffffu, ob, o));
+        nf = fmax(nf, __shfl_xor_sync(0xffffffffu, nf, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5][0] = mx;
+        red[threadIdx.x >> 5][1] = fb;
+        red[threadIdx.x >> 5][2] = ob;
+        red[threadIdx.x >> 5][3] = nf;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < kPartThreads / 32; ++w) {
+            if (!(red[w][0] <= t[0])) t[0] = red[w][0];
+            t[1] += red[w][1];
+            t[2] = __dadd_rn(t[2], red[w][2]);
+            t[3] = fmax(t[3], red[w][3]);
+        }
+        double* dst = part + ((size_t)k * gridDim.x + blockIdx.x) * 4;
         dst[0] = t[0];
         dst[1] = t[1];
         dst[2] = t[2];
@@ -567,6 +662,29 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     parallel_for(n_own, [&](int64_t r) { std::sort(ncol.begin() + nrp[(size_t)r], ncol.begin() + nrp[(size_t)r + 1]); });
     if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
+    // the long rows' pieces (fast mode), per range
+    std::vector<int32_t> pb, pe, lp;
+    for (int r = 0; r < 2; ++r) {
+        P->pc0[r] = (int64_t)pb.size();
+        P->lp0[r] = (int64_t)lp.size();
+        for (int64_t q = 0; q < P->long_fast[r]; ++q) {
+            const int64_t row = rs[r] + q;
+            lp.push_back((int32_t)pb.size());
+            for (int64_t e = nrp[(size_t)row]; e < nrp[(size_t)row + 1]; e += kPiece) {
+                pb.push_back((int32_t)e);
+                pe.push_back((int32_t)std::min<int64_t>(e + kPiece, nrp[(size_t)row + 1]));
+            }
+        }
+        lp.push_back((int32_t)pb.size());
+        P->npc[r] = (int64_t)pb.size() - P->pc0[r];
+    }
+    cudaFree(P->pc_sum);
+    P->pc_sum = nullptr;
+    GN_CUDA(cudaMalloc((void**)&P->pc_sum, 8 * std::max<size_t>(pb.size(), 1)));
+    if ((rcode = upload_into(&P->pc_beg, pb)) || (rcode = upload_into(&P->pc_end, pe)) ||
+        (rcode = upload_into(&P->lp, lp)))
+        return rcode;
+    P->gen++;
     return GN_OK;
 }
 
@@ -582,11 +700,13 @@ static void part_free_push(gn_part* p) {
 }
 
 static void part_free_run(gn_part* p) {
-    void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part[0], p->part[1]};
+    void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part[0], p->part[1], p->part_long[0],
+                    p->part_long[1]};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
-    p->gam = p->part[0] = p->part[1] = nullptr;
+    p->gam = p->part[0] = p->part[1] = p->part_long[0] = p->part_long[1] = nullptr;
+    p->alloc_ncomb[0] = p->alloc_ncomb[1] = 0;
     p->alloc_nall = -1;
     p->alloc_dtype = -1;
     p->alloc_iters = 0;
@@ -600,6 +720,38 @@ static void part_free_graph(gn_part* p) {
     p->g_gen = 0;
 }
 
+// f(TS{}, TG{}) with the state / gathered types of the partition's dtype
+template <typename F>
+static void by_dtype(int dtype, F f) {
+    if (dtype == GN_F64) f(double(), double());
+    else if (dtype == GN_F32) f(double(), float());
+    else f(float(), float());
+}
+
+// one k_part_step launch over range r (the counts select which branches run)
+template <typename TS, typename TG>
+static void launch_step(gn_part* p, int r, int k, int nb, int64_t n_long, int nbl, int64_t ncsr, int ncb, int64_t nsl,
+                        PartPush push, PartLong lng, cudaStream_t s) {
+    const int cur = k & 1;
+    const bool fast = !(p->flags & GN_EXACT);
+    k_part_step<TS, TG><<<nb, kPartThreads, 0, s>>>(
+        n_long, nbl, ncsr, ncb, p->r_count[r], p->order + p->r_start[r], p->rowptr, fast ? p->col_fast : p->col,
+        fast ? p->sell_fast : p->sell, p->slice_ptr + p->sl0[r], nsl, p->w64, (const TS*)p->v, (const TS*)p->x[cur],
+        (TS*)p->x[cur ^ 1], (const TG*)p->yg[cur], (TG*)p->yg[cur ^ 1], p->gam, k, p->part[r], push, lng);
+}
+
+template <typename TS, typename TG>
+static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
+    const int cur = k & 1;
+    k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
+        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->pc_sum, p->w64, (const TS*)p->v, (const TS*)p->x[cur],
+        (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
+}
+
+static PartLong part_long_of(gn_part* p, int r) {
+    return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r], p->r_long[r] ? p->npc[r] : 0};
+}
+
 }  // namespace gn
 
 using namespace gn;
@@ -608,6 +760,7 @@ extern "C" {
 
 int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const int32_t* indices, const double* w,
                    int dtype, int device, gn_part** out) {
+    GN_NVTX("gn_part_create");
     *out = nullptr;
     if (n_own < 0 || n_ghost < 0) return fail(GN_ERR_ARG, "bad partition sizes");
     if (!valid_dtype(dtype)) return fail(GN_ERR_ARG, "dtype must be GN_F64, GN_F32 or GN_F32_PURE");
@@ -652,7 +805,13 @@ int gn_part_destroy(gn_part* p) {
     cudaSetDevice(p->device);
     part_free_graph(p);
     part_free_run(p);
+    cudaFree(p->io);
+    cudaFree(p->dout);
     cudaFree(p->d_epoch);
+    cudaFree(p->pc_beg);
+    cudaFree(p->pc_end);
+    cudaFree(p->lp);
+    cudaFree(p->pc_sum);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -674,6 +833,7 @@ int gn_part_destroy(gn_part* p) {
 }
 
 int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters, uint32_t flags) {
+    GN_NVTX("gn_part_begin");
     if (!p || iters < 1 || !gammas) return fail(GN_ERR_ARG, "bad gn_part_begin arguments");
     GN_CUDA(cudaSetDevice(p->device));
     const int64_t nall = p->n_own + p->n_ghost;
@@ -688,7 +848,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_start[r] = r ? p->n_bnd : 0;
         p->r_count[r] = r ? p->n_own - p->n_bnd : p->n_bnd;
         p->r_long[r] = (flags & GN_EXACT) ? 0 : p->long_fast[r];
-        p->r_nbl[r] = p->r_long[r] ? (int)std::min<int64_t>((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
+        p->r_nbl[r] = p->r_long[r] ? (int)std::min<int64_t>((p->npc[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
+        p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads - 1) / kPartThreads) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
         p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
         const int sblocks = (int)std::min<int64_t>((p->nsl[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 16);
@@ -698,7 +859,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     // buffers are mapped by the peers (CUDA IPC) and named by the captured
     // schedule
     if (p->alloc_nall != nall || p->alloc_dtype != p->dtype || p->alloc_iters != iters ||
-        p->alloc_nblocks[0] != p->r_nblocks[0] || p->alloc_nblocks[1] != p->r_nblocks[1]) {
+        p->alloc_nblocks[0] != p->r_nblocks[0] || p->alloc_nblocks[1] != p->r_nblocks[1] ||
+        p->alloc_ncomb[0] != p->r_ncomb[0] || p->alloc_ncomb[1] != p->r_ncomb[1]) {
         part_free_run(p);
         GN_CUDA(cudaMalloc(&p->x[0], es * nb));
         GN_CUDA(cudaMalloc(&p->x[1], es * nb));
@@ -709,11 +871,15 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
         for (int r = 0; r < 2; ++r)
             if (p->r_nblocks[r]) GN_CUDA(cudaMalloc((void**)&p->part[r], 32 * (size_t)iters * p->r_nblocks[r]));
+        for (int r = 0; r < 2; ++r)
+            if (p->r_ncomb[r]) GN_CUDA(cudaMalloc((void**)&p->part_long[r], 32 * (size_t)iters * p->r_ncomb[r]));
         p->alloc_nall = nall;
         p->alloc_dtype = p->dtype;
         p->alloc_iters = iters;
         p->alloc_nblocks[0] = p->r_nblocks[0];
         p->alloc_nblocks[1] = p->r_nblocks[1];
+        p->alloc_ncomb[0] = p->r_ncomb[0];
+        p->alloc_ncomb[1] = p->r_ncomb[1];
     }
     GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 1)));
     GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 1)));
@@ -722,8 +888,13 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     if (!p->d_epoch) GN_CUDA(cudaMalloc((void**)&p->d_epoch, sizeof(int64_t)));
     p->epoch++;
     GN_CUDA(cudaMemcpy(p->d_epoch, &p->epoch, sizeof(int64_t), cudaMemcpyHostToDevice));
-    double* dx0 = nullptr;
-    GN_CUDA(cudaMalloc((void**)&dx0, 8 * nb));
+    if (p->io_n < (int64_t)nb) {
+        cudaFree(p->io);
+        p->io = nullptr;
+        GN_CUDA(cudaMalloc((void**)&p->io, 8 * nb));
+        p->io_n = (int64_t)nb;
+    }
+    double* dx0 = p->io;
     if (nall) GN_CUDA(cudaMemcpy(dx0, x0, 8 * (size_t)nall, cudaMemcpyHostToDevice));
     if (nall > 0) {
         const int blocks = pblocks(nall);
@@ -748,47 +919,30 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     // of this one, and a peer may already have signalled this epoch)
     if (p->halo_bad) GN_CUDA(cudaMemset(p->halo_bad, 0, sizeof(int)));
     GN_CUDA(cudaDeviceSynchronize());
-    cudaFree(dx0);
     return GN_OK;
 }
 
 // one range of the owned rows (0: boundary, 1: interior) for iteration k
+// one range of the owned rows (0: boundary, 1: interior) for iteration k:
+// the step kernel, then (fast mode) the long rows' combine
 static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
     if (p->r_count[r] == 0 && !(r == 1 && p->n_push > 0)) return GN_OK;
-    const int cur = k & 1;
-    const int32_t* ord = p->order + p->r_start[r];
     PartPush push{nullptr, nullptr, nullptr, nullptr, 0, 0};
     // the boundary rows' pushes ride on the interior launch
     if (r == 1 && p->n_push > 0)
         push = PartPush{p->push_src, p->push_peer, p->push_slot, p->push_dst[(k + 1) & 1], p->n_push,
                         (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
     const int nb = (p->r_count[r] ? p->r_nblocks[r] : 0) + push.nblocks;
-    const bool fast = !(p->flags & GN_EXACT);
-    const int32_t* col = fast ? p->col_fast : p->col;
-    const int32_t* sell = fast ? p->sell_fast : p->sell;
-    switch (p->dtype) {
-        case GN_F64:
-            k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
-                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
-                (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const double*)p->yg[cur],
-                (double*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
-            break;
-        case GN_F32:
-            k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
-                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
-                (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1], (const float*)p->yg[cur],
-                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
-            break;
-        default:
-            k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r], p->r_count[r], ord, p->rowptr, col,
-                sell, p->slice_ptr + p->sl0[r], p->nsl[r], p->w64,
-                (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1], (const float*)p->yg[cur],
-                (float*)p->yg[cur ^ 1], p->gam, k, p->part[r], push);
-    }
+    const PartLong lng = part_long_of(p, r);
+    by_dtype(p->dtype, [&](auto ts, auto tg) {
+        launch_step<decltype(ts), decltype(tg)>(p, r, k, nb, p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r],
+                                                p->nsl[r], push, lng, s);
+    });
     GN_LAUNCHED();
+    if (p->r_long[r] > 0 && p->r_count[r] > 0) {
+        by_dtype(p->dtype, [&](auto ts, auto tg) { launch_combine<decltype(ts), decltype(tg)>(p, r, k, s); });
+        GN_LAUNCHED();
+    }
     return GN_OK;
 }
 
@@ -843,18 +997,35 @@ int gn_part_unpack(gn_part* p, int k, const void* d_in, int64_t ghost_first, int
 
 // stats of the owned rows after `done` iterations, x clipped
 int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* fallbacks, double* mass, int* bad) {
+    GN_NVTX("gn_part_end");
     if (!p || done < 0 || done > p->iters) return fail(GN_ERR_ARG, "bad gn_part_end arguments");
     GN_CUDA(cudaSetDevice(p->device));
     GN_CUDA(cudaDeviceSynchronize());
-    double *dout = nullptr, *dx = nullptr;
-    GN_CUDA(cudaMalloc((void**)&dout, 64 * (size_t)std::max(done, 1)));  // per range
-    GN_CUDA(cudaMalloc((void**)&dx, 8 * (size_t)std::max<int64_t>(p->n_own, 1)));
-    GN_CUDA(cudaMemset(dout, 0, 64 * (size_t)std::max(done, 1)));
-    for (int r = 0; r < 2 && done > 0; ++r)
+    if (p->dout_n < std::max(done, 1)) {  // per (range, kernel), per iteration: 4 doubles
+        cudaFree(p->dout);
+        p->dout = nullptr;
+        GN_CUDA(cudaMalloc((void**)&p->dout, 128 * (size_t)std::max(done, 1)));
+        p->dout_n = std::max(done, 1);
+    }
+    if (p->io_n < std::max<int64_t>(p->n_own, 1)) {
+        cudaFree(p->io);
+        p->io = nullptr;
+        GN_CUDA(cudaMalloc((void**)&p->io, 8 * (size_t)std::max<int64_t>(p->n_own, 1)));
+        p->io_n = std::max<int64_t>(p->n_own, 1);
+    }
+    double *dout = p->dout, *dx = p->io;
+    GN_CUDA(cudaMemset(dout, 0, 128 * (size_t)std::max(done, 1)));
+    for (int r = 0; r < 2 && done > 0; ++r) {
         if (p->r_nblocks[r]) {
             k_part_fold<<<(done + 7) / 8, 256>>>(p->part[r], p->r_nblocks[r], done, dout + (size_t)r * 4 * done);
             GN_LAUNCHED();
         }
+        if (p->r_long[r] && p->r_ncomb[r]) {  // the long rows' combine blocks of the range
+            k_part_fold<<<(done + 7) / 8, 256>>>(p->part_long[r], p->r_ncomb[r], done,
+                                                 dout + (size_t)(2 + r) * 4 * done);
+            GN_LAUNCHED();
+        }
+    }
     if (p->n_own > 0) {
         if (state_bytes(p->dtype) == 8)
             k_part_out<double, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const double*)p->x[done & 1], p->perm, dx);
@@ -862,21 +1033,23 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
             k_part_out<float, double><<<pblocks(p->n_own), kPartThreads>>>(p->n_own, (const float*)p->x[done & 1], p->perm, dx);
         GN_LAUNCHED();
     }
-    std::vector<double> h2(8 * (size_t)std::max(done, 1));
-    GN_CUDA(cudaMemcpy(h2.data(), dout, 64 * (size_t)std::max(done, 1), cudaMemcpyDeviceToHost));
-    // boundary range, then interior range: max / sum / fp64 sum / max, fixed order
+    std::vector<double> h2(16 * (size_t)std::max(done, 1));
+    GN_CUDA(cudaMemcpy(h2.data(), dout, 128 * (size_t)std::max(done, 1), cudaMemcpyDeviceToHost));
+    // boundary range (step blocks, long-row combine), then the interior range
+    // likewise: max / sum / fp64 sum / max, in this fixed order
     std::vector<double> h(4 * (size_t)std::max(done, 1));
     for (int k = 0; k < done; ++k) {
-        const double* a0 = &h2[(size_t)k * 4];
-        const double* a1 = &h2[(size_t)(done + k) * 4];
-        h[(size_t)k * 4] = a1[0] > a0[0] || a1[0] != a1[0] ? a1[0] : a0[0];
-        h[(size_t)k * 4 + 1] = a0[1] + a1[1];
-        h[(size_t)k * 4 + 2] = a0[2] + a1[2];
-        h[(size_t)k * 4 + 3] = std::max(a0[3], a1[3]);
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int sec : {0, 2, 1, 3}) {
+            const double* a = &h2[((size_t)sec * done + k) * 4];
+            if (a[0] > t[0] || a[0] != a[0]) t[0] = a[0];
+            t[1] += a[1];
+            t[2] += a[2];
+            t[3] = std::max(t[3], a[3]);
+        }
+        for (int c = 0; c < 4; ++c) h[(size_t)k * 4 + c] = t[c];
     }
     if (x_out && p->n_own) GN_CUDA(cudaMemcpy(x_out, dx, 8 * (size_t)p->n_own, cudaMemcpyDeviceToHost));
-    cudaFree(dout);
-    cudaFree(dx);
     if (p->halo_bad) {
         int hb = 0;
         GN_CUDA(cudaMemcpy(&hb, p->halo_bad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1022,6 +1195,7 @@ int gn_part_peer_signal(gn_part* p, int k, uintptr_t stream) {
 // the same length and mode; it is rebuilt when the buffers or the push list
 // change.
 int gn_part_run(gn_part* p, int k0, int k1, uintptr_t stream) {
+    GN_NVTX("gn_part_run");
     if (!p || k0 < 0 || k1 > p->iters || k0 >= k1 || !p->gam) return fail(GN_ERR_ARG, "bad gn_part_run arguments");
     GN_CUDA(cudaSetDevice(p->device));
     const bool peer = p->peer_flags != nullptr || p->nexpect > 0;
@@ -1070,6 +1244,7 @@ int gn_part_run(gn_part* p, int k0, int k1, uintptr_t stream) {
 // of the multi-GPU run with the parts serialised; built, launched once and
 // released (tests and single-GPU measurements).
 int gn_part_run_group(gn_part* const* parts, int nparts, int k0, int k1, uintptr_t stream) {
+    GN_NVTX("gn_part_run_group");
     if (!parts || nparts < 1) return fail(GN_ERR_ARG, "bad gn_part_run_group arguments");
     for (int i = 0; i < nparts; ++i)
         if (!parts[i] || k0 < 0 || k1 > parts[i]->iters || k0 >= k1 || !parts[i]->gam ||
@@ -1141,16 +1316,17 @@ int gn_ipc_close(void* dptr) {
 //   mode 1  k_part_step, only the warp-split long rows
 //   mode 2  k_part_step, only the SELL slices (thread per row)
 //   mode 3..6  the probe walk of the slices (k_part_probe MODE 1..4)
+//   mode 7  the direct halo's push blocks alone (no rows; after
+//           gn_part_peer_commit): the coalesced stores into the peers' slots
 int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
-    if (!p || !p->gam || mode < 0 || mode > 6 || reps < 1 || !ms) return fail(GN_ERR_ARG, "bad gn_part_probe arguments");
+    if (!p || !p->gam || mode < 0 || mode > 7 || reps < 1 || !ms) return fail(GN_ERR_ARG, "bad gn_part_probe arguments");
+    if (mode == 7 && p->n_push == 0) { *ms = 0.0; return GN_OK; }
     GN_CUDA(cudaSetDevice(p->device));
     const int r = p->r_count[1] ? 1 : 0;
     if (!p->r_count[r]) { *ms = 0.0; return GN_OK; }
     cudaStream_t s = p->own_stream;
     const bool fast = !(p->flags & GN_EXACT);
-    const int32_t* col = fast ? p->col_fast : p->col;
     const int32_t* sell = fast ? p->sell_fast : p->sell;
-    const int32_t* ord = p->order + p->r_start[r];
     const int64_t pos0 = p->r_long[r] + p->r_csr[r];
     const int nsb = p->r_nblocks[r] - p->r_nbl[r] - p->r_ncb[r];
     double* out = nullptr;
@@ -1160,31 +1336,26 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
     cudaEventCreate(&e1);
     PartPush none{nullptr, nullptr, nullptr, nullptr, 0, 0};
     auto launch = [&]() {
-        const int cur = 0;
-        if (mode <= 2) {
-            const int64_t nl = p->r_long[r];
+        if (mode == 7) {
+            PartPush push{p->push_src, p->push_peer, p->push_slot, p->push_dst[1], p->n_push,
+                          (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
+            const PartLong no_long{nullptr, nullptr, nullptr, 0};
+            by_dtype(p->dtype, [&](auto ts, auto tg) {
+                launch_step<decltype(ts), decltype(tg)>(p, r, 0, push.nblocks, 0, 0, 0, 0, 0, push, no_long, s);
+            });
+        } else if (mode <= 2) {
             const int nbl = mode == 2 ? 0 : p->r_nbl[r];
             const int64_t ncsr = mode == 0 ? p->r_csr[r] : 0;
             const int ncb = mode == 0 ? p->r_ncb[r] : 0;
             const int64_t nsl = mode == 1 ? 0 : p->nsl[r];
             const int nb = mode == 1 ? std::max(nbl, 1) : mode == 2 ? std::max(nsb, 1) : p->r_nblocks[r];
             // mode 2 keeps the slices' order positions (pos0 = n_long + n_csr)
-            const int64_t nlong_arg = mode == 2 ? pos0 : nl;
-            if (p->dtype == GN_F32)
-                k_part_step<double, float><<<nb, kPartThreads, 0, s>>>(
-                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
-                    p->w64, (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1],
-                    (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
-            else if (p->dtype == GN_F64)
-                k_part_step<double, double><<<nb, kPartThreads, 0, s>>>(
-                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
-                    p->w64, (const double*)p->v, (const double*)p->x[cur], (double*)p->x[cur ^ 1],
-                    (const double*)p->yg[cur], (double*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
-            else
-                k_part_step<float, float><<<nb, kPartThreads, 0, s>>>(
-                    nlong_arg, nbl, ncsr, ncb, p->r_count[r], ord, p->rowptr, col, sell, p->slice_ptr + p->sl0[r], nsl,
-                    p->w64, (const float*)p->v, (const float*)p->x[cur], (float*)p->x[cur ^ 1],
-                    (const float*)p->yg[cur], (float*)p->yg[cur ^ 1], p->gam, 0, p->part[r], none);
+            const int64_t nlong_arg = mode == 2 ? pos0 : p->r_long[r];
+            const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0} : part_long_of(p, r);
+            by_dtype(p->dtype, [&](auto ts, auto tg) {
+                launch_step<decltype(ts), decltype(tg)>(p, r, 0, nb, nlong_arg, nbl, ncsr, ncb, nsl, none, lng, s);
+                if (mode != 2 && p->r_long[r] > 0) launch_combine<decltype(ts), decltype(tg)>(p, r, 0, s);
+            });
         } else {
             const int nb = std::max(nsb, 1);
             const uint32_t nall = (uint32_t)(p->n_own + p->n_ghost);

@@ -473,6 +473,7 @@ extern "C" {
 
 int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected, double* weight, int* independent,
              int* maximal, int64_t* count) {
+    GN_NVTX("gn_round");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (g->n > 0 && !x) return fail(GN_ERR_ARG, "null state");
     return round_batch(g, 1, (const double*)x, (flags & GN_DEVICE_IO) != 0, selected, weight, independent, maximal,
@@ -481,6 +482,7 @@ int gn_round(gn_graph* g, const void* x, uint32_t flags, uint8_t* selected, doub
 
 int gn_round_members(gn_graph* g, const void* x, uint32_t flags, int64_t* members, double* weight, int* independent,
                      int* maximal, int64_t* count) {
+    GN_NVTX("gn_round_members");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (g->n > 0 && (!x || !members)) return fail(GN_ERR_ARG, "null state or member buffer");
     return round_batch(g, 1, (const double*)x, (flags & GN_DEVICE_IO) != 0, nullptr, weight, independent, maximal,
@@ -489,6 +491,7 @@ int gn_round_members(gn_graph* g, const void* x, uint32_t flags, int64_t* member
 
 int gn_round_many(gn_graph* g, int num_states, const void* x, uint32_t flags, uint8_t* selected, double* weight,
                   int* independent, int* maximal, int64_t* count) {
+    GN_NVTX("gn_round_many");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     if (num_states < 1 || !weight || !independent || !maximal) return fail(GN_ERR_ARG, "bad gn_round_many arguments");
     if (g->n > 0 && !x) return fail(GN_ERR_ARG, "null state");
@@ -498,6 +501,7 @@ int gn_round_many(gn_graph* g, int num_states, const void* x, uint32_t flags, ui
 
 int gn_check_members(gn_graph* g, const uint8_t* mask, double* weight, int* independent, int* maximal,
                      int64_t* count) {
+    GN_NVTX("gn_check_members");
     if (!g) return fail(GN_ERR_ARG, "null graph");
     CallCtx ctx;
     int rc = ctx.open(g->device);

@@ -500,16 +500,25 @@ def run_partition(backend, exchange, x0_local: np.ndarray, schedule: GammaSchedu
     the ranks, reset the run, then every iteration -- from the device-side
     schedule (one CUDA-graph launch) when the exchange allows it, else one
     host-driven step per iteration (dynamics.py:155-178)."""
+    import time
+
     gam = gamma_table(schedule)
+    t = [time.perf_counter()]
     exchange.fence()
+    t.append(time.perf_counter())
     backend.begin(x0_local, gam)
+    t.append(time.perf_counter())
     exchange.setup()
+    t.append(time.perf_counter())
     if device_schedule and exchange.device_schedule and hasattr(backend, "run"):
         backend.run(0, len(gam))
     else:
         for k in range(len(gam)):
             partitioned_step(backend, exchange, k)
+    t.append(time.perf_counter())
     x, si, fb, ms, bad = backend.end(len(gam))
+    t.append(time.perf_counter())
+    backend.last_times = dict(zip(("fence", "begin", "setup", "launch", "end (sync + out)"), np.diff(t)))
     return PartResult(x, si, fb, ms, bad)
 
 
