@@ -71,6 +71,19 @@ struct gn_part {
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
     int r_ncomb[2] = {0, 0};                 // per range: combine blocks
+    // band mode (fast, default): the pieces are the runs of a long row's
+    // sorted neighbour list inside one column band of kBandBytes of gathered
+    // values.  A unit is a set of pieces of one band (about kBandUnit
+    // entries); its CTA stages the band's published values in shared memory
+    // and sums every piece from there (ids stored as 16-bit offsets in the
+    // band), writing each piece's sum to pc_sum[row-major piece id]
+    int band = 1;                            // 0: pieces of kPiece entries (GN_PART_BAND=0)
+    int band_w = 0;                          // vertices per band
+    uint16_t* bstream = nullptr;             // band offsets, unit order
+    int32_t* bpoff = nullptr;                // [pieces+1] offsets into bstream, unit order
+    int32_t* bpdst = nullptr;                // [pieces] row-major piece id
+    int4* units = nullptr;                   // {band, first piece, end piece, warp pieces | direct << 30}
+    int64_t u0[2] = {0, 0}, nu[2] = {0, 0};
     double* part_long[2] = {nullptr, nullptr};  // per range [iters][r_ncomb][4]
     // per range (0 boundary, 1 interior), set by gn_part_begin
     int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0}, r_csr[2] = {0, 0};
@@ -352,6 +365,67 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
         dst[1] = t[1];
         dst[2] = t[2];
         dst[3] = t[3];
+    }
+}
+
+// Long rows, band mode: one CTA per unit (pieces of one column band).  The
+// band's published values are staged in shared memory (coalesced 16-byte
+// loads) unless the unit is sparse ("direct": read them where they are);
+// pieces of >= 32 entries get a warp each (lanes stride, fixed butterfly),
+// the others a thread each (sequential).  Sums go to pc_sum[row-major id].
+constexpr int kBandBytes = 65536;  // shared memory per unit: 8192 fp64 / 16384 fp32 values
+template <typename TS, typename TG>
+__global__ void __launch_bounds__(kPartThreads, 3) k_part_band(const int4* __restrict__ units,
+                                                               const uint16_t* __restrict__ bs,
+                                                               const int32_t* __restrict__ poff,
+                                                               const int32_t* __restrict__ pdst,
+                                                               const TG* __restrict__ yg, int64_t nall, int W,
+                                                               double* __restrict__ psum) {
+    using A = Arith<TS>;
+    extern __shared__ __align__(16) unsigned char band_smem[];
+    TG* sy = reinterpret_cast<TG*>(band_smem);
+    const int4 u = units[blockIdx.x];
+    const int64_t base = (int64_t)u.x * W;
+    const bool direct = (u.w >> 30) & 1;
+    const int nwp = u.w & ((1 << 30) - 1);
+    const TG* src;
+    if (!direct) {
+        const int cnt = (int)(nall - base < (int64_t)W ? nall - base : (int64_t)W);
+        constexpr int V = 16 / sizeof(TG);
+        const int nv = cnt / V;
+        const uint4* g4 = reinterpret_cast<const uint4*>(yg + base);
+        uint4* s4 = reinterpret_cast<uint4*>(sy);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) s4[i] = __ldg(g4 + i);
+        for (int i = nv * V + threadIdx.x; i < cnt; i += blockDim.x) sy[i] = yg[base + i];
+        __syncthreads();
+        src = sy;
+    } else {
+        src = yg + base;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q0 = u.y, q1 = u.z;
+    for (int q = q0 + warp; q < q0 + nwp; q += kPartThreads / 32) {
+        const int32_t b = __ldg(poff + q), e = __ldg(poff + q + 1);
+        TS s = TS(0);
+        int32_t p = b + lane;
+        for (; p + 96 < e; p += 128) {
+            const TG y0 = src[__ldg(bs + p)], y1 = src[__ldg(bs + p + 32)], y2 = src[__ldg(bs + p + 64)],
+                     y3 = src[__ldg(bs + p + 96)];
+            s = A::add(s, (TS)y0);
+            s = A::add(s, (TS)y1);
+            s = A::add(s, (TS)y2);
+            s = A::add(s, (TS)y3);
+        }
+        for (; p < e; p += 32) s = A::add(s, (TS)src[__ldg(bs + p)]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
+        if (lane == 0) psum[__ldg(pdst + q)] = (double)s;
+    }
+    for (int q = q0 + nwp + threadIdx.x; q < q1; q += kPartThreads) {
+        const int32_t b = __ldg(poff + q), e = __ldg(poff + q + 1);
+        TS s = TS(0);
+        for (int32_t p = b; p < e; ++p) s = A::add(s, (TS)src[__ldg(bs + p)]);
+        psum[__ldg(pdst + q)] = (double)s;
     }
 }
 
@@ -662,17 +736,38 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     parallel_for(n_own, [&](int64_t r) { std::sort(ncol.begin() + nrp[(size_t)r], ncol.begin() + nrp[(size_t)r + 1]); });
     if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
-    // the long rows' pieces (fast mode), per range
-    std::vector<int32_t> pb, pe, lp;
+    // the long rows' pieces (fast mode), per range: runs inside one column
+    // band (band mode), or kPiece consecutive entries (GN_PART_BAND=0)
+    P->band = 1;
+    if (const char* e = getenv("GN_PART_BAND")) P->band = atoi(e) != 0;
+    const int W = kBandBytes / (int)gather_bytes(P->dtype);
+    P->band_w = W;
+    int64_t unit_entries = 32768;  // entries per unit (about; a unit holds whole pieces)
+    if (const char* e = getenv("GN_BAND_UNIT")) unit_entries = std::max(256, atoi(e));
+    int64_t direct_below = W / 8;  // units with fewer entries read the values in place
+    if (const char* e = getenv("GN_BAND_DIRECT")) direct_below = atoi(e);
+    std::vector<int32_t> pb, pe, lp, pband;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
         P->lp0[r] = (int64_t)lp.size();
         for (int64_t q = 0; q < P->long_fast[r]; ++q) {
             const int64_t row = rs[r] + q;
             lp.push_back((int32_t)pb.size());
-            for (int64_t e = nrp[(size_t)row]; e < nrp[(size_t)row + 1]; e += kPiece) {
+            int64_t e = nrp[(size_t)row];
+            const int64_t end = nrp[(size_t)row + 1];
+            while (e < end) {
+                int64_t f;
+                if (P->band) {  // the run of this row's (ascending) neighbours in one band
+                    const int32_t bnd = ncol[(size_t)e] / W;
+                    f = e + 1;
+                    while (f < end && ncol[(size_t)f] / W == bnd) ++f;
+                    pband.push_back(bnd);
+                } else {
+                    f = std::min<int64_t>(e + kPiece, end);
+                }
                 pb.push_back((int32_t)e);
-                pe.push_back((int32_t)std::min<int64_t>(e + kPiece, nrp[(size_t)row + 1]));
+                pe.push_back((int32_t)f);
+                e = f;
             }
         }
         lp.push_back((int32_t)pb.size());
@@ -684,6 +779,61 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     if ((rcode = upload_into(&P->pc_beg, pb)) || (rcode = upload_into(&P->pc_end, pe)) ||
         (rcode = upload_into(&P->lp, lp)))
         return rcode;
+    if (P->band) {
+        // per range: pieces grouped by band (counting sort, stable), longest
+        // first inside a band; units of about unit_entries entries
+        const int nbands = (int)(nall / W + 1);
+        std::vector<int32_t> order_pc;  // processing order -> row-major piece id
+        std::vector<int4> units;
+        order_pc.reserve(pb.size());
+        for (int r = 0; r < 2; ++r) {
+            P->u0[r] = (int64_t)units.size();
+            const int64_t a = P->pc0[r], b = a + P->npc[r];
+            std::vector<int64_t> cnt((size_t)nbands + 1, 0);
+            for (int64_t j = a; j < b; ++j) cnt[(size_t)pband[(size_t)j] + 1]++;
+            for (int t = 0; t < nbands; ++t) cnt[(size_t)t + 1] += cnt[(size_t)t];
+            std::vector<int32_t> by((size_t)(b - a));
+            {
+                std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+                for (int64_t j = a; j < b; ++j) by[(size_t)fill[(size_t)pband[(size_t)j]]++] = (int32_t)j;
+            }
+            for (int t = 0; t < nbands; ++t) {
+                auto lo = by.begin() + cnt[(size_t)t], hi = by.begin() + cnt[(size_t)t + 1];
+                if (lo == hi) continue;
+                std::stable_sort(lo, hi, [&](int32_t x, int32_t y) { return pe[(size_t)x] - pb[(size_t)x] > pe[(size_t)y] - pb[(size_t)y]; });
+                for (auto it = lo; it != hi;) {
+                    const int32_t first = (int32_t)order_pc.size();
+                    int64_t ent = 0;
+                    int nwp = 0;
+                    while (it != hi && (ent == 0 || ent + (pe[(size_t)*it] - pb[(size_t)*it]) <= unit_entries)) {
+                        const int32_t len = pe[(size_t)*it] - pb[(size_t)*it];
+                        if (len >= 32) ++nwp;  // longest first: the warp pieces lead the unit
+                        ent += len;
+                        order_pc.push_back(*it);
+                        ++it;
+                    }
+                    const int direct = ent < direct_below ? 1 : 0;
+                    units.push_back(make_int4(t, first, (int32_t)order_pc.size(), nwp | (direct << 30)));
+                }
+            }
+            P->nu[r] = (int64_t)units.size() - P->u0[r];
+        }
+        // the entries, as offsets inside their band, in processing order
+        std::vector<int32_t> poff(order_pc.size() + 1, 0);
+        for (size_t j = 0; j < order_pc.size(); ++j)
+            poff[j + 1] = poff[j] + (pe[(size_t)order_pc[j]] - pb[(size_t)order_pc[j]]);
+        std::vector<uint16_t> bs((size_t)std::max<int32_t>(poff.back(), 1));
+        parallel_for((int64_t)order_pc.size(), [&](int64_t j) {
+            const int32_t pcid = order_pc[(size_t)j];
+            const int32_t bnd = pband[(size_t)pcid];
+            uint16_t* dst = bs.data() + poff[(size_t)j];
+            for (int32_t e = pb[(size_t)pcid]; e < pe[(size_t)pcid]; ++e)
+                *dst++ = (uint16_t)(ncol[(size_t)e] - bnd * W);
+        });
+        if ((rcode = upload_into(&P->bstream, bs)) || (rcode = upload_into(&P->bpoff, poff)) ||
+            (rcode = upload_into(&P->bpdst, order_pc)) || (rcode = upload_into(&P->units, units)))
+            return rcode;
+    }
     P->gen++;
     return GN_OK;
 }
@@ -749,7 +899,17 @@ static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
 }
 
 static PartLong part_long_of(gn_part* p, int r) {
-    return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r], p->r_long[r] ? p->npc[r] : 0};
+    return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r],
+                    p->r_long[r] && !p->band ? p->npc[r] : 0};
+}
+
+template <typename TS, typename TG>
+static void launch_band(gn_part* p, int r, int k, cudaStream_t s) {
+    const int cur = k & 1;
+    const int64_t u0 = p->u0[r];
+    k_part_band<TS, TG><<<(int)p->nu[r], kPartThreads, kBandBytes, s>>>(
+        p->units + u0, p->bstream, p->bpoff, p->bpdst, (const TG*)p->yg[cur], p->n_own + p->n_ghost, p->band_w,
+        p->pc_sum);
 }
 
 }  // namespace gn
@@ -794,6 +954,9 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
         return rc;
     }
     GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
     *out = P;
     return GN_OK;
 }
@@ -812,6 +975,10 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_end);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
+    cudaFree(p->bstream);
+    cudaFree(p->bpoff);
+    cudaFree(p->bpdst);
+    cudaFree(p->units);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -848,7 +1015,10 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_start[r] = r ? p->n_bnd : 0;
         p->r_count[r] = r ? p->n_own - p->n_bnd : p->n_bnd;
         p->r_long[r] = (flags & GN_EXACT) ? 0 : p->long_fast[r];
-        p->r_nbl[r] = p->r_long[r] ? (int)std::min<int64_t>((p->npc[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12) : 0;
+        // band mode: the long rows' pieces run in k_part_band, not in k_part_step
+        p->r_nbl[r] = p->r_long[r] && !p->band
+                          ? (int)std::min<int64_t>((p->npc[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12)
+                          : 0;
         p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads - 1) / kPartThreads) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
         p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
@@ -934,6 +1104,10 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
                         (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
     const int nb = (p->r_count[r] ? p->r_nblocks[r] : 0) + push.nblocks;
     const PartLong lng = part_long_of(p, r);
+    if (p->band && p->r_long[r] > 0 && p->nu[r] > 0) {  // the long rows' band pieces
+        by_dtype(p->dtype, [&](auto ts, auto tg) { launch_band<decltype(ts), decltype(tg)>(p, r, k, s); });
+        GN_LAUNCHED();
+    }
     by_dtype(p->dtype, [&](auto ts, auto tg) {
         launch_step<decltype(ts), decltype(tg)>(p, r, k, nb, p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r],
                                                 p->nsl[r], push, lng, s);
@@ -1353,7 +1527,10 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
             const int64_t nlong_arg = mode == 2 ? pos0 : p->r_long[r];
             const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0} : part_long_of(p, r);
             by_dtype(p->dtype, [&](auto ts, auto tg) {
-                launch_step<decltype(ts), decltype(tg)>(p, r, 0, nb, nlong_arg, nbl, ncsr, ncb, nsl, none, lng, s);
+                if (mode != 2 && p->band && p->r_long[r] > 0 && p->nu[r] > 0)
+                    launch_band<decltype(ts), decltype(tg)>(p, r, 0, s);
+                if (mode != 1 || nbl > 0)
+                    launch_step<decltype(ts), decltype(tg)>(p, r, 0, nb, nlong_arg, nbl, ncsr, ncb, nsl, none, lng, s);
                 if (mode != 2 && p->r_long[r] > 0) launch_combine<decltype(ts), decltype(tg)>(p, r, 0, s);
             });
         } else {

@@ -48,6 +48,7 @@ def main():
     tab = P.GammaSchedule.pursuit(iterations=args.iters).table()
     be.begin(spec.local_x0(inst.x0), tab)
     out = {"lib": os.environ.get("GN_LIB", "libgnb200.so"), "scale": args.scale, "dtype": args.dtype,
+           "env": {k: v for k, v in os.environ.items() if k.startswith("GN_")},
            "n": g.n, "nnz": int(len(g.indices))}
     deg = np.diff(np.asarray(g.indptr))
     out["nnz_long_rows"] = int(deg[deg > 512].sum())
