@@ -71,18 +71,33 @@ struct gn_part {
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
     int r_ncomb[2] = {0, 0};                 // per range: combine blocks
-    // band mode (fast, default): the pieces are the runs of a long row's
-    // sorted neighbour list inside one column band of kBandBytes of gathered
-    // values.  A unit is a set of pieces of one band (about kBandUnit
-    // entries); its CTA stages the band's published values in shared memory
-    // and sums every piece from there (ids stored as 16-bit offsets in the
-    // band), writing each piece's sum to pc_sum[row-major piece id]
+    // band mode (fast, default): a piece is the run of a long row's sorted
+    // neighbour list inside one column band (kBandBytes of published values,
+    // at most kUnitMax entries).  Per range the pieces are grouped by band,
+    // longest first, and cut into units of at most kUnitMax index entries:
+    // a unit's index stream holds its warp pieces (>= 32 entries, one after
+    // the other) and then its short pieces in groups of 32, position-major
+    // (lane l's k-th entry at 32 k + l), 16-bit offsets inside the band.
+    // k_part_band runs persistent CTAs over contiguous unit ranges: the band
+    // is staged in shared memory by a TMA bulk copy when it changes, the next
+    // unit's index stream is prefetched by TMA while the current one is
+    // summed; each piece's sum goes to psum in stream order, and
+    // k_part_long_combine (a warp per row) adds a row's pieces in band order
+    // through lpidx.
     int band = 1;                            // 0: pieces of kPiece entries (GN_PART_BAND=0)
     int band_w = 0;                          // vertices per band
-    uint16_t* bstream = nullptr;             // band offsets, unit order
-    int32_t* bpoff = nullptr;                // [pieces+1] offsets into bstream, unit order
-    int32_t* bpdst = nullptr;                // [pieces] row-major piece id
-    int4* units = nullptr;                   // {band, first piece, end piece, warp pieces | direct << 30}
+    int band_ctas = 0;                       // persistent CTAs per range launch
+    uint16_t* bstream = nullptr;             // all units' index streams
+    int4* unit_a = nullptr;                  // {band, first warp piece, warp pieces, first group}
+    int4* unit_b = nullptr;                  // {groups, stream offset, stream entries, 0}
+    int32_t* wp_off = nullptr;               // warp piece: offset in its unit's stream
+    int32_t* wp_len = nullptr;
+    int32_t* g_off = nullptr;                // group: offset in its unit's stream
+    int32_t* g_lmax = nullptr;               // group: longest piece (= its rows in the stream)
+    int32_t* g_len = nullptr;                // [groups * 32] piece lengths (0: empty slot)
+    int32_t* lpidx = nullptr;                // row-major piece -> psum slot
+    int32_t* cta_u = nullptr;                // [ranges][band_ctas + 1] unit ranges
+    int64_t nwp_all = 0;                     // warp pieces (psum slots [0, nwp_all)), then 32 per group
     int64_t u0[2] = {0, 0}, nu[2] = {0, 0};
     double* part_long[2] = {nullptr, nullptr};  // per range [iters][r_ncomb][4]
     // per range (0 boundary, 1 interior), set by gn_part_begin
@@ -368,82 +383,156 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
     }
 }
 
-// Long rows, band mode: one CTA per unit (pieces of one column band).  The
-// band's published values are staged in shared memory (coalesced 16-byte
-// loads) unless the unit is sparse ("direct": read them where they are);
-// pieces of >= 32 entries get a warp each (lanes stride, fixed butterfly),
-// the others a thread each (sequential).  Sums go to pc_sum[row-major id].
-constexpr int kBandBytes = 65536;  // shared memory per unit: 8192 fp64 / 16384 fp32 values
+// ---- band mode (see gn_part::band): TMA bulk copies with mbarriers
+constexpr int kBandBytes = 65536;  // one band of published values: 8192 fp64 / 16384 fp32
+constexpr int kUnitMax = 8192;     // index entries per unit (16 KB of 16-bit offsets)
+constexpr int kBandThreads = 512;  // 2 CTAs per SM: 96 KB of shared memory each
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// one thread: expect `bytes`, then the bulk copy global -> shared completes them
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+struct BandArgs {
+    const int4* unit_a;
+    const int4* unit_b;
+    const int32_t* cta_u;  // this range's [band_ctas + 1]
+    const uint16_t* bs;
+    const int32_t* wp_off;
+    const int32_t* wp_len;
+    const int32_t* g_off;
+    const int32_t* g_lmax;
+    const int32_t* g_len;
+    int64_t nall;
+    int W;
+    int64_t nwp_all;
+    double* psum;
+};
+
 template <typename TS, typename TG>
-__global__ void __launch_bounds__(kPartThreads, 3) k_part_band(const int4* __restrict__ units,
-                                                               const uint16_t* __restrict__ bs,
-                                                               const int32_t* __restrict__ poff,
-                                                               const int32_t* __restrict__ pdst,
-                                                               const TG* __restrict__ yg, int64_t nall, int W,
-                                                               double* __restrict__ psum) {
+__global__ void __launch_bounds__(kBandThreads, 2) k_part_band(BandArgs a, const TG* __restrict__ yg) {
     using A = Arith<TS>;
-    extern __shared__ __align__(16) unsigned char band_smem[];
-    TG* sy = reinterpret_cast<TG*>(band_smem);
-    const int4 u = units[blockIdx.x];
-    const int64_t base = (int64_t)u.x * W;
-    const bool direct = (u.w >> 30) & 1;
-    const int nwp = u.w & ((1 << 30) - 1);
-    const TG* src;
-    if (!direct) {
-        const int cnt = (int)(nall - base < (int64_t)W ? nall - base : (int64_t)W);
-        constexpr int V = 16 / sizeof(TG);
-        const int nv = cnt / V;
-        const uint4* g4 = reinterpret_cast<const uint4*>(yg + base);
-        uint4* s4 = reinterpret_cast<uint4*>(sy);
-        for (int i = threadIdx.x; i < nv; i += blockDim.x) s4[i] = __ldg(g4 + i);
-        for (int i = nv * V + threadIdx.x; i < cnt; i += blockDim.x) sy[i] = yg[base + i];
-        __syncthreads();
-        src = sy;
-    } else {
-        src = yg + base;
+    extern __shared__ __align__(128) unsigned char band_smem[];
+    TG* sy = reinterpret_cast<TG*>(band_smem);                                  // kBandBytes
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(band_smem + kBandBytes);       // 2 x kUnitMax
+    uint64_t* bars = reinterpret_cast<uint64_t*>(band_smem + kBandBytes + 4 * kUnitMax);  // band, idx0, idx1
+    const int j0 = __ldg(a.cta_u + blockIdx.x), j1 = __ldg(a.cta_u + blockIdx.x + 1);
+    if (j0 >= j1) return;
+    if (threadIdx.x == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        mbar_init(bars + 2, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
+    auto issue_idx = [&](int j, int buf) {
+        const int4 ub = __ldg(a.unit_b + j);
+        tma_load_1d(sidx + buf * kUnitMax, a.bs + ub.y, (uint32_t)ub.z * 2u, bars + 1 + buf);
+    };
+    if (threadIdx.x == 0) issue_idx(j0, 0);
+    uint32_t ph_band = 0, ph_idx = 0;  // bit b: the phase of index buffer b
+    int cur_band = -1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q0 = u.y, q1 = u.z;
-    for (int q = q0 + warp; q < q0 + nwp; q += kPartThreads / 32) {
-        const int32_t b = __ldg(poff + q), e = __ldg(poff + q + 1);
-        TS s = TS(0);
-        int32_t p = b + lane;
-        for (; p + 96 < e; p += 128) {
-            const TG y0 = src[__ldg(bs + p)], y1 = src[__ldg(bs + p + 32)], y2 = src[__ldg(bs + p + 64)],
-                     y3 = src[__ldg(bs + p + 96)];
-            s = A::add(s, (TS)y0);
-            s = A::add(s, (TS)y1);
-            s = A::add(s, (TS)y2);
-            s = A::add(s, (TS)y3);
+    constexpr int kWarps = kBandThreads / 32;
+    for (int j = j0; j < j1; ++j) {
+        const int buf = (j - j0) & 1;
+        const int4 ua = __ldg(a.unit_a + j);
+        if (ua.x != cur_band) {  // stage the band (everyone finished the previous one: loop-end barrier)
+            cur_band = ua.x;
+            if (threadIdx.x == 0) {
+                const int64_t base = (int64_t)ua.x * a.W;
+                const int64_t cnt = min((int64_t)a.W, a.nall - base);
+                const uint32_t bytes = (uint32_t)((cnt * (int64_t)sizeof(TG) + 15) & ~(int64_t)15);
+                tma_load_1d(sy, yg + base, bytes, bars + 0);
+            }
+            mbar_wait(bars + 0, ph_band);
+            ph_band ^= 1u;
         }
-        for (; p < e; p += 32) s = A::add(s, (TS)src[__ldg(bs + p)]);
+        if (threadIdx.x == 0 && j + 1 < j1) issue_idx(j + 1, buf ^ 1);  // prefetch under this unit
+        mbar_wait(bars + 1 + buf, (ph_idx >> buf) & 1u);
+        ph_idx ^= 1u << buf;
+        const uint16_t* ix = sidx + buf * kUnitMax;
+        // warp pieces: lanes stride the entries, fixed butterfly fold
+        for (int q = ua.y + warp; q < ua.y + ua.z; q += kWarps) {
+            const int32_t o = __ldg(a.wp_off + q), n = __ldg(a.wp_len + q);
+            TS s = TS(0);
+            int32_t p = lane;
+            for (; p + 96 < n; p += 128) {
+                const TG y0 = sy[ix[o + p]], y1 = sy[ix[o + p + 32]], y2 = sy[ix[o + p + 64]], y3 = sy[ix[o + p + 96]];
+                s = A::add(s, (TS)y0);
+                s = A::add(s, (TS)y1);
+                s = A::add(s, (TS)y2);
+                s = A::add(s, (TS)y3);
+            }
+            for (; p < n; p += 32) s = A::add(s, (TS)sy[ix[o + p]]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if (lane == 0) psum[__ldg(pdst + q)] = (double)s;
-    }
-    for (int q = q0 + nwp + threadIdx.x; q < q1; q += kPartThreads) {
-        const int32_t b = __ldg(poff + q), e = __ldg(poff + q + 1);
-        TS s = TS(0);
-        for (int32_t p = b; p < e; ++p) s = A::add(s, (TS)src[__ldg(bs + p)]);
-        psum[__ldg(pdst + q)] = (double)s;
+            for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
+            if (lane == 0) a.psum[q] = (double)s;
+        }
+        // short pieces: a warp per group of 32, a lane per piece, sequential
+        const int4 ub = __ldg(a.unit_b + j);
+        for (int g = ua.w + warp; g < ua.w + ub.x; g += kWarps) {
+            const int32_t o = __ldg(a.g_off + g), lm = __ldg(a.g_lmax + g);
+            const int32_t n = __ldg(a.g_len + (int64_t)g * 32 + lane);
+            TS s = TS(0);
+            int32_t k = 0;
+            for (; k + 3 < lm; k += 4) {
+                const TG y0 = k < n ? sy[ix[o + 32 * k + lane]] : TG(0);
+                const TG y1 = k + 1 < n ? sy[ix[o + 32 * (k + 1) + lane]] : TG(0);
+                const TG y2 = k + 2 < n ? sy[ix[o + 32 * (k + 2) + lane]] : TG(0);
+                const TG y3 = k + 3 < n ? sy[ix[o + 32 * (k + 3) + lane]] : TG(0);
+                s = A::add(s, (TS)y0);  // +0.0 past the piece's end: bits unchanged
+                s = A::add(s, (TS)y1);
+                s = A::add(s, (TS)y2);
+                s = A::add(s, (TS)y3);
+            }
+            for (; k < lm; ++k) s = A::add(s, (TS)(k < n ? sy[ix[o + 32 * k + lane]] : TG(0)));
+            if (n > 0) a.psum[a.nwp_all + (int64_t)g * 32 + lane] = (double)s;
+        }
+        __syncthreads();  // this unit's buffer and (maybe) the band are free again
     }
 }
 
-// Long rows, fast mode: row q of the range adds its pieces' sums in piece
-// order and is updated (dynamics.py:104-107); per-block stats as k_part_step.
+// Long rows, fast mode: one warp per row adds its pieces' sums in piece order
+// (lanes stride the pieces, fixed butterfly fold; piece j's sum is
+// pc_sum[lpidx[j]], or pc_sum[j] without lpidx) and lane 0 updates the row
+// (dynamics.py:104-107); per-block stats as k_part_step.
 template <typename TS, typename TG>
 __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
-    int64_t n_long, int64_t first, const int32_t* __restrict__ lp, const double* __restrict__ pc_sum,
-    const double* __restrict__ w64, const TS* __restrict__ v, const TS* __restrict__ x, TS* __restrict__ xo,
-    TG* __restrict__ ygo, const double* __restrict__ gam, int k, double* __restrict__ part) {
+    int64_t n_long, int64_t first, const int32_t* __restrict__ lp, const int32_t* __restrict__ lpidx,
+    const double* __restrict__ pc_sum, const double* __restrict__ w64, const TS* __restrict__ v,
+    const TS* __restrict__ x, TS* __restrict__ xo, TG* __restrict__ ygo, const double* __restrict__ gam, int k,
+    double* __restrict__ part) {
     using A = Arith<TS>;
     const TS g = (TS)gam[k];
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (kPartThreads / 32) + (threadIdx.x >> 5);
     if (q < n_long) {
+        const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
         TS s = TS(0);
-        for (int32_t j = lp[q]; j < lp[q + 1]; ++j) s = A::add(s, (TS)pc_sum[j]);
-        part_update<TS, TG>(first + q, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+        for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[lpidx ? __ldg(lpidx + j) : j]);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
+        if (lane == 0) part_update<TS, TG>(first + q, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
     }
     __shared__ double red[kPartThreads / 32][4];
 #pragma unroll
@@ -737,15 +826,12 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
     // the long rows' pieces (fast mode), per range: runs inside one column
-    // band (band mode), or kPiece consecutive entries (GN_PART_BAND=0)
+    // band of at most kUnitMax entries (band mode), or kPiece consecutive
+    // entries (GN_PART_BAND=0)
     P->band = 1;
     if (const char* e = getenv("GN_PART_BAND")) P->band = atoi(e) != 0;
     const int W = kBandBytes / (int)gather_bytes(P->dtype);
     P->band_w = W;
-    int64_t unit_entries = 32768;  // entries per unit (about; a unit holds whole pieces)
-    if (const char* e = getenv("GN_BAND_UNIT")) unit_entries = std::max(256, atoi(e));
-    int64_t direct_below = W / 8;  // units with fewer entries read the values in place
-    if (const char* e = getenv("GN_BAND_DIRECT")) direct_below = atoi(e);
     std::vector<int32_t> pb, pe, lp, pband;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
@@ -760,7 +846,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                 if (P->band) {  // the run of this row's (ascending) neighbours in one band
                     const int32_t bnd = ncol[(size_t)e] / W;
                     f = e + 1;
-                    while (f < end && ncol[(size_t)f] / W == bnd) ++f;
+                    while (f < end && f - e < kUnitMax && ncol[(size_t)f] / W == bnd) ++f;
                     pband.push_back(bnd);
                 } else {
                     f = std::min<int64_t>(e + kPiece, end);
@@ -773,67 +859,147 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         lp.push_back((int32_t)pb.size());
         P->npc[r] = (int64_t)pb.size() - P->pc0[r];
     }
-    cudaFree(P->pc_sum);
-    P->pc_sum = nullptr;
-    GN_CUDA(cudaMalloc((void**)&P->pc_sum, 8 * std::max<size_t>(pb.size(), 1)));
     if ((rcode = upload_into(&P->pc_beg, pb)) || (rcode = upload_into(&P->pc_end, pe)) ||
         (rcode = upload_into(&P->lp, lp)))
         return rcode;
+    int64_t slots = (int64_t)pb.size();
     if (P->band) {
         // per range: pieces grouped by band (counting sort, stable), longest
-        // first inside a band; units of about unit_entries entries
+        // first; units of <= kUnitMax stream entries: warp pieces (>= 32
+        // entries) one after the other, then the short ones in groups of 32
+        // stored position-major (group size = its first, longest piece)
         const int nbands = (int)(nall / W + 1);
-        std::vector<int32_t> order_pc;  // processing order -> row-major piece id
-        std::vector<int4> units;
-        order_pc.reserve(pb.size());
+        int dev_sms = 148;
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, P->device);
+        P->band_ctas = 2 * dev_sms;
+        struct Unit {
+            int band;
+            std::vector<int32_t> warp, shrt;
+        };
+        std::vector<Unit> all_units;
+        auto len = [&](int32_t j) { return pe[(size_t)j] - pb[(size_t)j]; };
         for (int r = 0; r < 2; ++r) {
-            P->u0[r] = (int64_t)units.size();
-            const int64_t a = P->pc0[r], b = a + P->npc[r];
+            P->u0[r] = (int64_t)all_units.size();
+            const int64_t a0 = P->pc0[r], a1 = a0 + P->npc[r];
             std::vector<int64_t> cnt((size_t)nbands + 1, 0);
-            for (int64_t j = a; j < b; ++j) cnt[(size_t)pband[(size_t)j] + 1]++;
+            for (int64_t j = a0; j < a1; ++j) cnt[(size_t)pband[(size_t)j] + 1]++;
             for (int t = 0; t < nbands; ++t) cnt[(size_t)t + 1] += cnt[(size_t)t];
-            std::vector<int32_t> by((size_t)(b - a));
+            std::vector<int32_t> by((size_t)(a1 - a0));
             {
                 std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-                for (int64_t j = a; j < b; ++j) by[(size_t)fill[(size_t)pband[(size_t)j]]++] = (int32_t)j;
+                for (int64_t j = a0; j < a1; ++j) by[(size_t)fill[(size_t)pband[(size_t)j]]++] = (int32_t)j;
             }
             for (int t = 0; t < nbands; ++t) {
                 auto lo = by.begin() + cnt[(size_t)t], hi = by.begin() + cnt[(size_t)t + 1];
                 if (lo == hi) continue;
-                std::stable_sort(lo, hi, [&](int32_t x, int32_t y) { return pe[(size_t)x] - pb[(size_t)x] > pe[(size_t)y] - pb[(size_t)y]; });
+                std::stable_sort(lo, hi, [&](int32_t x, int32_t y) { return len(x) > len(y); });
+                Unit u{t, {}, {}};
+                int64_t cost = 0;
                 for (auto it = lo; it != hi;) {
-                    const int32_t first = (int32_t)order_pc.size();
-                    int64_t ent = 0;
-                    int nwp = 0;
-                    while (it != hi && (ent == 0 || ent + (pe[(size_t)*it] - pb[(size_t)*it]) <= unit_entries)) {
-                        const int32_t len = pe[(size_t)*it] - pb[(size_t)*it];
-                        if (len >= 32) ++nwp;  // longest first: the warp pieces lead the unit
-                        ent += len;
-                        order_pc.push_back(*it);
-                        ++it;
+                    const int32_t l = len(*it);
+                    // a short piece that opens a group of 32 reserves the group (its length, longest first)
+                    const int64_t add = l >= 32 ? l : (u.shrt.size() % 32 == 0 ? 32 * (int64_t)l : 0);
+                    if (cost + add > kUnitMax && (!u.warp.empty() || !u.shrt.empty())) {
+                        all_units.push_back(std::move(u));
+                        u = Unit{t, {}, {}};
+                        cost = 0;
+                        continue;  // the same piece opens the next unit
                     }
-                    const int direct = ent < direct_below ? 1 : 0;
-                    units.push_back(make_int4(t, first, (int32_t)order_pc.size(), nwp | (direct << 30)));
+                    cost += add;
+                    (l >= 32 ? u.warp : u.shrt).push_back(*it);
+                    ++it;
                 }
+                if (!u.warp.empty() || !u.shrt.empty()) all_units.push_back(std::move(u));
             }
-            P->nu[r] = (int64_t)units.size() - P->u0[r];
+            P->nu[r] = (int64_t)all_units.size() - P->u0[r];
         }
-        // the entries, as offsets inside their band, in processing order
-        std::vector<int32_t> poff(order_pc.size() + 1, 0);
-        for (size_t j = 0; j < order_pc.size(); ++j)
-            poff[j + 1] = poff[j] + (pe[(size_t)order_pc[j]] - pb[(size_t)order_pc[j]]);
-        std::vector<uint16_t> bs((size_t)std::max<int32_t>(poff.back(), 1));
-        parallel_for((int64_t)order_pc.size(), [&](int64_t j) {
-            const int32_t pcid = order_pc[(size_t)j];
-            const int32_t bnd = pband[(size_t)pcid];
-            uint16_t* dst = bs.data() + poff[(size_t)j];
-            for (int32_t e = pb[(size_t)pcid]; e < pe[(size_t)pcid]; ++e)
-                *dst++ = (uint16_t)(ncol[(size_t)e] - bnd * W);
+        // descriptors, psum slots (warp pieces, then 32 per group) and the
+        // row-major piece -> slot map for the combine
+        int64_t nwp = 0, ng = 0;
+        for (const Unit& u : all_units) {
+            nwp += (int64_t)u.warp.size();
+            ng += ((int64_t)u.shrt.size() + 31) / 32;
+        }
+        P->nwp_all = nwp;
+        slots = nwp + 32 * ng;
+        std::vector<int4> ua, ub;
+        std::vector<int32_t> wpo, wpl, go, glm, gl, cta_u, lpidx(pb.size(), -1);
+        std::vector<int64_t> ustart;
+        int64_t stream_len = 0, wq = 0, gq = 0;
+        for (const Unit& u : all_units) {
+            int64_t off = 0;
+            const int32_t wp_first = (int32_t)wq, g_first = (int32_t)gq;
+            for (int32_t j : u.warp) {
+                wpo.push_back((int32_t)off);
+                wpl.push_back(len(j));
+                lpidx[(size_t)j] = (int32_t)wq++;
+                off += len(j);
+            }
+            for (size_t g0 = 0; g0 < u.shrt.size(); g0 += 32) {
+                const int32_t lmax = len(u.shrt[g0]);
+                go.push_back((int32_t)off);
+                glm.push_back(lmax);
+                for (size_t l = 0; l < 32; ++l) {
+                    if (g0 + l < u.shrt.size()) {
+                        const int32_t j = u.shrt[g0 + l];
+                        gl.push_back(len(j));
+                        lpidx[(size_t)j] = (int32_t)(nwp + gq * 32 + (int64_t)l);
+                    } else {
+                        gl.push_back(0);
+                    }
+                }
+                ++gq;
+                off += 32 * (int64_t)lmax;
+            }
+            const int64_t padded = (off + 7) / 8 * 8;  // bulk copies move multiples of 16 bytes
+            ua.push_back(make_int4(u.band, wp_first, (int32_t)u.warp.size(), g_first));
+            ub.push_back(make_int4((int32_t)(gq - g_first), (int32_t)stream_len, (int32_t)padded, 0));
+            ustart.push_back(stream_len);
+            stream_len += padded;
+        }
+        // the stream: 16-bit offsets in the band, each unit written in parallel
+        std::vector<uint16_t> bs((size_t)std::max<int64_t>(stream_len, 8), 0);
+        parallel_for((int64_t)all_units.size(), [&](int64_t ui) {
+            const Unit& u = all_units[(size_t)ui];
+            const int64_t base = (int64_t)u.band * W;
+            uint16_t* dst = bs.data() + ustart[(size_t)ui];
+            for (int32_t j : u.warp)
+                for (int32_t e = pb[(size_t)j]; e < pe[(size_t)j]; ++e) *dst++ = (uint16_t)(ncol[(size_t)e] - base);
+            for (size_t g0 = 0; g0 < u.shrt.size(); g0 += 32) {
+                const int32_t lmax = len(u.shrt[g0]);
+                for (size_t l = 0; l < 32 && g0 + l < u.shrt.size(); ++l) {
+                    const int32_t j = u.shrt[g0 + l];
+                    for (int32_t e = pb[(size_t)j]; e < pe[(size_t)j]; ++e)
+                        dst[(size_t)(e - pb[(size_t)j]) * 32 + l] = (uint16_t)(ncol[(size_t)e] - base);
+                }
+                dst += (size_t)lmax * 32;
+            }
         });
-        if ((rcode = upload_into(&P->bstream, bs)) || (rcode = upload_into(&P->bpoff, poff)) ||
-            (rcode = upload_into(&P->bpdst, order_pc)) || (rcode = upload_into(&P->units, units)))
-            return rcode;
+        // persistent CTAs: contiguous unit ranges of about equal stream length, per range
+        for (int r = 0; r < 2; ++r) {
+            const int64_t a0 = P->u0[r], a1 = a0 + P->nu[r];
+            int64_t tot = 0;
+            for (int64_t u = a0; u < a1; ++u) tot += ub[(size_t)u].z;
+            int64_t acc = 0, u = a0;
+            cta_u.push_back((int32_t)a0);
+            for (int c = 1; c < P->band_ctas; ++c) {
+                const int64_t target = tot * c / P->band_ctas;
+                while (u < a1 && acc + ub[(size_t)u].z / 2 < target) acc += ub[(size_t)u++].z;
+                cta_u.push_back((int32_t)u);
+            }
+            cta_u.push_back((int32_t)a1);
+        }
+        int rc2;
+        if ((rc2 = upload_into(&P->bstream, bs)) || (rc2 = upload_into(&P->unit_a, ua)) ||
+            (rc2 = upload_into(&P->unit_b, ub)) || (rc2 = upload_into(&P->wp_off, wpo)) ||
+            (rc2 = upload_into(&P->wp_len, wpl)) || (rc2 = upload_into(&P->g_off, go)) ||
+            (rc2 = upload_into(&P->g_lmax, glm)) || (rc2 = upload_into(&P->g_len, gl)) ||
+            (rc2 = upload_into(&P->lpidx, lpidx)) || (rc2 = upload_into(&P->cta_u, cta_u)))
+            return rc2;
     }
+    cudaFree(P->pc_sum);
+    P->pc_sum = nullptr;
+    GN_CUDA(cudaMalloc((void**)&P->pc_sum, 8 * (size_t)std::max<int64_t>(slots, 1)));
     P->gen++;
     return GN_OK;
 }
@@ -894,8 +1060,8 @@ template <typename TS, typename TG>
 static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
     k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
-        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->pc_sum, p->w64, (const TS*)p->v, (const TS*)p->x[cur],
-        (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
+        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->band ? p->lpidx : nullptr, p->pc_sum, p->w64,
+        (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
 }
 
 static PartLong part_long_of(gn_part* p, int r) {
@@ -903,13 +1069,14 @@ static PartLong part_long_of(gn_part* p, int r) {
                     p->r_long[r] && !p->band ? p->npc[r] : 0};
 }
 
+constexpr int kBandSmem = kBandBytes + 4 * kUnitMax + 64;
+
 template <typename TS, typename TG>
 static void launch_band(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
-    const int64_t u0 = p->u0[r];
-    k_part_band<TS, TG><<<(int)p->nu[r], kPartThreads, kBandBytes, s>>>(
-        p->units + u0, p->bstream, p->bpoff, p->bpdst, (const TG*)p->yg[cur], p->n_own + p->n_ghost, p->band_w,
-        p->pc_sum);
+    BandArgs a{p->unit_a, p->unit_b, p->cta_u + (size_t)r * (p->band_ctas + 1), p->bstream, p->wp_off, p->wp_len,
+               p->g_off, p->g_lmax, p->g_len, p->n_own + p->n_ghost, p->band_w, p->nwp_all, p->pc_sum};
+    k_part_band<TS, TG><<<p->band_ctas, kBandThreads, kBandSmem, s>>>(a, (const TG*)p->yg[cur]);
 }
 
 }  // namespace gn
@@ -954,9 +1121,9 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
         return rc;
     }
     GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandBytes));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
+    GN_CUDA(cudaFuncSetAttribute(k_part_band<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
     *out = P;
     return GN_OK;
 }
@@ -976,9 +1143,9 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
     cudaFree(p->bstream);
-    cudaFree(p->bpoff);
-    cudaFree(p->bpdst);
-    cudaFree(p->units);
+    for (void* q : {(void*)p->unit_a, (void*)p->unit_b, (void*)p->wp_off, (void*)p->wp_len, (void*)p->g_off,
+                    (void*)p->g_lmax, (void*)p->g_len, (void*)p->lpidx, (void*)p->cta_u})
+        cudaFree(q);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -1019,7 +1186,7 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_nbl[r] = p->r_long[r] && !p->band
                           ? (int)std::min<int64_t>((p->npc[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12)
                           : 0;
-        p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads - 1) / kPartThreads) : 0;
+        p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32)) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
         p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
         const int sblocks = (int)std::min<int64_t>((p->nsl[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 16);
@@ -1035,8 +1202,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         GN_CUDA(cudaMalloc(&p->x[0], es * nb));
         GN_CUDA(cudaMalloc(&p->x[1], es * nb));
         // published values + the zero-valued padding slot n_all
-        GN_CUDA(cudaMalloc(&p->yg[0], gs * (nb + 1)));
-        GN_CUDA(cudaMalloc(&p->yg[1], gs * (nb + 1)));
+        GN_CUDA(cudaMalloc(&p->yg[0], gs * (nb + 4)));  // + the zero slot n_all, and 16-byte tails
+        GN_CUDA(cudaMalloc(&p->yg[1], gs * (nb + 4)));
         GN_CUDA(cudaMalloc(&p->v, es * nb));
         GN_CUDA(cudaMalloc((void**)&p->gam, 8 * (size_t)iters));
         for (int r = 0; r < 2; ++r)
@@ -1051,8 +1218,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->alloc_ncomb[0] = p->r_ncomb[0];
         p->alloc_ncomb[1] = p->r_ncomb[1];
     }
-    GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 1)));
-    GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 1)));
+    GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 4)));
+    GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 4)));
     GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
     // a new run epoch (see gn_part::epoch)
     if (!p->d_epoch) GN_CUDA(cudaMalloc((void**)&p->d_epoch, sizeof(int64_t)));

@@ -20,6 +20,10 @@ KEYS = [
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size", "launch__block_size",
     "launch__registers_per_thread", "smsp__inst_executed.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "l1tex__t_sector_hit_rate.pct", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smsp__warps_launched.sum",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1}
@@ -44,10 +48,12 @@ def num(s):
         return None
 
 
-def summarize_rep(rep, label, config, iters):
+def summarize_rep(rep, label, config, iters, names=None):
     out = {}
-    for d, u in raw(rep):
+    for idx, (d, u) in enumerate(raw(rep)):
         name = d.get("Kernel Name", "?")
+        if names is not None:  # one entry per launch, labelled
+            name = f"{idx}: {names[idx] if idx < len(names) else '?'}: {name.split('(')[0]}"
         m = {}
         for k in KEYS:
             if k in d:
@@ -111,8 +117,9 @@ if __name__ == "__main__":
     ap.add_argument("--label", required=True)
     ap.add_argument("--config")
     ap.add_argument("--iters", type=int)
+    ap.add_argument("--names", help="comma-separated labels, one per launch (one entry per launch)")
     a = ap.parse_args()
     if a.kind == "rep":
-        summarize_rep(a.path, a.label, a.config, a.iters)
+        summarize_rep(a.path, a.label, a.config, a.iters, a.names.split(",") if a.names else None)
     else:
         summarize_launches(a.path, a.label)
