@@ -95,7 +95,8 @@ struct gn_part {
     int32_t* g_off = nullptr;                // group: offset in its unit's stream
     int32_t* g_lmax = nullptr;               // group: longest piece (= its rows in the stream)
     int32_t* g_len = nullptr;                // [groups * 32] piece lengths (0: empty slot)
-    int32_t* lpidx = nullptr;                // row-major piece -> psum slot
+    int32_t* wp_dst = nullptr;               // warp piece -> row-major piece id (its psum slot)
+    int32_t* g_dst = nullptr;                // [groups * 32] short piece -> row-major piece id
     int32_t* cta_u = nullptr;                // [ranges][band_ctas + 1] unit ranges
     int64_t nwp_all = 0;                     // warp pieces (psum slots [0, nwp_all)), then 32 per group
     int64_t u0[2] = {0, 0}, nu[2] = {0, 0};
@@ -421,6 +422,8 @@ struct BandArgs {
     const int32_t* g_off;
     const int32_t* g_lmax;
     const int32_t* g_len;
+    const int32_t* wp_dst;  // warp piece -> row-major piece id (its psum slot)
+    const int32_t* g_dst;   // [groups * 32] short piece -> row-major piece id
     int64_t nall;
     int W;
     int64_t nwp_all;
@@ -431,83 +434,72 @@ template <typename TS, typename TG>
 __global__ void __launch_bounds__(kBandThreads, 2) k_part_band(BandArgs a, const TG* __restrict__ yg) {
     using A = Arith<TS>;
     extern __shared__ __align__(128) unsigned char band_smem[];
-    TG* sy = reinterpret_cast<TG*>(band_smem);                                  // kBandBytes
-    uint16_t* sidx = reinterpret_cast<uint16_t*>(band_smem + kBandBytes);       // 2 x kUnitMax
-    uint64_t* bars = reinterpret_cast<uint64_t*>(band_smem + kBandBytes + 4 * kUnitMax);  // band, idx0, idx1
+    TG* sy = reinterpret_cast<TG*>(band_smem);                                 // kBandBytes
+    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem + kBandBytes);
     const int j0 = __ldg(a.cta_u + blockIdx.x), j1 = __ldg(a.cta_u + blockIdx.x + 1);
     if (j0 >= j1) return;
     if (threadIdx.x == 0) {
-        mbar_init(bars + 0, 1);
-        mbar_init(bars + 1, 1);
-        mbar_init(bars + 2, 1);
+        mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue_idx = [&](int j, int buf) {
-        const int4 ub = __ldg(a.unit_b + j);
-        tma_load_1d(sidx + buf * kUnitMax, a.bs + ub.y, (uint32_t)ub.z * 2u, bars + 1 + buf);
-    };
-    if (threadIdx.x == 0) issue_idx(j0, 0);
-    uint32_t ph_band = 0, ph_idx = 0;  // bit b: the phase of index buffer b
+    uint32_t ph = 0;
     int cur_band = -1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarps = kBandThreads / 32;
     for (int j = j0; j < j1; ++j) {
-        const int buf = (j - j0) & 1;
         const int4 ua = __ldg(a.unit_a + j);
-        if (ua.x != cur_band) {  // stage the band (everyone finished the previous one: loop-end barrier)
+        if (ua.x != cur_band) {  // a new band: everyone is done with the old one, then one bulk copy
+            __syncthreads();
             cur_band = ua.x;
             if (threadIdx.x == 0) {
                 const int64_t base = (int64_t)ua.x * a.W;
                 const int64_t cnt = min((int64_t)a.W, a.nall - base);
                 const uint32_t bytes = (uint32_t)((cnt * (int64_t)sizeof(TG) + 15) & ~(int64_t)15);
-                tma_load_1d(sy, yg + base, bytes, bars + 0);
+                tma_load_1d(sy, yg + base, bytes, bar);
             }
-            mbar_wait(bars + 0, ph_band);
-            ph_band ^= 1u;
+            mbar_wait(bar, ph);
+            ph ^= 1u;
         }
-        if (threadIdx.x == 0 && j + 1 < j1) issue_idx(j + 1, buf ^ 1);  // prefetch under this unit
-        mbar_wait(bars + 1 + buf, (ph_idx >> buf) & 1u);
-        ph_idx ^= 1u << buf;
-        const uint16_t* ix = sidx + buf * kUnitMax;
+        const int4 ub = __ldg(a.unit_b + j);
+        const uint16_t* ix = a.bs + ub.y;
+        const int rot = j % kWarps;  // spread the units' first pieces over the warps
+        const int wv = (warp + kWarps - rot) % kWarps;
         // warp pieces: lanes stride the entries, fixed butterfly fold
-        for (int q = ua.y + warp; q < ua.y + ua.z; q += kWarps) {
+        for (int q = ua.y + wv; q < ua.y + ua.z; q += kWarps) {
             const int32_t o = __ldg(a.wp_off + q), n = __ldg(a.wp_len + q);
             TS s = TS(0);
             int32_t p = lane;
             for (; p + 96 < n; p += 128) {
-                const TG y0 = sy[ix[o + p]], y1 = sy[ix[o + p + 32]], y2 = sy[ix[o + p + 64]], y3 = sy[ix[o + p + 96]];
-                s = A::add(s, (TS)y0);
-                s = A::add(s, (TS)y1);
-                s = A::add(s, (TS)y2);
-                s = A::add(s, (TS)y3);
+                const uint16_t i0 = __ldg(ix + o + p), i1 = __ldg(ix + o + p + 32), i2 = __ldg(ix + o + p + 64),
+                               i3 = __ldg(ix + o + p + 96);
+                s = A::add(s, (TS)sy[i0]);
+                s = A::add(s, (TS)sy[i1]);
+                s = A::add(s, (TS)sy[i2]);
+                s = A::add(s, (TS)sy[i3]);
             }
-            for (; p < n; p += 32) s = A::add(s, (TS)sy[ix[o + p]]);
+            for (; p < n; p += 32) s = A::add(s, (TS)sy[__ldg(ix + o + p)]);
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
-            if (lane == 0) a.psum[q] = (double)s;
+            if (lane == 0) a.psum[__ldg(a.wp_dst + q)] = (double)s;
         }
         // short pieces: a warp per group of 32, a lane per piece, sequential
-        const int4 ub = __ldg(a.unit_b + j);
-        for (int g = ua.w + warp; g < ua.w + ub.x; g += kWarps) {
+        for (int g = ua.w + wv; g < ua.w + ub.x; g += kWarps) {
             const int32_t o = __ldg(a.g_off + g), lm = __ldg(a.g_lmax + g);
             const int32_t n = __ldg(a.g_len + (int64_t)g * 32 + lane);
+            const uint16_t* gx = ix + o + lane;
             TS s = TS(0);
             int32_t k = 0;
-            for (; k + 3 < lm; k += 4) {
-                const TG y0 = k < n ? sy[ix[o + 32 * k + lane]] : TG(0);
-                const TG y1 = k + 1 < n ? sy[ix[o + 32 * (k + 1) + lane]] : TG(0);
-                const TG y2 = k + 2 < n ? sy[ix[o + 32 * (k + 2) + lane]] : TG(0);
-                const TG y3 = k + 3 < n ? sy[ix[o + 32 * (k + 3) + lane]] : TG(0);
-                s = A::add(s, (TS)y0);  // +0.0 past the piece's end: bits unchanged
-                s = A::add(s, (TS)y1);
-                s = A::add(s, (TS)y2);
-                s = A::add(s, (TS)y3);
+            for (; k + 7 < lm; k += 8) {
+                uint16_t id[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) id[t] = __ldg(gx + 32 * (k + t));
+#pragma unroll
+                for (int t = 0; t < 8; ++t) s = A::add(s, (TS)(k + t < n ? sy[id[t]] : TG(0)));  // +0.0: bits unchanged
             }
-            for (; k < lm; ++k) s = A::add(s, (TS)(k < n ? sy[ix[o + 32 * k + lane]] : TG(0)));
-            if (n > 0) a.psum[a.nwp_all + (int64_t)g * 32 + lane] = (double)s;
+            for (; k < lm; ++k) s = A::add(s, (TS)(k < n ? sy[__ldg(gx + 32 * k)] : TG(0)));
+            if (n > 0) a.psum[__ldg(a.g_dst + (int64_t)g * 32 + lane)] = (double)s;
         }
-        __syncthreads();  // this unit's buffer and (maybe) the band are free again
     }
 }
 
@@ -913,17 +905,15 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             }
             P->nu[r] = (int64_t)all_units.size() - P->u0[r];
         }
-        // descriptors, psum slots (warp pieces, then 32 per group) and the
-        // row-major piece -> slot map for the combine
+        // descriptors; every piece writes its sum to pc_sum[its row-major id]
         int64_t nwp = 0, ng = 0;
         for (const Unit& u : all_units) {
             nwp += (int64_t)u.warp.size();
             ng += ((int64_t)u.shrt.size() + 31) / 32;
         }
         P->nwp_all = nwp;
-        slots = nwp + 32 * ng;
         std::vector<int4> ua, ub;
-        std::vector<int32_t> wpo, wpl, go, glm, gl, cta_u, lpidx(pb.size(), -1);
+        std::vector<int32_t> wpo, wpl, go, glm, gl, cta_u, wdst, gdst;
         std::vector<int64_t> ustart;
         int64_t stream_len = 0, wq = 0, gq = 0;
         for (const Unit& u : all_units) {
@@ -932,7 +922,8 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             for (int32_t j : u.warp) {
                 wpo.push_back((int32_t)off);
                 wpl.push_back(len(j));
-                lpidx[(size_t)j] = (int32_t)wq++;
+                wdst.push_back(j);
+                ++wq;
                 off += len(j);
             }
             for (size_t g0 = 0; g0 < u.shrt.size(); g0 += 32) {
@@ -943,9 +934,10 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                     if (g0 + l < u.shrt.size()) {
                         const int32_t j = u.shrt[g0 + l];
                         gl.push_back(len(j));
-                        lpidx[(size_t)j] = (int32_t)(nwp + gq * 32 + (int64_t)l);
+                        gdst.push_back(j);
                     } else {
                         gl.push_back(0);
+                        gdst.push_back(0);
                     }
                 }
                 ++gq;
@@ -994,7 +986,8 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             (rc2 = upload_into(&P->unit_b, ub)) || (rc2 = upload_into(&P->wp_off, wpo)) ||
             (rc2 = upload_into(&P->wp_len, wpl)) || (rc2 = upload_into(&P->g_off, go)) ||
             (rc2 = upload_into(&P->g_lmax, glm)) || (rc2 = upload_into(&P->g_len, gl)) ||
-            (rc2 = upload_into(&P->lpidx, lpidx)) || (rc2 = upload_into(&P->cta_u, cta_u)))
+            (rc2 = upload_into(&P->wp_dst, wdst)) || (rc2 = upload_into(&P->g_dst, gdst)) ||
+            (rc2 = upload_into(&P->cta_u, cta_u)))
             return rc2;
     }
     cudaFree(P->pc_sum);
@@ -1060,7 +1053,7 @@ template <typename TS, typename TG>
 static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
     k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
-        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->band ? p->lpidx : nullptr, p->pc_sum, p->w64,
+        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], nullptr, p->pc_sum, p->w64,
         (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
 }
 
@@ -1069,13 +1062,14 @@ static PartLong part_long_of(gn_part* p, int r) {
                     p->r_long[r] && !p->band ? p->npc[r] : 0};
 }
 
-constexpr int kBandSmem = kBandBytes + 4 * kUnitMax + 64;
+constexpr int kBandSmem = kBandBytes + 64;
 
 template <typename TS, typename TG>
 static void launch_band(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
     BandArgs a{p->unit_a, p->unit_b, p->cta_u + (size_t)r * (p->band_ctas + 1), p->bstream, p->wp_off, p->wp_len,
-               p->g_off, p->g_lmax, p->g_len, p->n_own + p->n_ghost, p->band_w, p->nwp_all, p->pc_sum};
+               p->g_off, p->g_lmax, p->g_len, p->wp_dst, p->g_dst, p->n_own + p->n_ghost, p->band_w, p->nwp_all,
+               p->pc_sum};
     k_part_band<TS, TG><<<p->band_ctas, kBandThreads, kBandSmem, s>>>(a, (const TG*)p->yg[cur]);
 }
 
@@ -1144,7 +1138,7 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_sum);
     cudaFree(p->bstream);
     for (void* q : {(void*)p->unit_a, (void*)p->unit_b, (void*)p->wp_off, (void*)p->wp_len, (void*)p->g_off,
-                    (void*)p->g_lmax, (void*)p->g_len, (void*)p->lpidx, (void*)p->cta_u})
+                    (void*)p->g_lmax, (void*)p->g_len, (void*)p->wp_dst, (void*)p->g_dst, (void*)p->cta_u})
         cudaFree(q);
     cudaFree(p->rowptr);
     cudaFree(p->col);

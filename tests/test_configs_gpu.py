@@ -2,11 +2,12 @@
 the pinned CPU oracle.
 
 Sizes: C1 and C3 at full size; C2 at full size for a bounded number of
-iterations (the oracle runs at ~60 ms per iteration per core); C4 on a shard
-of graphs; C5 at R-MAT scale 16 (same generator as scale 24).  Full-size runs
-of the long configs are covered by size-independent properties (independence
-and maximality of the rounded set, fp64 weight recomputation, objective
-monotonicity where the theory guarantees it) in test_properties_gpu.py.
+iterations in the same-precision bitwise checks; C4 on a shard of graphs; C5
+at R-MAT scale 16 and 18 (same generator as scale 24).  The benched modes at
+full size and full budget -- C2 and C3 fp64 x1000, the whole 1024-graph C4
+shard, C5 at scale 24 through the partitioned engine -- are in
+test_fullbudget_gpu.py (sampled per-iteration states against the oracle,
+identical fallbacks, members and weight).
 """
 
 import numpy as np
