@@ -59,6 +59,12 @@ struct gn_part {
     int64_t* slice_ptr = nullptr;   // [nslices+1] element offsets
     int64_t sl0[2] = {0, 0}, nsl[2] = {0, 0};  // per range: first slice, slice count
     int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
+    // settled isolated rows: the last n_iso interior rows (see part_order);
+    // fast-mode steps from iteration 3 on walk only the first iso_nsl slices
+    // of the interior range and add iso_mass (the skipped rows' w . 1) to
+    // the objective
+    int64_t n_iso = 0, iso_nsl = -1;
+    double iso_mass[2] = {0.0, 0.0};  // [binary64 state, binary32 state]
     // fast mode: the long rows of each range cut into pieces of kPiece
     // adjacency entries (fixed sizes: the sum tree, and every bit, is the
     // same on any grid).  Piece j covers col[pc_beg[j], pc_end[j]); long row
@@ -67,6 +73,8 @@ struct gn_part {
     // piece order and updates the row.
     int32_t* pc_beg = nullptr;
     int32_t* pc_end = nullptr;
+    int32_t* pc_order = nullptr;  // GN_PIECE_SORT: pieces by their first column, per range
+    int piece_blocked = 0;
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
@@ -186,6 +194,8 @@ struct PartLong {
     const int32_t* __restrict__ end;
     double* __restrict__ sum;
     int64_t n;
+    const int32_t* __restrict__ order;  // processing position -> piece (null: piece order)
+    int blocked;                        // 1: each warp takes one contiguous run of positions
 };
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
@@ -269,7 +279,11 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
         // stride the positions, 8 gathers in flight per lane with the next 8
         // indices loading under them; fixed butterfly fold.  The rows are
         // updated by k_part_long_combine (pieces added in piece order).
-        for (int64_t q = (int64_t)bid * kWarpsPerBlock + warp; q < lng.n; q += (int64_t)nbl * kWarpsPerBlock) {
+        const int64_t gw = (int64_t)bid * kWarpsPerBlock + warp, tw = (int64_t)nbl * kWarpsPerBlock;
+        const int64_t qa = lng.blocked ? gw * lng.n / tw : gw, qb = lng.blocked ? (gw + 1) * lng.n / tw : lng.n;
+        const int64_t qs = lng.blocked ? 1 : tw;
+        for (int64_t qp = qa; qp < qb; qp += qs) {
+            const int64_t q = lng.order ? __ldg(lng.order + qp) : qp;
             const int32_t pb = __ldg(lng.beg + q), pe = __ldg(lng.end + q);
             TS s = TS(0);
             constexpr int U = 8;
@@ -749,6 +763,17 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                 std::stable_sort(v->begin() + w0, v->begin() + std::min(v->size(), w0 + win), by_deg);
         }
     }
+    // isolated rows that settle (degree 0 and v = sqrt(w) > 2e-9: from any
+    // finite x0 > 0 the step gives 1.0, or 0.5 and then 1.0; from iteration
+    // 3 on both state buffers hold 1.0 and the row no longer changes) go to
+    // the end of the interior range, where fast-mode steps skip them
+    {
+        auto settles = [&](int32_t r) { return deg(r) == 0 && P->h_w[(size_t)r] > 4e-18; };
+        std::stable_partition(ri.begin(), ri.end(), [&](int32_t r) { return !settles(r); });
+        int64_t t = 0;
+        for (auto it = ri.rbegin(); it != ri.rend() && settles(*it); ++it) ++t;
+        P->n_iso = t;
+    }
     P->n_bnd = (int64_t)rb.size();
     P->long_fast[0] = P->long_fast[1] = 0;
     while (P->long_fast[0] < (int64_t)rb.size() && deg(rb[(size_t)P->long_fast[0]]) > kPartLongDegree) ++P->long_fast[0];
@@ -783,6 +808,16 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         P->sl0[r] = (int64_t)sp.size() - 1;
         const int64_t p0 = rs[r] + P->long_fast[r], p1 = rs[r] + rc[r];
         P->nsl[r] = (p1 - p0 + 31) / 32;
+        if (r == 1) {  // the slices wholly inside the settled tail
+            const int64_t f = std::min(P->nsl[1], std::max<int64_t>(0, (p1 - P->n_iso - p0 + 31) / 32));
+            P->iso_nsl = f < P->nsl[1] ? f : -1;
+            P->iso_mass[0] = P->iso_mass[1] = 0.0;
+            for (int64_t q = p0 + 32 * f; P->iso_nsl >= 0 && q < p1; ++q) {  // fixed order
+                const double wq = P->h_w[(size_t)perm[(size_t)q]];
+                P->iso_mass[0] += wq;
+                P->iso_mass[1] += (double)(float)wq;
+            }
+        }
         for (int64_t q = p0; q < p1; q += 32) {
             int32_t len = 0;
             for (int64_t t = q; t < std::min(p1, q + 32); ++t) len = std::max(len, nrp[(size_t)t + 1] - nrp[(size_t)t]);
@@ -820,10 +855,12 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // the long rows' pieces (fast mode), per range: runs inside one column
     // band of at most kUnitMax entries (band mode), or kPiece consecutive
     // entries (GN_PART_BAND=0)
-    P->band = 1;
+    P->band = 0;  // measured slower than kPiece pieces on C5 (profiles/r02_c5s24_band_v3_ncu.json)
     if (const char* e = getenv("GN_PART_BAND")) P->band = atoi(e) != 0;
     const int W = kBandBytes / (int)gather_bytes(P->dtype);
     P->band_w = W;
+    int64_t piece_len = kPiece;
+    if (const char* e = getenv("GN_PIECE_LEN")) piece_len = std::max(32, atoi(e));
     std::vector<int32_t> pb, pe, lp, pband;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
@@ -841,7 +878,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                     while (f < end && f - e < kUnitMax && ncol[(size_t)f] / W == bnd) ++f;
                     pband.push_back(bnd);
                 } else {
-                    f = std::min<int64_t>(e + kPiece, end);
+                    f = std::min<int64_t>(e + piece_len, end);
                 }
                 pb.push_back((int32_t)e);
                 pe.push_back((int32_t)f);
@@ -855,6 +892,27 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         (rcode = upload_into(&P->lp, lp)))
         return rcode;
     int64_t slots = (int64_t)pb.size();
+    // GN_PIECE_SORT=1: pieces processed in order of their first column (so
+    // pieces over the same columns run close together: L1 reuse), 2: and
+    // each warp takes one contiguous run of that order
+    cudaFree(P->pc_order);
+    P->pc_order = nullptr;
+    P->piece_blocked = 0;
+    if (const char* e = getenv("GN_PIECE_SORT")) {
+        const int mode = atoi(e);
+        if (mode > 0 && !P->band) {
+            std::vector<int32_t> ord(pb.size());
+            for (int r = 0; r < 2; ++r) {
+                const int64_t a0 = P->pc0[r], a1 = a0 + P->npc[r];
+                for (int64_t j = a0; j < a1; ++j) ord[(size_t)j] = (int32_t)(j - a0);
+                std::stable_sort(ord.begin() + a0, ord.begin() + a1, [&](int32_t x, int32_t y) {
+                    return ncol[(size_t)pb[(size_t)(a0 + x)]] < ncol[(size_t)pb[(size_t)(a0 + y)]];
+                });
+            }
+            if ((rcode = upload_into(&P->pc_order, ord))) return rcode;
+            P->piece_blocked = mode >= 2;
+        }
+    }
     if (P->band) {
         // per range: pieces grouped by band (counting sort, stable), longest
         // first; units of <= kUnitMax stream entries: warp pieces (>= 32
@@ -1059,7 +1117,8 @@ static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
 
 static PartLong part_long_of(gn_part* p, int r) {
     return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r],
-                    p->r_long[r] && !p->band ? p->npc[r] : 0};
+                    p->r_long[r] && !p->band ? p->npc[r] : 0, p->pc_order ? p->pc_order + p->pc0[r] : nullptr,
+                    p->piece_blocked};
 }
 
 constexpr int kBandSmem = kBandBytes + 64;
@@ -1134,6 +1193,7 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->d_epoch);
     cudaFree(p->pc_beg);
     cudaFree(p->pc_end);
+    cudaFree(p->pc_order);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
     cudaFree(p->bstream);
@@ -1269,9 +1329,11 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
         by_dtype(p->dtype, [&](auto ts, auto tg) { launch_band<decltype(ts), decltype(tg)>(p, r, k, s); });
         GN_LAUNCHED();
     }
+    // fast mode, iteration >= 3: the settled isolated tail is skipped
+    const int64_t nsl = (r == 1 && k >= 3 && p->iso_nsl >= 0 && !(p->flags & GN_EXACT)) ? p->iso_nsl : p->nsl[r];
     by_dtype(p->dtype, [&](auto ts, auto tg) {
         launch_step<decltype(ts), decltype(tg)>(p, r, k, nb, p->r_long[r], p->r_nbl[r], p->r_csr[r], p->r_ncb[r],
-                                                p->nsl[r], push, lng, s);
+                                                nsl, push, lng, s);
     });
     GN_LAUNCHED();
     if (p->r_long[r] > 0 && p->r_count[r] > 0) {
@@ -1382,6 +1444,8 @@ int gn_part_end(gn_part* p, int done, double* x_out, double* step_inf, int64_t* 
             t[2] += a[2];
             t[3] = std::max(t[3], a[3]);
         }
+        if (k >= 3 && p->iso_nsl >= 0 && !(p->flags & GN_EXACT))  // the skipped rows' w . 1.0
+            t[2] += p->iso_mass[state_bytes(p->dtype) == 8 ? 0 : 1];
         for (int c = 0; c < 4; ++c) h[(size_t)k * 4 + c] = t[c];
     }
     if (x_out && p->n_own) GN_CUDA(cudaMemcpy(x_out, dx, 8 * (size_t)p->n_own, cudaMemcpyDeviceToHost));
@@ -1674,7 +1738,7 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
         if (mode == 7) {
             PartPush push{p->push_src, p->push_peer, p->push_slot, p->push_dst[1], p->n_push,
                           (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
-            const PartLong no_long{nullptr, nullptr, nullptr, 0};
+            const PartLong no_long{nullptr, nullptr, nullptr, 0, nullptr, 0};
             by_dtype(p->dtype, [&](auto ts, auto tg) {
                 launch_step<decltype(ts), decltype(tg)>(p, r, 0, push.nblocks, 0, 0, 0, 0, 0, push, no_long, s);
             });
@@ -1686,7 +1750,7 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
             const int nb = mode == 1 ? std::max(nbl, 1) : mode == 2 ? std::max(nsb, 1) : p->r_nblocks[r];
             // mode 2 keeps the slices' order positions (pos0 = n_long + n_csr)
             const int64_t nlong_arg = mode == 2 ? pos0 : p->r_long[r];
-            const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0} : part_long_of(p, r);
+            const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0, nullptr, 0} : part_long_of(p, r);
             by_dtype(p->dtype, [&](auto ts, auto tg) {
                 if (mode != 2 && p->band && p->r_long[r] > 0 && p->nu[r] > 0)
                     launch_band<decltype(ts), decltype(tg)>(p, r, 0, s);
