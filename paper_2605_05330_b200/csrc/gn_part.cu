@@ -73,8 +73,9 @@ struct gn_part {
     // piece order and updates the row.
     int32_t* pc_beg = nullptr;
     int32_t* pc_end = nullptr;
-    int32_t* pc_order = nullptr;  // GN_PIECE_SORT: pieces by their first column, per range
+    int32_t* pc_order = nullptr;  // pieces by their first column, per range (GN_PIECE_SORT)
     int piece_blocked = 0;
+    int interleave = 1;           // GN_PART_INTERLEAVE=0: long-row blocks first
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
@@ -186,7 +187,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
 }
 
 constexpr int kPartLongDegree = 512;
-constexpr int kPiece = 2048;  // adjacency entries per long-row piece (fast mode)
+constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
 // The long rows' pieces (fast mode; see gn_part::pc_beg)
 struct PartLong {
@@ -196,6 +197,7 @@ struct PartLong {
     int64_t n;
     const int32_t* __restrict__ order;  // processing position -> piece (null: piece order)
     int blocked;                        // 1: each warp takes one contiguous run of positions
+    int interleave;                     // 1: long-row blocks spread among the slice blocks
 };
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
@@ -204,11 +206,10 @@ constexpr int kPartUnroll = GN_PART_UNROLL;  // gathers in flight per thread  //
 
 // dynamics.py:104-107 for owned row i with neighbour sum s; stats of the thread
 template <typename TS, typename TG>
-__device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double* __restrict__ w64,
-                                            const TS* __restrict__ v, const TS* __restrict__ x, TS* __restrict__ xo,
-                                            TG* __restrict__ ygo, double& mx, double& fb, double& ob, double& nf) {
+__device__ __forceinline__ void part_update_pre(int64_t i, TS s, TS g, TS xi, TS vi, double wi,
+                                                TS* __restrict__ xo, TG* __restrict__ ygo, double& mx, double& fb,
+                                                double& ob, double& nf) {
     using A = Arith<TS>;
-    const TS xi = x[i], vi = v[i];
     const TS yi = A::mul(vi, xi);
     const TS d = A::add(yi, A::mul(g, s));          // dynamics.py:105
     const bool ok = (double)d > kSafeDiv;            // dynamics.py:106
@@ -220,7 +221,15 @@ __device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double*
     if (!(diff <= mx)) mx = diff;
     fb += ok ? 0.0 : 1.0;
     if (!isfinite((double)o)) nf = 1.0;
-    ob = __dadd_rn(ob, __dmul_rn((double)(TS)w64[i], (double)o));
+    ob = __dadd_rn(ob, __dmul_rn((double)(TS)wi, (double)o));
+}
+
+// the same with the row's state, weight and v loaded here
+template <typename TS, typename TG>
+__device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double* __restrict__ w64,
+                                            const TS* __restrict__ v, const TS* __restrict__ x, TS* __restrict__ xo,
+                                            TG* __restrict__ ygo, double& mx, double& fb, double& ob, double& nf) {
+    part_update_pre<TS, TG>(i, s, g, x[i], v[i], w64[i], xo, ygo, mx, fb, ob, nf);
 }
 
 // Direct halo: the interior step's first `nblocks` blocks copy the boundary
@@ -270,16 +279,25 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
         return;
     }
     const int bid = (int)blockIdx.x - push.nblocks, nbid = (int)gridDim.x - push.nblocks;
+    // the block's role: [0, nbl) long-row pieces, [nbl, nbl + ncb) CSR rows,
+    // then slices.  In fast mode (no CSR blocks) the long-row blocks are
+    // spread evenly among the slice blocks (lng.interleave), so the two
+    // kinds -- L2-throughput-bound pieces, latency-bound slices -- run side by side
+    int rb = bid;
+    if (lng.interleave && ncb == 0 && nbl > 0) {
+        const int before = (int)((int64_t)bid * nbl / nbid), upto = (int)((int64_t)(bid + 1) * nbl / nbid);
+        rb = upto > before ? before : nbl + (bid - before);
+    }
     const TS g = (TS)gam[k];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
-    if (bid < nbl) {
+    if (rb < nbl) {
         // long rows, fast mode: one warp per piece of kPiece entries; lanes
         // stride the positions, 8 gathers in flight per lane with the next 8
         // indices loading under them; fixed butterfly fold.  The rows are
         // updated by k_part_long_combine (pieces added in piece order).
-        const int64_t gw = (int64_t)bid * kWarpsPerBlock + warp, tw = (int64_t)nbl * kWarpsPerBlock;
+        const int64_t gw = (int64_t)rb * kWarpsPerBlock + warp, tw = (int64_t)nbl * kWarpsPerBlock;
         const int64_t qa = lng.blocked ? gw * lng.n / tw : gw, qb = lng.blocked ? (gw + 1) * lng.n / tw : lng.n;
         const int64_t qs = lng.blocked ? 1 : tw;
         for (int64_t qp = qa; qp < qb; qp += qs) {
@@ -312,8 +330,8 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
             for (int o = 16; o > 0; o >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, o));
             if (lane == 0) lng.sum[q] = (double)s;
         }
-    } else if (bid < nbl + ncb) {
-        for (int64_t q = (int64_t)(bid - nbl) * blockDim.x + threadIdx.x; q < n_csr;
+    } else if (rb < nbl + ncb) {
+        for (int64_t q = (int64_t)(rb - nbl) * blockDim.x + threadIdx.x; q < n_csr;
              q += (int64_t)ncb * blockDim.x) {
             const int64_t i = order[n_long + q];
             const int32_t rb = rowptr[i], re = rowptr[i + 1];
@@ -332,10 +350,14 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
     } else {
         const int64_t pos0 = n_long + n_csr;  // first order position of slice 0
         const int64_t nw = (int64_t)(nbid - nbl - ncb) * kWarpsPerBlock;
-        for (int64_t sl = (int64_t)(bid - nbl - ncb) * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
+        for (int64_t sl = (int64_t)(rb - nbl - ncb) * kWarpsPerBlock + warp; sl < nsl; sl += nw) {
             const int64_t pos = pos0 + sl * 32 + lane;
             const bool valid = pos < count;
-            const int64_t i = valid ? order[pos] : 0;
+            // rows are numbered in processing order (part_order): order[pos] == order[0] + pos,
+            // so the row's state, v and weight load at once, under the gathers
+            const int64_t i = order[0] + (valid ? pos : 0);
+            const TS xi = x[i], vi = v[i];
+            const double wi = w64[i];
             const int64_t e0 = slice_ptr[sl];
             const int nblk = (int)((slice_ptr[sl + 1] - e0) / 128);
             const uint4* base = reinterpret_cast<const uint4*>(sell + e0) + lane;
@@ -363,7 +385,7 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(int64_
 #pragma unroll
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
-            if (valid) part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            if (valid) part_update_pre<TS, TG>(i, s, g, xi, vi, wi, xo, ygo, mx, fb, ob, nf);
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -861,6 +883,8 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     P->band_w = W;
     int64_t piece_len = kPiece;
     if (const char* e = getenv("GN_PIECE_LEN")) piece_len = std::max(32, atoi(e));
+    P->interleave = 1;
+    if (const char* e = getenv("GN_PART_INTERLEAVE")) P->interleave = atoi(e) != 0;
     std::vector<int32_t> pb, pe, lp, pband;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
@@ -898,8 +922,10 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     cudaFree(P->pc_order);
     P->pc_order = nullptr;
     P->piece_blocked = 0;
-    if (const char* e = getenv("GN_PIECE_SORT")) {
-        const int mode = atoi(e);
+    {
+        // default 2 (C5 scale 24 fp64: 1.737 -> 1.698 ms per iteration; with 512-entry pieces 1.677)
+        const char* e = getenv("GN_PIECE_SORT");
+        const int mode = e ? atoi(e) : 2;
         if (mode > 0 && !P->band) {
             std::vector<int32_t> ord(pb.size());
             for (int r = 0; r < 2; ++r) {
@@ -1118,7 +1144,7 @@ static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
 static PartLong part_long_of(gn_part* p, int r) {
     return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r],
                     p->r_long[r] && !p->band ? p->npc[r] : 0, p->pc_order ? p->pc_order + p->pc0[r] : nullptr,
-                    p->piece_blocked};
+                    p->piece_blocked, p->interleave};
 }
 
 constexpr int kBandSmem = kBandBytes + 64;
@@ -1738,7 +1764,7 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
         if (mode == 7) {
             PartPush push{p->push_src, p->push_peer, p->push_slot, p->push_dst[1], p->n_push,
                           (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
-            const PartLong no_long{nullptr, nullptr, nullptr, 0, nullptr, 0};
+            const PartLong no_long{nullptr, nullptr, nullptr, 0, nullptr, 0, 0};
             by_dtype(p->dtype, [&](auto ts, auto tg) {
                 launch_step<decltype(ts), decltype(tg)>(p, r, 0, push.nblocks, 0, 0, 0, 0, 0, push, no_long, s);
             });
@@ -1750,7 +1776,7 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
             const int nb = mode == 1 ? std::max(nbl, 1) : mode == 2 ? std::max(nsb, 1) : p->r_nblocks[r];
             // mode 2 keeps the slices' order positions (pos0 = n_long + n_csr)
             const int64_t nlong_arg = mode == 2 ? pos0 : p->r_long[r];
-            const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0, nullptr, 0} : part_long_of(p, r);
+            const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0, nullptr, 0, 0} : part_long_of(p, r);
             by_dtype(p->dtype, [&](auto ts, auto tg) {
                 if (mode != 2 && p->band && p->r_long[r] > 0 && p->nu[r] > 0)
                     launch_band<decltype(ts), decltype(tg)>(p, r, 0, s);
