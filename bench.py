@@ -335,6 +335,28 @@ def ncu_traffic(key: str, iters: int):
     return None
 
 
+def gather_ceiling(key: str, ms_per_iter: float) -> dict | None:
+    """The step kernel against the measured gather ceiling: the L1-missing
+    sectors one iteration issues (lts__t_sectors_srcunit_tex_op_read from the
+    committed ncu capture of the same kernel, profiles/ncu_summary.json) per
+    second of this run, over the rate random L1-missing loads reach on this
+    GPU (tools/gather_ceiling.cu, profiles/r02_gather_ceiling.jsonl: the
+    L2-resident 64 MB table)."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(key, {})
+        sectors = d.get("l2_read_sectors_per_launch") and d["l2_read_sectors_per_launch"] / d.get("iters_per_launch", 1)
+        ceil = [json.loads(s) for s in (ROOT / "profiles" / "r02_gather_ceiling.jsonl").read_text().splitlines()]
+        ceil = max(c["gloads_per_s"] for c in ceil if c["case"] == "global" and c.get("table_mb") == 64) * 1e9
+    except Exception:
+        return None
+    if not sectors:
+        return None
+    rate = sectors / (ms_per_iter * 1e-3)
+    return {"l2_read_sectors_per_iter": sectors, "sectors_per_s": rate, "ceiling_loads_per_s": ceil,
+            "frac": rate / ceil, "source": f"{d.get('label')} (ncu) / tools/gather_ceiling.cu (random 8-byte "
+                                          "loads over a 64 MB L2-resident table, 1.0 per SM per cycle)"}
+
+
 def peak_hbm() -> tuple[float, str]:
     pf = ROOT / "MEASURED_PEAKS.json"
     if pf.exists():
@@ -467,7 +489,10 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                          "kernel": "gn::k_part_step (1 launch per iteration per part, replayed from a CUDA graph)" + (
                              "" if ws == 1 else (" + coalesced pushes into the peers' ghost slots (CUDA IPC)"
                                                  if args.halo == "peer" else " + NCCL halo")),
-                         "b_iter": b_iter, "peak_source": peak_src + (f" x {ws} GPUs" if ws > 1 else "")},
+                         "b_iter": b_iter, "peak_source": peak_src + (f" x {ws} GPUs" if ws > 1 else ""),
+                         "achieved_over": "the whole iteration (step + long-row combine launches)",
+                         "gather_ceiling": gather_ceiling("C5part", total_ms / (args.steps * iters))
+                         if ws == 1 and dtype == "fp64" else None},
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "gpu_launches": int(launches),

@@ -77,9 +77,12 @@ def summarize_rep(rep, label, config, iters, names=None):
     if config:
         sf = ROOT / "profiles" / "ncu_summary.json"
         s = json.loads(sf.read_text()) if sf.exists() else {}
-        loop = [m for n, m in out.items() if "k_gn_loop" in n or "k_gn_batch" in n or "k_gn_multi" in n]
+        loop = [m for n, m in out.items()
+                if any(k in n for k in ("k_gn_loop", "k_gn_batch", "k_gn_multi", "k_part_step"))]
         if loop:
             s[config] = {"label": label, "dram_bytes_per_launch": loop[0]["dram_bytes_per_launch"],
+                         "l2_read_sectors_per_launch":
+                             loop[0].get("lts__t_sectors_srcunit_tex_op_read.sum", {}).get("value"),
                          "iters_per_launch": iters}
             sf.write_text(json.dumps(s, indent=1))
     print(path)
