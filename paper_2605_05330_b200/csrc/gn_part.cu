@@ -186,7 +186,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
     if (i < n_own) x[i] = xi;
 }
 
-constexpr int kPartLongDegree = 512;
+constexpr int kPartLongDegreeDefault = 512;
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
 // The long rows' pieces (fast mode; see gn_part::pc_beg)
@@ -858,6 +858,10 @@ static int upload_into(T** dst, const std::vector<T>& h) {
 // are relabeled to their position in this order and the device graph (CSR,
 // weights, blocked SELL) is rebuilt in the new numbering.
 static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
+    // rows above this degree are "long": split into pieces over warps in
+    // fast mode, one thread over the CSR in EXACT mode (GN_PART_LONG overrides)
+    int kPartLongDegree = kPartLongDegreeDefault;
+    if (const char* e = getenv("GN_PART_LONG")) kPartLongDegree = std::max(32, atoi(e));
     const int64_t n_own = P->n_own, nall = P->n_own + P->n_ghost;
     const std::vector<int32_t>& rp = P->h_rowptr;
     std::vector<uint8_t> is_b((size_t)std::max<int64_t>(n_own, 1), 0);
