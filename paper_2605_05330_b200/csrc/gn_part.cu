@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "gn_internal.cuh"
@@ -58,7 +59,8 @@ struct gn_part {
     int32_t* col_fast = nullptr;
     int64_t* slice_ptr = nullptr;   // [nslices+1] element offsets
     int64_t sl0[2] = {0, 0}, nsl[2] = {0, 0};  // per range: first slice, slice count
-    int64_t long_fast[2] = {0, 0};  // per range: leading rows above kPartLongDegree
+    int64_t long_fast[2] = {0, 0};  // per range: leading rows above long_degree
+    int long_degree = 512;          // set by part_order
     // settled isolated rows: the last n_iso interior rows (see part_order);
     // fast-mode steps from iteration 3 on walk only the first iso_nsl slices
     // of the interior range and add iso_mass (the skipped rows' w . 1) to
@@ -186,7 +188,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
     if (i < n_own) x[i] = xi;
 }
 
-constexpr int kPartLongDegreeDefault = 512;
+constexpr int kPartLongDegreeMin = 512, kPartLongDegreeMax = 4096;
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
 // The long rows' pieces (fast mode; see gn_part::pc_beg)
@@ -859,9 +861,20 @@ static int upload_into(T** dst, const std::vector<T>& h) {
 // weights, blocked SELL) is rebuilt in the new numbering.
 static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // rows above this degree are "long": split into pieces over warps in
-    // fast mode, one thread over the CSR in EXACT mode (GN_PART_LONG overrides)
-    int kPartLongDegree = kPartLongDegreeDefault;
+    // fast mode, one thread over the CSR in EXACT mode.  The others run one
+    // thread per row over the blocked SELL, which gathers more cheaply (a
+    // slice's rows, ordered by their hottest neighbours, share lines at the
+    // same positions) but as one serial chain per row; the threshold grows
+    // with the part so a row's chain stays well inside an iteration:
+    // nnz / 65536 rounded down to a power of two, in [512, 4096].  C5 scale
+    // 24, one part (520 M entries: 4096), fp64, ms per iteration: 512 1.62,
+    // 1024 1.50, 4096 1.44, 8192 1.47, 65536 5.96 (R-MAT degrees cluster
+    // near 2^28 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).
+    // GN_PART_LONG overrides.
+    int kPartLongDegree = kPartLongDegreeMin;
+    while (kPartLongDegree < kPartLongDegreeMax && (int64_t)kPartLongDegree * 2 * 65536 <= P->nnz) kPartLongDegree *= 2;
     if (const char* e = getenv("GN_PART_LONG")) kPartLongDegree = std::max(32, atoi(e));
+    P->long_degree = kPartLongDegree;
     const int64_t n_own = P->n_own, nall = P->n_own + P->n_ghost;
     const std::vector<int32_t>& rp = P->h_rowptr;
     std::vector<uint8_t> is_b((size_t)std::max<int64_t>(n_own, 1), 0);
@@ -918,19 +931,20 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             }
             parallel_for((int64_t)runs.size(), [&](int64_t ri2) {
                 const size_t q0 = runs[(size_t)ri2].first, q1 = runs[(size_t)ri2].second;
-                std::vector<std::pair<uint64_t, int32_t>> kv(q1 - q0);
+                // key: the row's `lex` hottest neighbours (GN_PART_LEX=3: three)
+                std::vector<std::tuple<uint64_t, uint32_t, int32_t>> kv(q1 - q0);
                 for (size_t q = q0; q < q1; ++q) {
                     const int32_t r = (*v)[q];
-                    uint32_t a = ~0u, b = ~0u;
+                    uint32_t a = ~0u, b = ~0u, c3 = ~0u;
                     for (int32_t p = rp[(size_t)r]; p < rp[(size_t)r + 1]; ++p) {
                         const int32_t c = P->h_col[(size_t)p];
                         const uint32_t id = c < n_own ? pinv[(size_t)c] : (uint32_t)c;
-                        if (id < a) { b = a; a = id; } else if (id < b) b = id;
+                        if (id < a) { c3 = b; b = a; a = id; } else if (id < b) { c3 = b; b = id; } else if (id < c3) c3 = id;
                     }
-                    kv[q - q0] = {((uint64_t)a << 32) | b, r};
+                    kv[q - q0] = {((uint64_t)a << 32) | b, lex >= 3 ? c3 : 0u, r};
                 }
                 std::sort(kv.begin(), kv.end());
-                for (size_t q = q0; q < q1; ++q) (*v)[q] = kv[q - q0].second;
+                for (size_t q = q0; q < q1; ++q) (*v)[q] = std::get<2>(kv[q - q0]);
             });
         }
     }
