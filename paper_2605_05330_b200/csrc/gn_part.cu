@@ -78,39 +78,19 @@ struct gn_part {
     int32_t* pc_order = nullptr;  // pieces by their first column, per range (GN_PIECE_SORT)
     int piece_blocked = 0;
     int interleave = 1;           // GN_PART_INTERLEAVE=0: long-row blocks first
+    // chunk mode (default; GN_PART_CHUNK=len, 0 = off): the long rows' pieces (chunks) summed one
+    // thread per chunk over a blocked SELL of chunks -- 32 chunks per slice,
+    // sorted by (length, first column) -- instead of one warp per piece; the
+    // chunk sums go to their pc_sum slots (cslot), combined as pieces
+    int chunk = 0;
+    int32_t* csell = nullptr;
+    int64_t* cslice_ptr = nullptr;
+    int32_t* cslot = nullptr;
+    int64_t cg0[2] = {0, 0}, ncg[2] = {0, 0};
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
     int r_ncomb[2] = {0, 0};                 // per range: combine blocks
-    // band mode (fast, default): a piece is the run of a long row's sorted
-    // neighbour list inside one column band (kBandBytes of published values,
-    // at most kUnitMax entries).  Per range the pieces are grouped by band,
-    // longest first, and cut into units of at most kUnitMax index entries:
-    // a unit's index stream holds its warp pieces (>= 32 entries, one after
-    // the other) and then its short pieces in groups of 32, position-major
-    // (lane l's k-th entry at 32 k + l), 16-bit offsets inside the band.
-    // k_part_band runs persistent CTAs over contiguous unit ranges: the band
-    // is staged in shared memory by a TMA bulk copy when it changes, the next
-    // unit's index stream is prefetched by TMA while the current one is
-    // summed; each piece's sum goes to psum in stream order, and
-    // k_part_long_combine (a warp per row) adds a row's pieces in band order
-    // through lpidx.
-    int band = 1;                            // 0: pieces of kPiece entries (GN_PART_BAND=0)
-    int band_w = 0;                          // vertices per band
-    int band_ctas = 0;                       // persistent CTAs per range launch
-    uint16_t* bstream = nullptr;             // all units' index streams
-    int4* unit_a = nullptr;                  // {band, first warp piece, warp pieces, first group}
-    int4* unit_b = nullptr;                  // {groups, stream offset, stream entries, 0}
-    int32_t* wp_off = nullptr;               // warp piece: offset in its unit's stream
-    int32_t* wp_len = nullptr;
-    int32_t* g_off = nullptr;                // group: offset in its unit's stream
-    int32_t* g_lmax = nullptr;               // group: longest piece (= its rows in the stream)
-    int32_t* g_len = nullptr;                // [groups * 32] piece lengths (0: empty slot)
-    int32_t* wp_dst = nullptr;               // warp piece -> row-major piece id (its psum slot)
-    int32_t* g_dst = nullptr;                // [groups * 32] short piece -> row-major piece id
-    int32_t* cta_u = nullptr;                // [ranges][band_ctas + 1] unit ranges
-    int64_t nwp_all = 0;                     // warp pieces (psum slots [0, nwp_all)), then 32 per group
-    int64_t u0[2] = {0, 0}, nu[2] = {0, 0};
     double* part_long[2] = {nullptr, nullptr};  // per range [iters][r_ncomb][4]
     // per range (0 boundary, 1 interior), set by gn_part_begin
     int64_t r_start[2] = {0, 0}, r_count[2] = {0, 0}, r_long[2] = {0, 0}, r_csr[2] = {0, 0};
@@ -188,7 +168,8 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
     if (i < n_own) x[i] = xi;
 }
 
-constexpr int kPartLongDegreeMin = 512, kPartLongDegreeMax = 4096;
+constexpr int kPartLongDegreeDefault = 1024;
+constexpr int kChunkDefault = 128;  // long-row chunk length (thread per chunk; 0: warp pieces)
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
 // The long rows' pieces (fast mode; see gn_part::pc_beg)
@@ -200,6 +181,10 @@ struct PartLong {
     const int32_t* __restrict__ order;  // processing position -> piece (null: piece order)
     int blocked;                        // 1: each warp takes one contiguous run of positions
     int interleave;                     // 1: long-row blocks spread among the slice blocks
+    const int32_t* __restrict__ csell;  // chunk mode: SELL of chunks (null: warp per piece)
+    const int64_t* __restrict__ cslice_ptr;
+    const int32_t* __restrict__ cslot;  // [ncg * 32] chunk -> its pc_sum slot (-1: empty lane)
+    int64_t ncg;
 };
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
@@ -390,7 +375,41 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
-    if (rb < nbl) {
+    if (rb < nbl && lng.csell) {
+        // long rows, chunk mode: one thread per chunk over the chunks' SELL
+        // (sequential in ascending new id), the sum to the chunk's slot
+        for (int64_t g = (int64_t)rb * kWarpsPerBlock + warp; g < lng.ncg; g += (int64_t)nbl * kWarpsPerBlock) {
+            const int64_t e0 = lng.cslice_ptr[g];
+            const int nblk = (int)((lng.cslice_ptr[g + 1] - e0) / 128);
+            const uint4* base = reinterpret_cast<const uint4*>(lng.csell + e0) + lane;
+            constexpr int NV = kPartUnroll / 4;
+            uint4 cv[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+            TS s = TS(0);
+            for (int b = 0; b < nblk; b += NV) {
+                uint4 nv[NV];
+#pragma unroll
+                for (int u = 0; u < NV; ++u)
+                    nv[u] = b + NV + u < nblk ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+                TG y[4 * NV];
+#pragma unroll
+                for (int u = 0; u < NV; ++u) {
+                    const bool in = b + u < nblk;
+                    y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
+                    y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
+                    y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
+                    y[4 * u + 3] = in ? ld_val(yg + cv[u].w) : TG(0);
+                }
+#pragma unroll
+                for (int q = 0; q < 4 * NV; ++q) s = A::add(s, (TS)y[q]);
+#pragma unroll
+                for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+            }
+            const int32_t slot = __ldg(lng.cslot + g * 32 + lane);
+            if (slot >= 0) lng.sum[slot] = (double)s;
+        }
+    } else if (rb < nbl) {
         // long rows, fast mode: one warp per piece of kPiece entries; lanes
         // stride the positions, 8 gathers in flight per lane with the next 8
         // indices loading under them; fixed butterfly fold.  The rows are
@@ -524,132 +543,12 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(const 
     part_step_vb<TS, TG>(a, (int)blockIdx.x, (int)threadIdx.x, red);
 }
 
-// ---- band mode (see gn_part::band): TMA bulk copies with mbarriers
-constexpr int kBandBytes = 65536;  // one band of published values: 8192 fp64 / 16384 fp32
-constexpr int kUnitMax = 8192;     // index entries per unit (16 KB of 16-bit offsets)
-constexpr int kBandThreads = 512;  // 2 CTAs per SM: 96 KB of shared memory each
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-// one thread: expect `bytes`, then the bulk copy global -> shared completes them
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-struct BandArgs {
-    const int4* unit_a;
-    const int4* unit_b;
-    const int32_t* cta_u;  // this range's [band_ctas + 1]
-    const uint16_t* bs;
-    const int32_t* wp_off;
-    const int32_t* wp_len;
-    const int32_t* g_off;
-    const int32_t* g_lmax;
-    const int32_t* g_len;
-    const int32_t* wp_dst;  // warp piece -> row-major piece id (its psum slot)
-    const int32_t* g_dst;   // [groups * 32] short piece -> row-major piece id
-    int64_t nall;
-    int W;
-    int64_t nwp_all;
-    double* psum;
-};
-
-template <typename TS, typename TG>
-__global__ void __launch_bounds__(kBandThreads, 2) k_part_band(BandArgs a, const TG* __restrict__ yg) {
-    using A = Arith<TS>;
-    extern __shared__ __align__(128) unsigned char band_smem[];
-    TG* sy = reinterpret_cast<TG*>(band_smem);                                 // kBandBytes
-    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem + kBandBytes);
-    const int j0 = __ldg(a.cta_u + blockIdx.x), j1 = __ldg(a.cta_u + blockIdx.x + 1);
-    if (j0 >= j1) return;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t ph = 0;
-    int cur_band = -1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int kWarps = kBandThreads / 32;
-    for (int j = j0; j < j1; ++j) {
-        const int4 ua = __ldg(a.unit_a + j);
-        if (ua.x != cur_band) {  // a new band: everyone is done with the old one, then one bulk copy
-            __syncthreads();
-            cur_band = ua.x;
-            if (threadIdx.x == 0) {
-                const int64_t base = (int64_t)ua.x * a.W;
-                const int64_t cnt = min((int64_t)a.W, a.nall - base);
-                const uint32_t bytes = (uint32_t)((cnt * (int64_t)sizeof(TG) + 15) & ~(int64_t)15);
-                tma_load_1d(sy, yg + base, bytes, bar);
-            }
-            mbar_wait(bar, ph);
-            ph ^= 1u;
-        }
-        const int4 ub = __ldg(a.unit_b + j);
-        const uint16_t* ix = a.bs + ub.y;
-        const int rot = j % kWarps;  // spread the units' first pieces over the warps
-        const int wv = (warp + kWarps - rot) % kWarps;
-        // warp pieces: lanes stride the entries, fixed butterfly fold
-        for (int q = ua.y + wv; q < ua.y + ua.z; q += kWarps) {
-            const int32_t o = __ldg(a.wp_off + q), n = __ldg(a.wp_len + q);
-            TS s = TS(0);
-            int32_t p = lane;
-            for (; p + 96 < n; p += 128) {
-                const uint16_t i0 = __ldg(ix + o + p), i1 = __ldg(ix + o + p + 32), i2 = __ldg(ix + o + p + 64),
-                               i3 = __ldg(ix + o + p + 96);
-                s = A::add(s, (TS)sy[i0]);
-                s = A::add(s, (TS)sy[i1]);
-                s = A::add(s, (TS)sy[i2]);
-                s = A::add(s, (TS)sy[i3]);
-            }
-            for (; p < n; p += 32) s = A::add(s, (TS)sy[__ldg(ix + o + p)]);
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
-            if (lane == 0) a.psum[__ldg(a.wp_dst + q)] = (double)s;
-        }
-        // short pieces: a warp per group of 32, a lane per piece, sequential
-        for (int g = ua.w + wv; g < ua.w + ub.x; g += kWarps) {
-            const int32_t o = __ldg(a.g_off + g), lm = __ldg(a.g_lmax + g);
-            const int32_t n = __ldg(a.g_len + (int64_t)g * 32 + lane);
-            const uint16_t* gx = ix + o + lane;
-            TS s = TS(0);
-            int32_t k = 0;
-            for (; k + 7 < lm; k += 8) {
-                uint16_t id[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) id[t] = __ldg(gx + 32 * (k + t));
-#pragma unroll
-                for (int t = 0; t < 8; ++t) s = A::add(s, (TS)(k + t < n ? sy[id[t]] : TG(0)));  // +0.0: bits unchanged
-            }
-            for (; k < lm; ++k) s = A::add(s, (TS)(k < n ? sy[__ldg(gx + 32 * k)] : TG(0)));
-            if (n > 0) a.psum[__ldg(a.g_dst + (int64_t)g * 32 + lane)] = (double)s;
-        }
-    }
-}
-
 // Long rows, fast mode: one warp per row adds its pieces' sums in piece order
-// (lanes stride the pieces, fixed butterfly fold; piece j's sum is
-// pc_sum[lpidx[j]], or pc_sum[j] without lpidx) and lane 0 updates the row
+// (lanes stride the pieces, fixed butterfly fold) and lane 0 updates the row
 // (dynamics.py:104-107); per-block stats as k_part_step.
 template <typename TS, typename TG>
 __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
-    int64_t n_long, int64_t first, const int32_t* __restrict__ lp, const int32_t* __restrict__ lpidx,
+    int64_t n_long, int64_t first, const int32_t* __restrict__ lp,
     const double* __restrict__ pc_sum, const double* __restrict__ w64, const TS* __restrict__ v,
     const TS* __restrict__ x, TS* __restrict__ xo, TG* __restrict__ ygo, const double* __restrict__ gam, int k,
     double* __restrict__ part) {
@@ -661,7 +560,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
     if (q < n_long) {
         const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
         TS s = TS(0);
-        for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[lpidx ? __ldg(lpidx + j) : j]);
+        for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[j]);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
         if (lane == 0) part_update<TS, TG>(first + q, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
@@ -860,19 +759,21 @@ static int upload_into(T** dst, const std::vector<T>& h) {
 // are relabeled to their position in this order and the device graph (CSR,
 // weights, blocked SELL) is rebuilt in the new numbering.
 static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
-    // rows above this degree are "long": split into pieces over warps in
-    // fast mode, one thread over the CSR in EXACT mode.  The others run one
-    // thread per row over the blocked SELL, which gathers more cheaply (a
-    // slice's rows, ordered by their hottest neighbours, share lines at the
-    // same positions) but as one serial chain per row; the threshold grows
-    // with the part so a row's chain stays well inside an iteration:
-    // nnz / 65536 rounded down to a power of two, in [512, 4096].  C5 scale
-    // 24, one part (520 M entries: 4096), fp64, ms per iteration: 512 1.62,
-    // 1024 1.50, 4096 1.44, 8192 1.47, 65536 5.96 (R-MAT degrees cluster
-    // near 2^28 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).
+    // rows above this degree are "long": in fast mode cut into chunks of
+    // GN_PART_CHUNK entries (default 128) summed one thread per chunk over a
+    // blocked SELL of chunks and combined per row (0: one warp per 512-entry
+    // piece); in EXACT mode one thread per row over the CSR.  The others run
+    // one thread per row over the blocked SELL.  Both thread-per-row walks
+    // gather more cheaply than warp-split pieces (a slice's rows or chunks,
+    // ordered by their hottest neighbours or first column, share lines at the
+    // same positions) but each is one serial chain; the threshold and the
+    // chunk length bound the chain.  C5 scale 24, one part, fp64, ms per
+    // iteration -- warp pieces: threshold 512 1.62, 1024 1.50, 4096 1.44,
+    // 8192 1.47, 65536 5.96; chunks of 128: threshold 1024 (= 2048) 1.335,
+    // 4096 1.374; chunks of 64 / 256: 1.348 / 1.365 (R-MAT degrees cluster
+    // near 2^29 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).
     // GN_PART_LONG overrides.
-    int kPartLongDegree = kPartLongDegreeMin;
-    while (kPartLongDegree < kPartLongDegreeMax && (int64_t)kPartLongDegree * 2 * 65536 <= P->nnz) kPartLongDegree *= 2;
+    int kPartLongDegree = kPartLongDegreeDefault;
     if (const char* e = getenv("GN_PART_LONG")) kPartLongDegree = std::max(32, atoi(e));
     P->long_degree = kPartLongDegree;
     const int64_t n_own = P->n_own, nall = P->n_own + P->n_ghost;
@@ -1037,18 +938,18 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     parallel_for(n_own, [&](int64_t r) { std::sort(ncol.begin() + nrp[(size_t)r], ncol.begin() + nrp[(size_t)r + 1]); });
     if ((rcode = upload_into(&P->col_fast, ncol)) || (rcode = upload_into(&P->sell_fast, fill_sell(ncol))))
         return rcode;
-    // the long rows' pieces (fast mode), per range: runs inside one column
-    // band of at most kUnitMax entries (band mode), or kPiece consecutive
-    // entries (GN_PART_BAND=0)
-    P->band = 0;  // measured slower than kPiece pieces on C5 (profiles/r02_c5s24_band_v3_ncu.json)
-    if (const char* e = getenv("GN_PART_BAND")) P->band = atoi(e) != 0;
-    const int W = kBandBytes / (int)gather_bytes(P->dtype);
-    P->band_w = W;
+    // the long rows' pieces (fast mode), per range: kPiece consecutive entries
     int64_t piece_len = kPiece;
     if (const char* e = getenv("GN_PIECE_LEN")) piece_len = std::max(32, atoi(e));
+    P->chunk = kChunkDefault;
+    if (const char* e = getenv("GN_PART_CHUNK")) P->chunk = std::max(0, atoi(e));
+    if (P->chunk > 0) {
+        P->chunk = std::max(32, P->chunk);
+        piece_len = P->chunk;
+    }
     P->interleave = 1;
     if (const char* e = getenv("GN_PART_INTERLEAVE")) P->interleave = atoi(e) != 0;
-    std::vector<int32_t> pb, pe, lp, pband;
+    std::vector<int32_t> pb, pe, lp;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
         P->lp0[r] = (int64_t)lp.size();
@@ -1058,15 +959,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             int64_t e = nrp[(size_t)row];
             const int64_t end = nrp[(size_t)row + 1];
             while (e < end) {
-                int64_t f;
-                if (P->band) {  // the run of this row's (ascending) neighbours in one band
-                    const int32_t bnd = ncol[(size_t)e] / W;
-                    f = e + 1;
-                    while (f < end && f - e < kUnitMax && ncol[(size_t)f] / W == bnd) ++f;
-                    pband.push_back(bnd);
-                } else {
-                    f = std::min<int64_t>(e + piece_len, end);
-                }
+                const int64_t f = std::min<int64_t>(e + piece_len, end);
                 pb.push_back((int32_t)e);
                 pe.push_back((int32_t)f);
                 e = f;
@@ -1089,7 +982,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         // default 2 (C5 scale 24 fp64: 1.737 -> 1.698 ms per iteration; with 512-entry pieces 1.677)
         const char* e = getenv("GN_PIECE_SORT");
         const int mode = e ? atoi(e) : 2;
-        if (mode > 0 && !P->band) {
+        if (mode > 0) {
             std::vector<int32_t> ord(pb.size());
             for (int r = 0; r < 2; ++r) {
                 const int64_t a0 = P->pc0[r], a1 = a0 + P->npc[r];
@@ -1102,140 +995,58 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             P->piece_blocked = mode >= 2;
         }
     }
-    if (P->band) {
-        // per range: pieces grouped by band (counting sort, stable), longest
-        // first; units of <= kUnitMax stream entries: warp pieces (>= 32
-        // entries) one after the other, then the short ones in groups of 32
-        // stored position-major (group size = its first, longest piece)
-        const int nbands = (int)(nall / W + 1);
-        int dev_sms = 148;
-        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, P->device);
-        P->band_ctas = 2 * dev_sms;
-        struct Unit {
-            int band;
-            std::vector<int32_t> warp, shrt;
-        };
-        std::vector<Unit> all_units;
-        auto len = [&](int32_t j) { return pe[(size_t)j] - pb[(size_t)j]; };
+    cudaFree(P->csell);
+    cudaFree(P->cslice_ptr);
+    cudaFree(P->cslot);
+    P->csell = nullptr;
+    P->cslice_ptr = nullptr;
+    P->cslot = nullptr;
+    if (P->chunk > 0) {
+        // per range: chunks sorted by (length desc, first column), 32 per
+        // slice; slice g's block b holds, lane after lane, entries 4b..4b+3
+        // of each lane's chunk (padding: the zero-valued slot nall)
+        std::vector<int64_t> csp(1, 0);
+        std::vector<int32_t> cslot;
+        std::vector<std::pair<int64_t, int32_t>> gfirst;  // per slice: (first chunk position, range)
+        std::vector<int32_t> corder;
         for (int r = 0; r < 2; ++r) {
-            P->u0[r] = (int64_t)all_units.size();
+            P->cg0[r] = (int64_t)csp.size() - 1;
             const int64_t a0 = P->pc0[r], a1 = a0 + P->npc[r];
-            std::vector<int64_t> cnt((size_t)nbands + 1, 0);
-            for (int64_t j = a0; j < a1; ++j) cnt[(size_t)pband[(size_t)j] + 1]++;
-            for (int t = 0; t < nbands; ++t) cnt[(size_t)t + 1] += cnt[(size_t)t];
-            std::vector<int32_t> by((size_t)(a1 - a0));
-            {
-                std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-                for (int64_t j = a0; j < a1; ++j) by[(size_t)fill[(size_t)pband[(size_t)j]]++] = (int32_t)j;
+            std::vector<int32_t> ord;
+            for (int64_t j = a0; j < a1; ++j) ord.push_back((int32_t)(j - a0));
+            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                const int32_t lx = pe[(size_t)(a0 + x)] - pb[(size_t)(a0 + x)], ly = pe[(size_t)(a0 + y)] - pb[(size_t)(a0 + y)];
+                if (lx != ly) return lx > ly;
+                return ncol[(size_t)pb[(size_t)(a0 + x)]] < ncol[(size_t)pb[(size_t)(a0 + y)]];
+            });
+            for (size_t g = 0; g < ord.size(); g += 32) {
+                int32_t len = 0;
+                for (size_t l = g; l < std::min(ord.size(), g + 32); ++l)
+                    len = std::max(len, pe[(size_t)(a0 + ord[l])] - pb[(size_t)(a0 + ord[l])]);
+                for (size_t l = g; l < g + 32; ++l) cslot.push_back(l < ord.size() ? ord[l] : -1);
+                csp.push_back(csp.back() + (int64_t)(len + 3) / 4 * 128);
             }
-            for (int t = 0; t < nbands; ++t) {
-                auto lo = by.begin() + cnt[(size_t)t], hi = by.begin() + cnt[(size_t)t + 1];
-                if (lo == hi) continue;
-                std::stable_sort(lo, hi, [&](int32_t x, int32_t y) { return len(x) > len(y); });
-                Unit u{t, {}, {}};
-                int64_t cost = 0;
-                for (auto it = lo; it != hi;) {
-                    const int32_t l = len(*it);
-                    // a short piece that opens a group of 32 reserves the group (its length, longest first)
-                    const int64_t add = l >= 32 ? l : (u.shrt.size() % 32 == 0 ? 32 * (int64_t)l : 0);
-                    if (cost + add > kUnitMax && (!u.warp.empty() || !u.shrt.empty())) {
-                        all_units.push_back(std::move(u));
-                        u = Unit{t, {}, {}};
-                        cost = 0;
-                        continue;  // the same piece opens the next unit
-                    }
-                    cost += add;
-                    (l >= 32 ? u.warp : u.shrt).push_back(*it);
-                    ++it;
-                }
-                if (!u.warp.empty() || !u.shrt.empty()) all_units.push_back(std::move(u));
-            }
-            P->nu[r] = (int64_t)all_units.size() - P->u0[r];
+            P->ncg[r] = (int64_t)csp.size() - 1 - P->cg0[r];
+            for (int32_t o : ord) corder.push_back((int32_t)(a0 + o));
         }
-        // descriptors; every piece writes its sum to pc_sum[its row-major id]
-        int64_t nwp = 0, ng = 0;
-        for (const Unit& u : all_units) {
-            nwp += (int64_t)u.warp.size();
-            ng += ((int64_t)u.shrt.size() + 31) / 32;
-        }
-        P->nwp_all = nwp;
-        std::vector<int4> ua, ub;
-        std::vector<int32_t> wpo, wpl, go, glm, gl, cta_u, wdst, gdst;
-        std::vector<int64_t> ustart;
-        int64_t stream_len = 0, wq = 0, gq = 0;
-        for (const Unit& u : all_units) {
-            int64_t off = 0;
-            const int32_t wp_first = (int32_t)wq, g_first = (int32_t)gq;
-            for (int32_t j : u.warp) {
-                wpo.push_back((int32_t)off);
-                wpl.push_back(len(j));
-                wdst.push_back(j);
-                ++wq;
-                off += len(j);
-            }
-            for (size_t g0 = 0; g0 < u.shrt.size(); g0 += 32) {
-                const int32_t lmax = len(u.shrt[g0]);
-                go.push_back((int32_t)off);
-                glm.push_back(lmax);
-                for (size_t l = 0; l < 32; ++l) {
-                    if (g0 + l < u.shrt.size()) {
-                        const int32_t j = u.shrt[g0 + l];
-                        gl.push_back(len(j));
-                        gdst.push_back(j);
-                    } else {
-                        gl.push_back(0);
-                        gdst.push_back(0);
-                    }
+        std::vector<int32_t> cs((size_t)std::max<int64_t>(csp.back(), 1), (int32_t)nall);
+        const int64_t ngs = (int64_t)csp.size() - 1;
+        parallel_for(ngs, [&](int64_t g) {
+            const int r = g >= P->cg0[1] ? 1 : 0;
+            const int64_t a0 = P->pc0[r];
+            for (int l = 0; l < 32; ++l) {
+                const int32_t sl = cslot[(size_t)(g * 32 + l)];
+                if (sl < 0) continue;
+                const int32_t e0 = pb[(size_t)(a0 + sl)], e1 = pe[(size_t)(a0 + sl)];
+                for (int32_t e = e0; e < e1; ++e) {
+                    const int32_t pos = e - e0;
+                    cs[(size_t)(csp[(size_t)g] + (pos / 4) * 128 + l * 4 + pos % 4)] = ncol[(size_t)e];
                 }
-                ++gq;
-                off += 32 * (int64_t)lmax;
-            }
-            const int64_t padded = (off + 7) / 8 * 8;  // bulk copies move multiples of 16 bytes
-            ua.push_back(make_int4(u.band, wp_first, (int32_t)u.warp.size(), g_first));
-            ub.push_back(make_int4((int32_t)(gq - g_first), (int32_t)stream_len, (int32_t)padded, 0));
-            ustart.push_back(stream_len);
-            stream_len += padded;
-        }
-        // the stream: 16-bit offsets in the band, each unit written in parallel
-        std::vector<uint16_t> bs((size_t)std::max<int64_t>(stream_len, 8), 0);
-        parallel_for((int64_t)all_units.size(), [&](int64_t ui) {
-            const Unit& u = all_units[(size_t)ui];
-            const int64_t base = (int64_t)u.band * W;
-            uint16_t* dst = bs.data() + ustart[(size_t)ui];
-            for (int32_t j : u.warp)
-                for (int32_t e = pb[(size_t)j]; e < pe[(size_t)j]; ++e) *dst++ = (uint16_t)(ncol[(size_t)e] - base);
-            for (size_t g0 = 0; g0 < u.shrt.size(); g0 += 32) {
-                const int32_t lmax = len(u.shrt[g0]);
-                for (size_t l = 0; l < 32 && g0 + l < u.shrt.size(); ++l) {
-                    const int32_t j = u.shrt[g0 + l];
-                    for (int32_t e = pb[(size_t)j]; e < pe[(size_t)j]; ++e)
-                        dst[(size_t)(e - pb[(size_t)j]) * 32 + l] = (uint16_t)(ncol[(size_t)e] - base);
-                }
-                dst += (size_t)lmax * 32;
             }
         });
-        // persistent CTAs: contiguous unit ranges of about equal stream length, per range
-        for (int r = 0; r < 2; ++r) {
-            const int64_t a0 = P->u0[r], a1 = a0 + P->nu[r];
-            int64_t tot = 0;
-            for (int64_t u = a0; u < a1; ++u) tot += ub[(size_t)u].z;
-            int64_t acc = 0, u = a0;
-            cta_u.push_back((int32_t)a0);
-            for (int c = 1; c < P->band_ctas; ++c) {
-                const int64_t target = tot * c / P->band_ctas;
-                while (u < a1 && acc + ub[(size_t)u].z / 2 < target) acc += ub[(size_t)u++].z;
-                cta_u.push_back((int32_t)u);
-            }
-            cta_u.push_back((int32_t)a1);
-        }
-        int rc2;
-        if ((rc2 = upload_into(&P->bstream, bs)) || (rc2 = upload_into(&P->unit_a, ua)) ||
-            (rc2 = upload_into(&P->unit_b, ub)) || (rc2 = upload_into(&P->wp_off, wpo)) ||
-            (rc2 = upload_into(&P->wp_len, wpl)) || (rc2 = upload_into(&P->g_off, go)) ||
-            (rc2 = upload_into(&P->g_lmax, glm)) || (rc2 = upload_into(&P->g_len, gl)) ||
-            (rc2 = upload_into(&P->wp_dst, wdst)) || (rc2 = upload_into(&P->g_dst, gdst)) ||
-            (rc2 = upload_into(&P->cta_u, cta_u)))
-            return rc2;
+        if ((rcode = upload_into(&P->csell, cs)) || (rcode = upload_into(&P->cslice_ptr, csp)) ||
+            (rcode = upload_into(&P->cslot, cslot)))
+            return rcode;
     }
     cudaFree(P->pc_sum);
     P->pc_sum = nullptr;
@@ -1301,25 +1112,16 @@ template <typename TS, typename TG>
 static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
     k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
-        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], nullptr, p->pc_sum, p->w64,
+        p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->pc_sum, p->w64,
         (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
 }
 
 static PartLong part_long_of(gn_part* p, int r) {
     return PartLong{p->pc_beg + p->pc0[r], p->pc_end + p->pc0[r], p->pc_sum + p->pc0[r],
-                    p->r_long[r] && !p->band ? p->npc[r] : 0, p->pc_order ? p->pc_order + p->pc0[r] : nullptr,
-                    p->piece_blocked, p->interleave};
-}
-
-constexpr int kBandSmem = kBandBytes + 64;
-
-template <typename TS, typename TG>
-static void launch_band(gn_part* p, int r, int k, cudaStream_t s) {
-    const int cur = k & 1;
-    BandArgs a{p->unit_a, p->unit_b, p->cta_u + (size_t)r * (p->band_ctas + 1), p->bstream, p->wp_off, p->wp_len,
-               p->g_off, p->g_lmax, p->g_len, p->wp_dst, p->g_dst, p->n_own + p->n_ghost, p->band_w, p->nwp_all,
-               p->pc_sum};
-    k_part_band<TS, TG><<<p->band_ctas, kBandThreads, kBandSmem, s>>>(a, (const TG*)p->yg[cur]);
+                    p->r_long[r] ? p->npc[r] : 0, p->pc_order ? p->pc_order + p->pc0[r] : nullptr,
+                    p->piece_blocked, p->interleave, p->chunk ? p->csell : nullptr,
+                    p->chunk ? p->cslice_ptr + p->cg0[r] : nullptr, p->chunk ? p->cslot + 32 * p->cg0[r] : nullptr,
+                    p->chunk ? p->ncg[r] : 0};
 }
 
 }  // namespace gn
@@ -1364,9 +1166,6 @@ int gn_part_create(int64_t n_own, int64_t n_ghost, const int64_t* indptr, const 
         return rc;
     }
     GN_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
-    GN_CUDA(cudaFuncSetAttribute(k_part_band<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmem));
     *out = P;
     return GN_OK;
 }
@@ -1384,12 +1183,11 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_beg);
     cudaFree(p->pc_end);
     cudaFree(p->pc_order);
+    cudaFree(p->csell);
+    cudaFree(p->cslice_ptr);
+    cudaFree(p->cslot);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
-    cudaFree(p->bstream);
-    for (void* q : {(void*)p->unit_a, (void*)p->unit_b, (void*)p->wp_off, (void*)p->wp_len, (void*)p->g_off,
-                    (void*)p->g_lmax, (void*)p->g_len, (void*)p->wp_dst, (void*)p->g_dst, (void*)p->cta_u})
-        cudaFree(q);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -1426,9 +1224,9 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_start[r] = r ? p->n_bnd : 0;
         p->r_count[r] = r ? p->n_own - p->n_bnd : p->n_bnd;
         p->r_long[r] = (flags & GN_EXACT) ? 0 : p->long_fast[r];
-        // band mode: the long rows' pieces run in k_part_band, not in k_part_step
-        p->r_nbl[r] = p->r_long[r] && !p->band
-                          ? (int)std::min<int64_t>((p->npc[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12)
+        const int64_t lunits = p->chunk ? p->ncg[r] : p->npc[r];  // chunk slices or pieces, one per warp
+        p->r_nbl[r] = p->r_long[r]
+                          ? (int)std::min<int64_t>((lunits + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12)
                           : 0;
         p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32)) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
@@ -1515,10 +1313,6 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
                         (int)std::min<int64_t>((p->n_push + 8 * kPartThreads - 1) / (8 * kPartThreads), 148)};
     const int nb = (p->r_count[r] ? p->r_nblocks[r] : 0) + push.nblocks;
     const PartLong lng = part_long_of(p, r);
-    if (p->band && p->r_long[r] > 0 && p->nu[r] > 0) {  // the long rows' band pieces
-        by_dtype(p->dtype, [&](auto ts, auto tg) { launch_band<decltype(ts), decltype(tg)>(p, r, k, s); });
-        GN_LAUNCHED();
-    }
     // fast mode, iteration >= 3: the settled isolated tail is skipped
     const int64_t nsl = (r == 1 && k >= 3 && p->iso_nsl >= 0 && !(p->flags & GN_EXACT)) ? p->iso_nsl : p->nsl[r];
     by_dtype(p->dtype, [&](auto ts, auto tg) {
@@ -1942,8 +1736,6 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
             const int64_t nlong_arg = mode == 2 ? pos0 : p->r_long[r];
             const PartLong lng = mode == 2 ? PartLong{nullptr, nullptr, nullptr, 0, nullptr, 0, 0} : part_long_of(p, r);
             by_dtype(p->dtype, [&](auto ts, auto tg) {
-                if (mode != 2 && p->band && p->r_long[r] > 0 && p->nu[r] > 0)
-                    launch_band<decltype(ts), decltype(tg)>(p, r, 0, s);
                 if (mode != 1 || nbl > 0)
                     launch_step<decltype(ts), decltype(tg)>(p, r, 0, nb, nlong_arg, nbl, ncsr, ncb, nsl, none, lng, s);
                 if (mode != 2 && p->r_long[r] > 0) launch_combine<decltype(ts), decltype(tg)>(p, r, 0, s);

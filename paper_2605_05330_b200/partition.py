@@ -1,10 +1,12 @@
 """Vertex-range partitioning of one graph over several GPUs.
 
 Each partition owns a contiguous range of vertices, chosen so every part
-holds about the same number of adjacency entries (R-MAT concentrates its hubs
-at low ids, so equal vertex counts would be badly imbalanced).  A part's
-neighbours outside its range are its ghosts, sorted by global id -- which
-groups them by owning peer, since ranges are contiguous.  Every iteration:
+has about the same step cost (adjacency entries plus a per-row term; R-MAT
+concentrates its hubs at low ids, so equal vertex counts would be badly
+imbalanced).  A part's neighbours outside its range are its ghosts, grouped
+by owning peer and, inside a peer's group, hubs first (global degree
+descending, then global id) -- the gathers of hot ghosts then share lines as
+the owned hubs' do.  Every iteration:
 
     step     each part updates its owned rows (csrc/gn_part.cu), reading the
              published values of owned vertices and ghosts
@@ -43,7 +45,7 @@ class PartSpec:
     parts: int
     lo: int
     hi: int
-    ghosts: np.ndarray        # global ids, ascending
+    ghosts: np.ndarray        # global ids: grouped by owner, then global degree descending, then id
     ghost_ptr: np.ndarray     # [parts+1]: ghosts owned by peer q are ghosts[ghost_ptr[q]:ghost_ptr[q+1]]
     indptr: np.ndarray        # owned rows, local column ids
     indices: np.ndarray       # int32 in [0, n_own + n_ghost)
@@ -62,13 +64,26 @@ class PartSpec:
         return np.concatenate([x0_global[self.lo:self.hi], x0_global[self.ghosts]]).astype(np.float64)
 
 
+ROW_COST = 6  # adjacency entries one non-isolated row's update costs (state in, x' and y' out)
+
+
+def vertex_cost(indptr: np.ndarray) -> np.ndarray:
+    """Per-vertex step cost in adjacency-entry units: its entries, plus
+    ROW_COST for a row with neighbours (the update's state traffic), plus 1.
+    Fitted to one-GPU timings of the parts of C5 at scale 24 (2/4/8 parts,
+    tools/probe_scaling.py): time ~ entries + ~4 per owned row, isolated rows
+    being skipped after their third iteration."""
+    deg = np.diff(np.asarray(indptr, dtype=np.int64))
+    return deg + 1 + ROW_COST * (deg > 0)
+
+
 def partition_ranges(indptr: np.ndarray, parts: int) -> np.ndarray:
-    """Contiguous vertex ranges with about equal adjacency entries (+1 per
-    vertex so empty rows still count): [parts+1] boundaries."""
+    """Contiguous vertex ranges with about equal step cost (vertex_cost:
+    adjacency entries plus a per-row term): [parts+1] boundaries."""
     n = len(indptr) - 1
     if parts < 1:
         raise ValueError("parts must be positive")
-    cost = np.diff(np.asarray(indptr, dtype=np.int64)) + 1
+    cost = vertex_cost(indptr)
     cum = np.concatenate([[0], np.cumsum(cost)])
     targets = cum[-1] * np.arange(1, parts) / parts
     cuts = np.searchsorted(cum, targets, side="left")
@@ -81,20 +96,27 @@ def build_partition(g, parts: int, p: int, bounds: Optional[np.ndarray] = None) 
     setup, once per rank): O(nnz of the part), whatever the part count.
 
     The graph is symmetric (graph.py:112-119), so the owned vertices peer q
-    holds as ghosts are exactly the owned rows with a neighbour in q's range;
-    q's ghost list is ascending in global id, hence so is p's send list to q
-    (p's ids are a contiguous range), and no rank needs another's rows."""
+    holds as ghosts are exactly the owned rows with a neighbour in q's range.
+    q orders the ghosts p owns by (global degree descending, global id); p
+    knows its own rows' degrees, so it orders its send list to q the same
+    way, and no rank needs another's rows."""
     indptr = np.asarray(g.indptr)
     bounds = partition_ranges(indptr, parts) if bounds is None else np.asarray(bounds, dtype=np.int64)
     lo, hi = int(bounds[p]), int(bounds[p + 1])
     e0, e1 = int(indptr[lo]), int(indptr[hi])
     cols = np.asarray(g.indices[e0:e1]).astype(np.int64, copy=False)
     outside = (cols < lo) | (cols >= hi)
-    ghosts = np.unique(cols[outside])
-    owner = np.searchsorted(bounds, ghosts, side="right") - 1
+    uniq = np.unique(cols[outside])                      # ascending global id
+    owner_u = np.searchsorted(bounds, uniq, side="right") - 1
+    gdeg = (np.asarray(indptr[uniq + 1], dtype=np.int64) - np.asarray(indptr[uniq], dtype=np.int64))
+    order = np.lexsort((uniq, -gdeg, owner_u))           # by owner, hubs first, then id
+    ghosts = uniq[order]
+    owner = owner_u[order]
+    slot = np.empty(len(uniq), dtype=np.int64)
+    slot[order] = np.arange(len(uniq), dtype=np.int64)
     ghost_ptr = np.searchsorted(owner, np.arange(parts + 1), side="left").astype(np.int64)
     local = cols - lo
-    local[outside] = (hi - lo) + np.searchsorted(ghosts, cols[outside])
+    local[outside] = (hi - lo) + slot[np.searchsorted(uniq, cols[outside])]
     w = np.asarray(g.w, dtype=np.float64)
     row_ptr = (np.asarray(indptr[lo:hi + 1], dtype=np.int64) - e0)
     spec = PartSpec(p, parts, lo, hi, ghosts, ghost_ptr, row_ptr, local.astype(np.int32),
@@ -104,8 +126,10 @@ def build_partition(g, parts: int, p: int, bounds: Optional[np.ndarray] = None) 
         peer = np.searchsorted(bounds, cols[outside], side="right") - 1
         key = np.unique(peer * (hi - lo + 1) + rows)          # (peer, row), ascending row per peer
         kp, kr = key // (hi - lo + 1), key % (hi - lo + 1)
+        rdeg = np.diff(row_ptr)
         for q in np.unique(kp).tolist():
-            spec.send_idx[int(q)] = kr[kp == q].astype(np.int32)
+            r_q = kr[kp == q]
+            spec.send_idx[int(q)] = r_q[np.lexsort((r_q, -rdeg[r_q]))].astype(np.int32)  # q's ghost order
     return spec
 
 

@@ -101,3 +101,26 @@ def test_one_part_device_schedule_equals_host_loop():
     ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma, dtype="fp32")
     assert np.max(np.abs(c.x - ref.x)) <= 1e-4
     be.close()
+
+
+@pytest.mark.parametrize("env", [{"GN_PART_LONG": "64", "GN_PART_CHUNK": "0"}, {"GN_PART_LONG": "64"},
+                                 {"GN_PART_LONG": "256", "GN_PART_CHUNK": "96"}, {"GN_PART_LEX": "0"},
+                                 {"GN_PART_LEX": "3"}])
+@pytest.mark.parametrize("parts", [1, 3])
+def test_partition_layout_options(env, parts, monkeypatch):
+    """The numbering and long-row layouts (the degree threshold of the long
+    rows, their chunks or warp pieces, the equal-degree ordering): fast mode
+    within 1e-9 of the oracle with identical fallbacks and deterministic;
+    EXACT bitwise (layouts never change its reference-order sums)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inst = G.c5_rmat(14)
+    s = P.GammaSchedule.pursuit(iterations=200)
+    ref = O.run(inst.graph, inst.x0, s.table(), s.final_gamma)
+    out = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"), halo="peer")
+    np.testing.assert_allclose(out["x"], ref.x, rtol=1e-9, atol=1e-250)
+    np.testing.assert_array_equal(out["fallbacks"], ref.fallbacks)
+    again = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"), halo="peer")
+    np.testing.assert_array_equal(again["x"], out["x"])
+    ex = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64", exact=True))
+    np.testing.assert_array_equal(ex["x"], ref.x)
