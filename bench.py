@@ -198,6 +198,9 @@ def flush_l2(torch, dev):
 
 # ---------------------------------------------------------------- CPU arms
 
+_CPU_WARM: set = set()
+
+
 def cpu_port(inst, seconds: float, threads: int) -> dict:
     """The oracle port (oracle/gn_oracle.c: the reference's fp64 arithmetic,
     bitwise; rows in fixed 4096-row chunks over `threads` OpenMP threads) on
@@ -206,10 +209,14 @@ def cpu_port(inst, seconds: float, threads: int) -> dict:
     from paper_2605_05330_b200 import GammaSchedule
 
     tab = GammaSchedule.pursuit().table()
+    key = (id(inst), threads)
+    if key not in _CPU_WARM:  # first touch of the graph's pages and the threads: not timed
+        O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)
+        _CPU_WARM.add(key)
     t0 = time.perf_counter()
-    O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)  # also warms pages and threads
+    O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)
     dt, k = time.perf_counter() - t0, 1
-    if dt < seconds / 3:  # room for a real sample: calibrate on 3 steps, then time k
+    if dt < seconds / 3:  # room for a longer sample: calibrate on 3 steps, then time k
         t0 = time.perf_counter()
         O.run(inst.graph, inst.x0, tab[:3], 1.5, threads=threads)
         per = max((time.perf_counter() - t0) / 4, 1e-6)  # 3 steps + the x0 check's SpMV
