@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--dtype", default="fp64")
     ap.add_argument("--gpus", default="1,2,4,8")
+    ap.add_argument("--parts", default=None, help="only these part indices (e.g. for an ncu launch list)")
     args = ap.parse_args()
     import torch
 
@@ -53,6 +54,8 @@ def main():
     for n in [int(v) for v in args.gpus.split(",")]:
         parts = []
         for p in range(n):
+            if args.parts is not None and p not in [int(v) for v in args.parts.split(",")]:
+                continue
             t0 = time.perf_counter()
             spec = build_partition(g, n, p)
             be = EngineBackend(spec, dtype=args.dtype)
