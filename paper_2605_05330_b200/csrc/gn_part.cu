@@ -82,10 +82,18 @@ struct gn_part {
     // thread per chunk over a blocked SELL of chunks -- 32 chunks per slice,
     // sorted by (length, first column) -- instead of one warp per piece; the
     // chunk sums go to their pc_sum slots (cslot), combined as pieces
+    // Chunks whose consecutive ids differ by < 65536 are stored as 16-bit
+    // deltas (8 per lane per 16-byte vector, the lane's first id in cbase,
+    // its length in clen), the others as int32 ids (4 per vector, padded
+    // with the zero-valued slot nall); cfmt marks each slice (GN_PART_DELTA=0:
+    // all int32)
     int chunk = 0;
-    int32_t* csell = nullptr;
+    int32_t* csell = nullptr;        // slices' vectors (uint4), offsets in cslice_ptr (in vectors)
     int64_t* cslice_ptr = nullptr;
     int32_t* cslot = nullptr;
+    int8_t* cfmt = nullptr;          // per slice: 1 = 16-bit deltas
+    int32_t* cbase = nullptr;        // [slices * 32] first id of the lane's chunk
+    int32_t* clen = nullptr;         // [slices * 32] its length
     int64_t cg0[2] = {0, 0}, ncg[2] = {0, 0};
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
@@ -182,8 +190,11 @@ struct PartLong {
     int blocked;                        // 1: each warp takes one contiguous run of positions
     int interleave;                     // 1: long-row blocks spread among the slice blocks
     const int32_t* __restrict__ csell;  // chunk mode: SELL of chunks (null: warp per piece)
-    const int64_t* __restrict__ cslice_ptr;
+    const int64_t* __restrict__ cslice_ptr;  // per slice: first vector (uint4 units)
     const int32_t* __restrict__ cslot;  // [ncg * 32] chunk -> its pc_sum slot (-1: empty lane)
+    const int8_t* __restrict__ cfmt;    // per slice: 1 = 16-bit deltas
+    const int32_t* __restrict__ cbase;  // [ncg * 32] first id (delta slices)
+    const int32_t* __restrict__ clen;   // [ncg * 32] chunk length (delta slices)
     int64_t ncg;
 };
 #ifndef GN_PART_UNROLL
@@ -379,32 +390,54 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
         // long rows, chunk mode: one thread per chunk over the chunks' SELL
         // (sequential in ascending new id), the sum to the chunk's slot
         for (int64_t g = (int64_t)rb * kWarpsPerBlock + warp; g < lng.ncg; g += (int64_t)nbl * kWarpsPerBlock) {
-            const int64_t e0 = lng.cslice_ptr[g];
-            const int nblk = (int)((lng.cslice_ptr[g + 1] - e0) / 128);
-            const uint4* base = reinterpret_cast<const uint4*>(lng.csell + e0) + lane;
-            constexpr int NV = kPartUnroll / 4;
-            uint4 cv[NV];
-#pragma unroll
-            for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+            const int64_t v0 = lng.cslice_ptr[g];
+            const int nblk = (int)((lng.cslice_ptr[g + 1] - v0) / 32);
+            const uint4* base = reinterpret_cast<const uint4*>(lng.csell) + v0 + lane;
             TS s = TS(0);
-            for (int b = 0; b < nblk; b += NV) {
-                uint4 nv[NV];
+            if (lng.cfmt[g]) {
+                // 16-bit deltas: 8 entries per vector; the running id starts at
+                // the chunk's first id (its first delta is 0); entries past the
+                // chunk's length add nothing
+                int32_t id = __ldg(lng.cbase + g * 32 + lane);
+                const int len = __ldg(lng.clen + g * 32 + lane);
+                uint4 cv = nblk > 0 ? ld_idx4(base) : make_uint4(0, 0, 0, 0);
+                for (int b = 0; b < nblk; ++b) {
+                    const uint4 nv = b + 1 < nblk ? ld_idx4(base + (size_t)(b + 1) * 32) : make_uint4(0, 0, 0, 0);
+                    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+                    TG y[8];
 #pragma unroll
-                for (int u = 0; u < NV; ++u)
-                    nv[u] = b + NV + u < nblk ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
-                TG y[4 * NV];
+                    for (int j = 0; j < 8; ++j) {
+                        id += (int32_t)((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+                        y[j] = 8 * b + j < len ? ld_val(yg + id) : TG(0);
+                    }
 #pragma unroll
-                for (int u = 0; u < NV; ++u) {
-                    const bool in = b + u < nblk;
-                    y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
-                    y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
-                    y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
-                    y[4 * u + 3] = in ? ld_val(yg + cv[u].w) : TG(0);
+                    for (int j = 0; j < 8; ++j) s = A::add(s, (TS)y[j]);
+                    cv = nv;
                 }
+            } else {
+                constexpr int NV = kPartUnroll / 4;
+                uint4 cv[NV];
 #pragma unroll
-                for (int q = 0; q < 4 * NV; ++q) s = A::add(s, (TS)y[q]);
+                for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+                for (int b = 0; b < nblk; b += NV) {
+                    uint4 nv[NV];
 #pragma unroll
-                for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+                    for (int u = 0; u < NV; ++u)
+                        nv[u] = b + NV + u < nblk ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+                    TG y[4 * NV];
+#pragma unroll
+                    for (int u = 0; u < NV; ++u) {
+                        const bool in = b + u < nblk;
+                        y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
+                        y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
+                        y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
+                        y[4 * u + 3] = in ? ld_val(yg + cv[u].w) : TG(0);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4 * NV; ++q) s = A::add(s, (TS)y[q]);
+#pragma unroll
+                    for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+                }
             }
             const int32_t slot = __ldg(lng.cslot + g * 32 + lane);
             if (slot >= 0) lng.sum[slot] = (double)s;
@@ -995,57 +1028,93 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             P->piece_blocked = mode >= 2;
         }
     }
-    cudaFree(P->csell);
-    cudaFree(P->cslice_ptr);
-    cudaFree(P->cslot);
+    for (void* q : {(void*)P->csell, (void*)P->cslice_ptr, (void*)P->cslot, (void*)P->cfmt, (void*)P->cbase,
+                    (void*)P->clen})
+        cudaFree(q);
     P->csell = nullptr;
     P->cslice_ptr = nullptr;
     P->cslot = nullptr;
+    P->cfmt = nullptr;
+    P->cbase = nullptr;
+    P->clen = nullptr;
     if (P->chunk > 0) {
-        // per range: chunks sorted by (length desc, first column), 32 per
-        // slice; slice g's block b holds, lane after lane, entries 4b..4b+3
-        // of each lane's chunk (padding: the zero-valued slot nall)
+        // per range: chunks sorted by (16-bit deltas fit, length desc, first
+        // column), 32 per slice.  A slice whose chunks all fit stores, in
+        // block b, lane after lane, the deltas of entries 8b..8b+7 (16-byte
+        // vectors); the others store entries 4b..4b+3 as int32 ids (padding:
+        // the zero-valued slot nall)
+        int delta = 1;
+        if (const char* e = getenv("GN_PART_DELTA")) delta = atoi(e) != 0;
+        auto clen_of = [&](int64_t j) { return pe[(size_t)j] - pb[(size_t)j]; };
+        std::vector<uint8_t> fits(pb.size(), 0);
+        parallel_for((int64_t)pb.size(), [&](int64_t j) {
+            bool ok = delta != 0;
+            for (int32_t e = pb[(size_t)j] + 1; ok && e < pe[(size_t)j]; ++e)
+                ok = ncol[(size_t)e] - ncol[(size_t)e - 1] < 65536;
+            fits[(size_t)j] = ok;
+        });
         std::vector<int64_t> csp(1, 0);
-        std::vector<int32_t> cslot;
-        std::vector<std::pair<int64_t, int32_t>> gfirst;  // per slice: (first chunk position, range)
-        std::vector<int32_t> corder;
+        std::vector<int32_t> cslot, cbase, clen;
+        std::vector<int8_t> cfmt;
         for (int r = 0; r < 2; ++r) {
             P->cg0[r] = (int64_t)csp.size() - 1;
             const int64_t a0 = P->pc0[r], a1 = a0 + P->npc[r];
             std::vector<int32_t> ord;
             for (int64_t j = a0; j < a1; ++j) ord.push_back((int32_t)(j - a0));
             std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
-                const int32_t lx = pe[(size_t)(a0 + x)] - pb[(size_t)(a0 + x)], ly = pe[(size_t)(a0 + y)] - pb[(size_t)(a0 + y)];
+                if (fits[(size_t)(a0 + x)] != fits[(size_t)(a0 + y)]) return fits[(size_t)(a0 + x)] > fits[(size_t)(a0 + y)];
+                const int32_t lx = clen_of(a0 + x), ly = clen_of(a0 + y);
                 if (lx != ly) return lx > ly;
                 return ncol[(size_t)pb[(size_t)(a0 + x)]] < ncol[(size_t)pb[(size_t)(a0 + y)]];
             });
             for (size_t g = 0; g < ord.size(); g += 32) {
                 int32_t len = 0;
-                for (size_t l = g; l < std::min(ord.size(), g + 32); ++l)
-                    len = std::max(len, pe[(size_t)(a0 + ord[l])] - pb[(size_t)(a0 + ord[l])]);
-                for (size_t l = g; l < g + 32; ++l) cslot.push_back(l < ord.size() ? ord[l] : -1);
-                csp.push_back(csp.back() + (int64_t)(len + 3) / 4 * 128);
+                bool all_fit = true;
+                for (size_t l = g; l < std::min(ord.size(), g + 32); ++l) {
+                    len = std::max(len, clen_of(a0 + ord[l]));
+                    all_fit = all_fit && fits[(size_t)(a0 + ord[l])];
+                }
+                for (size_t l = g; l < g + 32; ++l) {
+                    const bool in = l < ord.size();
+                    cslot.push_back(in ? ord[l] : -1);
+                    cbase.push_back(in ? ncol[(size_t)pb[(size_t)(a0 + ord[l])]] : 0);
+                    clen.push_back(in ? clen_of(a0 + ord[l]) : 0);
+                }
+                cfmt.push_back(all_fit ? 1 : 0);
+                const int per = all_fit ? 8 : 4;  // entries per lane per vector
+                csp.push_back(csp.back() + (int64_t)(len + per - 1) / per * 32);
             }
             P->ncg[r] = (int64_t)csp.size() - 1 - P->cg0[r];
-            for (int32_t o : ord) corder.push_back((int32_t)(a0 + o));
         }
-        std::vector<int32_t> cs((size_t)std::max<int64_t>(csp.back(), 1), (int32_t)nall);
+        std::vector<uint32_t> cs((size_t)std::max<int64_t>(csp.back(), 1) * 4, 0);
         const int64_t ngs = (int64_t)csp.size() - 1;
         parallel_for(ngs, [&](int64_t g) {
             const int r = g >= P->cg0[1] ? 1 : 0;
             const int64_t a0 = P->pc0[r];
+            const int64_t nvec = csp[(size_t)g + 1] - csp[(size_t)g];
+            uint32_t* dst = cs.data() + (size_t)csp[(size_t)g] * 4;
+            if (!cfmt[(size_t)g])
+                for (int64_t t = 0; t < nvec * 4; ++t) dst[t] = (uint32_t)nall;  // int32 padding
             for (int l = 0; l < 32; ++l) {
                 const int32_t sl = cslot[(size_t)(g * 32 + l)];
                 if (sl < 0) continue;
                 const int32_t e0 = pb[(size_t)(a0 + sl)], e1 = pe[(size_t)(a0 + sl)];
                 for (int32_t e = e0; e < e1; ++e) {
                     const int32_t pos = e - e0;
-                    cs[(size_t)(csp[(size_t)g] + (pos / 4) * 128 + l * 4 + pos % 4)] = ncol[(size_t)e];
+                    if (cfmt[(size_t)g]) {  // vector pos/8 of lane l, half-word pos%8
+                        const uint32_t d = e == e0 ? 0u : (uint32_t)(ncol[(size_t)e] - ncol[(size_t)e - 1]);
+                        uint32_t& word = dst[((size_t)(pos / 8) * 32 + l) * 4 + (pos % 8) / 2];
+                        word |= d << (16 * (pos % 2));
+                    } else {
+                        dst[((size_t)(pos / 4) * 32 + l) * 4 + pos % 4] = (uint32_t)ncol[(size_t)e];
+                    }
                 }
             }
         });
-        if ((rcode = upload_into(&P->csell, cs)) || (rcode = upload_into(&P->cslice_ptr, csp)) ||
-            (rcode = upload_into(&P->cslot, cslot)))
+        std::vector<int32_t> cs32(cs.begin(), cs.end());
+        if ((rcode = upload_into(&P->csell, cs32)) || (rcode = upload_into(&P->cslice_ptr, csp)) ||
+            (rcode = upload_into(&P->cslot, cslot)) || (rcode = upload_into(&P->cfmt, cfmt)) ||
+            (rcode = upload_into(&P->cbase, cbase)) || (rcode = upload_into(&P->clen, clen)))
             return rcode;
     }
     cudaFree(P->pc_sum);
@@ -1121,7 +1190,8 @@ static PartLong part_long_of(gn_part* p, int r) {
                     p->r_long[r] ? p->npc[r] : 0, p->pc_order ? p->pc_order + p->pc0[r] : nullptr,
                     p->piece_blocked, p->interleave, p->chunk ? p->csell : nullptr,
                     p->chunk ? p->cslice_ptr + p->cg0[r] : nullptr, p->chunk ? p->cslot + 32 * p->cg0[r] : nullptr,
-                    p->chunk ? p->ncg[r] : 0};
+                    p->chunk ? p->cfmt + p->cg0[r] : nullptr, p->chunk ? p->cbase + 32 * p->cg0[r] : nullptr,
+                    p->chunk ? p->clen + 32 * p->cg0[r] : nullptr, p->chunk ? p->ncg[r] : 0};
 }
 
 }  // namespace gn
@@ -1183,9 +1253,9 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_beg);
     cudaFree(p->pc_end);
     cudaFree(p->pc_order);
-    cudaFree(p->csell);
-    cudaFree(p->cslice_ptr);
-    cudaFree(p->cslot);
+    for (void* q : {(void*)p->csell, (void*)p->cslice_ptr, (void*)p->cslot, (void*)p->cfmt, (void*)p->cbase,
+                    (void*)p->clen})
+        cudaFree(q);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
     cudaFree(p->rowptr);

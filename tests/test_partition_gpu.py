@@ -104,7 +104,8 @@ def test_one_part_device_schedule_equals_host_loop():
 
 
 @pytest.mark.parametrize("env", [{"GN_PART_LONG": "64", "GN_PART_CHUNK": "0"}, {"GN_PART_LONG": "64"},
-                                 {"GN_PART_LONG": "256", "GN_PART_CHUNK": "96"}, {"GN_PART_LEX": "0"},
+                                 {"GN_PART_LONG": "256", "GN_PART_CHUNK": "96"},
+                                 {"GN_PART_LONG": "64", "GN_PART_DELTA": "0"}, {"GN_PART_LEX": "0"},
                                  {"GN_PART_LEX": "3"}])
 @pytest.mark.parametrize("parts", [1, 3])
 def test_partition_layout_options(env, parts, monkeypatch):
