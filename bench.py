@@ -471,7 +471,7 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
         s_bytes = 8 if dtype == "fp64" else 4
         b_iter = algorithmic_bytes(n, 2 * m, s_bytes)
         achieved = b_iter * iters * args.steps / (total_ms * 1e-3) / 1e9
-        traffic = ncu_traffic("C5part", iters) if ws == 1 else None
+        traffic = ncu_traffic("C5part", 1) if ws == 1 else None  # per step launch = one iteration
         clk = clocks.summary()
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
@@ -491,8 +491,8 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                     "d2h_bytes_per_step": 8 * spec.n_own + 32 * iters,
                     "api": "partition.run_partition (host x0 in, owned x and per-iteration stats out), rank 0 shown"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
-                         "frac": achieved / (peak * ws), "traffic": traffic,
-                         "traffic_note": traffic_note(traffic, b_iter * iters),
+                         "frac": achieved / (peak * ws), "traffic": traffic, "traffic_per": "step launch (one iteration)",
+                         "traffic_note": traffic_note(traffic, b_iter),
                          "kernel": "gn::k_part_step (1 launch per iteration per part, replayed from a CUDA graph)" + (
                              "" if ws == 1 else (" + coalesced pushes into the peers' ghost slots (CUDA IPC)"
                                                  if args.halo == "peer" else " + NCCL halo")),

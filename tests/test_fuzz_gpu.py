@@ -67,3 +67,23 @@ def test_multistart_and_partitioned_exact(kind, n, seed):
     for halo in ("copy", "peer"):
         out = run_local_partitions(g, x0, s, 3, lambda sp: EngineBackend(sp, dtype="fp64", exact=True), halo=halo)
         np.testing.assert_array_equal(out["x"], ref.x)
+
+
+@pytest.mark.parametrize("kind,n,seed", CASES)
+@pytest.mark.parametrize("long_degree", ["1024", "48"])
+def test_partitioned_fast_mode(kind, n, seed, long_degree, monkeypatch):
+    """The partitioned engine's fast mode (rows above the long threshold as
+    128-entry chunks, 16-bit delta slices where the gaps fit, equal-degree
+    rows ordered by their hottest neighbours, hubs-first ghosts) on every
+    graph class, 1 and 3 parts: within the fp64 contract, identical
+    fallbacks, deterministic."""
+    monkeypatch.setenv("GN_PART_LONG", long_degree)
+    g, x0 = _graph(kind, n, seed)
+    s = P.GammaSchedule.pursuit(iterations=80)
+    ref = O.run(g, x0, s.table(), s.final_gamma, threads=O.default_threads())
+    for parts in (1, 3):
+        out = run_local_partitions(g, x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"), halo="peer")
+        np.testing.assert_allclose(out["x"], ref.x, rtol=1e-9, atol=1e-300)
+        np.testing.assert_array_equal(out["fallbacks"], ref.fallbacks)
+        again = run_local_partitions(g, x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64"), halo="peer")
+        np.testing.assert_array_equal(again["x"], out["x"])
