@@ -176,7 +176,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
     if (i < n_own) x[i] = xi;
 }
 
-constexpr int kPartLongDegreeDefault = 1024;
+constexpr int kPartLongDegreeMin = 128, kPartLongDegreeMax = 1024;
 constexpr int kChunkDefault = 128;  // long-row chunk length (thread per chunk; 0: warp pieces)
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
@@ -805,8 +805,14 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // 8192 1.47, 65536 5.96; chunks of 128: threshold 1024 (= 2048) 1.335,
     // 4096 1.374; chunks of 64 / 256: 1.348 / 1.365 (R-MAT degrees cluster
     // near 2^29 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).
-    // GN_PART_LONG overrides.
-    int kPartLongDegree = kPartLongDegreeDefault;
+    // On a small part the longest thread-per-row chain bounds the iteration
+    // instead: the threshold is nnz / 16384 rounded down to a power of two
+    // in [128, 1024] (C3, 2 M entries, us per iteration at threshold 32 / 64
+    // / 128 / 256 / 512 / 1024: 19.9 / 19.1 / 18.0 / 23.1 / 33.8 / 54.0; an
+    // 8-way part of C5, 65 M entries, ms: 128 0.238, 256 0.226, 512 0.225,
+    // 1024 0.222).  GN_PART_LONG overrides.
+    int kPartLongDegree = kPartLongDegreeMin;
+    while (kPartLongDegree < kPartLongDegreeMax && (int64_t)kPartLongDegree * 2 * 16384 <= P->nnz) kPartLongDegree *= 2;
     if (const char* e = getenv("GN_PART_LONG")) kPartLongDegree = std::max(32, atoi(e));
     P->long_degree = kPartLongDegree;
     const int64_t n_own = P->n_own, nall = P->n_own + P->n_ghost;

@@ -39,10 +39,12 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     out = {"config": args.config, "dtype": args.dtype, "n": g.n, "m": inst.m, "iters": args.iters}
 
-    def timed(fn):
+    def timed(fn, pre=None):
         best = None
         for _ in range(args.reps):
             flush.fill_(1)
+            if pre is not None:
+                pre()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -66,6 +68,13 @@ def main():
 
     part()
     out["part_ms_per_iter"] = timed(part)
+    out["part_run_only_ms_per_iter"] = timed(lambda: be.run(0, len(tab)), pre=lambda: be.begin(x0l, tab))
+    import time
+
+    t0 = time.perf_counter()
+    be.begin(x0l, tab)
+    torch.cuda.synchronize()
+    out["part_begin_ms"] = round(1e3 * (time.perf_counter() - t0), 3)
     be.close()
     print(json.dumps(out), flush=True)
 
