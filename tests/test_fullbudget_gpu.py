@@ -182,12 +182,19 @@ def test_c5_scale24_partitioned_full_budget(c5_scale24):
             dx = d.max(axis=1)
             report_excursions("C5_scale24_partitioned_fp32", ks, dx, d.argmax(axis=1))
             assert dx.max() <= 1e-3
-    # the fp64 persistent loop kernel (bench --engine loop) over the same pursuit
-    r = P.run_engine(g, inst.x0, s, dtype="fp64")
+    # the fp64 persistent loop kernel (bench --engine loop) over the same
+    # pursuit, and the public run_wrgn, which routes a graph this large to
+    # the partitioned engine (engine="auto")
+    r = P.run_engine(g, inst.x0, s, dtype="fp64", engine="loop")
     np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
     np.testing.assert_allclose(r.x, ref.x, rtol=RTOL, atol=ATOL)
     np.testing.assert_allclose(r.trace.step_inf, ref.step_inf, rtol=RTOL, atol=1e-15)
     check_rounding(g, r.x, ref.x)
+    x, tr = P.run_wrgn(g, inst.x0, s)
+    np.testing.assert_array_equal(tr.fallbacks, ref.fallbacks.tolist())
+    np.testing.assert_allclose(x, ref.x, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(tr.step_inf, ref.step_inf, rtol=RTOL, atol=1e-15)
+    assert tr.gamma == tab.tolist() and len(tr.step_inf) == 1000
 
 
 class _Sched:

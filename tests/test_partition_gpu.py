@@ -125,3 +125,39 @@ def test_partition_layout_options(env, parts, monkeypatch):
     np.testing.assert_array_equal(again["x"], out["x"])
     ex = run_local_partitions(inst.graph, inst.x0, s, parts, lambda sp: EngineBackend(sp, dtype="fp64", exact=True))
     np.testing.assert_array_equal(ex["x"], ref.x)
+
+
+def test_run_wrgn_partitioned_route():
+    """run_engine(engine="part") -- the route run_wrgn takes for large graphs
+    in fast mode -- within the fp64 contract of the oracle and of the loop
+    kernel, the reference's x0 errors raised in the same order with the same
+    messages, the non-finite stop at the same iteration, and the options it
+    cannot serve refused."""
+    inst = G.c5_rmat(14)
+    g, s = inst.graph, P.GammaSchedule.pursuit(iterations=150)
+    ref = O.run(g, inst.x0, s.table(), s.final_gamma)
+    r = P.run_engine(g, inst.x0, s, engine="part")
+    np.testing.assert_allclose(r.x, ref.x, rtol=1e-9, atol=1e-250)
+    np.testing.assert_array_equal(r.trace.fallbacks, ref.fallbacks)
+    np.testing.assert_allclose(r.trace.step_inf, ref.step_inf, rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose(r.trace.objective, ref.mass, rtol=1e-12)
+    again = P.run_engine(g, inst.x0, s, engine="part")  # the cached backend
+    np.testing.assert_array_equal(again.x, r.x)
+    bad = inst.x0.copy()
+    bad[5] = -0.1
+    with pytest.raises(P.NormalizationError, match="nonnegative"):
+        P.run_engine(g, bad, s, engine="part")
+    bad[5] = np.nan
+    with pytest.raises(P.NormalizationError, match="zero closed neighborhood"):
+        P.run_engine(g, bad, s, engine="part")
+    iso = int(np.flatnonzero(np.diff(np.asarray(g.indptr)) == 0)[0])
+    bad = inst.x0.copy()
+    bad[iso] = 0.0
+    with pytest.raises(P.NormalizationError, match="zero closed neighborhood"):
+        P.run_engine(g, bad, s, engine="part")
+    bad = inst.x0.copy()
+    bad[3] = np.inf
+    with pytest.raises(P.NormalizationError, match="non-finite state at iteration 0"):
+        P.run_engine(g, bad, s, engine="part")
+    with pytest.raises(ValueError):
+        P.run_engine(g, inst.x0, s, engine="part", record_trace=True)
