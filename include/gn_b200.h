@@ -260,6 +260,13 @@ int gn_part_run_group(gn_part* const* parts, int nparts, int k0, int k1, uintptr
  * slices' gather walk alone with real gathers / no gathers (index stream
  * only) / L1-resident gathers / random gathers.  Call after gn_part_begin. */
 int gn_part_probe(gn_part* p, int mode, int reps, double* ms);
+/* Measurement aid: with GN_PART_COUNT=1 set at gn_part_begin, the value
+ * gathers the run issued per iteration (index-vector entries walked, padding
+ * included; zero-row certificate checks; witness searches) -- how much of the
+ * adjacency the zero-row certificates let the steps skip (out[k] = 0 when
+ * counting was off).  Replaces nothing in the reference: dynamics.py:105
+ * always gathers every entry. */
+int gn_part_gathers(gn_part* p, int done, int64_t* out);
 /* CUDA IPC of one device allocation between the processes of a node. */
 int gn_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */);
 int gn_ipc_open_handle(const void* handle, int device, void** dptr);

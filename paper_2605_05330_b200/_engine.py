@@ -92,6 +92,7 @@ EXPORTED = (
     "gn_part_run",
     "gn_part_run_group",
     "gn_part_probe",
+    "gn_part_gathers",
     "gn_ipc_get_handle",
     "gn_ipc_open_handle",
     "gn_ipc_close",
@@ -194,6 +195,7 @@ _SIGNATURES = {
     "gn_part_run": (_I32, [_P, _I32, _I32, ctypes.c_uint64]),
     "gn_part_run_group": (_I32, [_P, _I32, _I32, _I32, ctypes.c_uint64]),
     "gn_part_probe": (_I32, [_P, _I32, _I32, ctypes.POINTER(ctypes.c_double)]),
+    "gn_part_gathers": (_I32, [_P, _I32, _P]),
     "gn_ipc_get_handle": (_I32, [_P, _P]),
     "gn_ipc_open_handle": (_I32, [_P, _I32, ctypes.POINTER(_P)]),
     "gn_ipc_close": (_I32, [_P]),

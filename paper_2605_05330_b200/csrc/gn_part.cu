@@ -95,6 +95,22 @@ struct gn_part {
     int32_t* cbase = nullptr;        // [slices * 32] first id of the lane's chunk
     int32_t* clen = nullptr;         // [slices * 32] its length
     int64_t cg0[2] = {0, 0}, ncg[2] = {0, 0};
+    // zero-row certificates (every mode; GN_PART_WITNESS=0: off).  A row
+    // whose state is exactly 0 has y_i = +-0 and stays y_i/d = +-0 for any d =
+    // y_i + gamma*s > 1e-9.  Its neighbour sum is a sum of non-negative terms,
+    // monotone in every addend in any fixed order and precision, so s >= y_j
+    // for each neighbour j: one neighbour ("witness") with y_i + gamma*y_j >
+    // 1e-9 settles the row bit for bit without its walk (the update runs with
+    // s = y_j: the same d > 1e-9 test, the same +-0).  Rows whose witness
+    // fails walk as before and are queued; k_part_witness then picks the
+    // neighbour of largest y as the new witness.
+    int witness = 1;
+    int32_t* wit = nullptr;      // [n_own] witness per row (local id), -1 none
+    int32_t* rq = nullptr;       // [n_own] rows queued for a witness (one range's step at a time)
+    int* rq_cnt = nullptr;       // [2 * iters] queue length per (iteration, range)
+    int32_t* crow = nullptr;     // chunk mode: [ncg * 32] the (new) row of the lane's chunk, -1 empty
+    unsigned long long* gat = nullptr;  // [iters * 64] gathers issued (GN_PART_COUNT=1: counted; measurement)
+    int gat_on = 0;
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
@@ -196,6 +212,16 @@ struct PartLong {
     const int32_t* __restrict__ cbase;  // [ncg * 32] first id (delta slices)
     const int32_t* __restrict__ clen;   // [ncg * 32] chunk length (delta slices)
     int64_t ncg;
+    const int32_t* __restrict__ crow;   // [ncg * 32] the chunk's row (zero-row certificates)
+};
+
+// The zero-row certificates of one step launch (gn_part::witness); wit null: off
+struct PartWit {
+    const int32_t* __restrict__ wit;
+    int32_t* __restrict__ rq;           // queue of rows without a certificate
+    int* __restrict__ rqn;              // its length for this (iteration, range)
+    unsigned long long* __restrict__ gat;  // null, or [64] gathers issued this iteration
+    int cap;                            // queue capacity (n_own)
 };
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
@@ -287,6 +313,23 @@ __device__ __forceinline__ void part_update_pre(int64_t i, TS s, TS g, TS xi, TS
     ob = __dadd_rn(ob, __dmul_rn((double)(TS)wi, (double)o));
 }
 
+// A zero row's certificate (gn_part::witness): x_i == 0 and its witness j
+// gives y_i + g*y_j > 1e-9 -- then the row's own d = y_i + g*s passes the same
+// test (s >= y_j) and its new state is y_i/d = y_i.  yw: y_j in the state
+// precision, the row's stand-in neighbour sum.
+template <typename TS, typename TG>
+__device__ __forceinline__ bool part_certified(TS xi, TS vi, TS g, int32_t wj, const TG* __restrict__ yg, TS& yw) {
+    using A = Arith<TS>;
+    if (wj < 0) return false;
+    yw = (TS)ld_val(yg + wj);
+    return (double)A::add(A::mul(vi, xi), A::mul(g, yw)) > kSafeDiv;
+}
+
+__device__ __forceinline__ void part_enqueue(const PartWit& w, int64_t i) {
+    const int e = atomicAdd(w.rqn, 1);
+    if (e < w.cap) w.rq[e] = (int32_t)i;  // (a repeated launch of one step cannot overrun it)
+}
+
 // the same with the row's state, weight and v loaded here
 template <typename TS, typename TG>
 __device__ __forceinline__ void part_update(int64_t i, TS s, TS g, const double* __restrict__ w64,
@@ -347,6 +390,7 @@ struct StepArgs {
     double* __restrict__ part;
     PartPush push;
     PartLong lng;
+    PartWit wt;
     int nvb;  // blocks (push blocks included)
 };
 
@@ -383,15 +427,33 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
         rb = upto > before ? before : nbl + (bid - before);
     }
     const TS g = (TS)a.gam[a.k];
+    const PartWit& wt = a.wt;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int kWarpsPerBlock = kPartThreads / 32;
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
+    unsigned long long ng = 0;  // gathers issued (GN_PART_COUNT)
     if (rb < nbl && lng.csell) {
         // long rows, chunk mode: one thread per chunk over the chunks' SELL
-        // (sequential in ascending new id), the sum to the chunk's slot
+        // (sequential in ascending new id), the sum to the chunk's slot; the
+        // chunks of a certified zero row are not walked (k_part_long_combine
+        // takes the same certificate and does not read their slots)
+        const TS gk = g;
         for (int64_t g = (int64_t)rb * kWarpsPerBlock + warp; g < lng.ncg; g += (int64_t)nbl * kWarpsPerBlock) {
             const int64_t v0 = lng.cslice_ptr[g];
-            const int nblk = (int)((lng.cslice_ptr[g + 1] - v0) / 32);
+            const int nblk_s = (int)((lng.cslice_ptr[g + 1] - v0) / 32);
+            int my = nblk_s;  // this lane's vectors
+            if (wt.wit) {
+                const int32_t row = __ldg(lng.crow + g * 32 + lane);
+                if (row < 0) {
+                    my = 0;
+                } else {
+                    const TS xr = a.x[row];
+                    TS yw;
+                    if (xr == TS(0) && part_certified<TS, TG>(xr, a.v[row], gk, wt.wit[row], yg, yw)) my = 0;
+                    if (xr == TS(0)) ++ng;
+                }
+            }
+            const int nblk = __reduce_max_sync(0xffffffffu, (unsigned)my);
             const uint4* base = reinterpret_cast<const uint4*>(lng.csell) + v0 + lane;
             TS s = TS(0);
             if (lng.cfmt[g]) {
@@ -399,10 +461,11 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                 // the chunk's first id (its first delta is 0); entries past the
                 // chunk's length add nothing
                 int32_t id = __ldg(lng.cbase + g * 32 + lane);
-                const int len = __ldg(lng.clen + g * 32 + lane);
-                uint4 cv = nblk > 0 ? ld_idx4(base) : make_uint4(0, 0, 0, 0);
+                const int len = my > 0 ? __ldg(lng.clen + g * 32 + lane) : 0;
+                if (wt.gat) ng += (unsigned)len;
+                uint4 cv = my > 0 ? ld_idx4(base) : make_uint4(0, 0, 0, 0);
                 for (int b = 0; b < nblk; ++b) {
-                    const uint4 nv = b + 1 < nblk ? ld_idx4(base + (size_t)(b + 1) * 32) : make_uint4(0, 0, 0, 0);
+                    const uint4 nv = b + 1 < my ? ld_idx4(base + (size_t)(b + 1) * 32) : make_uint4(0, 0, 0, 0);
                     const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
                     TG y[8];
 #pragma unroll
@@ -416,18 +479,19 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                 }
             } else {
                 constexpr int NV = kPartUnroll / 4;
+                if (wt.gat) ng += 4u * (unsigned)my;
                 uint4 cv[NV];
 #pragma unroll
-                for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
                 for (int b = 0; b < nblk; b += NV) {
                     uint4 nv[NV];
 #pragma unroll
                     for (int u = 0; u < NV; ++u)
-                        nv[u] = b + NV + u < nblk ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+                        nv[u] = b + NV + u < my ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
                     TG y[4 * NV];
 #pragma unroll
                     for (int u = 0; u < NV; ++u) {
-                        const bool in = b + u < nblk;
+                        const bool in = b + u < my;
                         y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
                         y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
                         y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
@@ -440,7 +504,7 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                 }
             }
             const int32_t slot = __ldg(lng.cslot + g * 32 + lane);
-            if (slot >= 0) lng.sum[slot] = (double)s;
+            if (slot >= 0 && my > 0) lng.sum[slot] = (double)s;
         }
     } else if (rb < nbl) {
         // long rows, fast mode: one warp per piece of kPiece entries; lanes
@@ -483,8 +547,22 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
     } else if (rb < nbl + ncb) {
         for (int64_t q = (int64_t)(rb - nbl) * kPartThreads + tid; q < a.n_csr; q += (int64_t)ncb * kPartThreads) {
             const int64_t i = a.order[a.n_long + q];
-            const int32_t r0 = a.rowptr[i], r1 = a.rowptr[i + 1];
+            int32_t r0 = a.rowptr[i], r1 = a.rowptr[i + 1];
             TS s = TS(0);
+            if (wt.wit) {
+                const TS xi = a.x[i];
+                if (xi == TS(0)) {
+                    TS yw;
+                    if (part_certified<TS, TG>(xi, a.v[i], g, wt.wit[i], yg, yw)) {
+                        s = yw;
+                        r1 = r0;
+                    } else {
+                        part_enqueue(wt, i);
+                    }
+                    ++ng;
+                }
+            }
+            if (wt.gat) ng += (unsigned)(r1 - r0);
             int32_t p = r0;
             for (; p + kPartUnroll <= r1; p += kPartUnroll) {  // scipy order, loads before the adds
                 TG y[kPartUnroll];
@@ -507,23 +585,40 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             const int64_t i = a.order[0] + (valid ? pos : 0);
             const TS xi = a.x[i], vi = a.v[i];
             const double wi = a.w64[i];
+            const int32_t wj = wt.wit ? wt.wit[i] : -1;
             const int64_t e0 = a.slice_ptr[sl];
-            const int nblk = (int)((a.slice_ptr[sl + 1] - e0) / 128);
+            const int nblk_s = (int)((a.slice_ptr[sl + 1] - e0) / 128);
+            // this lane's index vectors: none past the range's rows, none for
+            // a certified zero row (its stand-in sum is the witness's value)
+            int my = wt.wit && !valid ? 0 : nblk_s;
+            TS s = TS(0);
+            bool queue = false;
+            if (wt.wit && valid && xi == TS(0)) {
+                TS yw;
+                if (part_certified<TS, TG>(xi, vi, g, wj, yg, yw)) {
+                    s = yw;
+                    my = 0;
+                } else {
+                    queue = true;
+                }
+                ++ng;
+            }
+            if (wt.gat) ng += 4u * (unsigned)my;
+            const int nblk = wt.wit ? (int)__reduce_max_sync(0xffffffffu, (unsigned)my) : nblk_s;
             const uint4* base = reinterpret_cast<const uint4*>(a.sell + e0) + lane;
             constexpr int NV = kPartUnroll / 4;  // index vectors per batch
             uint4 cv[NV];
 #pragma unroll
-            for (int u = 0; u < NV; ++u) cv[u] = u < nblk ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
-            TS s = TS(0);
+            for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
             for (int b = 0; b < nblk; b += NV) {
                 uint4 nv[NV];
 #pragma unroll
                 for (int u = 0; u < NV; ++u)
-                    nv[u] = b + NV + u < nblk ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+                    nv[u] = b + NV + u < my ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
                 TG y[4 * NV];
 #pragma unroll
                 for (int u = 0; u < NV; ++u) {
-                    const bool in = b + u < nblk;
+                    const bool in = b + u < my;
                     y[4 * u + 0] = in ? ld_val(yg + (int32_t)cv[u].x) : TG(0);
                     y[4 * u + 1] = in ? ld_val(yg + (int32_t)cv[u].y) : TG(0);
                     y[4 * u + 2] = in ? ld_val(yg + (int32_t)cv[u].z) : TG(0);
@@ -535,7 +630,13 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
             if (valid) part_update_pre<TS, TG>(i, s, g, xi, vi, wi, a.xo, a.ygo, mx, fb, ob, nf);
+            if (queue) part_enqueue(wt, i);
         }
+    }
+    if (wt.gat) {  // measurement only: one atomic per warp, spread over 64 counters
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
+        if (lane == 0 && ng) atomicAdd(wt.gat + ((vb * kWarpsPerBlock + warp) & 63), ng);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -583,20 +684,38 @@ template <typename TS, typename TG>
 __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
     int64_t n_long, int64_t first, const int32_t* __restrict__ lp,
     const double* __restrict__ pc_sum, const double* __restrict__ w64, const TS* __restrict__ v,
-    const TS* __restrict__ x, TS* __restrict__ xo, TG* __restrict__ ygo, const double* __restrict__ gam, int k,
-    double* __restrict__ part) {
+    const TS* __restrict__ x, TS* __restrict__ xo, const TG* __restrict__ yg, TG* __restrict__ ygo,
+    const double* __restrict__ gam, int k, double* __restrict__ part, PartWit wt) {
     using A = Arith<TS>;
     const TS g = (TS)gam[k];
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
     const int lane = threadIdx.x & 31;
     const int64_t q = (int64_t)blockIdx.x * (kPartThreads / 32) + (threadIdx.x >> 5);
     if (q < n_long) {
-        const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
+        const int64_t i = first + q;
+        // a certified zero row: its chunks were not walked (k_part_step took
+        // the same certificate); the witness's value stands in for the sum
+        bool cert = false, zero = false;
         TS s = TS(0);
-        for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[j]);
+        if (wt.wit) {
+            const TS xi = x[i];
+            zero = xi == TS(0);
+            TS yw;
+            if (zero && part_certified<TS, TG>(xi, v[i], g, wt.wit[i], yg, yw)) {
+                cert = true;
+                s = yw;
+            }
+        }
+        if (!cert) {
+            const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
+            for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[j]);
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
-        if (lane == 0) part_update<TS, TG>(first + q, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
+        }
+        if (lane == 0) {
+            part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+            if (zero && !cert) part_enqueue(wt, i);
+        }
     }
     __shared__ double red[kPartThreads / 32][4];
 #pragma unroll
@@ -627,6 +746,48 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
         dst[1] = t[1];
         dst[2] = t[2];
         dst[3] = t[3];
+    }
+}
+
+// The zero rows one step launch walked without a certificate: one warp per
+// queued row picks the neighbour of largest y (this iteration's values, the
+// ones the step read; ties: the first in the row) as its witness for the next
+// iterations.  Runs after the range's step (and combine), before any peer
+// can overwrite the ghost values it reads.
+template <typename TG>
+__global__ void __launch_bounds__(kPartThreads) k_part_witness(const int32_t* __restrict__ rq,
+                                                               const int* __restrict__ rqn, int cap,
+                                                               const int32_t* __restrict__ rowptr,
+                                                               const int32_t* __restrict__ col,
+                                                               const TG* __restrict__ yg, int32_t* __restrict__ wit,
+                                                               unsigned long long* __restrict__ gat) {
+    const int n = min(*rqn, cap);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * kPartThreads + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kPartThreads) >> 5;
+    unsigned long long ng = 0;
+    for (int64_t e = w0; e < n; e += nw) {
+        const int32_t i = __ldg(rq + e);
+        const int32_t r0 = __ldg(rowptr + i), r1 = __ldg(rowptr + i + 1);
+        double best = -1.0;
+        int32_t bp = INT32_MAX;  // position of the best
+        for (int32_t p = r0 + lane; p < r1; p += 32) {
+            const double y = (double)ld_val(yg + __ldg(col + p));
+            if (y > best) { best = y; bp = p; }
+        }
+        ng += (unsigned)max(0, (r1 - r0 - lane + 31) / 32);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int32_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+        }
+        if (lane == 0) wit[i] = bp < r1 ? __ldg(col + bp) : -1;
+    }
+    if (gat) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
+        if (lane == 0 && ng) atomicAdd(gat + (w0 & 63), ng);
     }
 }
 
@@ -988,7 +1149,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     }
     P->interleave = 1;
     if (const char* e = getenv("GN_PART_INTERLEAVE")) P->interleave = atoi(e) != 0;
-    std::vector<int32_t> pb, pe, lp;
+    std::vector<int32_t> pb, pe, lp, prow;
     for (int r = 0; r < 2; ++r) {
         P->pc0[r] = (int64_t)pb.size();
         P->lp0[r] = (int64_t)lp.size();
@@ -1001,6 +1162,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                 const int64_t f = std::min<int64_t>(e + piece_len, end);
                 pb.push_back((int32_t)e);
                 pe.push_back((int32_t)f);
+                prow.push_back((int32_t)row);
                 e = f;
             }
         }
@@ -1035,8 +1197,9 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         }
     }
     for (void* q : {(void*)P->csell, (void*)P->cslice_ptr, (void*)P->cslot, (void*)P->cfmt, (void*)P->cbase,
-                    (void*)P->clen})
+                    (void*)P->clen, (void*)P->crow})
         cudaFree(q);
+    P->crow = nullptr;
     P->csell = nullptr;
     P->cslice_ptr = nullptr;
     P->cslot = nullptr;
@@ -1060,7 +1223,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
             fits[(size_t)j] = ok;
         });
         std::vector<int64_t> csp(1, 0);
-        std::vector<int32_t> cslot, cbase, clen;
+        std::vector<int32_t> cslot, cbase, clen, crow;
         std::vector<int8_t> cfmt;
         for (int r = 0; r < 2; ++r) {
             P->cg0[r] = (int64_t)csp.size() - 1;
@@ -1083,6 +1246,7 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
                 for (size_t l = g; l < g + 32; ++l) {
                     const bool in = l < ord.size();
                     cslot.push_back(in ? ord[l] : -1);
+                    crow.push_back(in ? prow[(size_t)(a0 + ord[l])] : -1);
                     cbase.push_back(in ? ncol[(size_t)pb[(size_t)(a0 + ord[l])]] : 0);
                     clen.push_back(in ? clen_of(a0 + ord[l]) : 0);
                 }
@@ -1120,9 +1284,16 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
         std::vector<int32_t> cs32(cs.begin(), cs.end());
         if ((rcode = upload_into(&P->csell, cs32)) || (rcode = upload_into(&P->cslice_ptr, csp)) ||
             (rcode = upload_into(&P->cslot, cslot)) || (rcode = upload_into(&P->cfmt, cfmt)) ||
-            (rcode = upload_into(&P->cbase, cbase)) || (rcode = upload_into(&P->clen, clen)))
+            (rcode = upload_into(&P->cbase, cbase)) || (rcode = upload_into(&P->clen, clen)) ||
+            (rcode = upload_into(&P->crow, crow)))
             return rcode;
     }
+    // zero-row certificates: one witness per row, the queue
+    cudaFree(P->wit);
+    cudaFree(P->rq);
+    P->wit = P->rq = nullptr;
+    GN_CUDA(cudaMalloc((void**)&P->wit, 4 * (size_t)std::max<int64_t>(n_own, 1)));
+    GN_CUDA(cudaMalloc((void**)&P->rq, 4 * (size_t)std::max<int64_t>(n_own, 1)));
     cudaFree(P->pc_sum);
     P->pc_sum = nullptr;
     GN_CUDA(cudaMalloc((void**)&P->pc_sum, 8 * (size_t)std::max<int64_t>(slots, 1)));
@@ -1143,9 +1314,11 @@ static void part_free_push(gn_part* p) {
 
 static void part_free_run(gn_part* p) {
     void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part[0], p->part[1], p->part_long[0],
-                    p->part_long[1]};
+                    p->part_long[1], p->rq_cnt, p->gat};
     for (void* q : ptrs)
         if (q) cudaFree(q);
+    p->rq_cnt = nullptr;
+    p->gat = nullptr;
     p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
     p->gam = p->part[0] = p->part[1] = p->part_long[0] = p->part_long[1] = nullptr;
     p->alloc_ncomb[0] = p->alloc_ncomb[1] = 0;
@@ -1170,6 +1343,13 @@ static void by_dtype(int dtype, F f) {
     else f(float(), float());
 }
 
+// the certificates of range r's launches at iteration k (null wit: off)
+static PartWit part_wit_of(gn_part* p, int r, int k) {
+    if (!p->witness || !p->rq_cnt) return PartWit{nullptr, nullptr, nullptr, nullptr, 0};
+    return PartWit{p->wit, p->rq, p->rq_cnt + 2 * (size_t)k + r, p->gat_on ? p->gat + 64 * (size_t)k : nullptr,
+                   (int)p->n_own};
+}
+
 // one k_part_step launch over range r (the counts select which branches run)
 template <typename TS, typename TG>
 static void launch_step(gn_part* p, int r, int k, int nb, int64_t n_long, int nbl, int64_t ncsr, int ncb, int64_t nsl,
@@ -1179,7 +1359,7 @@ static void launch_step(gn_part* p, int r, int k, int nb, int64_t n_long, int nb
     const StepArgs<TS, TG> a{n_long, nbl, ncsr, ncb, p->r_count[r], p->order + p->r_start[r], p->rowptr,
                              fast ? p->col_fast : p->col, fast ? p->sell_fast : p->sell, p->slice_ptr + p->sl0[r], nsl,
                              p->w64, (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (const TG*)p->yg[cur],
-                             (TG*)p->yg[cur ^ 1], p->gam, k, p->part[r], push, lng, nb};
+                             (TG*)p->yg[cur ^ 1], p->gam, k, p->part[r], push, lng, part_wit_of(p, r, k), nb};
     k_part_step<TS, TG><<<nb, kPartThreads, 0, s>>>(a);
 }
 
@@ -1188,7 +1368,16 @@ static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
     const int cur = k & 1;
     k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
         p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->pc_sum, p->w64,
-        (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (TG*)p->yg[cur ^ 1], p->gam, k, p->part_long[r]);
+        (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (const TG*)p->yg[cur], (TG*)p->yg[cur ^ 1], p->gam,
+        k, p->part_long[r], part_wit_of(p, r, k));
+}
+
+// the witness search for the zero rows range r's step queued at iteration k
+template <typename TG>
+static void launch_witness(gn_part* p, int r, int k, cudaStream_t s) {
+    const PartWit w = part_wit_of(p, r, k);
+    k_part_witness<TG><<<2 * 148, kPartThreads, 0, s>>>(w.rq, w.rqn, w.cap, p->rowptr, p->col,
+                                                      (const TG*)p->yg[k & 1], p->wit, w.gat);
 }
 
 static PartLong part_long_of(gn_part* p, int r) {
@@ -1197,7 +1386,8 @@ static PartLong part_long_of(gn_part* p, int r) {
                     p->piece_blocked, p->interleave, p->chunk ? p->csell : nullptr,
                     p->chunk ? p->cslice_ptr + p->cg0[r] : nullptr, p->chunk ? p->cslot + 32 * p->cg0[r] : nullptr,
                     p->chunk ? p->cfmt + p->cg0[r] : nullptr, p->chunk ? p->cbase + 32 * p->cg0[r] : nullptr,
-                    p->chunk ? p->clen + 32 * p->cg0[r] : nullptr, p->chunk ? p->ncg[r] : 0};
+                    p->chunk ? p->clen + 32 * p->cg0[r] : nullptr, p->chunk ? p->ncg[r] : 0,
+                    p->chunk ? p->crow + 32 * p->cg0[r] : nullptr};
 }
 
 }  // namespace gn
@@ -1260,7 +1450,7 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_end);
     cudaFree(p->pc_order);
     for (void* q : {(void*)p->csell, (void*)p->cslice_ptr, (void*)p->cslot, (void*)p->cfmt, (void*)p->cbase,
-                    (void*)p->clen})
+                    (void*)p->clen, (void*)p->crow, (void*)p->wit, (void*)p->rq})
         cudaFree(q);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
@@ -1328,6 +1518,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
             if (p->r_nblocks[r]) GN_CUDA(cudaMalloc((void**)&p->part[r], 32 * (size_t)iters * p->r_nblocks[r]));
         for (int r = 0; r < 2; ++r)
             if (p->r_ncomb[r]) GN_CUDA(cudaMalloc((void**)&p->part_long[r], 32 * (size_t)iters * p->r_ncomb[r]));
+        GN_CUDA(cudaMalloc((void**)&p->rq_cnt, 4 * 2 * (size_t)iters));
+        GN_CUDA(cudaMalloc((void**)&p->gat, 8 * 64 * (size_t)iters));
         p->alloc_nall = nall;
         p->alloc_dtype = p->dtype;
         p->alloc_iters = iters;
@@ -1338,6 +1530,17 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     }
     GN_CUDA(cudaMemset(p->yg[0], 0, gs * (nb + 4)));
     GN_CUDA(cudaMemset(p->yg[1], 0, gs * (nb + 4)));
+    // zero-row certificates: no witnesses yet, empty queues
+    int witness = 1;
+    if (const char* e = getenv("GN_PART_WITNESS")) witness = atoi(e) != 0;
+    if (witness != p->witness) p->gen++;
+    p->witness = witness;
+    GN_CUDA(cudaMemset(p->wit, 0xFF, 4 * (size_t)std::max<int64_t>(p->n_own, 1)));
+    GN_CUDA(cudaMemset(p->rq_cnt, 0, 4 * 2 * (size_t)iters));
+    const bool count = getenv("GN_PART_COUNT") && atoi(getenv("GN_PART_COUNT")) != 0;
+    if (count != (p->gat_on != 0)) p->gen++;
+    p->gat_on = count;
+    GN_CUDA(cudaMemset(p->gat, 0, 8 * 64 * (size_t)iters));
     GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
     // a new run epoch (see gn_part::epoch)
     if (!p->d_epoch) GN_CUDA(cudaMalloc((void**)&p->d_epoch, sizeof(int64_t)));
@@ -1398,6 +1601,10 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
     GN_LAUNCHED();
     if (p->r_long[r] > 0 && p->r_count[r] > 0) {
         by_dtype(p->dtype, [&](auto ts, auto tg) { launch_combine<decltype(ts), decltype(tg)>(p, r, k, s); });
+        GN_LAUNCHED();
+    }
+    if (p->witness && p->r_count[r] > 0) {
+        by_dtype(p->dtype, [&](auto, auto tg) { launch_witness<decltype(tg)>(p, r, k, s); });
         GN_LAUNCHED();
     }
     return GN_OK;
@@ -1849,6 +2056,24 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms) {
     if (e != cudaSuccess) return cuda_fail(e, "gn_part_probe", __FILE__, __LINE__);
     GN_LAUNCHED();
     *ms = (double)t / reps;
+    return GN_OK;
+}
+
+// Measurement aid (GN_PART_COUNT=1 at gn_part_begin): the gathers of values
+// the run issued per iteration -- index-vector entries walked (padding
+// included), certificate checks, the witness searches -- after `done`
+// iterations (0 when counting was off)
+int gn_part_gathers(gn_part* p, int done, int64_t* out) {
+    if (!p || done < 0 || done > p->iters || (done > 0 && !out)) return fail(GN_ERR_ARG, "bad gn_part_gathers arguments");
+    GN_CUDA(cudaSetDevice(p->device));
+    GN_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(64 * (size_t)std::max(done, 1), 0ull);
+    if (p->gat && done > 0) GN_CUDA(cudaMemcpy(h.data(), p->gat, 8 * 64 * (size_t)done, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < done; ++k) {
+        unsigned long long t = 0;
+        for (int j = 0; j < 64; ++j) t += h[(size_t)k * 64 + j];
+        out[k] = p->gat_on ? (int64_t)t : 0;
+    }
     return GN_OK;
 }
 

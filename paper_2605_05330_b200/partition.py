@@ -247,6 +247,14 @@ class EngineBackend:
         E.check(E.lib().gn_part_end(self.h, done, E.ptr(x), E.ptr(si), E.ptr(fb), E.ptr(ms), ctypes.byref(bad)))
         return x, si[:done], fb[:done], ms[:done], bad.value
 
+    def gathers(self, done: int) -> np.ndarray:
+        """Value gathers issued per iteration (GN_PART_COUNT=1 set before
+        begin(); zeros otherwise): what the zero-row certificates left of the
+        adjacency walk (measurement aid, gn_part_gathers)."""
+        out = np.zeros(max(done, 1), dtype=np.int64)
+        self.E.check(self.E.lib().gn_part_gathers(self.h, done, self.E.ptr(out)))
+        return out[:done]
+
     def close(self) -> None:
         if getattr(self, "h", None) is not None:
             self.E.lib().gn_part_destroy(self.h)
