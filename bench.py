@@ -213,22 +213,32 @@ def cpu_port(inst, seconds: float, threads: int) -> dict:
     if key not in _CPU_WARM:  # first touch of the graph's pages and the threads: not timed
         O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)
         _CPU_WARM.add(key)
+    # the loop's own rate: T(k) - T(1) over k - 1 iterations, so the call's fixed
+    # part (the x0 check's SpMV, the array hand-over) is not charged to the
+    # iterations -- the GPU arm's `value` times the loop alone as well
     t0 = time.perf_counter()
     O.run(inst.graph, inst.x0, tab[:1], 1.5, threads=threads)
-    dt, k = time.perf_counter() - t0, 1
-    if dt < seconds / 3:  # room for a longer sample: calibrate on 3 steps, then time k
-        t0 = time.perf_counter()
-        O.run(inst.graph, inst.x0, tab[:3], 1.5, threads=threads)
-        per = max((time.perf_counter() - t0) / 4, 1e-6)  # 3 steps + the x0 check's SpMV
-        k = int(min(1000, max(1, seconds / per)))
+    t1 = time.perf_counter() - t0
+    k = int(min(1000, max(3, seconds / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    O.run(inst.graph, inst.x0, tab[:k], 1.5, threads=threads)
+    tk = time.perf_counter() - t0
+    if tk - t1 < seconds / 2 and k < 1000:  # T(1) was mostly set-up: a sample of the asked length
+        k = int(min(1000, max(k + 1, (k - 1) * seconds / max(tk - t1, 1e-6))))
         t0 = time.perf_counter()
         O.run(inst.graph, inst.x0, tab[:k], 1.5, threads=threads)
-        dt = time.perf_counter() - t0
-    return {"value": inst.m * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {k} of the 1000 pursuit iterations of {inst.name} in fp64 on {threads} host "
+        tk = time.perf_counter() - t0
+    dt = tk - t1
+    if dt <= 0.05 * tk:  # a run too short to separate: charge everything
+        dt, per_k = tk, k
+    else:
+        per_k = k - 1
+    return {"value": inst.m * per_k / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"iterations 2..{k} of the 1000 pursuit iterations of {inst.name} in fp64 on {threads} host "
                       f"thread(s) (oracle/gn_oracle.c, OpenMP over fixed row chunks, bitwise the reference's "
-                      f"arithmetic), {dt:.2f} s incl. the x0 check",
-            "iters": k, "seconds": dt}
+                      f"arithmetic): T({k}) - T(1) = {dt:.2f} s (T(1) = {t1:.2f} s holds the x0 check and the "
+                      f"call's set-up)",
+            "iters": per_k, "seconds": dt}
 
 
 def reference_module():

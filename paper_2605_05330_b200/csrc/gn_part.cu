@@ -111,6 +111,23 @@ struct gn_part {
     int32_t* crow = nullptr;     // chunk mode: [ncg * 32] the (new) row of the lane's chunk, -1 empty
     unsigned long long* gat = nullptr;  // [iters * 64] gathers issued (GN_PART_COUNT=1: counted; measurement)
     int gat_on = 0;
+    // settled rows (with the certificates; GN_PART_SETTLE=0: off).  A member
+    // row m -- state exactly 1, every neighbour an owned row whose state is
+    // exactly 0, gmin[k]*y_m > 1e-9 for the smallest gamma still to come --
+    // is a fixed point together with its neighbours: m computes s = 0, d =
+    // v_m, x' = v_m/v_m = 1; each neighbour z has y_z = 0 and d_z >= gamma*y_m
+    // > 1e-9, x_z' = 0; by induction for every later iteration.  Such rows
+    // (frz 2), and the zero rows whose witness is one (frz 1), hold the same
+    // value in both state and both published buffers and are skipped: no
+    // loads but the flag, no stores; a member adds its w to the objective in
+    // the same place of the same sum.  Member candidates (state 1, walked sum
+    // exactly 0) are queued by the step; k_part_settle, after both ranges,
+    // checks the new states of their neighbours.
+    int settle = 1;
+    uint8_t* frz = nullptr;      // [n_own] 0 active, 1 settled zero row, 2 settled member row
+    int32_t* mq = nullptr;       // [n_own] member candidates of one iteration
+    int* mq_cnt = nullptr;       // [iters] their count
+    double* gmin = nullptr;      // [iters] min gamma over [k, iters) (0 when one of them is not finite and positive)
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
@@ -222,6 +239,11 @@ struct PartWit {
     int* __restrict__ rqn;              // its length for this (iteration, range)
     unsigned long long* __restrict__ gat;  // null, or [64] gathers issued this iteration
     int cap;                            // queue capacity (n_own)
+    uint8_t* frz;                       // settled rows (gn_part::frz); null: off
+    int32_t* __restrict__ mq;           // member candidates
+    int* __restrict__ mqn;              // their count this iteration
+    const double* __restrict__ gfut;    // min gamma over this and the later iterations (device: the captured
+                                        // schedule serves runs with other gammas)
 };
 #ifndef GN_PART_UNROLL
 #define GN_PART_UNROLL 8
@@ -295,7 +317,7 @@ __device__ __forceinline__ TG ld_val(const TG* p) {
 
 // dynamics.py:104-107 for owned row i with neighbour sum s; stats of the thread
 template <typename TS, typename TG>
-__device__ __forceinline__ void part_update_pre(int64_t i, TS s, TS g, TS xi, TS vi, double wi,
+__device__ __forceinline__ TS part_update_pre(int64_t i, TS s, TS g, TS xi, TS vi, double wi,
                                                 TS* __restrict__ xo, TG* __restrict__ ygo, double& mx, double& fb,
                                                 double& ob, double& nf) {
     using A = Arith<TS>;
@@ -311,6 +333,36 @@ __device__ __forceinline__ void part_update_pre(int64_t i, TS s, TS g, TS xi, TS
     fb += ok ? 0.0 : 1.0;
     if (!isfinite((double)o)) nf = 1.0;
     ob = __dadd_rn(ob, __dmul_rn((double)(TS)wi, (double)o));
+    return o;
+}
+
+// A settled member row's share of the objective: what part_update_pre adds
+// for o = 1 (w*1 = w exactly), in the same place of the thread's sum
+template <typename TS>
+__device__ __forceinline__ void part_member_mass(double wi, double& ob) {
+    ob = __dadd_rn(ob, (double)(TS)wi);
+}
+
+// After row i (state xi, walked neighbour sum s) was updated to o: a member
+// candidate -- state exactly 1 before and after, neighbour sum exactly 0 (every
+// published neighbour value is 0), and its published value keeps every
+// neighbour's d above 1e-9 under the smallest gamma still to come -- is queued
+// for k_part_settle, which looks at the neighbours' states.
+template <typename TS, typename TG>
+__device__ __forceinline__ void part_member_candidate(const PartWit& w, int64_t i, TS xi, TS s, TS o, TS vi) {
+    using A = Arith<TS>;
+    if (!(xi == TS(1) && o == TS(1) && s == TS(0))) return;
+    const TS pub = (TS)(TG)A::mul(vi, o);
+    if (!((double)A::mul((TS)*w.gfut, pub) > kSafeDiv)) return;
+    const int e = atomicAdd(w.mqn, 1);
+    if (e < w.cap) w.mq[e] = (int32_t)i;
+}
+
+// A certified zero row i whose witness wj is a settled member row is settled
+// too (its d stays above 1e-9 by the member's own test); looked at every
+// fourth iteration, staggered over the rows
+__device__ __forceinline__ void part_settle_zero(const PartWit& w, int64_t i, int32_t wj, int k) {
+    if (((k + (int)i) & 3) == 0 && wj < w.cap && w.frz[wj] == 2) w.frz[i] = 1;
 }
 
 // A zero row's certificate (gn_part::witness): x_i == 0 and its witness j
