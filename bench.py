@@ -470,6 +470,34 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
     e2e_total = sum(e2e)
+    # what the zero-row certificates and settled rows leave of the adjacency
+    # walk (one counting run, GN_PART_COUNT=1), and the same pursuit with them
+    # off (GN_PART_WITNESS=0: every row walks every iteration -- the plain
+    # streaming kernel the ncu captures and the gather ceiling describe).
+    # Both outside the timed steps; the outputs are bitwise the same.
+    walked, off_ms = None, None
+    if ws == 1 and not args.no_certificate_report:
+        saved = {k: os.environ.get(k) for k in ("GN_PART_COUNT", "GN_PART_WITNESS")}
+        try:
+            os.environ["GN_PART_COUNT"] = "1"
+            timed_run()
+            gat = be.gathers(iters)
+            be.end(iters)
+            walked = float(gat.sum()) / (2.0 * inst.m * iters)
+            os.environ["GN_PART_COUNT"] = "0"
+            os.environ["GN_PART_WITNESS"] = "0"
+            timed_run()
+            flush_l2(torch, dev)
+            off_ms = timed_run()
+            x_off = be.end(iters)[0]
+            if res is not None and not np.array_equal(x_off, res.x):
+                raise RuntimeError("certificates changed the result: bench aborted")
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
     t = torch.tensor([total_ms, e2e_total, setup_s], device=dev, dtype=torch.float64)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -508,8 +536,17 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                                                  if args.halo == "peer" else " + NCCL halo")),
                          "b_iter": b_iter, "peak_source": peak_src + (f" x {ws} GPUs" if ws > 1 else ""),
                          "achieved_over": "the whole iteration (step + long-row combine launches)",
-                         "gather_ceiling": gather_ceiling("C5part", total_ms / (args.steps * iters))
-                         if ws == 1 and dtype == "fp64" else None},
+                         "achieved_note": "algorithmic bytes of every iteration over the measured time; rows the "
+                                          "zero-row certificates settle are not walked (walked_fraction), so this is a "
+                                          "rate of work done or proven unnecessary, not of bytes moved; "
+                                          "certificates_off is the same pursuit with every row walked",
+                         "walked_fraction": walked,
+                         "certificates_off": None if off_ms is None else {
+                             "ms_per_step": off_ms, "value": m * iters / (off_ms * 1e-3),
+                             "achieved": b_iter * iters / (off_ms * 1e-3) / 1e9,
+                             "frac": b_iter * iters / (off_ms * 1e-3) / 1e9 / peak,
+                             "gather_ceiling": gather_ceiling("C5part", off_ms / iters) if dtype == "fp64" else None,
+                             "result": "bitwise equal to the timed runs' x"}},
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "gpu_launches": int(launches),
@@ -712,6 +749,8 @@ def main():
     ap.add_argument("--dtype", default=None, help="engine dtype (default: fp64 for C1-C3, fp32 for C4/C5)")
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ref-seconds", type=float, default=6.0)
+    ap.add_argument("--no-certificate-report", action="store_true",
+                    help="C5: skip the counting run and the certificates-off run after the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="C5 with N > 1: coalesced pushes into the peers' ghost slots (default) or NCCL send/recv")

@@ -22,7 +22,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <thread>
 #include <tuple>
 #include <vector>
@@ -130,6 +132,8 @@ struct gn_part {
     double* gmin = nullptr;      // [iters] min gamma over [k, iters) (0 when one of them is not finite and positive)
     int32_t* lp = nullptr;
     double* pc_sum = nullptr;
+    double* pc_max = nullptr;    // chunk mode: per chunk, an uncertified zero row's largest gathered value
+    int32_t* pc_arg = nullptr;   // and its id (the witness search rides on the walk)
     int64_t pc0[2] = {0, 0}, npc[2] = {0, 0}, lp0[2] = {0, 0};
     int r_ncomb[2] = {0, 0};                 // per range: combine blocks
     double* part_long[2] = {nullptr, nullptr};  // per range [iters][r_ncomb][4]
@@ -210,6 +214,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
 }
 
 constexpr int kPartLongDegreeMin = 128, kPartLongDegreeMax = 1024;
+constexpr int kSlicesPerWarp = 16;  // slice blocks: slices per warp (GN_PART_SPW; C5 scale 24: 1 / 4 / 16 / 64 -> 0.715 / 0.573 / 0.552 / 0.612 ms per iteration)
 constexpr int kChunkDefault = 128;  // long-row chunk length (thread per chunk; 0: warp pieces)
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
@@ -230,6 +235,8 @@ struct PartLong {
     const int32_t* __restrict__ clen;   // [ncg * 32] chunk length (delta slices)
     int64_t ncg;
     const int32_t* __restrict__ crow;   // [ncg * 32] the chunk's row (zero-row certificates)
+    double* __restrict__ cmax;          // per slot (as sum): an uncertified zero row's chunk maximum; null: no tracking
+    int32_t* __restrict__ carg;         // and the id that holds it (-1: every value 0)
 };
 
 // The zero-row certificates of one step launch (gn_part::witness); wit null: off
@@ -239,6 +246,7 @@ struct PartWit {
     int* __restrict__ rqn;              // its length for this (iteration, range)
     unsigned long long* __restrict__ gat;  // null, or [64] gathers issued this iteration
     int cap;                            // queue capacity (n_own)
+    int gat_mode;                       // what gat counts: 1 value gathers, 2 rows walked, 3 slices walked (slice path)
     uint8_t* frz;                       // settled rows (gn_part::frz); null: off
     int32_t* __restrict__ mq;           // member candidates
     int* __restrict__ mqn;              // their count this iteration
@@ -446,6 +454,77 @@ struct StepArgs {
     int nvb;  // blocks (push blocks included)
 };
 
+// One lane's chunk of a long row (chunk mode): `my` index vectors of the
+// chunks' SELL walked in ascending new id, 8 gathers in flight, the next
+// vector loading under them; delta slices hold 16-bit gaps from id0 (8 entries
+// per vector, `len` entries in all), the others int32 ids (4 per vector,
+// padded with the zero-valued slot).  TRACK: also the largest value gathered
+// and its id (the first such) -- the witness search of an uncertified zero
+// row rides on the walk the row does anyway.
+template <typename TS, typename TG, bool TRACK>
+__device__ __forceinline__ TS part_chunk_walk(const uint4* __restrict__ base, const TG* __restrict__ yg, int my, int nblk,
+                                              bool delta, int32_t id0, int len, TG& best, int32_t& barg) {
+    using A = Arith<TS>;
+    TS s = TS(0);
+    if (delta) {
+        int32_t id = id0;
+        uint4 cv = my > 0 ? ld_idx4(base) : make_uint4(0, 0, 0, 0);
+        for (int b = 0; b < nblk; ++b) {
+            const uint4 nv = b + 1 < my ? ld_idx4(base + (size_t)(b + 1) * 32) : make_uint4(0, 0, 0, 0);
+            const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+            TG y[8];
+            int32_t ids[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                id += (int32_t)((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+                ids[j] = id;
+                y[j] = 8 * b + j < len ? ld_val(yg + id) : TG(0);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                s = A::add(s, (TS)y[j]);
+                if (TRACK && y[j] > best) {
+                    best = y[j];
+                    barg = ids[j];
+                }
+            }
+            cv = nv;
+        }
+    } else {
+        constexpr int NV = kPartUnroll / 4;
+        uint4 cv[NV];
+#pragma unroll
+        for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+        for (int b = 0; b < nblk; b += NV) {
+            uint4 nv[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u)
+                nv[u] = b + NV + u < my ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
+            TG y[4 * NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const bool in = b + u < my;
+                y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
+                y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
+                y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
+                y[4 * u + 3] = in ? ld_val(yg + cv[u].w) : TG(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4 * NV; ++q) {
+                s = A::add(s, (TS)y[q]);
+                if (TRACK && y[q] > best) {
+                    best = y[q];
+                    const uint4 c = cv[q >> 2];
+                    barg = (int32_t)((q & 3) == 0 ? c.x : (q & 3) == 1 ? c.y : (q & 3) == 2 ? c.z : c.w);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+        }
+    }
+    return s;
+}
+
 // One virtual block (256 threads) of a step over one range.  Blocks [0, nbl)
 // split the n_long longest rows over warps (lanes stride the positions, fixed
 // butterfly fold: fast mode only); blocks [nbl, nbl + ncb) give one thread to
@@ -494,69 +573,43 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             const int64_t v0 = lng.cslice_ptr[g];
             const int nblk_s = (int)((lng.cslice_ptr[g + 1] - v0) / 32);
             int my = nblk_s;  // this lane's vectors
+            bool track = false;  // the chunk of a zero row without a certificate: its walk looks for a witness
             if (wt.wit) {
                 const int32_t row = __ldg(lng.crow + g * 32 + lane);
-                if (row < 0) {
+                if (row < 0 || (wt.frz && wt.frz[row])) {
                     my = 0;
                 } else {
                     const TS xr = a.x[row];
                     TS yw;
-                    if (xr == TS(0) && part_certified<TS, TG>(xr, a.v[row], gk, wt.wit[row], yg, yw)) my = 0;
-                    if (xr == TS(0)) ++ng;
+                    if (xr == TS(0)) {
+                        if (part_certified<TS, TG>(xr, a.v[row], gk, wt.wit[row], yg, yw)) my = 0;
+                        else track = true;
+                        ++ng;
+                    }
                 }
             }
             const int nblk = __reduce_max_sync(0xffffffffu, (unsigned)my);
+            if (nblk == 0) continue;  // every chunk of the slice belongs to a certified or settled row
             const uint4* base = reinterpret_cast<const uint4*>(lng.csell) + v0 + lane;
-            TS s = TS(0);
-            if (lng.cfmt[g]) {
-                // 16-bit deltas: 8 entries per vector; the running id starts at
-                // the chunk's first id (its first delta is 0); entries past the
-                // chunk's length add nothing
-                int32_t id = __ldg(lng.cbase + g * 32 + lane);
-                const int len = my > 0 ? __ldg(lng.clen + g * 32 + lane) : 0;
-                if (wt.gat) ng += (unsigned)len;
-                uint4 cv = my > 0 ? ld_idx4(base) : make_uint4(0, 0, 0, 0);
-                for (int b = 0; b < nblk; ++b) {
-                    const uint4 nv = b + 1 < my ? ld_idx4(base + (size_t)(b + 1) * 32) : make_uint4(0, 0, 0, 0);
-                    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
-                    TG y[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        id += (int32_t)((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
-                        y[j] = 8 * b + j < len ? ld_val(yg + id) : TG(0);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) s = A::add(s, (TS)y[j]);
-                    cv = nv;
-                }
-            } else {
-                constexpr int NV = kPartUnroll / 4;
-                if (wt.gat) ng += 4u * (unsigned)my;
-                uint4 cv[NV];
-#pragma unroll
-                for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
-                for (int b = 0; b < nblk; b += NV) {
-                    uint4 nv[NV];
-#pragma unroll
-                    for (int u = 0; u < NV; ++u)
-                        nv[u] = b + NV + u < my ? ld_idx4(base + (size_t)(b + NV + u) * 32) : make_uint4(0, 0, 0, 0);
-                    TG y[4 * NV];
-#pragma unroll
-                    for (int u = 0; u < NV; ++u) {
-                        const bool in = b + u < my;
-                        y[4 * u + 0] = in ? ld_val(yg + cv[u].x) : TG(0);
-                        y[4 * u + 1] = in ? ld_val(yg + cv[u].y) : TG(0);
-                        y[4 * u + 2] = in ? ld_val(yg + cv[u].z) : TG(0);
-                        y[4 * u + 3] = in ? ld_val(yg + cv[u].w) : TG(0);
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4 * NV; ++q) s = A::add(s, (TS)y[q]);
-#pragma unroll
-                    for (int u = 0; u < NV; ++u) cv[u] = nv[u];
+            TS s;
+            TG best = TG(0);     // an uncertified zero row's chunk: its largest published value
+            int32_t barg = -1;   // and whose it is (the first such, ascending id)
+            const bool delta = lng.cfmt[g] != 0;
+            const int32_t id0 = delta ? __ldg(lng.cbase + g * 32 + lane) : 0;
+            const int len = delta && my > 0 ? __ldg(lng.clen + g * 32 + lane) : 0;
+            if (wt.gat) ng += delta ? (unsigned)len : 4u * (unsigned)my;
+            if (lng.cmax && __any_sync(0xffffffffu, track))
+                s = part_chunk_walk<TS, TG, true>(base, yg, my, nblk, delta, id0, len, best, barg);
+            else
+                s = part_chunk_walk<TS, TG, false>(base, yg, my, nblk, delta, id0, len, best, barg);
+            const int32_t slot = __ldg(lng.cslot + g * 32 + lane);
+            if (slot >= 0 && my > 0) {
+                lng.sum[slot] = (double)s;
+                if (lng.cmax && track) {
+                    lng.cmax[slot] = (double)best;
+                    lng.carg[slot] = barg;
                 }
             }
-            const int32_t slot = __ldg(lng.cslot + g * 32 + lane);
-            if (slot >= 0 && my > 0) lng.sum[slot] = (double)s;
         }
     } else if (rb < nbl) {
         // long rows, fast mode: one warp per piece of kPiece entries; lanes
@@ -601,13 +654,24 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             const int64_t i = a.order[a.n_long + q];
             int32_t r0 = a.rowptr[i], r1 = a.rowptr[i + 1];
             TS s = TS(0);
+            bool cert = false;
+            if (wt.frz) {
+                const unsigned fz = wt.frz[i];
+                if (fz) {
+                    if (fz == 2) part_member_mass<TS>(a.w64[i], ob);
+                    continue;
+                }
+            }
             if (wt.wit) {
                 const TS xi = a.x[i];
                 if (xi == TS(0)) {
                     TS yw;
-                    if (part_certified<TS, TG>(xi, a.v[i], g, wt.wit[i], yg, yw)) {
+                    const int32_t wj = wt.wit[i];
+                    if (part_certified<TS, TG>(xi, a.v[i], g, wj, yg, yw)) {
                         s = yw;
                         r1 = r0;
+                        cert = true;
+                        if (wt.frz) part_settle_zero(wt, i, wj, a.k);
                     } else {
                         part_enqueue(wt, i);
                     }
@@ -624,14 +688,35 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                 for (int u = 0; u < kPartUnroll; ++u) s = A::add(s, (TS)y[u]);
             }
             for (; p < r1; ++p) s = A::add(s, (TS)ld_val(yg + col[p]));
-            part_update<TS, TG>(i, s, g, a.w64, a.v, a.x, a.xo, a.ygo, mx, fb, ob, nf);
+            const TS xi = a.x[i], vi = a.v[i];
+            const TS o = part_update_pre<TS, TG>(i, s, g, xi, vi, a.w64[i], a.xo, a.ygo, mx, fb, ob, nf);
+            if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi);
         }
     } else {
         const int64_t pos0 = a.n_long + a.n_csr;  // first order position of slice 0
         const int64_t nw = (int64_t)(nbid - nbl - ncb) * kWarpsPerBlock;
-        for (int64_t sl = (int64_t)(rb - nbl - ncb) * kWarpsPerBlock + warp; sl < a.nsl; sl += nw) {
+        const int64_t sl_first = (int64_t)(rb - nbl - ncb) * kWarpsPerBlock + warp;
+        // settled rows: the lane's flag for this slice was loaded one slice
+        // ago (lanes past the range count as settled zero rows)
+        unsigned fzn = 0;
+        if (wt.frz && sl_first < a.nsl) {
+            const int64_t pn = pos0 + sl_first * 32 + lane;
+            fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
+        }
+        for (int64_t sl = sl_first; sl < a.nsl; sl += nw) {
             const int64_t pos = pos0 + sl * 32 + lane;
             const bool valid = pos < a.count;
+            const unsigned fz = fzn;
+            if (wt.frz) {
+                if (sl + nw < a.nsl) {
+                    const int64_t pn = pos + nw * 32;
+                    fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
+                }
+                if (__all_sync(0xffffffffu, fz != 0)) {  // a settled slice: the members' mass only
+                    if (fz == 2) part_member_mass<TS>(a.w64[a.order[0] + pos], ob);
+                    continue;
+                }
+            }
             // rows are numbered in processing order (part_order): order[pos] == order[0] + pos,
             // so the row's state, v and weight load at once, under the gathers
             const int64_t i = a.order[0] + (valid ? pos : 0);
@@ -642,21 +727,27 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             const int nblk_s = (int)((a.slice_ptr[sl + 1] - e0) / 128);
             // this lane's index vectors: none past the range's rows, none for
             // a certified zero row (its stand-in sum is the witness's value)
-            int my = wt.wit && !valid ? 0 : nblk_s;
+            int my = wt.wit && (!valid || fz) ? 0 : nblk_s;
             TS s = TS(0);
-            bool queue = false;
-            if (wt.wit && valid && xi == TS(0)) {
+            bool queue = false, cert = false;
+            if (wt.wit && valid && !fz && xi == TS(0)) {
                 TS yw;
                 if (part_certified<TS, TG>(xi, vi, g, wj, yg, yw)) {
                     s = yw;
                     my = 0;
+                    cert = true;
+                    if (wt.frz) part_settle_zero(wt, i, wj, a.k);
                 } else {
                     queue = true;
                 }
                 ++ng;
             }
-            if (wt.gat) ng += 4u * (unsigned)my;
             const int nblk = wt.wit ? (int)__reduce_max_sync(0xffffffffu, (unsigned)my) : nblk_s;
+            if (wt.gat) {
+                if (wt.gat_mode == 1) ng += 4u * (unsigned)my;
+                else if (wt.gat_mode == 2) ng = ng - (xi == TS(0) && valid && !fz ? 1u : 0u) + (my > 0 ? 1u : 0u);
+                else ng = ng - (xi == TS(0) && valid && !fz ? 1u : 0u) + (lane == 0 && nblk > 0 ? 1u : 0u);
+            }
             const uint4* base = reinterpret_cast<const uint4*>(a.sell + e0) + lane;
             constexpr int NV = kPartUnroll / 4;  // index vectors per batch
             uint4 cv[NV];
@@ -681,11 +772,17 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
 #pragma unroll
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
-            if (valid) part_update_pre<TS, TG>(i, s, g, xi, vi, wi, a.xo, a.ygo, mx, fb, ob, nf);
+            if (valid && !fz) {
+                const TS o = part_update_pre<TS, TG>(i, s, g, xi, vi, wi, a.xo, a.ygo, mx, fb, ob, nf);
+                if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi);
+            } else if (fz == 2 && valid) {
+                part_member_mass<TS>(wi, ob);
+            }
             if (queue) part_enqueue(wt, i);
         }
     }
     if (wt.gat) {  // measurement only: one atomic per warp, spread over 64 counters
+        if (wt.gat_mode != 1 && rb < nbl + ncb) ng = 0;  // rows / slices walked: the slice path's only
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
         if (lane == 0 && ng) atomicAdd(wt.gat + ((vb * kWarpsPerBlock + warp) & 63), ng);
@@ -737,7 +834,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
     int64_t n_long, int64_t first, const int32_t* __restrict__ lp,
     const double* __restrict__ pc_sum, const double* __restrict__ w64, const TS* __restrict__ v,
     const TS* __restrict__ x, TS* __restrict__ xo, const TG* __restrict__ yg, TG* __restrict__ ygo,
-    const double* __restrict__ gam, int k, double* __restrict__ part, PartWit wt) {
+    const double* __restrict__ gam, int k, double* __restrict__ part, PartWit wt,
+    const double* __restrict__ pc_max, const int32_t* __restrict__ pc_arg, int32_t* __restrict__ wit_out) {
     using A = Arith<TS>;
     const TS g = (TS)gam[k];
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
@@ -749,24 +847,49 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
         // the same certificate); the witness's value stands in for the sum
         bool cert = false, zero = false;
         TS s = TS(0);
-        if (wt.wit) {
+        const unsigned fz = wt.frz ? wt.frz[i] : 0u;  // a settled row: nothing but a member's mass
+        if (fz == 2 && lane == 0) part_member_mass<TS>(w64[i], ob);
+        if (wt.wit && !fz) {
             const TS xi = x[i];
             zero = xi == TS(0);
             TS yw;
-            if (zero && part_certified<TS, TG>(xi, v[i], g, wt.wit[i], yg, yw)) {
+            const int32_t wj = wt.wit[i];
+            if (zero && part_certified<TS, TG>(xi, v[i], g, wj, yg, yw)) {
                 cert = true;
                 s = yw;
+                if (wt.frz && lane == 0) part_settle_zero(wt, i, wj, k);
             }
         }
-        if (!cert) {
+        bool searched = false;
+        if (!cert && !fz) {
             const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
             for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[j]);
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
+            if (zero && pc_max) {
+                // a zero row without a certificate: its chunks' walks kept their
+                // largest values; the largest of those (the first chunk on ties)
+                // is the row's new witness -- no second walk
+                double best = 0.0;
+                int32_t bj = INT32_MAX, arg = -1;
+                for (int32_t j = j0 + lane; j < j1; j += 32) {
+                    const double m = pc_max[j];
+                    if (m > best) { best = m; bj = j; arg = pc_arg[j]; }
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    const double ob2 = __shfl_xor_sync(0xffffffffu, best, d);
+                    const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, d);
+                    const int32_t oa = __shfl_xor_sync(0xffffffffu, arg, d);
+                    if (ob2 > best || (ob2 == best && oj < bj)) { best = ob2; bj = oj; arg = oa; }
+                }
+                if (lane == 0) wit_out[i] = arg;
+                searched = true;
+            }
         }
-        if (lane == 0) {
+        if (lane == 0 && !fz) {
             part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-            if (zero && !cert) part_enqueue(wt, i);
+            if (zero && !cert && !searched) part_enqueue(wt, i);
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -840,6 +963,34 @@ __global__ void __launch_bounds__(kPartThreads) k_part_witness(const int32_t* __
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
         if (lane == 0 && ng) atomicAdd(gat + (w0 & 63), ng);
+    }
+}
+
+// The member candidates one iteration queued (state 1 before and after, every
+// published neighbour value 0, the gamma test passed): one warp per candidate
+// looks at the NEW states of its neighbours; when every neighbour is an owned
+// row whose state is exactly 0 the row is a settled member (gn_part::frz).  A
+// published 0 alone is not enough -- a tiny state can underflow in v*x and
+// grow back.  Runs after both ranges' steps of the iteration.
+template <typename TS>
+__global__ void __launch_bounds__(kPartThreads) k_part_settle(const int32_t* __restrict__ mq,
+                                                              const int* __restrict__ mqn, int cap,
+                                                              const int32_t* __restrict__ rowptr,
+                                                              const int32_t* __restrict__ col,
+                                                              const TS* __restrict__ xnew, uint8_t* __restrict__ frz) {
+    const int n = min(*mqn, cap);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * kPartThreads + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kPartThreads) >> 5;
+    for (int64_t e = w0; e < n; e += nw) {
+        const int32_t i = __ldg(mq + e);
+        const int32_t r0 = __ldg(rowptr + i), r1 = __ldg(rowptr + i + 1);
+        bool ok = true;
+        for (int32_t p = r0 + lane; p < r1 && ok; p += 32) {
+            const int32_t j = __ldg(col + p);
+            ok = j < cap && xnew[j] == TS(0);
+        }
+        if (__all_sync(0xffffffffu, ok) && lane == 0) frz[i] = 2;
     }
 }
 
@@ -1343,12 +1494,22 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // zero-row certificates: one witness per row, the queue
     cudaFree(P->wit);
     cudaFree(P->rq);
-    P->wit = P->rq = nullptr;
+    cudaFree(P->mq);
+    cudaFree(P->frz);
+    P->wit = P->rq = P->mq = nullptr;
+    P->frz = nullptr;
     GN_CUDA(cudaMalloc((void**)&P->wit, 4 * (size_t)std::max<int64_t>(n_own, 1)));
     GN_CUDA(cudaMalloc((void**)&P->rq, 4 * (size_t)std::max<int64_t>(n_own, 1)));
+    GN_CUDA(cudaMalloc((void**)&P->mq, 4 * (size_t)std::max<int64_t>(n_own, 1)));
+    GN_CUDA(cudaMalloc((void**)&P->frz, (size_t)std::max<int64_t>(n_own, 1)));
     cudaFree(P->pc_sum);
-    P->pc_sum = nullptr;
+    cudaFree(P->pc_max);
+    cudaFree(P->pc_arg);
+    P->pc_sum = P->pc_max = nullptr;
+    P->pc_arg = nullptr;
     GN_CUDA(cudaMalloc((void**)&P->pc_sum, 8 * (size_t)std::max<int64_t>(slots, 1)));
+    GN_CUDA(cudaMalloc((void**)&P->pc_max, 8 * (size_t)std::max<int64_t>(slots, 1)));
+    GN_CUDA(cudaMalloc((void**)&P->pc_arg, 4 * (size_t)std::max<int64_t>(slots, 1)));
     P->gen++;
     return GN_OK;
 }
@@ -1366,11 +1527,13 @@ static void part_free_push(gn_part* p) {
 
 static void part_free_run(gn_part* p) {
     void* ptrs[] = {p->x[0], p->x[1], p->yg[0], p->yg[1], p->v, p->gam, p->part[0], p->part[1], p->part_long[0],
-                    p->part_long[1], p->rq_cnt, p->gat};
+                    p->part_long[1], p->rq_cnt, p->gat, p->mq_cnt, p->gmin};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     p->rq_cnt = nullptr;
     p->gat = nullptr;
+    p->mq_cnt = nullptr;
+    p->gmin = nullptr;
     p->x[0] = p->x[1] = p->yg[0] = p->yg[1] = p->v = nullptr;
     p->gam = p->part[0] = p->part[1] = p->part_long[0] = p->part_long[1] = nullptr;
     p->alloc_ncomb[0] = p->alloc_ncomb[1] = 0;
@@ -1397,9 +1560,18 @@ static void by_dtype(int dtype, F f) {
 
 // the certificates of range r's launches at iteration k (null wit: off)
 static PartWit part_wit_of(gn_part* p, int r, int k) {
-    if (!p->witness || !p->rq_cnt) return PartWit{nullptr, nullptr, nullptr, nullptr, 0};
+    if (!p->witness || !p->rq_cnt) return PartWit{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
+    const bool st = p->settle && p->frz && p->mq_cnt;
     return PartWit{p->wit, p->rq, p->rq_cnt + 2 * (size_t)k + r, p->gat_on ? p->gat + 64 * (size_t)k : nullptr,
-                   (int)p->n_own};
+                   (int)p->n_own, p->gat_on, st ? p->frz : nullptr, st ? p->mq : nullptr, st ? p->mq_cnt + k : nullptr,
+                   st ? p->gmin + k : nullptr};
+}
+
+// the member candidates of iteration k (both ranges), after the interior step
+template <typename TS>
+static void launch_settle(gn_part* p, int k, cudaStream_t s) {
+    k_part_settle<TS><<<2 * 148, kPartThreads, 0, s>>>(p->mq, p->mq_cnt + k, (int)p->n_own, p->rowptr, p->col,
+                                                     (const TS*)p->x[(k & 1) ^ 1], p->frz);
 }
 
 // one k_part_step launch over range r (the counts select which branches run)
@@ -1421,7 +1593,7 @@ static void launch_combine(gn_part* p, int r, int k, cudaStream_t s) {
     k_part_long_combine<TS, TG><<<p->r_ncomb[r], kPartThreads, 0, s>>>(
         p->r_long[r], p->r_start[r], p->lp + p->lp0[r], p->pc_sum, p->w64,
         (const TS*)p->v, (const TS*)p->x[cur], (TS*)p->x[cur ^ 1], (const TG*)p->yg[cur], (TG*)p->yg[cur ^ 1], p->gam,
-        k, p->part_long[r], part_wit_of(p, r, k));
+        k, p->part_long[r], part_wit_of(p, r, k), p->chunk && p->witness ? p->pc_max : nullptr, p->pc_arg, p->wit);
 }
 
 // the witness search for the zero rows range r's step queued at iteration k
@@ -1429,7 +1601,7 @@ template <typename TG>
 static void launch_witness(gn_part* p, int r, int k, cudaStream_t s) {
     const PartWit w = part_wit_of(p, r, k);
     k_part_witness<TG><<<2 * 148, kPartThreads, 0, s>>>(w.rq, w.rqn, w.cap, p->rowptr, p->col,
-                                                      (const TG*)p->yg[k & 1], p->wit, w.gat);
+                                                      (const TG*)p->yg[k & 1], p->wit, w.gat_mode == 1 ? w.gat : nullptr);
 }
 
 static PartLong part_long_of(gn_part* p, int r) {
@@ -1439,7 +1611,9 @@ static PartLong part_long_of(gn_part* p, int r) {
                     p->chunk ? p->cslice_ptr + p->cg0[r] : nullptr, p->chunk ? p->cslot + 32 * p->cg0[r] : nullptr,
                     p->chunk ? p->cfmt + p->cg0[r] : nullptr, p->chunk ? p->cbase + 32 * p->cg0[r] : nullptr,
                     p->chunk ? p->clen + 32 * p->cg0[r] : nullptr, p->chunk ? p->ncg[r] : 0,
-                    p->chunk ? p->crow + 32 * p->cg0[r] : nullptr};
+                    p->chunk ? p->crow + 32 * p->cg0[r] : nullptr,
+                    p->chunk && p->witness && p->pc_max ? p->pc_max + p->pc0[r] : nullptr,
+                    p->chunk && p->pc_arg ? p->pc_arg + p->pc0[r] : nullptr};
 }
 
 }  // namespace gn
@@ -1502,10 +1676,12 @@ int gn_part_destroy(gn_part* p) {
     cudaFree(p->pc_end);
     cudaFree(p->pc_order);
     for (void* q : {(void*)p->csell, (void*)p->cslice_ptr, (void*)p->cslot, (void*)p->cfmt, (void*)p->cbase,
-                    (void*)p->clen, (void*)p->crow, (void*)p->wit, (void*)p->rq})
+                    (void*)p->clen, (void*)p->crow, (void*)p->wit, (void*)p->rq, (void*)p->mq, (void*)p->frz})
         cudaFree(q);
     cudaFree(p->lp);
     cudaFree(p->pc_sum);
+    cudaFree(p->pc_max);
+    cudaFree(p->pc_arg);
     cudaFree(p->rowptr);
     cudaFree(p->col);
     cudaFree(p->order);
@@ -1549,7 +1725,14 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32)) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
         p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
-        const int sblocks = (int)std::min<int64_t>((p->nsl[r] + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 16);
+        // slice blocks: `spw` slices per warp (GN_PART_SPW).  One slice per warp
+        // leaves the balancing to the block scheduler; several make a settled
+        // slice cost one flag test of a running warp instead of a block's launch
+        // and its chain of dependent loads
+        int spw = kSlicesPerWarp;
+        if (const char* e = getenv("GN_PART_SPW")) spw = std::max(1, atoi(e));
+        const int64_t per_block = (int64_t)(kPartThreads / 32) * spw;
+        const int sblocks = (int)std::min<int64_t>((p->nsl[r] + per_block - 1) / per_block, 1 << 16);
         p->r_nblocks[r] = p->r_count[r] ? p->r_nbl[r] + p->r_ncb[r] + std::max(sblocks, 1) : 0;
     }
     // the run buffers stay where they are while their sizes hold: the yg
@@ -1572,6 +1755,8 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
             if (p->r_ncomb[r]) GN_CUDA(cudaMalloc((void**)&p->part_long[r], 32 * (size_t)iters * p->r_ncomb[r]));
         GN_CUDA(cudaMalloc((void**)&p->rq_cnt, 4 * 2 * (size_t)iters));
         GN_CUDA(cudaMalloc((void**)&p->gat, 8 * 64 * (size_t)iters));
+        GN_CUDA(cudaMalloc((void**)&p->mq_cnt, 4 * (size_t)iters));
+        GN_CUDA(cudaMalloc((void**)&p->gmin, 8 * (size_t)iters));
         p->alloc_nall = nall;
         p->alloc_dtype = p->dtype;
         p->alloc_iters = iters;
@@ -1589,8 +1774,26 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
     p->witness = witness;
     GN_CUDA(cudaMemset(p->wit, 0xFF, 4 * (size_t)std::max<int64_t>(p->n_own, 1)));
     GN_CUDA(cudaMemset(p->rq_cnt, 0, 4 * 2 * (size_t)iters));
-    const bool count = getenv("GN_PART_COUNT") && atoi(getenv("GN_PART_COUNT")) != 0;
-    if (count != (p->gat_on != 0)) p->gen++;
+    // settled rows: none yet; the smallest gamma still to come per iteration
+    int settle = witness;
+    if (const char* e = getenv("GN_PART_SETTLE")) settle = settle && atoi(e) != 0;
+    if (settle != p->settle) p->gen++;
+    p->settle = settle;
+    GN_CUDA(cudaMemset(p->frz, 0, (size_t)std::max<int64_t>(p->n_own, 1)));
+    GN_CUDA(cudaMemset(p->mq_cnt, 0, 4 * (size_t)iters));
+    {
+        std::vector<double> gm((size_t)iters);
+        double m = std::numeric_limits<double>::infinity();
+        for (int k = iters - 1; k >= 0; --k) {
+            const double g = gammas[k];
+            if (!(g > 0.0) || !std::isfinite(g)) m = 0.0;
+            else if (g < m) m = g;
+            gm[(size_t)k] = m;
+        }
+        GN_CUDA(cudaMemcpy(p->gmin, gm.data(), 8 * (size_t)iters, cudaMemcpyHostToDevice));
+    }
+    const int count = getenv("GN_PART_COUNT") ? atoi(getenv("GN_PART_COUNT")) : 0;  // 1 gathers, 2 rows walked, 3 slices walked
+    if (count != p->gat_on) p->gen++;
     p->gat_on = count;
     GN_CUDA(cudaMemset(p->gat, 0, 8 * 64 * (size_t)iters));
     GN_CUDA(cudaMemcpy(p->gam, gammas, 8 * (size_t)iters, cudaMemcpyHostToDevice));
@@ -1635,8 +1838,18 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
 // one range of the owned rows (0: boundary, 1: interior) for iteration k
 // one range of the owned rows (0: boundary, 1: interior) for iteration k:
 // the step kernel, then (fast mode) the long rows' combine
+static int part_settle_after(gn_part* p, int k, int r, cudaStream_t s) {
+    if (r != 1 || !p->witness || !p->settle || !p->frz || !p->mq_cnt || p->n_own == 0) return GN_OK;
+    if (state_bytes(p->dtype) == 8) launch_settle<double>(p, k, s);
+    else launch_settle<float>(p, k, s);
+    GN_LAUNCHED();
+    return GN_OK;
+}
+
 static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
-    if (p->r_count[r] == 0 && !(r == 1 && p->n_push > 0)) return GN_OK;
+    if (p->r_count[r] == 0 && !(r == 1 && p->n_push > 0)) {
+        return part_settle_after(p, k, r, s);
+    }
     PartPush push{nullptr, nullptr, nullptr, nullptr, 0, 0};
     // the boundary rows' pushes ride on the interior launch
     if (r == 1 && p->n_push > 0)
@@ -1659,7 +1872,7 @@ static int part_step_range(gn_part* p, int k, int r, cudaStream_t s) {
         by_dtype(p->dtype, [&](auto, auto tg) { launch_witness<decltype(tg)>(p, r, k, s); });
         GN_LAUNCHED();
     }
-    return GN_OK;
+    return part_settle_after(p, k, r, s);
 }
 
 int gn_part_step(gn_part* p, int k, uintptr_t stream) {

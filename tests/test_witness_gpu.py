@@ -1,5 +1,6 @@
-"""GPU: the partitioned engine's zero-row certificates (gn_part.cu,
-`gn_part::witness`) never change a bit of any output.
+"""GPU: the partitioned engine's zero-row certificates and settled rows
+(gn_part.cu, `gn_part::witness`, `gn_part::frz`) never change a bit of any
+output.
 
 A row whose state is exactly 0 keeps y_i = 0 and x_i' = 0/d = 0 for any
 d = y_i + gamma*s > 1e-9 (reference `_step`, dynamics.py:102-108); one
@@ -7,7 +8,14 @@ neighbour j with gamma*y_j > 1e-9 proves d > 1e-9 without the row's walk.
 These tests run every mode with the certificates on (default) and off
 (GN_PART_WITNESS=0) on inputs that have many exact zeros, compare every
 output bit for bit, check EXACT runs against the oracle, and use the gather
-counter (GN_PART_COUNT=1, gn_part_gathers) to show the certificates fired."""
+counter (GN_PART_COUNT=1, gn_part_gathers) to show the certificates fired.
+
+Settled rows (on with the certificates; GN_PART_SETTLE=0: off): a row with
+state exactly 1 whose neighbours are all owned rows with state exactly 0 is a
+fixed point together with them (it computes s = 0, x' = v/v = 1; each
+neighbour's d >= gamma*v > 1e-9 for the smallest gamma still to come), so
+these rows are skipped altogether.  Every test below runs three ways: both
+off, certificates only, certificates + settled rows."""
 
 import numpy as np
 import pytest
@@ -46,8 +54,9 @@ def _zeroed_x0(inst, frac, seed):
     return x0
 
 
-def _run(inst, x0, s, parts, monkeypatch, witness, **kw):
+def _run(inst, x0, s, parts, monkeypatch, witness, settle=True, **kw):
     monkeypatch.setenv("GN_PART_WITNESS", "1" if witness else "0")
+    monkeypatch.setenv("GN_PART_SETTLE", "1" if settle else "0")
     halo = kw.pop("halo", "copy")
     return run_local_partitions(inst.graph, x0, s, parts, lambda sp: EngineBackend(sp, **kw), halo=halo)
 
@@ -67,7 +76,9 @@ def test_certificates_change_no_bit(dtype, exact, parts, halo, monkeypatch):
     s = P.GammaSchedule.pursuit(iterations=200)
     on = _run(inst, x0, s, parts, monkeypatch, True, dtype=dtype, exact=exact, halo=halo)
     off = _run(inst, x0, s, parts, monkeypatch, False, dtype=dtype, exact=exact, halo=halo)
+    cert = _run(inst, x0, s, parts, monkeypatch, True, settle=False, dtype=dtype, exact=exact, halo=halo)
     _same(on, off)
+    _same(cert, off)
     if exact:
         ref = O.run(inst.graph, x0, s.table(), s.final_gamma, dtype=dtype)
         np.testing.assert_array_equal(on["x"], ref.x)
@@ -96,7 +107,9 @@ def test_certificates_on_long_rows(env, monkeypatch):
     for dtype in ("fp64", "fp32"):
         on = _run(inst, x0, s, 2, monkeypatch, True, dtype=dtype, halo="peer")
         off = _run(inst, x0, s, 2, monkeypatch, False, dtype=dtype, halo="peer")
+        cert = _run(inst, x0, s, 2, monkeypatch, True, settle=False, dtype=dtype, halo="peer")
         _same(on, off)
+        _same(cert, off)
 
 
 def test_certificates_with_fallback_rows(monkeypatch):
@@ -121,7 +134,9 @@ def test_certificates_with_fallback_rows(monkeypatch):
     assert ref.fallbacks.sum() > 0
     on = _run(inst, x0, s, 2, monkeypatch, True, dtype="fp64", exact=True)
     off = _run(inst, x0, s, 2, monkeypatch, False, dtype="fp64", exact=True)
+    cert = _run(inst, x0, s, 2, monkeypatch, True, settle=False, dtype="fp64", exact=True)
     _same(on, off)
+    _same(cert, off)
     np.testing.assert_array_equal(on["x"], ref.x)
     np.testing.assert_array_equal(on["fallbacks"], ref.fallbacks)
     fast = _run(inst, x0, s, 1, monkeypatch, True, dtype="fp64")
@@ -131,9 +146,9 @@ def test_certificates_with_fallback_rows(monkeypatch):
 
 def test_certificates_skip_gathers_and_repeat(monkeypatch):
     """The counter shows the certificates at work (fewer value gathers than
-    adjacency entries once zero rows hold a witness), a certificate-free run
-    gathers every entry, and repeated runs on one backend (witnesses reset
-    at begin) are bitwise equal."""
+    adjacency entries once zero rows hold a witness; fewer again with settled
+    rows), and repeated runs on one backend (witnesses and flags reset at
+    begin) are bitwise equal."""
     inst = G.c5_rmat(14)
     g = inst.graph
     nnz = int(np.asarray(g.indptr)[-1])
@@ -142,8 +157,9 @@ def test_certificates_skip_gathers_and_repeat(monkeypatch):
     spec = build_partition(g, 1, 0)
     monkeypatch.setenv("GN_PART_COUNT", "1")
     outs = {}
-    for wit in ("1", "0"):
+    for mode, (wit, settle) in {"settle": ("1", "1"), "cert": ("1", "0"), "off": ("0", "0")}.items():
         monkeypatch.setenv("GN_PART_WITNESS", wit)
+        monkeypatch.setenv("GN_PART_SETTLE", settle)
         be = EngineBackend(spec, dtype="fp64")
         a = run_partition(be, NoExchange(be), spec.local_x0(x0), s)
         ga = be.gathers(100)
@@ -151,12 +167,17 @@ def test_certificates_skip_gathers_and_repeat(monkeypatch):
         gb = be.gathers(100)
         np.testing.assert_array_equal(a.x, b.x)
         np.testing.assert_array_equal(ga, gb)
-        outs[wit] = (a, ga)
+        outs[mode] = (a, ga)
         be.close()
-    np.testing.assert_array_equal(outs["1"][0].x, outs["0"][0].x)
-    np.testing.assert_array_equal(outs["1"][0].step_inf, outs["0"][0].step_inf)
-    g_on, g_off = outs["1"][1], outs["0"][1]
-    assert (g_off >= nnz).all()
-    # iteration 0 has no witnesses yet: every zero row walks (and is queued)
-    assert g_on[0] >= nnz
-    assert g_on[5:].max() < 0.8 * g_off[5:].min()
+    for mode in ("settle", "cert"):
+        np.testing.assert_array_equal(outs[mode][0].x, outs["off"][0].x)
+        np.testing.assert_array_equal(outs[mode][0].step_inf, outs["off"][0].step_inf)
+        np.testing.assert_array_equal(outs[mode][0].mass, outs["off"][0].mass)
+    g_on, g_cert = outs["settle"][1], outs["cert"][1]
+    # iteration 0 has no witnesses yet: every row walks (the counter runs with
+    # the certificates only; zero rows add their certificate test)
+    assert g_cert[0] >= nnz and g_on[0] >= nnz
+    assert g_cert[5:].max() < 0.8 * g_cert[0]
+    # settled rows: the members whose neighbours were all zeroed stop walking,
+    # settled zero rows stop looking at their witness
+    assert (g_on <= g_cert).all() and g_on[10:].sum() < 0.98 * g_cert[10:].sum()
