@@ -368,9 +368,22 @@ __device__ __forceinline__ void part_member_candidate(const PartWit& w, int64_t 
 
 // A certified zero row i whose witness wj is a settled member row is settled
 // too (its d stays above 1e-9 by the member's own test); looked at every
-// fourth iteration, staggered over the rows
-__device__ __forceinline__ void part_settle_zero(const PartWit& w, int64_t i, int32_t wj, int k) {
+// fourth iteration, staggered over the rows.  Otherwise the row rests (flag
+// 3): this iteration's update writes its second 0, so both state and both
+// published buffers hold 0 and, while its certificate holds, the row needs
+// no state loaded and nothing stored -- only its witness's value tested.
+__device__ __forceinline__ void part_settle_zero(const PartWit& w, int64_t i, int32_t wj, int k, unsigned fz) {
     if (((k + (int)i) & 3) == 0 && wj < w.cap && w.frz[wj] == 2) w.frz[i] = 1;
+    else if (fz != 3) w.frz[i] = 3;
+}
+
+// A resting zero row (flag 3): x_i = 0 in both buffers, so its certificate
+// is gamma*y_w > 1e-9 alone (d = 0 + gamma*s >= gamma*y_w)
+template <typename TS, typename TG>
+__device__ __forceinline__ bool part_resting_ok(TS g, int32_t wj, const TG* __restrict__ yg) {
+    using A = Arith<TS>;
+    if (wj < 0) return false;
+    return (double)A::mul(g, (TS)ld_val(yg + wj)) > kSafeDiv;
 }
 
 // A zero row's certificate (gn_part::witness): x_i == 0 and its witness j
@@ -576,8 +589,13 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             bool track = false;  // the chunk of a zero row without a certificate: its walk looks for a witness
             if (wt.wit) {
                 const int32_t row = __ldg(lng.crow + g * 32 + lane);
-                if (row < 0 || (wt.frz && wt.frz[row])) {
+                const unsigned fzr = row >= 0 && wt.frz ? (unsigned)wt.frz[row] : 0u;
+                if (row < 0 || fzr == 1 || fzr == 2) {
                     my = 0;
+                } else if (fzr == 3) {  // a resting zero row: its witness's value alone
+                    if (part_resting_ok<TS, TG>(gk, wt.wit[row], yg)) my = 0;
+                    else track = true;
+                    ++ng;
                 } else {
                     const TS xr = a.x[row];
                     TS yw;
@@ -657,9 +675,18 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             bool cert = false;
             if (wt.frz) {
                 const unsigned fz = wt.frz[i];
-                if (fz) {
+                if (fz == 1 || fz == 2) {
                     if (fz == 2) part_member_mass<TS>(a.w64[i], ob);
                     continue;
+                }
+                if (fz == 3) {  // a resting zero row
+                    const int32_t wj = wt.wit[i];
+                    if (part_resting_ok<TS, TG>(g, wj, yg)) {
+                        part_settle_zero(wt, i, wj, a.k, 3u);
+                        ++ng;
+                        continue;
+                    }
+                    wt.frz[i] = 0;  // back to walking (the test below fails the same way and queues the row)
                 }
             }
             if (wt.wit) {
@@ -671,7 +698,7 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                         s = yw;
                         r1 = r0;
                         cert = true;
-                        if (wt.frz) part_settle_zero(wt, i, wj, a.k);
+                        if (wt.frz) part_settle_zero(wt, i, wj, a.k, 0u);
                     } else {
                         part_enqueue(wt, i);
                     }
@@ -712,7 +739,7 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
                     const int64_t pn = pos + nw * 32;
                     fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
                 }
-                if (__all_sync(0xffffffffu, fz != 0)) {  // a settled slice: the members' mass only
+                if (__all_sync(0xffffffffu, fz == 1 || fz == 2)) {  // a settled slice: the members' mass only
                     if (fz == 2) part_member_mass<TS>(a.w64[a.order[0] + pos], ob);
                     continue;
                 }
@@ -720,23 +747,43 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             // rows are numbered in processing order (part_order): order[pos] == order[0] + pos,
             // so the row's state, v and weight load at once, under the gathers
             const int64_t i = a.order[0] + (valid ? pos : 0);
-            const TS xi = a.x[i], vi = a.v[i];
-            const double wi = a.w64[i];
-            const int32_t wj = wt.wit ? wt.wit[i] : -1;
+            // the row's state: not for settled rows, not for a resting zero row
+            // whose certificate holds (its state is 0 in both buffers)
+            const int32_t wj = wt.wit && (!fz || fz == 3) ? wt.wit[i] : -1;
+            bool act = !wt.wit || (valid && !fz);  // updated this iteration (without certificates: every lane walks)
+            bool queue = false, cert = false;
+            if (fz == 3) {
+                ++ng;
+                if (part_resting_ok<TS, TG>(g, wj, yg)) {
+                    if (wt.frz) part_settle_zero(wt, i, wj, a.k, 3u);
+                } else {  // back to walking: the flag goes, the row is a zero row without a certificate
+                    wt.frz[i] = 0;
+                    act = true;
+                    queue = true;
+                }
+            }
+            TS xi = TS(0), vi = TS(1);
+            double wi = 0.0;
+            if (act) {
+                if (fz != 3) xi = a.x[i];
+                vi = a.v[i];
+                wi = a.w64[i];
+            } else if (fz == 2) {
+                wi = a.w64[i];
+            }
             const int64_t e0 = a.slice_ptr[sl];
             const int nblk_s = (int)((a.slice_ptr[sl + 1] - e0) / 128);
             // this lane's index vectors: none past the range's rows, none for
             // a certified zero row (its stand-in sum is the witness's value)
-            int my = wt.wit && (!valid || fz) ? 0 : nblk_s;
+            int my = wt.wit && !act ? 0 : nblk_s;
             TS s = TS(0);
-            bool queue = false, cert = false;
-            if (wt.wit && valid && !fz && xi == TS(0)) {
+            if (wt.wit && act && fz != 3 && xi == TS(0)) {
                 TS yw;
                 if (part_certified<TS, TG>(xi, vi, g, wj, yg, yw)) {
                     s = yw;
                     my = 0;
                     cert = true;
-                    if (wt.frz) part_settle_zero(wt, i, wj, a.k);
+                    if (wt.frz) part_settle_zero(wt, i, wj, a.k, 0u);
                 } else {
                     queue = true;
                 }
@@ -745,8 +792,8 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             const int nblk = wt.wit ? (int)__reduce_max_sync(0xffffffffu, (unsigned)my) : nblk_s;
             if (wt.gat) {
                 if (wt.gat_mode == 1) ng += 4u * (unsigned)my;
-                else if (wt.gat_mode == 2) ng = ng - (xi == TS(0) && valid && !fz ? 1u : 0u) + (my > 0 ? 1u : 0u);
-                else ng = ng - (xi == TS(0) && valid && !fz ? 1u : 0u) + (lane == 0 && nblk > 0 ? 1u : 0u);
+                else if (wt.gat_mode == 2) ng = ng - ((cert || queue || fz == 3) ? 1u : 0u) + (my > 0 ? 1u : 0u);
+                else ng = ng - ((cert || queue || fz == 3) ? 1u : 0u) + (lane == 0 && nblk > 0 ? 1u : 0u);
             }
             const uint4* base = reinterpret_cast<const uint4*>(a.sell + e0) + lane;
             constexpr int NV = kPartUnroll / 4;  // index vectors per batch
@@ -772,10 +819,10 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
 #pragma unroll
                 for (int u = 0; u < NV; ++u) cv[u] = nv[u];
             }
-            if (valid && !fz) {
+            if (valid && act) {
                 const TS o = part_update_pre<TS, TG>(i, s, g, xi, vi, wi, a.xo, a.ygo, mx, fb, ob, nf);
                 if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi);
-            } else if (fz == 2 && valid) {
+            } else if (fz == 2) {
                 part_member_mass<TS>(wi, ob);
             }
             if (queue) part_enqueue(wt, i);
@@ -847,8 +894,21 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
         // the same certificate); the witness's value stands in for the sum
         bool cert = false, zero = false;
         TS s = TS(0);
-        const unsigned fz = wt.frz ? wt.frz[i] : 0u;  // a settled row: nothing but a member's mass
+        unsigned fz = wt.frz ? wt.frz[i] : 0u;  // a settled row: nothing but a member's mass
         if (fz == 2 && lane == 0) part_member_mass<TS>(w64[i], ob);
+        if (fz == 3) {
+            // a resting zero row (the step's chunk lanes took the same test):
+            // while its certificate holds nothing is loaded or stored
+            const int32_t wj = wt.wit[i];
+            if (part_resting_ok<TS, TG>(g, wj, yg)) {
+                if (lane == 0) part_settle_zero(wt, i, wj, k, 3u);
+                fz = 1;  // nothing more this iteration
+            } else {
+                __syncwarp();
+                if (lane == 0) wt.frz[i] = 0;  // back to walking: a zero row without a certificate
+                fz = 0;
+            }
+        }
         if (wt.wit && !fz) {
             const TS xi = x[i];
             zero = xi == TS(0);
@@ -857,7 +917,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
             if (zero && part_certified<TS, TG>(xi, v[i], g, wj, yg, yw)) {
                 cert = true;
                 s = yw;
-                if (wt.frz && lane == 0) part_settle_zero(wt, i, wj, k);
+                if (wt.frz && lane == 0) part_settle_zero(wt, i, wj, k, 0u);
             }
         }
         bool searched = false;
