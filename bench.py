@@ -393,6 +393,9 @@ def peak_hbm() -> tuple[float, str]:
 def traffic_note(traffic, algo):
     if traffic is None:
         return None
+    if traffic < 0.5 * algo and algo > 1e9:
+        return (f"DRAM traffic is {traffic / algo:.2f}x the algorithmic bytes: rows settled by a zero-row certificate "
+                "are not walked (roofline.walked_fraction), so most of the adjacency is not read")
     if traffic < 0.5 * algo:
         return (f"DRAM traffic is {traffic / algo:.3f}x the algorithmic bytes: the graph stays in L2/shared memory "
                 "across the iterations of a launch, so achieved/frac are the algorithmic rate of SURVEY 8(d), not "
@@ -536,7 +539,9 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                     "d2h_bytes_per_step": 8 * spec.n_own + 32 * iters,
                     "api": "partition.run_partition (host x0 in, owned x and per-iteration stats out), rank 0 shown"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
-                         "frac": achieved / (peak * ws), "traffic": traffic, "traffic_per": "step launch (one iteration)",
+                         "frac": achieved / (peak * ws), "traffic": traffic,
+                         "traffic_per": "iteration: mean DRAM bytes of one iteration's launches over the whole pursuit "
+                                        "(ncu metrics sweep of every k_part_* launch, profiles/r02_c5s24_pursuit_sweep.json)",
                          "traffic_note": traffic_note(traffic, b_iter),
                          "kernel": "gn::k_part_step (1 launch per iteration per part, replayed from a CUDA graph)" + (
                              "" if ws == 1 else (" + coalesced pushes into the peers' ghost slots (CUDA IPC)"
@@ -552,7 +557,8 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                              "ms_per_step": off_ms, "value": m * iters / (off_ms * 1e-3),
                              "achieved": b_iter * iters / (off_ms * 1e-3) / 1e9,
                              "frac": b_iter * iters / (off_ms * 1e-3) / 1e9 / peak,
-                             "gather_ceiling": gather_ceiling("C5part", off_ms / iters) if dtype == "fp64" else None,
+                             "traffic": ncu_traffic("C5part_plain", 1),
+                             "gather_ceiling": gather_ceiling("C5part_plain", off_ms / iters) if dtype == "fp64" else None,
                              "result": "bitwise equal to the timed runs' x"}},
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},

@@ -357,9 +357,14 @@ __device__ __forceinline__ void part_member_mass(double wi, double& ob) {
 // neighbour's d above 1e-9 under the smallest gamma still to come -- is queued
 // for k_part_settle, which looks at the neighbours' states.
 template <typename TS, typename TG>
-__device__ __forceinline__ void part_member_candidate(const PartWit& w, int64_t i, TS xi, TS s, TS o, TS vi) {
+__device__ __forceinline__ void part_member_candidate(const PartWit& w, int64_t i, TS xi, TS s, TS o, TS vi, int k) {
     using A = Arith<TS>;
     if (!(xi == TS(1) && o == TS(1) && s == TS(0))) return;
+    // every eighth iteration, staggered over the rows: a candidate whose
+    // neighbours publish 0 but are not yet exactly 0 fails the check for many
+    // iterations (with binary32 published values: from 1e-38 down to 5e-324),
+    // and each check is a walk of the row
+    if (((k + (int)i) & 7) != 0) return;
     const TS pub = (TS)(TG)A::mul(vi, o);
     if (!((double)A::mul((TS)*w.gfut, pub) > kSafeDiv)) return;
     const int e = atomicAdd(w.mqn, 1);
@@ -717,89 +722,112 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             for (; p < r1; ++p) s = A::add(s, (TS)ld_val(yg + col[p]));
             const TS xi = a.x[i], vi = a.v[i];
             const TS o = part_update_pre<TS, TG>(i, s, g, xi, vi, a.w64[i], a.xo, a.ygo, mx, fb, ob, nf);
-            if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi);
+            if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi, a.k);
         }
     } else {
         const int64_t pos0 = a.n_long + a.n_csr;  // first order position of slice 0
         const int64_t nw = (int64_t)(nbid - nbl - ncb) * kWarpsPerBlock;
         const int64_t sl_first = (int64_t)(rb - nbl - ncb) * kWarpsPerBlock + warp;
-        // settled rows: the lane's flag for this slice was loaded one slice
-        // ago (lanes past the range count as settled zero rows)
+        // the lane's flag and the slice's extent were loaded one slice ago
+        // (lanes past the range count as settled zero rows), so a slice starts
+        // with one round of independent loads -- state, witness, first index
+        // vectors -- then the witnesses' values, then its gathers
         unsigned fzn = 0;
-        if (wt.frz && sl_first < a.nsl) {
-            const int64_t pn = pos0 + sl_first * 32 + lane;
-            fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
+        int64_t e0n = 0;
+        int nbn = 0;
+        if (sl_first < a.nsl) {
+            e0n = a.slice_ptr[sl_first];
+            nbn = (int)((a.slice_ptr[sl_first + 1] - e0n) / 128);
+            if (wt.frz) {
+                const int64_t pn = pos0 + sl_first * 32 + lane;
+                fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
+            }
         }
         for (int64_t sl = sl_first; sl < a.nsl; sl += nw) {
             const int64_t pos = pos0 + sl * 32 + lane;
             const bool valid = pos < a.count;
             const unsigned fz = fzn;
-            if (wt.frz) {
-                if (sl + nw < a.nsl) {
+            const int64_t e0 = e0n;
+            const int nblk_s = nbn;
+            if (sl + nw < a.nsl) {
+                e0n = a.slice_ptr[sl + nw];
+                nbn = (int)((a.slice_ptr[sl + nw + 1] - e0n) / 128);
+                if (wt.frz) {
                     const int64_t pn = pos + nw * 32;
                     fzn = pn < a.count ? wt.frz[a.order[0] + pn] : 1u;
                 }
-                if (__all_sync(0xffffffffu, fz == 1 || fz == 2)) {  // a settled slice: the members' mass only
-                    if (fz == 2) part_member_mass<TS>(a.w64[a.order[0] + pos], ob);
-                    continue;
-                }
             }
-            // rows are numbered in processing order (part_order): order[pos] == order[0] + pos,
-            // so the row's state, v and weight load at once, under the gathers
+            if (wt.frz && __all_sync(0xffffffffu, fz == 1 || fz == 2)) {  // a settled slice: the members' mass only
+                if (fz == 2) part_member_mass<TS>(a.w64[a.order[0] + pos], ob);
+                continue;
+            }
+            // rows are numbered in processing order (part_order): order[pos] == order[0] + pos
             const int64_t i = a.order[0] + (valid ? pos : 0);
-            // the row's state: not for settled rows, not for a resting zero row
-            // whose certificate holds (its state is 0 in both buffers)
-            const int32_t wj = wt.wit && (!fz || fz == 3) ? wt.wit[i] : -1;
-            bool act = !wt.wit || (valid && !fz);  // updated this iteration (without certificates: every lane walks)
-            bool queue = false, cert = false;
-            if (fz == 3) {
-                ++ng;
-                if (part_resting_ok<TS, TG>(g, wj, yg)) {
-                    if (wt.frz) part_settle_zero(wt, i, wj, a.k, 3u);
-                } else {  // back to walking: the flag goes, the row is a zero row without a certificate
-                    wt.frz[i] = 0;
-                    act = true;
-                    queue = true;
-                }
-            }
+            // round 1: the state of the rows that update (not settled rows, not
+            // resting zero rows: theirs is 0 in both buffers), the witnesses, and
+            // the first index vectors of the rows that may walk
+            const bool act0 = !wt.wit || (valid && !fz);  // (without certificates every lane walks, rows past the range padding)
+            const int32_t wj = wt.wit && (act0 || fz == 3) ? wt.wit[i] : -1;
             TS xi = TS(0), vi = TS(1);
             double wi = 0.0;
-            if (act) {
-                if (fz != 3) xi = a.x[i];
+            if (act0) {
+                xi = a.x[i];
                 vi = a.v[i];
                 wi = a.w64[i];
             } else if (fz == 2) {
                 wi = a.w64[i];
             }
-            const int64_t e0 = a.slice_ptr[sl];
-            const int nblk_s = (int)((a.slice_ptr[sl + 1] - e0) / 128);
-            // this lane's index vectors: none past the range's rows, none for
-            // a certified zero row (its stand-in sum is the witness's value)
-            int my = wt.wit && !act ? 0 : nblk_s;
+            const uint4* base = reinterpret_cast<const uint4*>(a.sell + e0) + lane;
+            constexpr int NV = kPartUnroll / 4;  // index vectors per batch
+            const int my0 = act0 ? nblk_s : 0;
+            uint4 cv[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) cv[u] = u < my0 ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+            // round 2: a zero row's certificate is its witness's value (a resting
+            // row's x is 0: the same test); one load for both kinds
+            const bool zrow = wt.wit && act0 && xi == TS(0);
+            bool okc = false;
+            TS yw = TS(0);
+            if ((zrow || fz == 3) && wj >= 0) {
+                yw = (TS)ld_val(yg + wj);
+                okc = (double)A::add(A::mul(vi, xi), A::mul(g, yw)) > kSafeDiv;
+            }
+            bool act = act0, queue = false, cert = false;
             TS s = TS(0);
-            if (wt.wit && act && fz != 3 && xi == TS(0)) {
-                TS yw;
-                if (part_certified<TS, TG>(xi, vi, g, wj, yg, yw)) {
+            if (fz == 3) {
+                ++ng;
+                if (okc) {
+                    if (wt.frz) part_settle_zero(wt, i, wj, a.k, 3u);
+                } else {  // back to walking: the flag goes, the row is a zero row without a certificate
+                    wt.frz[i] = 0;
+                    act = true;
+                    queue = true;
+                    vi = a.v[i];
+                    wi = a.w64[i];
+                }
+            } else if (zrow) {
+                ++ng;
+                if (okc) {
                     s = yw;
-                    my = 0;
                     cert = true;
                     if (wt.frz) part_settle_zero(wt, i, wj, a.k, 0u);
                 } else {
                     queue = true;
                 }
-                ++ng;
             }
+            // this lane's index vectors: none past the range's rows, none for a
+            // settled, resting or certified row (its stand-in sum is the witness's value)
+            const int my = !wt.wit ? nblk_s : (act && !cert ? nblk_s : 0);
             const int nblk = wt.wit ? (int)__reduce_max_sync(0xffffffffu, (unsigned)my) : nblk_s;
             if (wt.gat) {
                 if (wt.gat_mode == 1) ng += 4u * (unsigned)my;
-                else if (wt.gat_mode == 2) ng = ng - ((cert || queue || fz == 3) ? 1u : 0u) + (my > 0 ? 1u : 0u);
-                else ng = ng - ((cert || queue || fz == 3) ? 1u : 0u) + (lane == 0 && nblk > 0 ? 1u : 0u);
+                else if (wt.gat_mode == 2) ng = ng - ((zrow || fz == 3) ? 1u : 0u) + (my > 0 ? 1u : 0u);
+                else ng = ng - ((zrow || fz == 3) ? 1u : 0u) + (lane == 0 && nblk > 0 ? 1u : 0u);
             }
-            const uint4* base = reinterpret_cast<const uint4*>(a.sell + e0) + lane;
-            constexpr int NV = kPartUnroll / 4;  // index vectors per batch
-            uint4 cv[NV];
+            if (my > my0) {  // a resting row that lost its certificate
 #pragma unroll
-            for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < NV; ++u) cv[u] = u < my ? ld_idx4(base + (size_t)u * 32) : make_uint4(0, 0, 0, 0);
+            }
             for (int b = 0; b < nblk; b += NV) {
                 uint4 nv[NV];
 #pragma unroll
@@ -821,7 +849,7 @@ __device__ __forceinline__ void part_step_vb(const StepArgs<TS, TG>& a, int vb, 
             }
             if (valid && act) {
                 const TS o = part_update_pre<TS, TG>(i, s, g, xi, vi, wi, a.xo, a.ygo, mx, fb, ob, nf);
-                if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi);
+                if (wt.frz && !cert) part_member_candidate<TS, TG>(wt, i, xi, s, o, vi, a.k);
             } else if (fz == 2) {
                 part_member_mass<TS>(wi, ob);
             }
