@@ -263,8 +263,10 @@ int gn_part_probe(gn_part* p, int mode, int reps, double* ms);
 /* Measurement aid: with GN_PART_COUNT=1 set at gn_part_begin, the value
  * gathers the run issued per iteration (index-vector entries walked, padding
  * included; zero-row certificate checks; witness searches) -- how much of the
- * adjacency the zero-row certificates let the steps skip (out[k] = 0 when
- * counting was off).  Replaces nothing in the reference: dynamics.py:105
+ * adjacency the zero-row certificates and settled rows let the steps skip
+ * (out[k] = 0 when counting was off, or with the certificates off).
+ * GN_PART_COUNT=2: the rows of the slice path that walked; 3: its slices
+ * with a walking row.  Replaces nothing in the reference: dynamics.py:105
  * always gathers every entry. */
 int gn_part_gathers(gn_part* p, int done, int64_t* out);
 /* CUDA IPC of one device allocation between the processes of a node. */
