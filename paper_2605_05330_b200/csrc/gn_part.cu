@@ -214,6 +214,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
 }
 
 constexpr int kPartLongDegreeMin = 128, kPartLongDegreeMax = 1024;
+constexpr int kCombRows = 8;  // long rows per warp of k_part_long_combine
 constexpr int kSlicesPerWarp = 16;  // slice blocks: slices per warp (GN_PART_SPW; C5 scale 24: 1 / 4 / 16 / 64 -> 0.715 / 0.573 / 0.552 / 0.612 ms per iteration)
 constexpr int kChunkDefault = 128;  // long-row chunk length (thread per chunk; 0: warp pieces)
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
@@ -901,9 +902,9 @@ __global__ void __launch_bounds__(kPartThreads, GN_PART_MINB) k_part_step(const 
     part_step_vb<TS, TG>(a, (int)blockIdx.x, (int)threadIdx.x, red);
 }
 
-// Long rows, fast mode: one warp per row adds its pieces' sums in piece order
-// (lanes stride the pieces, fixed butterfly fold) and lane 0 updates the row
-// (dynamics.py:104-107); per-block stats as k_part_step.
+// Long rows, fast mode: a row's pieces' sums are added in piece order by one
+// warp (lanes stride the pieces, fixed butterfly fold) and lane 0 updates the
+// row (dynamics.py:104-107); per-block stats as k_part_step.
 template <typename TS, typename TG>
 __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
     int64_t n_long, int64_t first, const int32_t* __restrict__ lp,
@@ -915,46 +916,63 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
     const TS g = (TS)gam[k];
     double mx = 0.0, fb = 0.0, ob = 0.0, nf = 0.0;
     const int lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * (kPartThreads / 32) + (threadIdx.x >> 5);
-    if (q < n_long) {
-        const int64_t i = first + q;
-        // a certified zero row: its chunks were not walked (k_part_step took
-        // the same certificate); the witness's value stands in for the sum
-        bool cert = false, zero = false;
-        TS s = TS(0);
-        unsigned fz = wt.frz ? wt.frz[i] : 0u;  // a settled row: nothing but a member's mass
-        if (fz == 2 && lane == 0) part_member_mass<TS>(w64[i], ob);
-        if (fz == 3) {
-            // a resting zero row (the step's chunk lanes took the same test):
-            // while its certificate holds nothing is loaded or stored
-            const int32_t wj = wt.wit[i];
-            if (part_resting_ok<TS, TG>(g, wj, yg)) {
-                if (lane == 0) part_settle_zero(wt, i, wj, k, 3u);
-                fz = 1;  // nothing more this iteration
-            } else {
-                __syncwarp();
-                if (lane == 0) wt.frz[i] = 0;  // back to walking: a zero row without a certificate
-                fz = 0;
+    // a warp takes kCombRows rows.  First a lane per row looks at it on its own:
+    // settled rows cost their flag (a member adds its mass), resting rows
+    // their witness's value, certified zero rows are updated at once (their
+    // chunks were not walked: k_part_step took the same certificate; the
+    // witness's value stands in for the sum).  Then the warp adds the chunk
+    // sums of the rows that walked, one row after another.  (One warp per
+    // row made 7 k blocks of dependent loads per iteration, 23 us of a late
+    // iteration in which no long row walks -- 7 us now; 32 rows per warp made
+    // the early iterations, where every long row walks, 133 us instead of 36.)
+    const int64_t q0 = ((int64_t)blockIdx.x * (kPartThreads / 32) + (threadIdx.x >> 5)) * kCombRows;
+    {
+        const int64_t q = q0 + lane;
+        bool need = false, zero = false;
+        if (lane < kCombRows && q < n_long) {
+            const int64_t i = first + q;
+            unsigned fz = wt.frz ? wt.frz[i] : 0u;
+            if (fz == 2) part_member_mass<TS>(w64[i], ob);
+            if (fz == 3) {
+                // a resting zero row (the step's chunk lanes took the same test)
+                const int32_t wj = wt.wit[i];
+                if (part_resting_ok<TS, TG>(g, wj, yg)) {
+                    part_settle_zero(wt, i, wj, k, 3u);
+                    fz = 1;  // nothing more this iteration
+                } else {
+                    wt.frz[i] = 0;  // back to walking: a zero row without a certificate
+                    fz = 0;
+                }
+            }
+            if (!fz) {
+                need = true;
+                if (wt.wit) {
+                    const TS xi = x[i];
+                    zero = xi == TS(0);
+                    TS yw;
+                    const int32_t wj = wt.wit[i];
+                    if (zero && part_certified<TS, TG>(xi, v[i], g, wj, yg, yw)) {
+                        need = false;
+                        part_update<TS, TG>(i, yw, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+                        if (wt.frz) part_settle_zero(wt, i, wj, k, 0u);
+                    }
+                }
             }
         }
-        if (wt.wit && !fz) {
-            const TS xi = x[i];
-            zero = xi == TS(0);
-            TS yw;
-            const int32_t wj = wt.wit[i];
-            if (zero && part_certified<TS, TG>(xi, v[i], g, wj, yg, yw)) {
-                cert = true;
-                s = yw;
-                if (wt.frz && lane == 0) part_settle_zero(wt, i, wj, k, 0u);
-            }
-        }
-        bool searched = false;
-        if (!cert && !fz) {
-            const int32_t j0 = __ldg(lp + q), j1 = __ldg(lp + q + 1);
+        unsigned todo = __ballot_sync(0xffffffffu, need);
+        const unsigned zeros = __ballot_sync(0xffffffffu, zero);
+        while (todo) {
+            const int r = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t qq = q0 + r, i = first + qq;
+            const bool zr = (zeros >> r) & 1u;
+            TS s = TS(0);
+            const int32_t j0 = __ldg(lp + qq), j1 = __ldg(lp + qq + 1);
             for (int32_t j = j0 + lane; j < j1; j += 32) s = A::add(s, (TS)pc_sum[j]);
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) s = A::add(s, __shfl_xor_sync(0xffffffffu, s, d));
-            if (zero && pc_max) {
+            bool searched = false;
+            if (zr && pc_max) {
                 // a zero row without a certificate: its chunks' walks kept their
                 // largest values; the largest of those (the first chunk on ties)
                 // is the row's new witness -- no second walk
@@ -974,10 +992,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_long_combine(
                 if (lane == 0) wit_out[i] = arg;
                 searched = true;
             }
-        }
-        if (lane == 0 && !fz) {
-            part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
-            if (zero && !cert && !searched) part_enqueue(wt, i);
+            if (lane == 0) {
+                part_update<TS, TG>(i, s, g, w64, v, x, xo, ygo, mx, fb, ob, nf);
+                if (zr && !searched) part_enqueue(wt, i);
+            }
         }
     }
     __shared__ double red[kPartThreads / 32][4];
@@ -1810,14 +1828,19 @@ int gn_part_begin(gn_part* p, const double* x0, const double* gammas, int iters,
         p->r_nbl[r] = p->r_long[r]
                           ? (int)std::min<int64_t>((lunits + kPartThreads / 32 - 1) / (kPartThreads / 32), 1 << 12)
                           : 0;
-        p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + kPartThreads / 32 - 1) / (kPartThreads / 32)) : 0;
+        const int64_t rows_per_block = (int64_t)kCombRows * (kPartThreads / 32);
+        p->r_ncomb[r] = p->r_long[r] ? (int)((p->r_long[r] + rows_per_block - 1) / rows_per_block) : 0;
         p->r_csr[r] = p->long_fast[r] - p->r_long[r];  // EXACT: the long rows, one thread each
         p->r_ncb[r] = p->r_csr[r] ? pblocks(p->r_csr[r]) : 0;
         // slice blocks: `spw` slices per warp (GN_PART_SPW).  One slice per warp
         // leaves the balancing to the block scheduler; several make a settled
         // slice cost one flag test of a running warp instead of a block's launch
         // and its chain of dependent loads
-        int spw = kSlicesPerWarp;
+        // (at most kSlicesPerWarp, fewer on a small range so the blocks still
+        // fill the GPU about four times over: an 8-way part of C5 with 16 slices
+        // per warp had 270 blocks for 592 resident slots and ran at 0.51 ms per
+        // iteration instead of 0.22)
+        int spw = (int)std::min<int64_t>(kSlicesPerWarp, std::max<int64_t>(1, p->nsl[r] / (4 * 148 * GN_PART_MINB * (kPartThreads / 32))));
         if (const char* e = getenv("GN_PART_SPW")) spw = std::max(1, atoi(e));
         const int64_t per_block = (int64_t)(kPartThreads / 32) * spw;
         const int sblocks = (int)std::min<int64_t>((p->nsl[r] + per_block - 1) / per_block, 1 << 16);
