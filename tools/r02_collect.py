@@ -35,7 +35,7 @@ def sweep(csvfile: Path, out: Path, iters: int = 1000) -> dict:
     for r in rows[1:]:
         if len(r) < len(hdr):
             continue
-        d = per.setdefault(int(r[ci["ID"]]), {"kernel": r[ci["Kernel Name"]].split("(")[0].split("<")[0].split("::")[-1]})
+        d = per.setdefault(int(r[ci["ID"]]), {"kernel": r[ci["Kernel Name"]].split("(")[0].split("<")[0].split("::")[-1].replace("void ", "").strip()})
         v, unit = num(r[ci["Metric Value"]]), r[ci["Metric Unit"]]
         scale = {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
                  "sector": 1}.get(unit, 1)
