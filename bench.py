@@ -390,10 +390,10 @@ def peak_hbm() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_note(traffic, algo):
+def traffic_note(traffic, algo, certificates=False):
     if traffic is None:
         return None
-    if traffic < 0.5 * algo and algo > 1e9:
+    if certificates and traffic < 0.9 * algo:
         return (f"DRAM traffic is {traffic / algo:.2f}x the algorithmic bytes: rows settled by a zero-row certificate "
                 "are not walked (roofline.walked_fraction), so most of the adjacency is not read")
     if traffic < 0.5 * algo:
@@ -542,7 +542,7 @@ def run_partitioned(args, ws, rank, local, inst, torch, P, E, setup_t0) -> int:
                          "frac": achieved / (peak * ws), "traffic": traffic,
                          "traffic_per": "iteration: mean DRAM bytes of one iteration's launches over the whole pursuit "
                                         "(ncu metrics sweep of every k_part_* launch, profiles/r02_c5s24_pursuit_sweep.json)",
-                         "traffic_note": traffic_note(traffic, b_iter),
+                         "traffic_note": traffic_note(traffic, b_iter, certificates=True),
                          "kernel": "gn::k_part_step (1 launch per iteration per part, replayed from a CUDA graph)" + (
                              "" if ws == 1 else (" + coalesced pushes into the peers' ghost slots (CUDA IPC)"
                                                  if args.halo == "peer" else " + NCCL halo")),
