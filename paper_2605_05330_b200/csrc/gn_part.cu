@@ -216,7 +216,7 @@ __global__ void k_part_prepare(int64_t n_own, int64_t n_all, const double* __res
 constexpr int kPartLongDegreeMin = 128, kPartLongDegreeMax = 1024;
 constexpr int kCombRows = 8;  // long rows per warp of k_part_long_combine
 constexpr int kSlicesPerWarp = 16;  // slice blocks: slices per warp (GN_PART_SPW; C5 scale 24: 1 / 4 / 16 / 64 -> 0.715 / 0.573 / 0.552 / 0.612 ms per iteration)
-constexpr int kChunkDefault = 128;  // long-row chunk length (thread per chunk; 0: warp pieces)
+constexpr int kChunkDefault = 512;  // long-row chunk length (thread per chunk; 0: warp pieces)
 constexpr int kPiece = 512;  // adjacency entries per long-row piece (fast mode; 2048: +3.5% time on C5)
 
 // The long rows' pieces (fast mode; see gn_part::pc_beg)
@@ -1263,7 +1263,7 @@ static int upload_into(T** dst, const std::vector<T>& h) {
 // weights, blocked SELL) is rebuilt in the new numbering.
 static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // rows above this degree are "long": in fast mode cut into chunks of
-    // GN_PART_CHUNK entries (default 128) summed one thread per chunk over a
+    // GN_PART_CHUNK entries (default 512) summed one thread per chunk over a
     // blocked SELL of chunks and combined per row (0: one warp per 512-entry
     // piece); in EXACT mode one thread per row over the CSR.  The others run
     // one thread per row over the blocked SELL.  Both thread-per-row walks
@@ -1274,7 +1274,11 @@ static int part_order(gn_part* P, const int32_t* bnd, int64_t nb) {
     // iteration -- warp pieces: threshold 512 1.62, 1024 1.50, 4096 1.44,
     // 8192 1.47, 65536 5.96; chunks of 128: threshold 1024 (= 2048) 1.335,
     // 4096 1.374; chunks of 64 / 256: 1.348 / 1.365 (R-MAT degrees cluster
-    // near 2^29 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).
+    // near 2^29 * 0.76^(24-k) * 0.24^k: ~740, ~2300, ~7400, ...).  That
+    // is with every row walked; over the whole pursuit, where most long
+    // rows are certified zero rows whose chunks only test a flag, fewer
+    // chunks win: ms per 1000 iterations at 128 / 256 / 512 / 1024:
+    // 530.8 / 521.7 / 515.3 / 521.6 -- hence the default of 512.
     // On a small part the longest thread-per-row chain bounds the iteration
     // instead: the threshold is nnz / 16384 rounded down to a power of two
     // in [128, 1024] (C3, 2 M entries, us per iteration at threshold 32 / 64
